@@ -1,0 +1,269 @@
+"""Pins of the oracle's time stepping (§4.2; readings R1-R11 of
+DESIGN.md): closed forms (Hertz contact duration, restitution from the
+nondimensional ODE, static-stack overlaps, sliding-to-rolling), exact per-step
+invariants, conservation laws, and brute force vs the CDG."""
+import json
+import math
+import os
+
+import numpy as np
+import pytest
+from scipy.integrate import solve_ivp
+from scipy.special import beta
+
+from paper_1301_1714_b200 import scenes as S
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "worked_examples.json")))
+
+
+def test_free_fall_worked_example(orc):
+    """one semi-implicit Euler step from rest under g."""
+    ex = GOLD["free_fall"][0]
+    sp = S.SimParams(gravity=tuple(ex["g"]), dt=ex["dt"], box_hi=(100.0, 100.0, 100.0))
+    sc = S.make_scene("ff", sp, [[50.0, 50.0, 50.0]], radius=[1.0], mass=[1.0])
+    p = orc.make_params(sc.params, sc.radius)
+    st = orc.State.from_scene(sc)
+    r = orc.step(p, st, orc.History.empty(1, 4))
+    assert r.rc == 0
+    assert st.vel[0] == pytest.approx(ex["v"], abs=1e-6)
+    assert 50.0 - st.pos[0, 2] == pytest.approx(ex["dx"], rel=1e-6)
+
+
+# ------------------------------------------------ P7 head-on collision ----
+
+def ode_restitution(alpha):
+    """x'' + α x^{1/4} x' + x^{3/2} = 0, x(0)=0, x'(0)=1: the practical model's
+    normal contact (Eqs. 4, 9, 10) nondimensionalised by δ_max-type scales
+    (DESIGN.md §Pins). Returns (e, τ_c)."""
+    def f(t, y):
+        x = max(y[0], 0.0)
+        return [y[1], -alpha * x**0.25 * y[1] - x**1.5]
+
+    def hit(t, y):
+        return y[0]
+    hit.terminal, hit.direction = True, -1
+    s = solve_ivp(f, [0, 50], [0.0, 1.0], events=hit, rtol=1e-12, atol=1e-14, method="DOP853",
+                  first_step=1e-6)
+    return -s.y_events[0][0][1], s.t_events[0][0]
+
+
+def run_head_on(orc, alpha, v0, steps_per_tc=1000):
+    m = float(S.sphere_mass([S.R])[0])
+    mstar = m / 2
+    K = float(np.float32(7.326e6)) * math.sqrt(float(np.float32(S.R)) / 2)
+    tc_scale = (mstar / K) ** 0.4 * v0**-0.2
+    dt = float(np.float32(3.218 * tc_scale / steps_per_tc))
+    sc = S.two_body(v0, S.SimParams(damping=alpha, friction=0.5, dt=dt), gap=0.0)
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(2, 8)
+    steps, dmax = 0, 0.0
+    for _ in range(4 * steps_per_tc):
+        orc.step(p, st, h)
+        d = 2 * st.radius[0] - np.linalg.norm(st.pos[1] - st.pos[0])
+        if d > 0:
+            steps += 1
+            dmax = max(dmax, d)
+        elif steps:
+            break
+    lo = int(np.argmin(st.pos[:, 0]))
+    e = (st.vel[1 - lo, 0] - st.vel[lo, 0]) / v0
+    return e, steps * p.dt, dmax, tc_scale, K, mstar, p.dt
+
+
+def test_hertz_contact_duration_closed_form(orc):
+    """α = 0: t_c = 2 (2/5) B(2/5,1/2) (5/4)^{2/5} (m*/K)^{2/5} v0^{-1/5},
+    δ_max = (5 m* v0^2 / (4K))^{2/5}, e = 1 (energy conserved)."""
+    const = 2 * 0.4 * beta(0.4, 0.5) * 1.25**0.4
+    assert const == pytest.approx(3.218065, rel=1e-6)
+    for v0 in (0.01, 0.1, 1.0):
+        e, tc, dmax, scale, K, mstar, dt = run_head_on(orc, 0.0, v0)
+        assert tc == pytest.approx(const * scale, abs=2 * dt)
+        assert dmax == pytest.approx((5 * mstar * v0**2 / (4 * K)) ** 0.4, rel=2e-5)
+        assert e == pytest.approx(1.0, abs=1e-6)
+
+
+@pytest.mark.parametrize("alpha", [0.1, 0.2522, 0.5, 1.0])
+def test_restitution_matches_ode(orc, alpha):
+    """e(α) from the nondimensional ODE, independent of v0; first-order in dt
+    (|Δe|/e <= 2e-3 at t_c/dt ~ 1000); duration τ_c (m*/K)^{2/5} v0^{-1/5}."""
+    e_ode, tau = ode_restitution(alpha)
+    for v0 in (0.01, 0.1, 1.0):
+        e, tc, _, scale, _, _, dt = run_head_on(orc, alpha, v0)
+        assert e == pytest.approx(e_ode, rel=2e-3)
+        assert tc == pytest.approx(tau * scale, abs=2 * dt)
+
+
+def test_restitution_anchor_values():
+    """The ODE itself: α = 0 is the Hertz closed form; e(0.2522) ~ 0.70 is the
+    reading-R19 default."""
+    e0, tau0 = ode_restitution(0.0)
+    assert e0 == pytest.approx(1.0, abs=1e-9)
+    assert tau0 == pytest.approx(2 * 0.4 * beta(0.4, 0.5) * 1.25**0.4, rel=1e-9)
+    assert ode_restitution(0.2522)[0] == pytest.approx(0.70, abs=1e-3)
+
+
+# ------------------------------------------------------- P8 static stack --
+
+def test_static_stack_overlaps(orc):
+    """Settled column of n spheres: the contact with k spheres above it has
+    δ_k = (k m g / (C_n sqrt(R*)))^{2/3}, R* = r/2 between spheres, r at the
+    floor (Hertz: k_n δ = C_n sqrt(R* δ) δ = k m g)."""
+    n = 10
+    sc = S.stack(n, S.SimParams(damping=1.0))
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(n, 8)
+    rc, err, F, T = orc.run(p, st, h, 150000)
+    assert rc == 0
+    y = np.sort(st.pos[:, 1])
+    m, g, r = st.mass[0], -p.g[1], st.radius[0]
+    d_pair = 2 * r - np.diff(y)
+    k_above = np.arange(n - 1, 0, -1)
+    want = (k_above * m * g / (p.Cn * np.sqrt(r / 2))) ** (2 / 3)
+    assert d_pair == pytest.approx(want, rel=1e-7)
+    assert r - y[0] == pytest.approx((n * m * g / (p.wCn * np.sqrt(r))) ** (2 / 3), rel=1e-7)
+
+
+# ------------------------------------------------ P9 / P10 sliding sphere --
+
+def slider(orc, truncate):
+    sp = S.SimParams(truncate_dt=truncate)
+    m = float(S.sphere_mass([S.R])[0])
+    p0 = orc.make_params(sp, np.array([S.R], np.float32))
+    d_eq = (m * (-p0.g[1]) / (p0.wCn * np.sqrt(np.float32(S.R)))) ** (2 / 3)
+    L = 8 * S.D
+    sc = S.make_scene("slide", sp.replace(box_hi=(L, L, L)),
+                      [[0.5 * L, float(S.R) - d_eq, 0.5 * L]], vel=[[0.1, 0, 0]])
+    p = orc.make_params(sc.params, sc.radius)
+    return p, orc.State.from_scene(sc), orc.History.empty(1, 8)
+
+
+def test_sliding_to_rolling(orc):
+    """Angular momentum about the contact point is conserved, so the sphere
+    ends rolling at (5/7) v0 after t = 2 v0/(7 μ g) (textbook; reading R4 flag)."""
+    p, st, h = slider(orc, True)
+    v0 = 0.1
+    t_slip = 2 * v0 / (7 * p.mu * -p.g[1])
+    orc.run(p, st, h, int(1.5 * t_slip / p.dt))
+    assert st.vel[0, 0] == pytest.approx(5 / 7 * v0, rel=2e-5)
+    assert -st.omega[0, 2] * st.radius[0] == pytest.approx(5 / 7 * v0, rel=2e-5)
+    # during the slip phase the sphere is still sliding
+    p, st, h = slider(orc, True)
+    orc.run(p, st, h, int(0.7 * t_slip / p.dt))
+    assert st.vel[0, 0] > -st.omega[0, 2] * st.radius[0] + 0.01 * v0
+
+
+def test_wall_contact_impulse_invariant(orc):
+    """P10: with g ∥ n, every sliding step has r|Δω| = (5/2)|Δv_t| (Eq. 3 with
+    I = 0.4 m r^2), and the tangential impulse is μ times the normal one."""
+    p, st, h = slider(orc, False)
+    for k in range(1500):
+        v, w = st.vel.copy(), st.omega.copy()
+        r = orc.step(p, st, h)
+        dv, dw = st.vel - v, st.omega - w
+        dvt = math.hypot(dv[0, 0], dv[0, 2])
+        assert st.radius[0] * np.linalg.norm(dw) == pytest.approx(2.5 * dvt, rel=1e-9)
+        Fn = r.F[0, 1]
+        Ft = math.hypot(r.F[0, 0], r.F[0, 2])
+        assert Ft == pytest.approx(p.wmu * abs(Fn), rel=1e-9)
+
+
+# ------------------------------------------------------ P12/P13/P15 -------
+
+def test_momentum_conservation(orc):
+    """No walls touched, g = 0: Σ m v is constant (third law)."""
+    c1 = S.C1()
+    sp = S.SimParams(gravity=(0.0, 0.0, 0.0), box_hi=(0.016, 0.02, 0.016))
+    sc = S.make_scene("free", sp, c1.pos + np.float32(2e-3), c1.vel, c1.omega)
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(sc.n, 16)
+    P0 = (st.mass[:, None] * st.vel).sum(0)
+    A = (st.mass[:, None] * np.abs(st.vel)).sum()
+    contacts = 0
+    for _ in range(300):
+        r = orc.step(p, st, h)
+        assert r.rc == 0 and r.n_wall_contacts == 0
+        contacts += r.n_pair_contacts
+    assert contacts > 300 * 1000 * 2  # a dense, colliding set
+    assert np.abs((st.mass[:, None] * st.vel).sum(0) - P0).max() <= 1e-12 * A
+
+
+def total_energy(orc, st, p):
+    """KE + rotational KE + Hertz elastic energy (2/5) K δ^{5/2} of every
+    contact (K = C_n sqrt(R*); walls R* = r)."""
+    E = 0.5 * (st.mass * (st.vel**2).sum(1)).sum()
+    E += 0.5 * (0.4 * st.mass * st.radius**2 * (st.omega**2).sum(1)).sum()
+    x, r = st.pos, st.radius
+    for i, j in orc.contacts_brute(x, r):
+        d = r[i] + r[j] - np.linalg.norm(x[j] - x[i])
+        E += 0.4 * p.Cn * math.sqrt(1 / (1 / r[i] + 1 / r[j])) * d**2.5
+    for a in range(3):
+        for dist in (x[:, a] - p.lo[a], p.hi[a] - x[:, a]):
+            d = r - dist
+            k = d > 0
+            E += (0.4 * p.wCn * np.sqrt(r[k]) * d[k] ** 2.5).sum()
+    return E
+
+
+def test_energy_conservation_elastic_frictionless(orc):
+    """α = 0, μ = 0 (so F_t = 0), elastic walls, g = 0: total energy shows no
+    secular drift, and its oscillation shrinks with dt."""
+    devs = []
+    for dt in (2e-6, 1e-6):
+        c1 = S.C1()
+        sp = S.SimParams(gravity=(0.0, 0.0, 0.0), damping=0.0, friction=0.0, dt=dt)
+        sc = S.make_scene("c1", sp.replace(box_hi=c1.params.box_hi), c1.pos,
+                          c1.vel * np.float32(4), c1.omega)
+        p = orc.make_params(sc.params, sc.radius)
+        st, h = orc.State.from_scene(sc), orc.History.empty(sc.n, 16)
+        E0 = total_energy(orc, st, p)
+        every = int(round(100 * 2e-6 / dt))  # same physical sample times
+        dev = []
+        for k in range(20 * every):
+            orc.step(p, st, h)
+            if k % every == every - 1:
+                dev.append(abs(total_energy(orc, st, p) / E0 - 1))
+        devs.append(np.mean(dev))
+    assert devs[0] < 3e-3 and devs[1] < 0.7 * devs[0]
+
+
+def test_kissing_bound_and_history(orc):
+    """P15: monodisperse contacts per particle <= 12 every step;
+    history lists hold exactly the contacts of the step (reading R10)."""
+    sc = S.C1()
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(sc.n, 16)
+    for _ in range(30):
+        r = orc.step(p, st, h)
+        assert r.rc == 0
+        pair = (h.pid < orc.WALL_PID0) & (np.arange(16)[None, :] < h.cnt[:, None])
+        assert pair.sum(1).max() <= 12
+        assert pair.sum() == r.n_pair_contacts
+        assert h.cnt.sum() == r.n_pair_contacts + r.n_wall_contacts
+        got = {(int(st.id[i]), int(st.id[j])) for i, j in orc.contacts_brute(st.pos, st.radius)}
+    # after the last step the stored lists are those of the pre-integration
+    # positions; the contact set was found by the CDG and is symmetric
+    d = h.as_dict(st.id)
+    pairs = {k for k in d if k[1] < orc.WALL_PID0}
+    assert all((b, a) in pairs for a, b in pairs)
+    assert len(got) > 0
+
+
+def test_grid_step_equals_brute_force_step(orc):
+    """a step through the CDG equals a step with all-pairs
+    detection (same contacts; forces equal up to summation order)."""
+    sc = S.random_gas(700, 9.0, 8, r_range=(0.3e-3, 0.5e-3), v_sigma=0.02)
+    for brute in (False, True):
+        p = orc.make_params(sc.params, sc.radius, brute=brute)
+        st, h = orc.State.from_scene(sc), orc.History.empty(sc.n, 32)
+        r = orc.step(p, st, h)
+        if brute:
+            rb, stb, hb = r, st, h
+        else:
+            rg, stg, hg = r, st, h
+    assert rg.n_pair_contacts == rb.n_pair_contacts > 100
+    assert np.array_equal(stg.id, stb.id)
+    assert hg.as_dict(stg.id).keys() == hb.as_dict(stb.id).keys()
+    scale = np.abs(rb.F).max()
+    assert np.abs(rg.F - rb.F).max() <= 1e-12 * scale
+    assert np.abs(stg.pos - stb.pos).max() <= 1e-15
+    assert np.abs(stg.vel - stb.vel).max() <= 1e-12 * np.abs(stb.vel).max()
