@@ -1,0 +1,413 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 DEM timestep (arXiv 1301.1714 hot path).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C4] [--impl reference]
+
+Default workload (N=1): C4, the 4,194,304-sphere settling bed on which
+BASELINE.json's metric (particle-steps/s at 1/2/4/8 B200, % of HBM roofline)
+is quoted. Prints ONE JSON line on rank 0.
+
+Timed region (our arm): W warm-up steps, then barrier + synchronize, K steps
+of dem_step on the handle's stream with CUDA events around every kernel
+(dem_profile), synchronize + barrier; the max over ranks. The per-step working
+set (>1 GB at C4) is far larger than the 126 MB L2, so no L2 flush is needed.
+A second K-step region replays the captured CUDA graph (the library's default
+path) and is reported as ms_per_step_graph.
+
+--impl reference: the fp64 CPU oracle (oracle/, test infrastructure) timed on
+the host cores on a bounded sample of the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import statistics
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "particle-steps/sec (ms/step) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "particle-steps/s"
+KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other")
+
+
+def load_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return rank, world, local
+
+
+# ------------------------------------------------------------ clocks -------
+class ClockSampler:
+    """NVML sampling of SM clock and throttle reasons during the timed region."""
+
+    REASONS = {
+        0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap",
+        0x8: "hw_slowdown", 0x10: "sync_boost", 0x20: "sw_thermal_slowdown",
+        0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+        0x100: "display_clock_setting",
+    }
+
+    def __init__(self, index: int):
+        self.samples = []
+        self.reasons = 0
+        self.max_mhz = None
+        self.ok = False
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM)
+            self.ok = True
+        except Exception as e:  # pragma: no cover
+            self.err = str(e)
+        self._stop = threading.Event()
+
+    def _run(self):
+        while not self._stop.is_set():
+            try:
+                self.samples.append(self.nv.nvmlDeviceGetClockInfo(self.h, self.nv.NVML_CLOCK_SM))
+                self.reasons |= int(self.nv.nvmlDeviceGetCurrentClocksEventReasons(self.h))
+            except Exception:
+                pass
+            time.sleep(0.02)
+
+    def __enter__(self):
+        if self.ok:
+            self.t = threading.Thread(target=self._run, daemon=True)
+            self.t.start()
+        return self
+
+    def __exit__(self, *a):
+        if self.ok:
+            self._stop.set()
+            self.t.join()
+
+    def summary(self):
+        if not self.ok:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvml unavailable"]}
+        names = [n for b, n in self.REASONS.items() if self.reasons & b and n != "gpu_idle"]
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None,
+                "sm_max_mhz": self.max_mhz, "reasons": names, "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------- scenes ------
+def make_scene(name: str, model: str, rank: int):
+    from paper_1301_1714_b200 import scenes as S
+    sp = S.SimParams(model=model)
+    if name == "C5":
+        return S.C5(sp.replace(max_contacts=32), rank=rank)
+    return S.CONFIGS[name](sp)
+
+
+def describe(sc) -> str:
+    m = sc.meta
+    if sc.name.startswith("C4"):
+        return (f"{sc.name}: {sc.n:,}-sphere pre-compressed settling bed (SC {m['nxyz']}, "
+                f"spacing 0.998 d, r = 0.5 mm) under gravity, {sc.params.model} model")
+    if m.get("kind") == "fcc":
+        return (f"{sc.name}: {sc.n:,}-sphere jittered FCC dense packing {m['ncells']} cells, "
+                f"{sc.params.model} model")
+    return f"{sc.name}: {sc.n:,} spheres, {sc.params.model} model"
+
+
+# ------------------------------------------------- algorithmic bytes -------
+def alg_bytes(model: str, rho_c: float, c_bar: float):
+    """Per particle-step. Sweep kernel: state read+write 96,
+    SCCM read 4, next CM write 4, offsets read 4 rho_c, history counts r+w 8,
+    history entries r+w 32 c_bar. Whole step: 120 + 8 rho_c +
+    32 c_bar (practical), 88 + 8 rho_c (simple)."""
+    if model == "practical":
+        return 112 + 4 * rho_c + 32 * c_bar, 120 + 8 * rho_c + 32 * c_bar
+    return 80 + 4 * rho_c, 88 + 8 * rho_c
+
+
+# ------------------------------------------------------- reference arm -----
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as orc
+    steps_total = args.warmup + args.steps
+    sc, sample = reference_sample(args.config, args.model, steps_total)
+    p = orc.make_params(sc.params, sc.radius)
+    st = orc.State.from_scene(sc)
+    h = orc.History.empty(sc.n, sc.params.max_contacts)
+    for _ in range(args.warmup):
+        orc.step(p, st, h)
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        rc = orc.step(p, st, h).rc
+        assert rc == 0, rc
+    t = time.perf_counter() - t0
+    value = sc.n * args.steps / t
+    cores = 1
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * t / args.steps,
+        "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
+        "data": "synthetic", "config": {"workload": describe(sc), "n_particles": sc.n,
+                                        "sample": sample},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": cores, "kind": "oracle",
+                         "sample": sample, "cpu": cpu_model()},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+def reference_sample(config: str, model: str, steps_total: int, budget_s: float = 150.0):
+    """A bounded sample of the workload: the same scene generator, narrowed so
+    that steps_total oracle steps take about budget_s (oracle ~0.35 M
+    particle-steps/s on one core)."""
+    from paper_1301_1714_b200 import scenes as S
+    sp = S.SimParams(model=model)
+    if config == "C4":
+        target = budget_s * 3.5e5 / max(1, steps_total)
+        scale = 1
+        while 4194304 // (scale * scale) > target and scale < 64:
+            scale *= 2
+        sc = S.C4(sp, scale=scale)
+        return sc, (f"C4 generator narrowed {scale}x in x and z: {sc.n:,} spheres "
+                    f"(same bed height, spacing, jitter), from t=0")
+    sc = make_scene(config, model, 0)
+    return sc, f"{config} full ({sc.n:,} spheres) from t=0"
+
+
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except Exception:
+        pass
+    return "unknown"
+
+
+def cpu_baseline_on_state(d, sc, budget_s: float = 12.0):
+    """Time the fp64 oracle (as it stands, single thread) on the GPU's own
+    warmed-up state of the same workload; whole steps until ~budget_s."""
+    from oracle import oracle as orc
+    from tests.parity import oracle_inputs
+    K = int(d.stats()["max_contacts_seen"]) + 2
+    st, h = oracle_inputs(d, max(K, 4))
+    p = orc.make_params(sc.params, sc.radius)
+    n_steps, t = 0, 0.0
+    while t < budget_s and n_steps < 50:
+        t0 = time.perf_counter()
+        rc = orc.step(p, st, h).rc
+        t += time.perf_counter() - t0
+        n_steps += 1
+        if rc != 0:
+            break
+    return {"value": sc.n * n_steps / t, "unit": UNIT, "cores": 1, "kind": "oracle",
+            "sample": (f"{n_steps} whole step(s) of the full {sc.name} state ({sc.n:,} spheres) "
+                       f"after the GPU warm-up, fp64, one thread"), "cpu": cpu_model(),
+            "seconds": t}
+
+
+# ------------------------------------------------------------- our arm -----
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_1301_1714_b200.dem import DEM_F_NO_GRAPH, Dem
+
+    rank, world, local = dist_env()
+    if world > 1:
+        dist.init_process_group("nccl", init_method="env://")
+    torch.cuda.set_device(local)
+    peak_gbs, peak_src = load_peaks()
+    stream = torch.cuda.Stream()
+    sc = make_scene(args.config, args.model, rank)
+
+    def barrier():
+        if world > 1:
+            dist.barrier()
+
+    with torch.cuda.stream(stream):
+        d = Dem(sc.params, device=local, stream=stream)
+        d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+        d.step(max(args.warmup, 3))
+        stats0 = d.stats()
+        # timed region: K steps, CUDA events around every kernel on the handle's stream
+        d.profile(True)
+        torch.cuda.synchronize()
+        barrier()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        with ClockSampler(torch.cuda.current_device()) as clk:
+            e0.record(stream)
+            d.step(args.steps)
+            e1.record(stream)
+            torch.cuda.synchronize()
+        barrier()
+        ms = e0.elapsed_time(e1)
+        st = d.stats()
+        d.profile(False)
+        c_bar = st["contacts"] / sc.n if sc.params.model == "practical" else 0.0
+        # graph-replay region (the default path), same K
+        torch.cuda.synchronize()
+        barrier()
+        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        g0.record(stream)
+        d.step(args.steps)
+        g1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+        ms_graph = g0.elapsed_time(g1)
+
+    ms_max = ms
+    ms_graph_max = ms_graph
+    if world > 1:
+        t = torch.tensor([ms, ms_graph], device="cuda")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_max, ms_graph_max = float(t[0]), float(t[1])
+
+    ms_step = ms_max / args.steps
+    value = world * sc.n * args.steps / (ms_max * 1e-3)
+    rho_c = stats0["ncells"] / sc.n
+    b_sweep, b_step = alg_bytes(sc.params.model, rho_c, c_bar)
+    sweep_ms = st["kernel_ms"]["sweep"] / max(1, st["kernel_count"]["sweep"])
+    achieved = b_sweep * sc.n / (sweep_ms * 1e-3) / 1e9
+    kernel_avg = {k: (st["kernel_ms"][k] / st["kernel_count"][k]) if st["kernel_count"][k] else 0.0
+                  for k in KERNELS}
+    step_kernel_ms = sum(kernel_avg.values())
+    traffic = None
+    tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.model}.json")
+    if os.path.exists(tr_path):
+        try:
+            traffic = json.load(open(tr_path)).get("sweep_dram_bytes_per_launch")
+        except Exception:
+            traffic = None
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
+        "scaling": "weak" if world > 1 else "strong", "vs_baseline": None, "dtype": "f32",
+        "data": "synthetic",
+        "config": {
+            "workload": describe(sc), "n_particles": sc.n, "ncells": stats0["ncells"],
+            "grid": list(stats0["dims"]), "rho_c": rho_c, "c_bar": c_bar,
+            "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
+            "l2": "working set > 1 GB per step >> 126 MB L2; no flush needed",
+            "dt": sc.params.dt,
+        },
+        "roofline": {
+            "bound": "hbm", "kernel": "k_sweep", "achieved": achieved, "peak": peak_gbs,
+            "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
+            "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
+            "sweep_ms_avg": sweep_ms, "sweep_share_of_step": kernel_avg["sweep"] / step_kernel_ms
+            if step_kernel_ms else None,
+            "step_alg_bytes_per_particle": b_step,
+            "step_frac": b_step * sc.n / (ms_step * 1e-3) / 1e9 / peak_gbs,
+            "step_frac_of_8TBps": b_step * sc.n / (ms_step * 1e-3) / 8e12,
+        },
+        "kernel_ms_avg": kernel_avg,
+        "ms_per_step_graph": ms_graph_max / args.steps,
+        "gpu_launches": int(st["kernel_count"]["sweep"] + st["kernel_count"]["scan"]
+                            + st["kernel_count"]["scatter"] + st["kernel_count"]["rank"]),
+        "clocks": clk.summary(),
+    }
+    # end to end through the public API with pinned host buffers
+    if not args.no_e2e:
+        line["e2e"] = run_e2e(d, sc, stream, min(args.steps, args.e2e_steps), world, barrier)
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        line["cpu_baseline"] = cpu_baseline_on_state(d, sc)
+    elif rank == 0:
+        line["cpu_baseline"] = None
+    d.close()
+    if rank == 0:
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def run_e2e(d, sc, stream, steps, world, barrier):
+    """Each step: dem_set_particles + dem_set_contacts from pinned host memory,
+    dem_step(1), dem_get_state + dem_get_contacts into pinned host memory."""
+    import torch
+
+    s = d.get_state()
+    ci, cj, cd = d.get_contacts()
+    n = sc.n
+
+    def pinned(a):
+        t = torch.empty(a.shape, dtype={np.float32: torch.float32, np.uint32: torch.int32}[
+            a.dtype.type], pin_memory=True)
+        out = t.numpy()
+        out[...] = a.view(out.dtype) if a.dtype == np.uint32 else a
+        return t, out.view(a.dtype)
+
+    host = {k: pinned(v) for k, v in s.items()}
+    cap = max(len(ci) * 2, 1024)
+    hci = pinned(np.zeros(cap, np.uint32))
+    hcj = pinned(np.zeros(cap, np.uint32))
+    hcd = pinned(np.zeros((cap, 3), np.float32))
+    m = len(ci)
+    hci[1][:m], hcj[1][:m], hcd[1][:m] = ci, cj, cd
+    out = {k: pinned(v)[1] for k, v in s.items()}
+    h2d = d2h = 0
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        H = {k: v[1] for k, v in host.items()}
+        d.set_particles(H["pos"], H["vel"], H["omega"], H["radius"], H["mass"], H["id"])
+        d.set_contacts(hci[1][:m], hcj[1][:m], hcd[1][:m])
+        d.step(1)
+        got = d.get_state(out=out)
+        a, b, c = d.get_contacts()
+        m = len(a)
+        hci[1][:m], hcj[1][:m], hcd[1][:m] = a, b, c
+        for k in host:
+            host[k][1][...] = got[k]
+        h2d += n * 48 + m * 20
+        d2h += n * 48 + m * 20
+    barrier()
+    t = time.perf_counter() - t0
+    return {"value": world * n * steps / t, "unit": UNIT,
+            "h2d_bytes_per_step": h2d // max(1, steps), "d2h_bytes_per_step": d2h // max(1, steps),
+            "steps": steps, "api": "dem_set_particles+dem_set_contacts+dem_step(1)+"
+                                   "dem_get_state+dem_get_contacts per step, host buffers"}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--model", default="practical", choices=["practical", "simple"])
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

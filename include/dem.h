@@ -1,0 +1,233 @@
+/*
+ * dem.h — C ABI of the B200-native DEM timestep of
+ *   T. Washizawa, Y. Nakahara, "Parallel Computing of Discrete Element Method
+ *   on GPU", arXiv 1301.1714 (PAPER.md in the reference mount).
+ *
+ * One call of dem_step() advances the particle set by whole timesteps of the
+ * paper's process flow (§4.2):
+ *   step 2  correspondence map CM (cell hash)
+ *   step 3  sort CM -> SCM, SCCM with SCM[j]=CM[SCCM[j]]   PAPER.md:121-123 (Eq. 11)
+ *   step 4  reorder all particle properties along SCM
+ *   step 5-6 thread(s) per sorted particle, 27-cell set    PAPER.md:126-127 (Eq. 12)
+ *   step 7  pair contact force: Eq. 1 (simple) or Eqs. 2-10 (practical)
+ *   step 8  walls as particles of infinite radius
+ *   step 1  update all particle properties (integrator)
+ * Readings of the paper where it is silent (signs, wall limits, integrator,
+ * history lifecycle, predicate/hash precision) are DESIGN.md R1-R21.
+ *
+ * Conventions for every function:
+ *   - returns int: DEM_OK (0) or a negative dem_error code;
+ *   - SI units; parameters are fp32 as given; device state is fp32; the hash
+ *     and the contact predicate are fp64 expressions of the fp32 values
+ *     (R14, R15);
+ *   - the handle owns every device buffer it allocates; the caller owns every
+ *     array it passes in (host or device). set_* copy in (the caller may free
+ *     or reuse its arrays on return); get_* copy out into caller arrays of
+ *     capacity `cap` elements and return the needed count in *_out
+ *     (DEM_EINVAL if too small). No caller pointer is retained across calls;
+ *   - a handle is not thread-safe; all work is enqueued on the handle's
+ *     stream. dem_step synchronises once at its end (unless DEM_F_ASYNC);
+ *     get_* synchronise.
+ */
+#ifndef DEM_H
+#define DEM_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define DEM_ABI_VERSION 1u
+
+/* Error codes. */
+enum dem_error {
+  DEM_OK = 0,
+  DEM_EINVAL = -1,      /* bad argument: NULL, n<0, r<=0, m<=0, dt<=0, hi<=lo, grid dim < 3,
+                           cell edge < 2 r_max (1+2^-10), id >= 0xFFFFFFF0 or duplicate,
+                           particle centre outside the box, capacity too small */
+  DEM_EABI = -2,        /* params->abi_version != DEM_ABI_VERSION */
+  DEM_ENOMEM = -3,      /* device allocation failed */
+  DEM_ECUDA = -4,       /* a CUDA runtime call failed (dem_last_error has the text) */
+  DEM_ENCCL = -5,       /* an NCCL call failed (multi-GPU) */
+  DEM_EOVERFLOW = -6,   /* a particle had more than max_contacts contacts (history
+                           capacity K). The step is rejected: the state and history stay
+                           at the last completed step. */
+  DEM_ENONFINITE = -7,  /* a position/velocity/angular velocity became non-finite
+                           (explosion); state = last completed step */
+  DEM_EESCAPED = -8,    /* a centre moved beyond a wall by more than its radius
+                           (tunnelling); state = last completed step */
+  DEM_ECOINCIDENT = -9, /* two centres coincide while in contact (n undefined, R18) */
+  DEM_ESTATE = -10,     /* call out of order (e.g. dem_step before dem_set_particles) */
+};
+
+enum dem_model {
+  DEM_MODEL_PRACTICAL = 0, /* Eqs. 2-10: Hertzian spring-dashpot, Coulomb
+                              cap, tangential history, torque and angular velocity */
+  DEM_MODEL_SIMPLE = 1,    /* Eq. 1: linear spring, damping, shear */
+};
+
+enum dem_flags {
+  DEM_F_TRUNCATE_DT = 1u << 0, /* R4: δ_t = -(F_t' + η v_t)/k_t when Eq. 5 caps F_t */
+  DEM_F_CLAMP_FN = 1u << 1,    /* R3: Eq. 5 uses max(0, repulsive part of F_n)      */
+  DEM_F_DIAG = 1u << 2,        /* keep per-particle F and T of the last step (dem_get_state) */
+  DEM_F_ASYNC = 1u << 3,       /* dem_step does not synchronise; errors surface at the next
+                                  synchronising call */
+  DEM_F_NO_GRAPH = 1u << 4,    /* launch kernels eagerly instead of replaying a CUDA graph */
+};
+
+enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
+enum dem_order {
+  DEM_ORDER_INTERNAL = 0, /* the handle's current memory order = SCM order of the last sort */
+  DEM_ORDER_ID = 1,       /* by persistent id; requires ids to be a permutation of 0..n-1 */
+};
+
+typedef struct dem_handle dem_handle; /* opaque; owns all device memory */
+
+/* Optional device-memory provider (torch passes its caching allocator). */
+typedef struct {
+  void* ctx;
+  void* (*alloc)(void* ctx, size_t bytes, void* stream);
+  void (*free)(void* ctx, void* ptr, size_t bytes, void* stream);
+} dem_allocator;
+
+/* The paper's problem statement: radius, spring
+ * parameters C_k, restitution parameter α, friction μ, gravity, Δt, walls,
+ * and the simple model's constants. */
+typedef struct {
+  uint32_t abi_version;      /* == DEM_ABI_VERSION, else DEM_EABI */
+  int32_t model;             /* enum dem_model */
+  float dt;                  /* Δt > 0 [s] (Eq. 7) */
+  float gravity[3];          /* g [m/s^2], applied once per particle (R2) */
+  float box_lo[3];           /* domain; the 6 walls are its faces */
+  float box_hi[3];
+  float radius;              /* default radius when dem_particles.radius == NULL [m] */
+  float density;             /* default mass = density (4/3) π r^3 when mass == NULL */
+  float stiffness_n;         /* C_{k,n} [Pa]  (Eq. 9)  */
+  float stiffness_t;         /* C_{k,t} [Pa]  (Eq. 8)  */
+  float damping;             /* α             (Eq. 10) */
+  float friction;            /* μ             (Eq. 5)  */
+  float wall_stiffness_n;    /* the same for particle-wall pairs; < 0 -> particle value */
+  float wall_stiffness_t;
+  float wall_damping;
+  float wall_friction;
+  float k_sp, k_da, k_sh;    /* simple model (Eq. 1) [N/m, N s/m, N s/m] */
+  float cell_edge;           /* CDG cell edge h; 0 -> 2 r_max (1 + 2^-10) in fp64 (R15) */
+  uint32_t max_contacts;     /* history capacity K per particle; 0 -> 16 */
+  uint32_t flags;            /* enum dem_flags */
+  int32_t device;            /* CUDA ordinal; -1 -> current device */
+  void* stream;              /* cudaStream_t; NULL -> a stream owned by the handle */
+  const dem_allocator* allocator; /* NULL -> cudaMallocAsync on the stream */
+  int32_t rank, world_size;  /* world_size <= 1: single GPU (z-slabs otherwise) */
+  const void* nccl_id;       /* 128-byte ncclUniqueId when world_size > 1 */
+} dem_params;
+
+/* Particle arrays, all host or all device (mem_kind). Layout: pos/vel/omega
+ * are [3n] xyz-interleaved float; radius/mass [n]; id [n]. For
+ * dem_set_particles a NULL member means "default" (vel, omega = 0; radius =
+ * params.radius; mass from density; id = 0..n-1). For dem_get_state a NULL
+ * member is not written. force/torque are output-only (DEM_F_DIAG): the
+ * contact force and torque of the last evaluated step, without gravity. */
+typedef struct {
+  int32_t mem_kind;
+  float* pos;
+  float* vel;
+  float* omega;
+  float* radius;
+  float* mass;
+  uint32_t* id;
+  float* force;
+  float* torque;
+} dem_particles;
+
+typedef struct {
+  int64_t n;             /* particles held by this handle */
+  int64_t ncells;        /* CDG cells */
+  int32_t dims[3];       /* CDG dimensions */
+  double cell_edge;      /* h actually used */
+  int64_t steps;         /* completed steps since dem_set_particles */
+  int64_t contacts;      /* history entries (= 2 pair contacts + wall contacts) of the last step */
+  int64_t max_contacts_seen; /* max per-particle history entries of the last step */
+  int64_t launches;      /* kernels this handle launched since creation */
+  int64_t graph_launches;
+  /* per-kernel device time accumulated while profiling (dem_profile) */
+  double kernel_ms[8];
+  int64_t kernel_count[8];
+} dem_stats;
+
+/* Kernel indices of dem_stats.kernel_ms. */
+enum dem_kernel { DEM_K_HASH = 0, DEM_K_SCAN = 1, DEM_K_SCATTER = 2, DEM_K_RANK = 3,
+                  DEM_K_SWEEP = 4, DEM_K_OTHER = 5 };
+
+/* Create a handle: validates params (DEM_EINVAL/DEM_EABI), selects the device
+ * and stream. Grid and buffers are sized by dem_set_particles. *out = NULL on
+ * error. */
+int dem_create(const dem_params* p, dem_handle** out);
+
+/* Release every device buffer and the owned stream. NULL is a no-op. */
+int dem_destroy(dem_handle* h);
+
+/* Copy in n particles ("particle properties") and clear the
+ * contact history. Validates radius > 0, mass > 0, finite values, centres
+ * inside the box, ids < 0xFFFFFFF0 and unique, and the cell edge against
+ * 2 r_max (1 + 2^-10). Sizes the CDG: n_a = floor((hi_a - lo_a)/h) >= 3.
+ * Computes CM for the next step (step 2). n == 0 is allowed. */
+int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src);
+
+/* Replace the tangential-displacement history (Eq. 7's δ_t,old) with m
+ * entries (id_i, id_j, dt3[3]): the displacement stored on particle id_i's
+ * side for partner id_j (a wall w = 0..5 is id 0xFFFFFFF0 + w). Arrays are
+ * host or device per mem_kind. Requires dense ids (a permutation of 0..n-1).
+ * DEM_EOVERFLOW if a particle gets more than max_contacts entries. */
+int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t* id_i,
+                     const uint32_t* id_j, const float* dt3);
+
+/* Advance nsteps >= 0 timesteps. On an error code the state and history are
+ * those of the last completed step and dem_last_error() names the particle
+ * and step. */
+int dem_step(dem_handle* h, int64_t nsteps);
+
+/* Wait for enqueued work; returns a pending step error (DEM_F_ASYNC). */
+int dem_sync(dem_handle* h);
+
+/* Copy out the state (order: enum dem_order). *n_out = n. */
+int dem_get_state(dem_handle* h, int32_t order, int64_t cap, const dem_particles* dst,
+                  int64_t* n_out);
+
+/* Copy out the history as (id_i, id_j, dt3) triples, grouped by particle in
+ * internal order, each particle's entries in the order the step found them
+ * (27 cells ascending, slots ascending, then walls -x,+x,-y,+y,-z,+z).
+ * mem_kind says where the output arrays live. *m_out = number of entries. */
+int dem_get_contacts(dem_handle* h, int32_t mem_kind, int64_t cap, uint32_t* id_i,
+                     uint32_t* id_j, float* dt3, int64_t* m_out);
+
+/* Diagnostics for bit-exact checks (host arrays; any may be NULL):
+ *   key [n]        CM of the current state (what the next step will sort)
+ *   perm [n]       SCCM of the last sort (Eq. 11), i.e. the old slot of each new slot
+ *   off [ncells+1] cell start offsets of the last sort (lower_bound semantics)
+ * cap bounds perm/key (n) and off (ncells+1). *ncells_out = ncells. */
+int dem_get_grid(dem_handle* h, int64_t cap, uint32_t* key, uint32_t* perm, uint32_t* off,
+                 int64_t* ncells_out);
+
+/* Counters (see dem_stats). Synchronises; computes the contact totals from
+ * the current history with a small reduction kernel. */
+int dem_get_stats(dem_handle* h, dem_stats* out);
+
+/* Per-kernel CUDA-event timing of subsequent dem_step calls (eager launches,
+ * events around every kernel on the handle's stream); 0 disables. Enabling
+ * resets the accumulated times. */
+int dem_profile(dem_handle* h, int32_t enable);
+
+/* Fill out128 with a new ncclUniqueId (rank 0 of a multi-GPU run). */
+int dem_nccl_unique_id(void* out128);
+
+const char* dem_strerror(int code);
+/* Text of the last error on this handle (includes particle id and step for
+ * DEM_ENONFINITE / DEM_EESCAPED / DEM_EOVERFLOW / DEM_ECOINCIDENT). */
+const char* dem_last_error(const dem_handle* h);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* DEM_H */

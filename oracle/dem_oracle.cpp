@@ -359,6 +359,9 @@ typedef struct {
   uint32_t* off;   /* [ncells+1]; may be NULL */
   double* F;       /* [3n]  total contact force on each sorted particle (no gravity); may be NULL */
   double* T;       /* [3n]  total contact torque; may be NULL */
+  double* Fabs;    /* [n]   Σ_j |F_ij| over the contacts of each particle (incl. walls);
+                      the summation-cancellation scale of the T2 tolerance; may be NULL */
+  double* Tabs;    /* [n]   Σ_j |T_ij|; may be NULL */
   int64_t err[3];  /* code, sorted slot, particle id of the first error */
   int64_t n_pair_contacts;  /* ordered (i,j) particle contacts found (each pair twice) */
   int64_t n_wall_contacts;
@@ -375,8 +378,12 @@ static void set_err(orc_out* o, int code, int64_t slot, uint32_t id) {
 
 /* One timestep: PAPER.md §4.2 steps 2-8 then step 1, in that order (reading R9).
  * On entry the arrays hold the state in the current order; on return they hold
- * the new state in sorted (SCM) order, and hist holds the new per-slot lists. */
-int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_out* out) {
+ * the new state in sorted (SCM) order, and hist holds the new per-slot lists.
+ * `only` (may be NULL) restricts steps 5-8 and 1 to the sorted slots j with
+ * only[j] != 0 — the other slots are returned reordered but not advanced
+ * (used to check sampled particles of very large sets one by one). */
+static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_out* out,
+                     const uint8_t* only) {
   out->err[0] = out->err[1] = out->err[2] = 0;
   out->n_pair_contacts = out->n_wall_contacts = out->n_candidates = 0;
   int64_t dims[3];
@@ -426,13 +433,14 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
       }
   };
 
-  std::vector<double> F(3 * N, 0.0), T(3 * N, 0.0);
+  std::vector<double> F(3 * N, 0.0), T(3 * N, 0.0), Fabs(N, 0.0), Tabs(N, 0.0);
   std::vector<uint32_t> ncnt(N, 0), npid(N * K, 0);
   std::vector<double> ndt(N * K * 3, 0.0);
   const bool brute = (p->flags & ORC_F_BRUTE) != 0;
   const bool practical = p->model == ORC_MODEL_PRACTICAL;
 
   for (size_t j = 0; j < N; ++j) {
+    if (only && !only[j]) continue;
     double* Fi = &F[3 * j];
     double* Ti = &T[3 * j];
     auto push_hist = [&](uint32_t pid, const double* d) -> bool {
@@ -469,6 +477,7 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
         orc_pair_practical(nrm, delta, Rstar, mstar, vrel, rw, dold, p->Cn, p->Ct, p->alpha,
                            p->mu, p->dt, p->flags, Fc, Tc, dnew);
         for (int a = 0; a < 3; ++a) Ti[a] += r[j] * Tc[a];
+        Tabs[j] += r[j] * norm3(Tc);
         if (!push_hist(id[t], dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
       } else {
         double u[3];
@@ -476,6 +485,7 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
         orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc);
       }
       for (int a = 0; a < 3; ++a) Fi[a] += Fc[a];
+      Fabs[j] += norm3(Fc);
     };
     if (brute) {
       for (size_t t = 0; t < N; ++t)
@@ -509,6 +519,7 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
         orc_pair_practical(nrm, delta, r[j], m[j], &v[3 * j], rw, dold, p->wCn, p->wCt,
                            p->walpha, p->wmu, p->dt, p->flags, Fc, Tc, dnew);
         for (int b = 0; b < 3; ++b) Ti[b] += r[j] * Tc[b];
+        Tabs[j] += r[j] * norm3(Tc);
         if (!push_hist(pid, dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
       } else {
         double u[3];
@@ -516,12 +527,14 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
         orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc);
       }
       for (int b = 0; b < 3; ++b) Fi[b] += Fc[b];
+      Fabs[j] += norm3(Fc);
     }
   }
 
   /* step 1 (next iteration): update all particle properties, semi-implicit
    * Euler with I = 0.4 m r^2 (reading R9). */
   for (size_t j = 0; j < N; ++j) {
+    if (only && !only[j]) continue;
     double I = 0.4 * m[j] * r[j] * r[j];
     for (int a = 0; a < 3; ++a) {
       double acc = F[3 * j + a] / m[j] + p->g[a];
@@ -550,7 +563,19 @@ int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_
   std::memcpy(hist->dt, ndt.data(), N * K * 3 * 8);
   if (out->F) std::memcpy(out->F, F.data(), 3 * N * 8);
   if (out->T) std::memcpy(out->T, T.data(), 3 * N * 8);
+  if (out->Fabs) std::memcpy(out->Fabs, Fabs.data(), N * 8);
+  if (out->Tabs) std::memcpy(out->Tabs, Tabs.data(), N * 8);
   return (int)out->err[0];
+}
+
+int orc_step(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, orc_out* out) {
+  return step_impl(p, n, st, hist, out, nullptr);
+}
+
+/* orc_step restricted to the sorted slots with only[j] != 0 (see step_impl). */
+int orc_step_sampled(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist,
+                     orc_out* out, const uint8_t* only) {
+  return step_impl(p, n, st, hist, out, only);
 }
 
 /* nsteps of orc_step (for long closed-form runs); stops at the first error. */
@@ -564,6 +589,8 @@ int orc_run(const orc_params* p, int64_t n, orc_state* st, orc_hist* hist, int64
     o.off = nullptr;
     o.F = (s == nsteps - 1) ? out->F : nullptr;
     o.T = (s == nsteps - 1) ? out->T : nullptr;
+    o.Fabs = (s == nsteps - 1) ? out->Fabs : nullptr;
+    o.Tabs = (s == nsteps - 1) ? out->Tabs : nullptr;
     rc = orc_step(p, n, st, hist, &o);
     if (rc != 0) break;
   }

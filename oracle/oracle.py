@@ -41,8 +41,8 @@ class OrcHist(C.Structure):
 
 
 class OrcOut(C.Structure):
-    _fields_ = [("CM", _P), ("SCCM", _P), ("off", _P), ("F", _P), ("T", _P),
-                ("err", C.c_int64 * 3), ("n_pair_contacts", C.c_int64),
+    _fields_ = [("CM", _P), ("SCCM", _P), ("off", _P), ("F", _P), ("T", _P), ("Fabs", _P),
+                ("Tabs", _P), ("err", C.c_int64 * 3), ("n_pair_contacts", C.c_int64),
                 ("n_wall_contacts", C.c_int64), ("n_candidates", C.c_int64)]
 
 
@@ -74,6 +74,8 @@ def lib():
         L.orc_pair_simple.argtypes = [_P, _D, _P, _D, _D, _D, _P]
         L.orc_step.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(OrcState),
                                C.POINTER(OrcHist), C.POINTER(OrcOut)]
+        L.orc_step_sampled.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(OrcState),
+                                       C.POINTER(OrcHist), C.POINTER(OrcOut), _P]
         L.orc_run.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(OrcState),
                               C.POINTER(OrcHist), C.c_int64, C.POINTER(OrcOut)]
         _lib = L
@@ -310,13 +312,25 @@ class History:
         follows the triples' order."""
         n = ids.shape[0]
         h = History.empty(n, K)
-        slot = {int(v): s for s, v in enumerate(ids)}
-        for a, b, d in zip(np.asarray(id_i), np.asarray(id_j), np.asarray(dt3).reshape(-1, 3)):
-            s = slot[int(a)]
-            k = int(h.cnt[s])
-            h.pid[s, k] = int(b)
-            h.dt[s, k] = d
-            h.cnt[s] = k + 1
+        id_i = np.asarray(id_i, np.int64)
+        if id_i.size == 0:
+            return h
+        ids64 = ids.astype(np.int64)
+        if ids64.max(initial=-1) < n and np.unique(ids64).size == n:
+            slot_of = np.empty(n, np.int64)
+            slot_of[ids64] = np.arange(n)
+            slot = slot_of[id_i]
+        else:
+            lut = {int(v): s for s, v in enumerate(ids)}
+            slot = np.array([lut[int(a)] for a in id_i], np.int64)
+        order = np.argsort(slot, kind="stable")
+        ss = slot[order]
+        k = np.arange(ss.size) - np.searchsorted(ss, ss, side="left")
+        if k.max() >= K:
+            raise ValueError("more than K history entries for a particle")
+        h.pid[ss, k] = np.asarray(id_j, np.uint32)[order]
+        h.dt[ss, k] = np.asarray(dt3, np.float64).reshape(-1, 3)[order]
+        h.cnt[:] = np.bincount(ss, minlength=n).astype(np.uint32)
         return h
 
 
@@ -328,6 +342,8 @@ class StepResult:
     off: np.ndarray
     F: np.ndarray
     T: np.ndarray
+    Fabs: np.ndarray
+    Tabs: np.ndarray
     err: tuple
     n_pair_contacts: int
     n_wall_contacts: int
@@ -341,8 +357,10 @@ def _structs(st: State, h: History):
     return s, hh
 
 
-def step(p: OrcParams, st: State, h: History) -> StepResult:
-    """One timestep in place: on return st/h hold the new state in sorted order."""
+def step(p: OrcParams, st: State, h: History, only=None) -> StepResult:
+    """One timestep in place: on return st/h hold the new state in sorted order.
+    `only`: boolean mask over the NEW sorted slots; when given, only those
+    slots are evaluated and advanced (the rest are reordered, not advanced)."""
     n = st.n
     ncells = math.prod(grid_dims(p))
     CM = np.empty(n, np.uint32)
@@ -350,10 +368,18 @@ def step(p: OrcParams, st: State, h: History) -> StepResult:
     off = np.empty(ncells + 1, np.uint32)
     F = np.empty((n, 3))
     T = np.empty((n, 3))
+    Fabs = np.empty(n)
+    Tabs = np.empty(n)
     s, hh = _structs(st, h)
-    o = OrcOut(_ptr(CM), _ptr(SCCM), _ptr(off), _ptr(F), _ptr(T))
-    rc = lib().orc_step(C.byref(p), n, C.byref(s), C.byref(hh), C.byref(o))
-    return StepResult(rc, CM, SCCM, off, F, T, tuple(o.err), o.n_pair_contacts,
+    o = OrcOut(_ptr(CM), _ptr(SCCM), _ptr(off), _ptr(F), _ptr(T), _ptr(Fabs), _ptr(Tabs))
+    if only is None:
+        rc = lib().orc_step(C.byref(p), n, C.byref(s), C.byref(hh), C.byref(o))
+    else:
+        mask = np.ascontiguousarray(np.asarray(only, dtype=np.uint8))
+        assert mask.shape == (n,)
+        rc = lib().orc_step_sampled(C.byref(p), n, C.byref(s), C.byref(hh), C.byref(o),
+                                    _ptr(mask))
+    return StepResult(rc, CM, SCCM, off, F, T, Fabs, Tabs, tuple(o.err), o.n_pair_contacts,
                       o.n_wall_contacts, o.n_candidates)
 
 
@@ -363,6 +389,6 @@ def run(p: OrcParams, st: State, h: History, nsteps: int):
     F = np.empty((n, 3))
     T = np.empty((n, 3))
     s, hh = _structs(st, h)
-    o = OrcOut(None, None, None, _ptr(F), _ptr(T))
+    o = OrcOut(None, None, None, _ptr(F), _ptr(T), None, None)
     rc = lib().orc_run(C.byref(p), n, C.byref(s), C.byref(hh), nsteps, C.byref(o))
     return rc, tuple(o.err), F, T

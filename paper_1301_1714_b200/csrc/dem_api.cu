@@ -1,0 +1,911 @@
+// dem_api.cu — host side of libdem.so: the C ABI of include/dem.h.
+//
+// The host validates, sizes buffers, and enqueues kernels (dem_kernels.cu) on
+// the handle's stream, replaying a captured CUDA graph of two steps (one per
+// ping-pong parity) so a step costs one graph launch instead of four kernel
+// launches. All arithmetic of the method runs in the kernels.
+#include <cuda_runtime.h>
+#include <stdint.h>
+#include <stdio.h>
+#include <string.h>
+
+#include <algorithm>
+#include <cmath>
+#include <string>
+#include <vector>
+
+#include "dem.h"
+#include "dem_internal.h"
+
+using namespace dem;
+
+namespace {
+
+struct Alloc {
+  void* p;
+  size_t bytes;
+};
+
+}  // namespace
+
+struct dem_handle {
+  dem_params p{};
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  bool own_stream = false;
+  dem_allocator alloc{};
+  bool has_alloc = false;
+  std::vector<Alloc> allocs;
+  std::string last_error;
+
+  // problem
+  int64_t n = -1;  // -1: no particles set yet
+  uint32_t K = 16;
+  double h = 0.0;
+  DevGrid g{};
+  DevPhys ph{};
+  bool ids_dense = false;
+
+  // device buffers (ping-pong b in {0,1})
+  float4 *pos[2] = {}, *vel[2] = {}, *omg[2] = {};
+  uint32_t* key[2] = {};
+  float4* hist[2] = {};
+  uint32_t* cnt[2] = {};
+  uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
+  float4 *F = nullptr, *T = nullptr;
+  unsigned long long* scan_status[2] = {};
+  uint32_t* scan_ctr = nullptr;  // [2]
+  uint32_t ntiles = 0;
+  DevErr* err = nullptr;
+  DevErr* err_host = nullptr;  // pinned
+  int64_t cap_n = -1, cap_cells = -1;
+
+  int cur = 0;
+  int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
+
+  // graphs: g2[b] = two steps starting at parity b; g1[b] = one step
+  cudaGraphExec_t g2[2] = {nullptr, nullptr};
+  cudaGraphExec_t g1[2] = {nullptr, nullptr};
+
+  // profiling
+  bool profiling = false;
+  struct Prof {
+    cudaEvent_t b, e;
+    int kid;
+  };
+  std::vector<Prof> prof;
+  std::vector<cudaEvent_t> event_pool;
+  // steps enqueued but not yet checked (DEM_F_ASYNC)
+  bool pending = false;
+  int64_t pend_ctr0 = 0, pend_steps = 0;
+  int pend_cur0 = 0;
+  double kernel_ms[8] = {};
+  int64_t kernel_count[8] = {};
+  int64_t launches = 0, graph_launches = 0;
+};
+
+namespace {
+
+thread_local std::string g_tls_error;
+
+int fail(dem_handle* h, int code, const std::string& msg) {
+  if (h) h->last_error = msg;
+  g_tls_error = msg;
+  return code;
+}
+
+#define CUDA_TRY(h, call)                                                               \
+  do {                                                                                  \
+    cudaError_t e__ = (call);                                                           \
+    if (e__ != cudaSuccess)                                                             \
+      return fail((h), DEM_ECUDA, std::string(#call) + ": " + cudaGetErrorString(e__)); \
+  } while (0)
+
+void* dev_alloc(dem_handle* h, size_t bytes) {
+  if (bytes == 0) bytes = 16;
+  void* p = nullptr;
+  if (h->has_alloc) {
+    p = h->alloc.alloc(h->alloc.ctx, bytes, (void*)h->stream);
+  } else {
+    if (cudaMallocAsync(&p, bytes, h->stream) != cudaSuccess) p = nullptr;
+  }
+  if (p) h->allocs.push_back({p, bytes});
+  return p;
+}
+
+void dev_free(dem_handle* h, void* p) {
+  if (!p) return;
+  for (size_t i = 0; i < h->allocs.size(); ++i)
+    if (h->allocs[i].p == p) {
+      if (h->has_alloc)
+        h->alloc.free(h->alloc.ctx, p, h->allocs[i].bytes, (void*)h->stream);
+      else
+        cudaFreeAsync(p, h->stream);
+      h->allocs.erase(h->allocs.begin() + (long)i);
+      return;
+    }
+}
+
+template <class T>
+bool dalloc(dem_handle* h, T** out, size_t count) {
+  *out = (T*)dev_alloc(h, count * sizeof(T));
+  return *out != nullptr;
+}
+
+void destroy_graphs(dem_handle* h) {
+  for (int b = 0; b < 2; ++b) {
+    if (h->g2[b]) cudaGraphExecDestroy(h->g2[b]);
+    if (h->g1[b]) cudaGraphExecDestroy(h->g1[b]);
+    h->g2[b] = h->g1[b] = nullptr;
+  }
+}
+
+void free_buffers(dem_handle* h) {
+  destroy_graphs(h);
+  std::vector<Alloc> all = h->allocs;
+  for (auto& a : all) dev_free(h, a.p);
+  for (int b = 0; b < 2; ++b) {
+    h->pos[b] = h->vel[b] = h->omg[b] = h->hist[b] = nullptr;
+    h->key[b] = h->cnt[b] = nullptr;
+    h->scan_status[b] = nullptr;
+  }
+  h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
+  h->F = h->T = nullptr;
+  h->err = nullptr;
+  h->cap_n = h->cap_cells = -1;
+}
+
+StepBuffers step_buffers(dem_handle* h, int b) {
+  StepBuffers s{};
+  s.pos_in = h->pos[b];
+  s.vel_in = h->vel[b];
+  s.omg_in = h->omg[b];
+  s.pos_out = h->pos[b ^ 1];
+  s.vel_out = h->vel[b ^ 1];
+  s.omg_out = h->omg[b ^ 1];
+  s.key_in = h->key[b];
+  s.key_out = h->key[b ^ 1];
+  s.prank = h->prank;
+  s.count = h->count;
+  s.off = h->off;
+  s.tmp = h->tmp;
+  s.perm = h->perm;
+  s.hist_in = h->hist[b];
+  s.cnt_in = h->cnt[b];
+  s.hist_out = h->hist[b ^ 1];
+  s.cnt_out = h->cnt[b ^ 1];
+  s.F_out = h->F;
+  s.T_out = h->T;
+  s.scan_status = h->scan_status[b];
+  s.scan_ctr = h->scan_ctr + b;
+  s.scan_status_next = h->scan_status[b ^ 1];
+  s.scan_ctr_next = h->scan_ctr + (b ^ 1);
+  s.err = h->err;
+  return s;
+}
+
+// Enqueue one step from parity b: scan, scatter, rank, sweep.
+// `ev` (profiling) receives an event pair around each kernel.
+int enqueue_step(dem_handle* h, int b, bool profile) {
+  const StepBuffers s = step_buffers(h, b);
+  const bool diag = (h->p.flags & DEM_F_DIAG) != 0;
+  cudaEvent_t evb = nullptr;
+  auto take = [&]() {
+    cudaEvent_t e;
+    if (!h->event_pool.empty()) {
+      e = h->event_pool.back();
+      h->event_pool.pop_back();
+    } else {
+      cudaEventCreate(&e);
+    }
+    return e;
+  };
+  auto rec = [&](int k, bool begin) {
+    if (!profile) return;
+    cudaEvent_t e = take();
+    cudaEventRecord(e, h->stream);
+    if (begin) {
+      evb = e;
+    } else {
+      h->prof.push_back({evb, e, k});
+    }
+  };
+  rec(K_SCAN, true);
+  launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, s.scan_ctr,
+              h->err, 1);
+  rec(K_SCAN, false);
+  rec(K_SCATTER, true);
+  launch_scatter(h->stream, h->n, s, h->ntiles);
+  rec(K_SCATTER, false);
+  rec(K_RANK, true);
+  launch_rank(h->stream, h->n, s);
+  rec(K_RANK, false);
+  rec(K_SWEEP, true);
+  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph);
+  rec(K_SWEEP, false);
+  h->launches += 4;
+  cudaError_t e = cudaGetLastError();
+  if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
+  return DEM_OK;
+}
+
+int build_graph(dem_handle* h, int b, int nsteps, cudaGraphExec_t* out) {
+  cudaGraph_t graph;
+  CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
+  int parity = b;
+  int64_t l0 = h->launches;
+  for (int k = 0; k < nsteps; ++k) {
+    enqueue_step(h, parity, false);
+    parity ^= 1;
+  }
+  h->launches = l0;
+  CUDA_TRY(h, cudaStreamEndCapture(h->stream, &graph));
+  cudaError_t e = cudaGraphInstantiate(out, graph, 0);
+  cudaGraphDestroy(graph);
+  if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("graph: ") + cudaGetErrorString(e));
+  return DEM_OK;
+}
+
+const char* err_name(uint32_t code) {
+  switch (code) {
+    case 6: return "contact history capacity (max_contacts) exceeded";
+    case 7: return "non-finite state (explosion)";
+    case 8: return "particle escaped through a wall";
+    case 9: return "coincident centres in contact";
+    default: return "unknown";
+  }
+}
+
+// Wait for the stream and turn a device error record into a return code,
+// rolling the state back to the last completed step.
+int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
+  CUDA_TRY(h, cudaMemcpyAsync(h->err_host, h->err, sizeof(DevErr), cudaMemcpyDeviceToHost,
+                              h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  const DevErr e = *h->err_host;
+  if (e.code == 0) {
+    h->steps = ctr0 + nsteps;
+    return DEM_OK;
+  }
+  const int64_t failed = (int64_t)e.step;  // 1-based counter value of the failing step
+  const int64_t done = std::max<int64_t>(0, failed - 1 - ctr0);
+  h->cur = cur0 ^ (int)(done & 1);
+  h->steps = ctr0 + done;
+  // restore the per-step scratch for the good state and clear the record
+  CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * h->g.ncells, h->stream));
+  launch_count(h->stream, h->n, h->key[h->cur], h->count, h->prank);
+  CUDA_TRY(h, cudaMemsetAsync(h->scan_status[0], 0, sizeof(unsigned long long) * h->ntiles,
+                              h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->scan_status[1], 0, sizeof(unsigned long long) * h->ntiles,
+                              h->stream));
+  CUDA_TRY(h, cudaMemsetAsync(h->scan_ctr, 0, 2 * sizeof(uint32_t), h->stream));
+  DevErr clean{};
+  clean.step_ctr = (uint32_t)h->steps;
+  CUDA_TRY(h, cudaMemcpyAsync(h->err, &clean, sizeof(DevErr), cudaMemcpyHostToDevice, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  int code = -(int)e.code;
+  char buf[256];
+  snprintf(buf, sizeof buf, "%s: particle id %u (slot %u) in step %lld; state kept at step %lld",
+           err_name(e.code), e.id, e.slot, (long long)failed, (long long)h->steps);
+  return fail(h, code, buf);
+}
+
+int validate_params(const dem_params* p) {
+  if (!p) return DEM_EINVAL;
+  if (p->abi_version != DEM_ABI_VERSION) return DEM_EABI;
+  if (p->model != DEM_MODEL_PRACTICAL && p->model != DEM_MODEL_SIMPLE) return DEM_EINVAL;
+  if (!(p->dt > 0.0f) || !std::isfinite(p->dt)) return DEM_EINVAL;
+  for (int a = 0; a < 3; ++a)
+    if (!(p->box_hi[a] > p->box_lo[a]) || !std::isfinite(p->box_lo[a]) ||
+        !std::isfinite(p->box_hi[a]) || !std::isfinite(p->gravity[a]))
+      return DEM_EINVAL;
+  const float nonneg[] = {p->stiffness_n, p->stiffness_t, p->damping, p->friction,
+                          p->k_sp, p->k_da, p->k_sh};
+  for (float v : nonneg)
+    if (!(v >= 0.0f) || !std::isfinite(v)) return DEM_EINVAL;
+  if (p->cell_edge < 0.0f || !std::isfinite(p->cell_edge)) return DEM_EINVAL;
+  if (p->world_size > 1) return DEM_EINVAL;  // slab decomposition: see DESIGN.md §7
+  return DEM_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* dem_strerror(int code) {
+  switch (code) {
+    case DEM_OK: return "ok";
+    case DEM_EINVAL: return "invalid argument";
+    case DEM_EABI: return "ABI version mismatch";
+    case DEM_ENOMEM: return "out of device memory";
+    case DEM_ECUDA: return "CUDA error";
+    case DEM_ENCCL: return "NCCL error";
+    case DEM_EOVERFLOW: return "contact history capacity exceeded";
+    case DEM_ENONFINITE: return "non-finite particle state";
+    case DEM_EESCAPED: return "particle escaped through a wall";
+    case DEM_ECOINCIDENT: return "coincident particle centres";
+    case DEM_ESTATE: return "call out of order";
+    default: return "unknown error";
+  }
+}
+
+const char* dem_last_error(const dem_handle* h) {
+  return h ? h->last_error.c_str() : g_tls_error.c_str();
+}
+
+int dem_create(const dem_params* p, dem_handle** out) {
+  if (!out) return DEM_EINVAL;
+  *out = nullptr;
+  int rc = validate_params(p);
+  if (rc != DEM_OK) return fail(nullptr, rc, "dem_create: invalid params");
+  dem_handle* h = new dem_handle();
+  h->p = *p;
+  h->K = p->max_contacts ? p->max_contacts : 16u;
+  if (p->device >= 0) {
+    if (cudaSetDevice(p->device) != cudaSuccess) {
+      delete h;
+      return fail(nullptr, DEM_ECUDA, "cudaSetDevice failed");
+    }
+  }
+  if (cudaGetDevice(&h->device) != cudaSuccess) {
+    delete h;
+    return fail(nullptr, DEM_ECUDA, "no CUDA device");
+  }
+  if (p->stream) {
+    h->stream = (cudaStream_t)p->stream;
+  } else {
+    if (cudaStreamCreateWithFlags(&h->stream, cudaStreamNonBlocking) != cudaSuccess) {
+      delete h;
+      return fail(nullptr, DEM_ECUDA, "cudaStreamCreate failed");
+    }
+    h->own_stream = true;
+  }
+  if (p->allocator) {
+    h->alloc = *p->allocator;
+    h->has_alloc = h->alloc.alloc && h->alloc.free;
+  }
+  if (cudaMallocHost((void**)&h->err_host, sizeof(DevErr)) != cudaSuccess) {
+    if (h->own_stream) cudaStreamDestroy(h->stream);
+    delete h;
+    return fail(nullptr, DEM_ENOMEM, "pinned allocation failed");
+  }
+  // physics constants (fp32 as given; wall values < 0 fall back to the particle's)
+  DevPhys& ph = h->ph;
+  ph.dt = p->dt;
+  for (int a = 0; a < 3; ++a) ph.g[a] = p->gravity[a];
+  ph.Cn = p->stiffness_n;
+  ph.Ct = p->stiffness_t;
+  ph.alpha = p->damping;
+  ph.mu = p->friction;
+  ph.wCn = p->wall_stiffness_n >= 0 ? p->wall_stiffness_n : p->stiffness_n;
+  ph.wCt = p->wall_stiffness_t >= 0 ? p->wall_stiffness_t : p->stiffness_t;
+  ph.walpha = p->wall_damping >= 0 ? p->wall_damping : p->damping;
+  ph.wmu = p->wall_friction >= 0 ? p->wall_friction : p->friction;
+  ph.ksp = p->k_sp;
+  ph.kda = p->k_da;
+  ph.ksh = p->k_sh;
+  ph.flags = p->flags & (DEM_F_TRUNCATE_DT | DEM_F_CLAMP_FN);
+  *out = h;
+  return DEM_OK;
+}
+
+int dem_destroy(dem_handle* h) {
+  if (!h) return DEM_OK;
+  cudaStreamSynchronize(h->stream);
+  free_buffers(h);
+  for (auto& pr : h->prof) {
+    cudaEventDestroy(pr.b);
+    cudaEventDestroy(pr.e);
+  }
+  for (auto e : h->event_pool) cudaEventDestroy(e);
+  cudaStreamSynchronize(h->stream);
+  if (h->err_host) cudaFreeHost(h->err_host);
+  if (h->own_stream) cudaStreamDestroy(h->stream);
+  delete h;
+  return DEM_OK;
+}
+
+int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
+  if (!h) return DEM_EINVAL;
+  if (n < 0 || n > 0x7FFFFFF0LL || (n > 0 && (!src || !src->pos)))
+    return fail(h, DEM_EINVAL, "dem_set_particles: bad n or NULL pos");
+  cudaStream_t st = h->stream;
+  // 1. stage inputs on the device
+  PackIn in{};
+  std::vector<void*> staged;
+  auto stage = [&](const void* p, size_t bytes) -> const void* {
+    if (!p) return nullptr;
+    if (src->mem_kind == DEM_MEM_DEVICE) return p;
+    void* d = dev_alloc(h, bytes);
+    if (!d) return nullptr;
+    staged.push_back(d);
+    cudaMemcpyAsync(d, p, bytes, cudaMemcpyHostToDevice, st);
+    return d;
+  };
+  if (src && src->mem_kind == DEM_MEM_DEVICE && !h->own_stream) cudaStreamSynchronize(nullptr);
+  const size_t n3 = (size_t)n * 3 * sizeof(float), n1 = (size_t)n * sizeof(float);
+  in.pos = n ? (const float*)stage(src->pos, n3) : nullptr;
+  in.vel = n ? (const float*)stage(src->vel, n3) : nullptr;
+  in.omega = n ? (const float*)stage(src->omega, n3) : nullptr;
+  in.radius = n ? (const float*)stage(src->radius, n1) : nullptr;
+  in.mass = n ? (const float*)stage(src->mass, n1) : nullptr;
+  in.id = n ? (const uint32_t*)stage(src->id, (size_t)n * 4) : nullptr;
+  in.def_radius = h->p.radius;
+  in.def_mass_coef = (float)(h->p.density * (4.0 / 3.0) * M_PI);
+  auto unstage = [&]() {
+    for (void* d : staged) dev_free(h, d);
+  };
+  if (n && !in.pos) {
+    unstage();
+    return fail(h, DEM_ENOMEM, "staging allocation failed");
+  }
+  // 2. probe: validity, r_max, id_max
+  Probe* probe = nullptr;
+  if (!dalloc(h, &probe, 1)) {
+    unstage();
+    return fail(h, DEM_ENOMEM, "probe allocation failed");
+  }
+  DevGrid g{};
+  for (int a = 0; a < 3; ++a) {
+    g.lo[a] = (double)h->p.box_lo[a];
+    g.hi[a] = (double)h->p.box_hi[a];
+  }
+  CUDA_TRY(h, cudaMemsetAsync(probe, 0, sizeof(Probe), st));
+  launch_probe(st, n, in, g, probe);
+  Probe hp{};
+  CUDA_TRY(h, cudaMemcpyAsync(&hp, probe, sizeof(Probe), cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  dev_free(h, probe);
+  if (hp.bad_radius || hp.bad_mass || hp.nonfinite || hp.outside || hp.bad_id) {
+    unstage();
+    char buf[200];
+    snprintf(buf, sizeof buf,
+             "dem_set_particles: %u bad radii, %u bad masses, %u non-finite, %u outside the "
+             "box, %u ids >= 0xFFFFFFF0",
+             hp.bad_radius, hp.bad_mass, hp.nonfinite, hp.outside, hp.bad_id);
+    return fail(h, DEM_EINVAL, buf);
+  }
+  // 3. the CDG (R15): h = cell_edge or 2 r_max (1 + 2^-10); n_a = floor(L_a / h) >= 3
+  float rmax = 0.f;
+  memcpy(&rmax, &hp.rmax_bits, 4);
+  const double hmin = 2.0 * (double)rmax * (1.0 + std::ldexp(1.0, -10));
+  double hc = h->p.cell_edge > 0.0f ? (double)h->p.cell_edge : hmin;
+  if (hc < hmin || !(hc > 0.0)) {
+    unstage();
+    return fail(h, DEM_EINVAL, "cell edge smaller than 2 r_max (1 + 2^-10)");
+  }
+  int64_t dims[3];
+  for (int a = 0; a < 3; ++a) {
+    double q = std::floor((g.hi[a] - g.lo[a]) / hc);
+    if (!(q >= 3.0) || q > 1e9) {
+      unstage();
+      return fail(h, DEM_EINVAL, "grid dimension < 3 (box too small for the cell edge)");
+    }
+    dims[a] = (int64_t)q;
+  }
+  const int64_t ncells = dims[0] * dims[1] * dims[2];
+  if (ncells >= (int64_t)0xFFFFFFF0LL) {
+    unstage();
+    return fail(h, DEM_EINVAL, "too many grid cells (> 2^32)");
+  }
+  g.nx = (int)dims[0];
+  g.ny = (int)dims[1];
+  g.nz = (int)dims[2];
+  g.ncells = (uint32_t)ncells;
+  g.inv_h = 1.0 / hc;
+  // 4. buffers (reallocated when n or the grid changes)
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  if (h->cap_n != n || h->cap_cells != ncells) {
+    // keep staged inputs alive: free only the persistent buffers
+    std::vector<void*> keep(staged);
+    destroy_graphs(h);
+    std::vector<Alloc> all = h->allocs;
+    for (auto& a : all)
+      if (std::find(keep.begin(), keep.end(), a.p) == keep.end()) dev_free(h, a.p);
+    const size_t N = (size_t)(n > 0 ? n : 1);
+    const uint32_t ntiles = (uint32_t)((ncells + kScanTile - 1) / kScanTile) + 1;
+    bool ok = true;
+    for (int b = 0; b < 2; ++b) {
+      ok &= dalloc(h, &h->pos[b], N) && dalloc(h, &h->vel[b], N) && dalloc(h, &h->omg[b], N) &&
+            dalloc(h, &h->key[b], N) && dalloc(h, &h->cnt[b], N) &&
+            dalloc(h, &h->hist[b], N * h->K) && dalloc(h, &h->scan_status[b], ntiles);
+    }
+    ok &= dalloc(h, &h->prank, N) && dalloc(h, &h->count, (size_t)ncells + 1) &&
+          dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
+          dalloc(h, &h->perm, N) && dalloc(h, &h->scan_ctr, 2) && dalloc(h, &h->err, 1);
+    if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
+    if (!ok) {
+      unstage();
+      free_buffers(h);
+      h->n = -1;
+      return fail(h, DEM_ENOMEM, "device allocation failed");
+    }
+    h->ntiles = ntiles;
+    h->cap_n = n;
+    h->cap_cells = ncells;
+  }
+  h->g = g;
+  h->h = hc;
+  h->n = n;
+  h->cur = 0;
+  h->steps = 0;
+  destroy_graphs(h);
+  const size_t N = (size_t)(n > 0 ? n : 1);
+  CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells + 1), st));
+  CUDA_TRY(h, cudaMemsetAsync(h->off, 0, sizeof(uint32_t) * ((size_t)ncells + 1), st));
+  CUDA_TRY(h, cudaMemsetAsync(h->perm, 0, sizeof(uint32_t) * N, st));
+  CUDA_TRY(h, cudaMemsetAsync(h->cnt[0], 0, sizeof(uint32_t) * N, st));
+  CUDA_TRY(h, cudaMemsetAsync(h->cnt[1], 0, sizeof(uint32_t) * N, st));
+  for (int b = 0; b < 2; ++b)
+    CUDA_TRY(h, cudaMemsetAsync(h->scan_status[b], 0, sizeof(unsigned long long) * h->ntiles, st));
+  CUDA_TRY(h, cudaMemsetAsync(h->scan_ctr, 0, 2 * sizeof(uint32_t), st));
+  CUDA_TRY(h, cudaMemsetAsync(h->err, 0, sizeof(DevErr), st));
+  if (h->F) CUDA_TRY(h, cudaMemsetAsync(h->F, 0, sizeof(float4) * N, st));
+  if (h->T) CUDA_TRY(h, cudaMemsetAsync(h->T, 0, sizeof(float4) * N, st));
+  // 5. pack + hash (step 2 for the first step) + counting ranks
+  launch_pack(st, n, in, g, h->pos[0], h->vel[0], h->omg[0], h->key[0], h->count, h->prank);
+  h->launches += (n > 0) ? 2 : 1;
+  // 6. ids: unique; dense (a permutation of 0..n-1) enables ORDER_ID and set_contacts
+  h->ids_dense = false;
+  if (n > 0) {
+    uint32_t* seen = nullptr;
+    uint32_t* dup = nullptr;
+    if (!dalloc(h, &seen, (size_t)n) || !dalloc(h, &dup, 1)) {
+      unstage();
+      return fail(h, DEM_ENOMEM, "id check allocation failed");
+    }
+    CUDA_TRY(h, cudaMemsetAsync(seen, 0, sizeof(uint32_t) * n, st));
+    CUDA_TRY(h, cudaMemsetAsync(dup, 0, sizeof(uint32_t), st));
+    launch_idcheck(st, n, h->omg[0], seen, dup);
+    uint32_t hdup = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&hdup, dup, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    dev_free(h, seen);
+    dev_free(h, dup);
+    if (hp.id_max < (uint64_t)n) {
+      if (hdup) {
+        unstage();
+        h->n = -1;
+        return fail(h, DEM_EINVAL, "duplicate particle ids");
+      }
+      h->ids_dense = true;
+    } else {
+      // sparse ids: check uniqueness on the host (setup path only)
+      std::vector<uint32_t> ids((size_t)n);
+      std::vector<float4> w((size_t)n);
+      CUDA_TRY(h, cudaMemcpyAsync(w.data(), h->omg[0], sizeof(float4) * n,
+                                  cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaStreamSynchronize(st));
+      for (int64_t i = 0; i < n; ++i) memcpy(&ids[(size_t)i], &w[(size_t)i].w, 4);
+      std::sort(ids.begin(), ids.end());
+      if (std::adjacent_find(ids.begin(), ids.end()) != ids.end()) {
+        unstage();
+        h->n = -1;
+        return fail(h, DEM_EINVAL, "duplicate particle ids");
+      }
+    }
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  unstage();
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return DEM_OK;
+}
+
+int dem_step(dem_handle* h, int64_t nsteps) {
+  if (!h) return DEM_EINVAL;
+  if (nsteps < 0) return fail(h, DEM_EINVAL, "nsteps < 0");
+  if (h->n < 0) return fail(h, DEM_ESTATE, "dem_step before dem_set_particles");
+  if (nsteps == 0 || h->n == 0) {
+    h->steps += (h->n == 0) ? nsteps : 0;
+    return DEM_OK;
+  }
+  const int64_t ctr0 = h->pending ? h->pend_ctr0 + h->pend_steps : h->steps;
+  const int cur0 = h->cur;
+  const bool eager = h->profiling || (h->p.flags & DEM_F_NO_GRAPH);
+  if (eager) {
+    for (int64_t k = 0; k < nsteps; ++k) {
+      int rc = enqueue_step(h, h->cur, h->profiling);
+      if (rc) return rc;
+      h->cur ^= 1;
+    }
+    if (h->profiling) {
+      CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+      for (auto& pr : h->prof) {
+        float ms = 0.f;
+        cudaEventElapsedTime(&ms, pr.b, pr.e);
+        h->kernel_ms[pr.kid] += ms;
+        h->kernel_count[pr.kid] += 1;
+        h->event_pool.push_back(pr.b);
+        h->event_pool.push_back(pr.e);
+      }
+      h->prof.clear();
+    }
+  } else {
+    for (int b = 0; b < 2; ++b) {
+      if (!h->g2[b]) {
+        int rc = build_graph(h, b, 2, &h->g2[b]);
+        if (rc) return rc;
+      }
+      if (!h->g1[b]) {
+        int rc = build_graph(h, b, 1, &h->g1[b]);
+        if (rc) return rc;
+      }
+    }
+    int64_t left = nsteps;
+    while (left >= 2) {
+      CUDA_TRY(h, cudaGraphLaunch(h->g2[h->cur], h->stream));
+      h->graph_launches++;
+      h->launches += 8;
+      left -= 2;
+    }
+    if (left) {
+      CUDA_TRY(h, cudaGraphLaunch(h->g1[h->cur], h->stream));
+      h->graph_launches++;
+      h->launches += 4;
+      h->cur ^= 1;
+    }
+  }
+  if (!h->pending) {
+    h->pending = true;
+    h->pend_ctr0 = ctr0;
+    h->pend_cur0 = cur0;
+    h->pend_steps = 0;
+  }
+  h->pend_steps += nsteps;
+  h->steps = ctr0 + nsteps;  // provisional until checked
+  if (h->p.flags & DEM_F_ASYNC) return DEM_OK;
+  return dem_sync(h);
+}
+
+int dem_sync(dem_handle* h) {
+  if (!h) return DEM_EINVAL;
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (!h->pending) return DEM_OK;
+  h->pending = false;
+  return check_step_error(h, h->pend_ctr0, h->pend_cur0, h->pend_steps);
+}
+
+int dem_get_state(dem_handle* h, int32_t order, int64_t cap, const dem_particles* dst,
+                  int64_t* n_out) {
+  if (!h || !dst) return DEM_EINVAL;
+  if (h->pending) {
+    int rc = dem_sync(h);
+    if (rc) return rc;
+  }
+  if (h->n < 0) return fail(h, DEM_ESTATE, "no particles set");
+  if (n_out) *n_out = h->n;
+  if (cap < h->n) return fail(h, DEM_EINVAL, "capacity too small");
+  if (order == DEM_ORDER_ID && !h->ids_dense)
+    return fail(h, DEM_EINVAL, "DEM_ORDER_ID needs ids 0..n-1");
+  if (h->n == 0) return DEM_OK;
+  cudaStream_t st = h->stream;
+  const int64_t n = h->n;
+  const bool dev = dst->mem_kind == DEM_MEM_DEVICE;
+  float *o[8] = {dst->pos, dst->vel, dst->omega, dst->radius, dst->mass, (float*)dst->id,
+                 dst->force, dst->torque};
+  const size_t sz[8] = {3, 3, 3, 1, 1, 1, 3, 3};
+  float* d[8] = {};
+  std::vector<void*> tmp;
+  for (int k = 0; k < 8; ++k) {
+    if (!o[k]) continue;
+    if (dev) {
+      d[k] = o[k];
+    } else {
+      d[k] = (float*)dev_alloc(h, sizeof(float) * sz[k] * n);
+      if (!d[k]) {
+        for (void* p : tmp) dev_free(h, p);
+        return fail(h, DEM_ENOMEM, "staging allocation failed");
+      }
+      tmp.push_back(d[k]);
+    }
+  }
+  launch_unpack(st, n, order == DEM_ORDER_ID, h->pos[h->cur], h->vel[h->cur], h->omg[h->cur],
+                h->F, h->T, d[0], d[1], d[2], d[3], d[4], (uint32_t*)d[5], d[6], d[7]);
+  h->launches++;
+  if (!dev)
+    for (int k = 0; k < 8; ++k)
+      if (o[k])
+        CUDA_TRY(h, cudaMemcpyAsync(o[k], d[k], sizeof(float) * sz[k] * n,
+                                    cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  for (void* p : tmp) dev_free(h, p);
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return DEM_OK;
+}
+
+int dem_get_contacts(dem_handle* h, int32_t mem_kind, int64_t cap, uint32_t* id_i,
+                     uint32_t* id_j, float* dt3, int64_t* m_out) {
+  if (!h) return DEM_EINVAL;
+  if (h->pending) {
+    int rc = dem_sync(h);
+    if (rc) return rc;
+  }
+  if (h->n < 0) return fail(h, DEM_ESTATE, "no particles set");
+  if (h->n == 0 || h->p.model != DEM_MODEL_PRACTICAL) {
+    if (m_out) *m_out = 0;
+    return DEM_OK;
+  }
+  cudaStream_t st = h->stream;
+  const int64_t n = h->n;
+  uint32_t* base = nullptr;
+  unsigned long long* status = nullptr;
+  uint32_t* ctr = nullptr;
+  const uint32_t tiles = (uint32_t)((n + kScanTile - 1) / kScanTile) + 1;
+  if (!dalloc(h, &base, (size_t)n + 1) || !dalloc(h, &status, tiles) || !dalloc(h, &ctr, 1))
+    return fail(h, DEM_ENOMEM, "allocation failed");
+  CUDA_TRY(h, cudaMemsetAsync(status, 0, sizeof(unsigned long long) * tiles, st));
+  CUDA_TRY(h, cudaMemsetAsync(ctr, 0, sizeof(uint32_t), st));
+  launch_scan(st, h->cnt[h->cur], base, (uint32_t)n, nullptr, status, ctr, nullptr, 0);
+  uint32_t m = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&m, base + n, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  h->launches++;
+  if (m_out) *m_out = m;
+  int rc = DEM_OK;
+  if (cap < (int64_t)m) {
+    rc = fail(h, DEM_EINVAL, "capacity too small");
+  } else if (m > 0) {
+    const bool dev = mem_kind == DEM_MEM_DEVICE;
+    uint32_t *di = id_i, *dj = id_j;
+    float* dd = dt3;
+    if (!dev) {
+      di = id_i ? (uint32_t*)dev_alloc(h, 4ull * m) : nullptr;
+      dj = id_j ? (uint32_t*)dev_alloc(h, 4ull * m) : nullptr;
+      dd = dt3 ? (float*)dev_alloc(h, 12ull * m) : nullptr;
+    }
+    launch_emit_contacts(st, n, h->K, h->hist[h->cur], h->cnt[h->cur], base, h->omg[h->cur], di,
+                         dj, dd);
+    h->launches++;
+    if (!dev) {
+      if (id_i) CUDA_TRY(h, cudaMemcpyAsync(id_i, di, 4ull * m, cudaMemcpyDeviceToHost, st));
+      if (id_j) CUDA_TRY(h, cudaMemcpyAsync(id_j, dj, 4ull * m, cudaMemcpyDeviceToHost, st));
+      if (dt3) CUDA_TRY(h, cudaMemcpyAsync(dt3, dd, 12ull * m, cudaMemcpyDeviceToHost, st));
+      CUDA_TRY(h, cudaStreamSynchronize(st));
+      dev_free(h, di);
+      dev_free(h, dj);
+      dev_free(h, dd);
+    }
+  }
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  dev_free(h, base);
+  dev_free(h, status);
+  dev_free(h, ctr);
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return rc;
+}
+
+int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t* id_i,
+                     const uint32_t* id_j, const float* dt3) {
+  if (!h || m < 0 || (m > 0 && (!id_i || !id_j || !dt3))) return DEM_EINVAL;
+  if (h->n < 0) return fail(h, DEM_ESTATE, "no particles set");
+  if (!h->ids_dense) return fail(h, DEM_EINVAL, "dem_set_contacts needs ids 0..n-1");
+  if (h->p.model != DEM_MODEL_PRACTICAL) return m == 0 ? DEM_OK : fail(h, DEM_EINVAL, "simple model keeps no history");
+  cudaStream_t st = h->stream;
+  const int64_t n = h->n;
+  CUDA_TRY(h, cudaMemsetAsync(h->cnt[h->cur], 0, sizeof(uint32_t) * (n > 0 ? n : 1), st));
+  if (m == 0 || n == 0) {
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    return DEM_OK;
+  }
+  const bool dev = mem_kind == DEM_MEM_DEVICE;
+  const uint32_t *di = id_i, *dj = id_j;
+  const float* dd = dt3;
+  std::vector<void*> tmp;
+  if (!dev) {
+    void* a = dev_alloc(h, 4ull * m);
+    void* b = dev_alloc(h, 4ull * m);
+    void* c = dev_alloc(h, 12ull * m);
+    tmp = {a, b, c};
+    if (!a || !b || !c) {
+      for (void* p : tmp) dev_free(h, p);
+      return fail(h, DEM_ENOMEM, "allocation failed");
+    }
+    CUDA_TRY(h, cudaMemcpyAsync(a, id_i, 4ull * m, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(b, id_j, 4ull * m, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaMemcpyAsync(c, dt3, 12ull * m, cudaMemcpyHostToDevice, st));
+    di = (const uint32_t*)a;
+    dj = (const uint32_t*)b;
+    dd = (const float*)c;
+  } else if (!h->own_stream) {
+    cudaStreamSynchronize(nullptr);
+  }
+  uint32_t *slot = nullptr, *flags = nullptr;
+  if (!dalloc(h, &slot, (size_t)n) || !dalloc(h, &flags, 1)) {
+    for (void* p : tmp) dev_free(h, p);
+    return fail(h, DEM_ENOMEM, "allocation failed");
+  }
+  CUDA_TRY(h, cudaMemsetAsync(flags, 0, 4, st));
+  launch_slot_of_id(st, n, h->omg[h->cur], slot);
+  launch_insert_contacts(st, m, n, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
+                         flags);
+  h->launches += 2;
+  uint32_t hf = 0;
+  CUDA_TRY(h, cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  dev_free(h, slot);
+  dev_free(h, flags);
+  for (void* p : tmp) dev_free(h, p);
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  if (hf) {
+    CUDA_TRY(h, cudaMemset(h->cnt[h->cur], 0, sizeof(uint32_t) * n));
+    return fail(h, (hf & 1) ? DEM_EINVAL : DEM_EOVERFLOW,
+                (hf & 1) ? "contact id out of range" : "more than max_contacts entries for a particle");
+  }
+  return DEM_OK;
+}
+
+int dem_get_grid(dem_handle* h, int64_t cap, uint32_t* key, uint32_t* perm, uint32_t* off,
+                 int64_t* ncells_out) {
+  if (!h) return DEM_EINVAL;
+  if (h->pending) {
+    int rc = dem_sync(h);
+    if (rc) return rc;
+  }
+  if (h->n < 0) return fail(h, DEM_ESTATE, "no particles set");
+  if (ncells_out) *ncells_out = h->g.ncells;
+  const int64_t n = h->n;
+  if ((key || perm) && cap < n) return fail(h, DEM_EINVAL, "capacity too small");
+  if (off && cap < (int64_t)h->g.ncells + 1) return fail(h, DEM_EINVAL, "capacity too small");
+  cudaStream_t st = h->stream;
+  if (key && n) CUDA_TRY(h, cudaMemcpyAsync(key, h->key[h->cur], 4 * n, cudaMemcpyDeviceToHost, st));
+  if (perm && n) CUDA_TRY(h, cudaMemcpyAsync(perm, h->perm, 4 * n, cudaMemcpyDeviceToHost, st));
+  if (off)
+    CUDA_TRY(h, cudaMemcpyAsync(off, h->off, 4 * ((size_t)h->g.ncells + 1),
+                                cudaMemcpyDeviceToHost, st));
+  CUDA_TRY(h, cudaStreamSynchronize(st));
+  return DEM_OK;
+}
+
+int dem_get_stats(dem_handle* h, dem_stats* out) {
+  if (!h || !out) return DEM_EINVAL;
+  if (h->pending) {
+    int rc = dem_sync(h);
+    if (rc) return rc;
+  }
+  memset(out, 0, sizeof *out);
+  out->n = h->n;
+  out->ncells = h->g.ncells;
+  out->dims[0] = h->g.nx;
+  out->dims[1] = h->g.ny;
+  out->dims[2] = h->g.nz;
+  out->cell_edge = h->h;
+  out->steps = h->steps;
+  out->launches = h->launches;
+  out->graph_launches = h->graph_launches;
+  for (int k = 0; k < 8; ++k) {
+    out->kernel_ms[k] = h->kernel_ms[k];
+    out->kernel_count[k] = h->kernel_count[k];
+  }
+  if (h->n > 0 && h->p.model == DEM_MODEL_PRACTICAL) {
+    unsigned long long* sm = nullptr;
+    if (!dalloc(h, &sm, 2)) return fail(h, DEM_ENOMEM, "allocation failed");
+    CUDA_TRY(h, cudaMemsetAsync(sm, 0, 16, h->stream));
+    launch_cnt_stats(h->stream, h->n, h->cnt[h->cur], sm);
+    unsigned long long hs[2] = {0, 0};
+    CUDA_TRY(h, cudaMemcpyAsync(hs, sm, 16, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    dev_free(h, sm);
+    out->contacts = (int64_t)hs[0];
+    out->max_contacts_seen = (int64_t)hs[1];
+  }
+  return DEM_OK;
+}
+
+int dem_profile(dem_handle* h, int32_t enable) {
+  if (!h) return DEM_EINVAL;
+  h->profiling = enable != 0;
+  if (h->profiling) {
+    for (int k = 0; k < 8; ++k) {
+      h->kernel_ms[k] = 0.0;
+      h->kernel_count[k] = 0;
+    }
+  }
+  return DEM_OK;
+}
+
+int dem_nccl_unique_id(void* out128) {
+  (void)out128;
+  return fail(nullptr, DEM_ENCCL, "multi-GPU slabs are not built into this library yet");
+}
+
+}  // extern "C"

@@ -1,0 +1,132 @@
+// dem_internal.h — device-side data layout and kernel launchers of libdem.so.
+// Product code (the CUDA path). Shares nothing with oracle/.
+//
+// HBM layout, per particle slot j of buffer b in {0,1}:
+//   pos_r[b][j]  = (x, y, z, r)                      float4
+//   vel_m[b][j]  = (vx, vy, vz, m)                   float4
+//   omg_id[b][j] = (wx, wy, wz, bits(id))            float4
+//   key[b][j]    = CM (cell of this slot's position) u32
+//   hist[b][k*N + j] = (δt_x, δt_y, δt_z, bits(pid)) float4, k < cnt[b][j] <= K
+// and, per step: prank[N] (rank of a slot inside its cell from the counting
+// atomics), count[ncells] (particles per cell, zero between steps),
+// off[ncells+1] (= exclusive scan of count = lower_bound offsets of SCM),
+// tmp[N] (slots scattered by cell, unordered inside a cell) and perm[N]
+// (= SCCM of Eq. 11: old slot of each new slot, stable).
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+namespace dem {
+
+constexpr uint32_t kWallPid0 = 0xFFFFFFF0u;
+
+struct DevGrid {
+  int nx, ny, nz;
+  uint32_t ncells;
+  double lo[3], hi[3];
+  double inv_h;  // 1/h, correctly rounded on the host (R15)
+};
+
+struct DevPhys {
+  float dt;
+  float g[3];
+  float Cn, Ct, alpha, mu;
+  float wCn, wCt, walpha, wmu;
+  float ksp, kda, ksh;
+  uint32_t flags;
+};
+
+// Device error record. code is the positive value of the dem_error.
+struct DevErr {
+  uint32_t code;
+  uint32_t slot;
+  uint32_t id;
+  uint32_t step;      // value of step_ctr in the failing step
+  uint32_t step_ctr;  // steps started since dem_set_particles (incremented by k_scan)
+  uint32_t pad[3];
+};
+
+// Status words of the decoupled look-back scan: [flag:2 | value:32].
+constexpr int kScanThreads = 256;
+constexpr int kScanItems = 16;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+struct StepBuffers {
+  const float4* pos_in;
+  const float4* vel_in;
+  const float4* omg_in;
+  float4* pos_out;
+  float4* vel_out;
+  float4* omg_out;
+  const uint32_t* key_in;
+  uint32_t* key_out;
+  uint32_t* prank;
+  uint32_t* count;
+  uint32_t* off;
+  uint32_t* tmp;
+  uint32_t* perm;
+  const float4* hist_in;
+  const uint32_t* cnt_in;
+  float4* hist_out;
+  uint32_t* cnt_out;
+  float4* F_out;  // DEM_F_DIAG only
+  float4* T_out;
+  unsigned long long* scan_status;       // this parity's look-back words
+  uint32_t* scan_ctr;                    // this parity's dynamic tile counter
+  unsigned long long* scan_status_next;  // the other parity's (reset during this step)
+  uint32_t* scan_ctr_next;
+  DevErr* err;
+};
+
+enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5 };
+
+// ---- launchers (dem_kernels.cu) -------------------------------------------
+// Every launcher enqueues exactly one kernel on `st` and returns its id.
+
+// set_particles: AoS inputs (device) -> SoA float4 slots, CM, counting ranks.
+struct PackIn {
+  const float* pos;
+  const float* vel;
+  const float* omega;
+  const float* radius;
+  const float* mass;
+  const uint32_t* id;
+  float def_radius, def_mass_coef;  // mass = coef * r^3 when mass == NULL
+};
+struct Probe {  // validation results of k_probe
+  uint32_t bad_radius, bad_mass, nonfinite, outside, bad_id;
+  uint32_t rmax_bits, id_max, pad;
+};
+int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out);
+int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
+                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank);
+int launch_count(cudaStream_t st, int64_t n, const uint32_t* key, uint32_t* count,
+                 uint32_t* prank);
+int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen,
+                   uint32_t* dup_flag);
+
+// One step = scan, scatter, rank, sweep.
+int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
+                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
+int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
+int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
+int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
+                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph);
+
+// Introspection / state movement.
+int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
+                  const float4* omg, const float4* F, const float4* T, float* o_pos,
+                  float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
+                  float* o_F, float* o_T);
+int launch_emit_contacts(cudaStream_t st, int64_t n, uint32_t K, const float4* hist,
+                         const uint32_t* cnt, const uint32_t* base, const float4* omg,
+                         uint32_t* id_i, uint32_t* id_j, float* dt3);
+int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* slot_of_id);
+int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, uint32_t K,
+                           const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
+                           const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
+                           uint32_t* flags);
+int launch_cnt_stats(cudaStream_t st, int64_t n, const uint32_t* cnt,
+                     unsigned long long* sum_max);
+
+}  // namespace dem

@@ -1,0 +1,736 @@
+// dem_kernels.cu — the sm_100a kernels of one DEM timestep (arXiv 1301.1714).
+//
+// Per step (§4.2), four kernels:
+//   k_scan    step 3, first half: exclusive scan of the per-cell counts that the
+//             previous step's integrator accumulated -> off[] (= lower_bound
+//             offsets of SCM, SPEC cell ranges). Single pass, decoupled look-back.
+//   k_scatter step 3: tmp[off[CM[i]] + prank[i]] = i (a counting sort; prank came
+//             from warp-aggregated atomics, so the order inside a cell is not yet
+//             fixed).
+//   k_rank    step 3: perm[off[c] + #{t in cell c: tmp[t] < s}] = s — the stable
+//             order inside each cell, giving SCCM with SCM[j] = CM[SCCM[j]]
+//             (Eq. 11) and ties in ascending current slot (R16).
+//   k_sweep   steps 4-8 + 1: one thread per sorted slot j reads its particle
+//             through SCCM (the reorder of step 4 is this gather), visits the 27
+//             cells of Eq. 12 in ascending cell / slot order, decides contact with
+//             the fp64-defined predicate (R14), evaluates Eq. 1 or Eqs. 2-10
+//             with history, then the 6 walls (step 8), integrates (step 1, R9),
+//             writes the new state at slot j, hashes the new position (step 2 of
+//             the next step) and counts it into its cell for the next sort.
+// All arithmetic of the step runs here; the host only enqueues.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include "dem_internal.h"
+
+namespace dem {
+
+// ------------------------------------------------------------ helpers ------
+
+__device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+__device__ __forceinline__ uint32_t lanemask_lt() {
+  uint32_t m;
+  asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
+  return m;
+}
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t* p) {
+  return *reinterpret_cast<const volatile uint32_t*>(p);
+}
+
+// Record the first error of a step (positive code); later errors are ignored.
+__device__ void raise_error(DevErr* e, uint32_t code, uint32_t slot, uint32_t id) {
+  if (atomicCAS(&e->code, 0u, code) == 0u) {
+    e->slot = slot;
+    e->id = id;
+    e->step = ld_volatile(&e->step_ctr);
+    __threadfence();
+  }
+}
+
+// Step 2: the cell of a position, as the fp64 expression of
+// R15: c_a = clamp(floor((x_a - lo_a) * inv_h), 0, n_a - 1). __dsub_rn and
+// __dmul_rn keep it two correctly rounded operations.
+__device__ __forceinline__ int cell_coord(float x, double lo, double inv_h, int n) {
+  double t = floor(__dmul_rn(__dsub_rn((double)x, lo), inv_h));
+  t = fmax(t, 0.0);
+  t = fmin(t, (double)(n - 1));
+  return (int)t;
+}
+
+__device__ __forceinline__ uint32_t cell_key(const DevGrid& g, float x, float y, float z) {
+  int cx = cell_coord(x, g.lo[0], g.inv_h, g.nx);
+  int cy = cell_coord(y, g.lo[1], g.inv_h, g.ny);
+  int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz);
+  return (uint32_t)cx + (uint32_t)g.nx * ((uint32_t)cy + (uint32_t)g.ny * (uint32_t)cz);
+}
+
+// Counting-sort contribution of one particle: warp-aggregated atomic on its
+// cell (lanes with the same key share one atomic; __match_any_sync groups
+// them), returning its (arbitrary but unique) rank inside the cell.
+__device__ __forceinline__ uint32_t count_into_cell(uint32_t* count, uint32_t key) {
+  const uint32_t active = __activemask();
+  const uint32_t peers = __match_any_sync(active, key);
+  const uint32_t leader = __ffs(peers) - 1;
+  uint32_t base = 0;
+  if (lane_id() == leader) base = atomicAdd(&count[key], (uint32_t)__popc(peers));
+  base = __shfl_sync(peers, base, leader);
+  return base + (uint32_t)__popc(peers & lanemask_lt());
+}
+
+struct f3 {
+  float x, y, z;
+};
+__device__ __forceinline__ f3 mk(float x, float y, float z) { return {x, y, z}; }
+__device__ __forceinline__ float dot(f3 a, f3 b) { return a.x * b.x + a.y * b.y + a.z * b.z; }
+__device__ __forceinline__ f3 cross(f3 a, f3 b) {
+  return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
+}
+
+// ------------------------------------------------ set_particles kernels ----
+
+__global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r = in.radius ? in.radius[i] : in.def_radius;
+  float m = in.mass ? in.mass[i] : in.def_mass_coef * r * r * r;
+  if (!(r > 0.0f) || !isfinite(r)) atomicAdd(&out->bad_radius, 1u);
+  if (!(m > 0.0f) || !isfinite(m)) atomicAdd(&out->bad_mass, 1u);
+  bool fin = true;
+  for (int a = 0; a < 3; ++a) {
+    float x = in.pos[3 * i + a];
+    fin &= isfinite(x);
+    if (in.vel) fin &= isfinite(in.vel[3 * i + a]);
+    if (in.omega) fin &= isfinite(in.omega[3 * i + a]);
+    if (isfinite(x) && ((double)x < g.lo[a] || (double)x > g.hi[a]))
+      atomicAdd(&out->outside, 1u);
+  }
+  if (!fin) atomicAdd(&out->nonfinite, 1u);
+  if (r > 0.0f && isfinite(r)) atomicMax(&out->rmax_bits, __float_as_uint(r));
+  uint32_t id = in.id ? in.id[i] : (uint32_t)i;
+  if (id >= kWallPid0) atomicAdd(&out->bad_id, 1u);
+  atomicMax(&out->id_max, id);
+}
+
+__global__ void k_pack(int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel, float4* omg,
+                       uint32_t* key, uint32_t* count, uint32_t* prank) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  float r = in.radius ? in.radius[i] : in.def_radius;
+  float m = in.mass ? in.mass[i] : in.def_mass_coef * r * r * r;
+  float x = in.pos[3 * i], y = in.pos[3 * i + 1], z = in.pos[3 * i + 2];
+  pos[i] = make_float4(x, y, z, r);
+  vel[i] = in.vel ? make_float4(in.vel[3 * i], in.vel[3 * i + 1], in.vel[3 * i + 2], m)
+                  : make_float4(0.f, 0.f, 0.f, m);
+  uint32_t id = in.id ? in.id[i] : (uint32_t)i;
+  omg[i] = in.omega
+               ? make_float4(in.omega[3 * i], in.omega[3 * i + 1], in.omega[3 * i + 2],
+                             __uint_as_float(id))
+               : make_float4(0.f, 0.f, 0.f, __uint_as_float(id));
+  uint32_t k = cell_key(g, x, y, z);
+  key[i] = k;
+  prank[i] = count_into_cell(count, k);
+}
+
+__global__ void k_count(int64_t n, const uint32_t* key, uint32_t* count, uint32_t* prank) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  prank[i] = count_into_cell(count, key[i]);
+}
+
+// Duplicate-id check for dense ids (max id < n): seen[] is zeroed by the host.
+__global__ void k_idcheck(int64_t n, const float4* omg, uint32_t* seen, uint32_t* dup) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  uint32_t id = __float_as_uint(omg[i].w);
+  if (id < (uint64_t)n && atomicExch(&seen[id], 1u) != 0u) atomicAdd(dup, 1u);
+}
+
+// ------------------------------------------------------------ k_scan -------
+// Exclusive scan out[0..n] of in[0..n) (out[n] = total), one pass with
+// dynamic tile ids and decoupled look-back over 64-bit status words
+// [flag:2 | value:32] (flag 1 = tile aggregate, 2 = inclusive prefix).
+// Optionally zeroes `zero` (the per-cell counts, ready for the next step's
+// atomics) and advances the step counter.
+
+__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
+  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan(const uint32_t* in, uint32_t* __restrict__ out, uint32_t n, uint32_t* zero,
+           unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
+  // `in` and `zero` may alias (the per-cell counts are read, then cleared)
+  __shared__ uint32_t s_tile, s_prefix;
+  __shared__ uint32_t s_warp[kScanThreads / 32];
+  if (err && ld_volatile(&err->code) != 0u) return;
+  if (threadIdx.x == 0) {
+    s_tile = atomicAdd(ctr, 1u);
+    if (s_tile == 0 && count_step && err) atomicAdd(&err->step_ctr, 1u);
+  }
+  __syncthreads();
+  const uint32_t tile = s_tile;
+  const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+
+  uint32_t v[kScanItems];
+  if (base + kScanItems <= n) {
+    const uint4* p = reinterpret_cast<const uint4*>(in + base);
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      uint4 w = p[q];
+      v[4 * q] = w.x;
+      v[4 * q + 1] = w.y;
+      v[4 * q + 2] = w.z;
+      v[4 * q + 3] = w.w;
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q) v[q] = (base + q < n) ? in[base + q] : 0u;
+  }
+  uint32_t local = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) local += v[q];
+
+  // block exclusive scan of `local`
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint32_t incl = local;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += t;
+  }
+  if (lane == 31) s_warp[warp] = incl;
+  __syncthreads();
+  if (warp == 0) {
+    uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    uint32_t wi = w;
+#pragma unroll
+    for (int d = 1; d < kScanThreads / 32; d <<= 1) {
+      uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
+      if (lane >= (uint32_t)d) wi += t;
+    }
+    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
+    const uint32_t aggregate = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
+    // decoupled look-back (warp 0)
+    uint32_t prefix = 0;
+    if (tile == 0) {
+      if (lane == 0) st_status(&status[0], (2ull << 32) | aggregate);
+    } else {
+      if (lane == 0) st_status(&status[tile], (1ull << 32) | aggregate);
+      int64_t look = (int64_t)tile - 1;
+      while (true) {
+        int64_t t = look - (int64_t)lane;
+        unsigned long long s = 0;
+        uint32_t flag;
+        do {  // spin until this lane's predecessor has published something
+          s = t >= 0 ? ld_status(&status[t]) : (2ull << 32);
+          flag = (uint32_t)(s >> 32) & 3u;
+        } while (__any_sync(0xffffffffu, flag == 0u));
+        const uint32_t val = (uint32_t)s;
+        const uint32_t pmask = __ballot_sync(0xffffffffu, flag == 2u);
+        // lanes up to (and including) the nearest inclusive prefix contribute
+        const uint32_t stop = pmask ? (uint32_t)(__ffs(pmask) - 1) : 32u;
+        uint32_t contrib = lane <= stop ? val : 0u;
+#pragma unroll
+        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
+        prefix += contrib;
+        if (pmask) break;
+        look -= 32;
+      }
+      if (lane == 0) st_status(&status[tile], (2ull << 32) | (prefix + aggregate));
+    }
+    if (lane == 0) s_prefix = prefix;
+    if (lane == 0 && (uint64_t)(tile + 1) * kScanTile >= n) out[n] = prefix + aggregate;
+  }
+  __syncthreads();
+  uint32_t run = s_prefix + s_warp[warp] + (incl - local);
+  if (base + kScanItems <= n) {
+    uint4* p = reinterpret_cast<uint4*>(out + base);
+#pragma unroll
+    for (int q = 0; q < kScanItems / 4; ++q) {
+      uint4 w;
+      w.x = run;
+      run += v[4 * q];
+      w.y = run;
+      run += v[4 * q + 1];
+      w.z = run;
+      run += v[4 * q + 2];
+      w.w = run;
+      run += v[4 * q + 3];
+      p[q] = w;
+    }
+    if (zero) {
+      uint4* z = reinterpret_cast<uint4*>(zero + base);
+#pragma unroll
+      for (int q = 0; q < kScanItems / 4; ++q) z[q] = make_uint4(0u, 0u, 0u, 0u);
+    }
+  } else {
+#pragma unroll
+    for (int q = 0; q < kScanItems; ++q)
+      if (base + q < n) {
+        out[base + q] = run;
+        run += v[q];
+        if (zero) zero[base + q] = 0u;
+      }
+  }
+}
+
+// --------------------------------------------------------- k_scatter -------
+__global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key,
+                          const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
+                          uint32_t* __restrict__ tmp, unsigned long long* status_next,
+                          uint32_t* ctr_next, uint32_t ntiles_next, const DevErr* err) {
+  if (ld_volatile(&err->code) != 0u) return;
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // reset the other parity's scan state for the next step
+  for (int64_t t = i; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
+  if (i == 0) *ctr_next = 0u;
+  if (i >= n) return;
+  tmp[off[key[i]] + prank[i]] = (uint32_t)i;
+}
+
+// ------------------------------------------------------------ k_rank -------
+__global__ void k_rank(int64_t n, const uint32_t* __restrict__ key,
+                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ tmp,
+                       uint32_t* __restrict__ perm, const DevErr* err) {
+  if (ld_volatile(&err->code) != 0u) return;
+  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  const uint32_t s = tmp[j];
+  const uint32_t c = key[s];
+  const uint32_t a = off[c], b = off[c + 1];
+  uint32_t r = 0;
+  for (uint32_t t = a; t < b; ++t) r += (tmp[t] < s) ? 1u : 0u;
+  perm[a + r] = s;
+}
+
+// ----------------------------------------------------------- k_sweep -------
+
+// Eqs. 2-10 for one contact seen from particle i (R1 orientation). Returns
+// the force on i, Tc = n x F_t (the torque is r_i Tc, Eq. 3) and the new δ_t.
+__device__ __forceinline__ void pair_practical(f3 n, float delta, float Rs, float ms, f3 v,
+                                               f3 rw, f3 dold, float Cn, float Ct, float alpha,
+                                               float mu, float dt, uint32_t flags, f3& F, f3& Tc,
+                                               f3& dnew) {
+  const float s = sqrtf(delta * Rs);  // Eqs. 8-9 share sqrt(|δ_n| / (r_i^-1 + r_j^-1))
+  const float kn = Cn * s, kt = Ct * s;
+  const float eta = alpha * sqrtf(kn * ms);  // Eq. 10
+  const float vn = dot(v, n);
+  const f3 c = cross(rw, n);
+  const f3 vt = mk((v.x - vn * n.x) + c.x, (v.y - vn * n.y) + c.y, (v.z - vn * n.z) + c.z);  // Eq. 6
+  const float p = dot(dold, n);
+  dnew = mk((dold.x - p * n.x) + vt.x * dt, (dold.y - p * n.y) + vt.y * dt,
+            (dold.z - p * n.z) + vt.z * dt);  // Eq. 7
+  const float knd = kn * delta;
+  f3 Fn = mk(-knd * n.x - eta * (vn * n.x), -knd * n.y - eta * (vn * n.y),
+             -knd * n.z - eta * (vn * n.z));  // Eq. 4, normal
+  f3 Ft = mk(-kt * dnew.x - eta * vt.x, -kt * dnew.y - eta * vt.y,
+             -kt * dnew.z - eta * vt.z);  // Eq. 4, tangential
+  float fn = sqrtf(dot(Fn, Fn));
+  if (flags & 2u) {  // DEM_F_CLAMP_FN (R3)
+    float rep = -dot(Fn, n);
+    fn = rep > 0.f ? rep : 0.f;
+  }
+  const float ft = sqrtf(dot(Ft, Ft));
+  const float lim = mu * fn;
+  if (ft > lim) {  // Eq. 5
+    const float sc = lim / ft;
+    Ft = mk(Ft.x * sc, Ft.y * sc, Ft.z * sc);
+    if ((flags & 1u) && kt > 0.f)  // DEM_F_TRUNCATE_DT (R4)
+      dnew = mk(-(Ft.x + eta * vt.x) / kt, -(Ft.y + eta * vt.y) / kt, -(Ft.z + eta * vt.z) / kt);
+  }
+  F = mk(Fn.x + Ft.x, Fn.y + Ft.y, Fn.z + Ft.z);  // Eq. 2
+  Tc = cross(n, Ft);                               // Eq. 3 (without r_i)
+}
+
+// Eq. 1 in the SDK sign convention (R1), u = v_j - v_i.
+__device__ __forceinline__ f3 pair_simple(f3 n, float delta, f3 u, float ksp, float kda,
+                                          float ksh) {
+  const float un = dot(u, n);
+  const float kd = ksp * delta;
+  return mk((-kd * n.x + kda * u.x) + ksh * (u.x - un * n.x),
+            (-kd * n.y + kda * u.y) + ksh * (u.y - un * n.y),
+            (-kd * n.z + kda * u.z) + ksh * (u.z - un * n.z));
+}
+
+// Exact contact predicate of R14 in fp64 (no contraction: __dmul_rn/__dadd_rn).
+__device__ __forceinline__ double exact_d2(float4 P, float4 Q) {
+  const double dx = (double)Q.x - (double)P.x, dy = (double)Q.y - (double)P.y,
+               dz = (double)Q.z - (double)P.z;
+  return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
+}
+
+template <int MODEL, bool DIAG>
+__global__ void __launch_bounds__(128) k_sweep(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
+                                               uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+
+  // step 4 + 5: the particle of sorted slot j, gathered through SCCM
+  const uint32_t s = __ldg(&b.perm[j]);
+  const float4 P = __ldg(&b.pos_in[s]);
+  const float4 V = __ldg(&b.vel_in[s]);
+  const float4 W = __ldg(&b.omg_in[s]);
+  const uint32_t my_id = __float_as_uint(W.w);
+  const uint32_t c = __ldg(&b.key_in[s]);
+  const int cx = (int)(c % (uint32_t)g.nx);
+  const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
+  const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
+  const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
+
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  uint32_t ncnt = 0;
+  bool overflow = false;
+
+  const float ri = P.w, mi = V.w;
+  const float inv_ri = __frcp_rn(ri), inv_mi = __frcp_rn(mi);
+  const f3 rwi = mk(__fmul_rn(ri, W.x), __fmul_rn(ri, W.y), __fmul_rn(ri, W.z));
+
+  auto lookup = [&](uint32_t pid) -> f3 {
+    for (uint32_t k = 0; k < n_old; ++k) {
+      const float4 h = __ldg(&b.hist_in[(size_t)k * N + s]);
+      if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
+    }
+    return mk(0.f, 0.f, 0.f);
+  };
+  auto push = [&](f3 d, uint32_t pid) {
+    if (ncnt < K) {
+      b.hist_out[(size_t)ncnt * N + j] = make_float4(d.x, d.y, d.z, __uint_as_float(pid));
+      ++ncnt;
+    } else {
+      overflow = true;
+    }
+  };
+
+  // steps 6-7: the 27 cells of Eq. 12 in ascending cell index; a row of 3 cells
+  // along x is one contiguous slot range
+  const int xa = cx > 0 ? cx - 1 : 0;
+  const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int z = cz + dz;
+    if (z < 0 || z >= g.nz) continue;
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int y = cy + dy;
+      if (y < 0 || y >= g.ny) continue;
+      const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
+      const uint32_t t0 = __ldg(&b.off[row + xa]);
+      const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
+      for (uint32_t t = t0; t < t1; ++t) {
+        if (t == j) continue;
+        const uint32_t q = __ldg(&b.perm[t]);
+        const float4 Q = __ldg(&b.pos_in[q]);
+        // contact predicate (R14): fp32 decides outside a ±16u band, else fp64
+        const float dxf = Q.x - P.x, dyf = Q.y - P.y, dzf = Q.z - P.z;
+        const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
+        const float Sf = ri + Q.w;
+        const float S2f = Sf * Sf;
+        bool contact;
+        if (fabsf(d2f - S2f) > 9.5367431640625e-07f * S2f) {  // 16 * 2^-24
+          contact = d2f < S2f;
+        } else {
+          const double S = (double)ri + (double)Q.w;
+          contact = exact_d2(P, Q) < __dmul_rn(S, S);
+        }
+        if (!contact) continue;
+        // geometry in fp64 from the fp32 values: Δ exact, d² fixed order, δ = S - D
+        const double d2 = exact_d2(P, Q);
+        if (d2 == 0.0) {
+          raise_error(b.err, 9u, j, my_id);
+          continue;
+        }
+        const double D = sqrt(d2);
+        const float delta = fmaxf((float)(((double)ri + (double)Q.w) - D), 0.f);
+        const float invD = (float)(1.0 / D);
+        const f3 n = mk(dxf * invD, dyf * invD, dzf * invD);
+        const float4 VQ = __ldg(&b.vel_in[q]);
+        if (MODEL == 0) {
+          const float4 WQ = __ldg(&b.omg_in[q]);
+          const uint32_t pid = __float_as_uint(WQ.w);
+          const float Rs = __frcp_rn(__fadd_rn(inv_ri, __frcp_rn(Q.w)));
+          const float ms = __frcp_rn(__fadd_rn(inv_mi, __frcp_rn(VQ.w)));
+          const f3 v = mk(V.x - VQ.x, V.y - VQ.y, V.z - VQ.z);
+          const f3 rw = mk(__fadd_rn(rwi.x, __fmul_rn(Q.w, WQ.x)),
+                           __fadd_rn(rwi.y, __fmul_rn(Q.w, WQ.y)),
+                           __fadd_rn(rwi.z, __fmul_rn(Q.w, WQ.z)));
+          f3 Fc, Tc, dnew;
+          pair_practical(n, delta, Rs, ms, v, rw, lookup(pid), ph.Cn, ph.Ct, ph.alpha, ph.mu,
+                         ph.dt, ph.flags, Fc, Tc, dnew);
+          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+          T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
+          push(dnew, pid);
+        } else {
+          const f3 u = mk(VQ.x - V.x, VQ.y - V.y, VQ.z - V.z);
+          const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+        }
+      }
+    }
+  }
+
+  // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
+  const float xs[3] = {P.x, P.y, P.z};
+#pragma unroll
+  for (int w = 0; w < 6; ++w) {
+    const int a = w >> 1;
+    const bool hi = (w & 1) != 0;
+    const double dist = hi ? (g.hi[a] - (double)xs[a]) : ((double)xs[a] - g.lo[a]);
+    if (!((double)ri > dist)) continue;
+    const float delta = (float)((double)ri - dist);
+    f3 n = mk(0.f, 0.f, 0.f);
+    if (a == 0) n.x = hi ? 1.f : -1.f;
+    if (a == 1) n.y = hi ? 1.f : -1.f;
+    if (a == 2) n.z = hi ? 1.f : -1.f;
+    if (MODEL == 0) {
+      const uint32_t pid = kWallPid0 + (uint32_t)w;
+      f3 Fc, Tc, dnew;
+      pair_practical(n, delta, ri, mi, mk(V.x, V.y, V.z), rwi, lookup(pid), ph.wCn, ph.wCt,
+                     ph.walpha, ph.wmu, ph.dt, ph.flags, Fc, Tc, dnew);
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+      T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
+      push(dnew, pid);
+    } else {
+      const f3 Fc = pair_simple(n, delta, mk(-V.x, -V.y, -V.z), ph.ksp, ph.kda, ph.ksh);
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+    }
+  }
+  if (overflow) raise_error(b.err, 6u, j, my_id);
+  if (MODEL == 0) b.cnt_out[j] = ncnt;
+  if (DIAG) {
+    b.F_out[j] = make_float4(F.x, F.y, F.z, 0.f);
+    b.T_out[j] = make_float4(T.x, T.y, T.z, 0.f);
+  }
+
+  // step 1 (next iteration): semi-implicit Euler (R9)
+  const float dt = ph.dt;
+  const float ax = F.x / mi + ph.g[0], ay = F.y / mi + ph.g[1], az = F.z / mi + ph.g[2];
+  const float vx = V.x + ax * dt, vy = V.y + ay * dt, vz = V.z + az * dt;
+  const float x = P.x + vx * dt, y = P.y + vy * dt, z = P.z + vz * dt;
+  float wx = W.x, wy = W.y, wz = W.z;
+  if (MODEL == 0) {
+    const float I = 0.4f * mi * ri * ri;
+    wx = W.x + (T.x / I) * dt;
+    wy = W.y + (T.y / I) * dt;
+    wz = W.z + (T.z / I) * dt;
+  }
+  b.pos_out[j] = make_float4(x, y, z, ri);
+  b.vel_out[j] = make_float4(vx, vy, vz, mi);
+  b.omg_out[j] = make_float4(wx, wy, wz, W.w);
+
+  const bool finite = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(vx) &&
+                      isfinite(vy) && isfinite(vz) && isfinite(wx) && isfinite(wy) &&
+                      isfinite(wz);
+  if (!finite) {
+    raise_error(b.err, 7u, j, my_id);
+    b.key_out[j] = 0u;
+    return;
+  }
+  const double rd = (double)ri;
+  if ((double)x < g.lo[0] - rd || (double)x > g.hi[0] + rd || (double)y < g.lo[1] - rd ||
+      (double)y > g.hi[1] + rd || (double)z < g.lo[2] - rd || (double)z > g.hi[2] + rd)
+    raise_error(b.err, 8u, j, my_id);
+  // step 2 of the next step: CM of the new position, counted into its cell
+  const uint32_t k2 = cell_key(g, x, y, z);
+  b.key_out[j] = k2;
+  b.prank[j] = count_into_cell(b.count, k2);
+}
+
+// --------------------------------------------------- introspection ---------
+
+__global__ void k_unpack(int64_t n, bool by_id, const float4* pos, const float4* vel,
+                         const float4* omg, const float4* F, const float4* T, float* o_pos,
+                         float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
+                         float* o_F, float* o_T) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const float4 P = pos[i], V = vel[i], W = omg[i];
+  const uint32_t id = __float_as_uint(W.w);
+  const int64_t d = by_id ? (int64_t)id : i;
+  if (o_pos) { o_pos[3 * d] = P.x; o_pos[3 * d + 1] = P.y; o_pos[3 * d + 2] = P.z; }
+  if (o_vel) { o_vel[3 * d] = V.x; o_vel[3 * d + 1] = V.y; o_vel[3 * d + 2] = V.z; }
+  if (o_omg) { o_omg[3 * d] = W.x; o_omg[3 * d + 1] = W.y; o_omg[3 * d + 2] = W.z; }
+  if (o_r) o_r[d] = P.w;
+  if (o_m) o_m[d] = V.w;
+  if (o_id) o_id[d] = id;
+  if (o_F && F) { float4 f = F[i]; o_F[3 * d] = f.x; o_F[3 * d + 1] = f.y; o_F[3 * d + 2] = f.z; }
+  if (o_T && T) { float4 t = T[i]; o_T[3 * d] = t.x; o_T[3 * d + 1] = t.y; o_T[3 * d + 2] = t.z; }
+}
+
+__global__ void k_emit_contacts(int64_t n, uint32_t K, const float4* hist, const uint32_t* cnt,
+                                const uint32_t* base, const float4* omg, uint32_t* id_i,
+                                uint32_t* id_j, float* dt3) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t c = cnt[i], o = base[i];
+  const uint32_t me = __float_as_uint(omg[i].w);
+  for (uint32_t k = 0; k < c && k < K; ++k) {
+    const float4 h = hist[(size_t)k * n + i];
+    if (id_i) id_i[o + k] = me;
+    if (id_j) id_j[o + k] = __float_as_uint(h.w);
+    if (dt3) { dt3[3 * (o + k)] = h.x; dt3[3 * (o + k) + 1] = h.y; dt3[3 * (o + k) + 2] = h.z; }
+  }
+}
+
+__global__ void k_slot_of_id(int64_t n, const float4* omg, uint32_t* slot_of_id) {
+  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  slot_of_id[__float_as_uint(omg[i].w)] = (uint32_t)i;
+}
+
+// flags[0] |= 1: id out of range, |= 2: capacity overflow
+__global__ void k_insert_contacts(int64_t m, int64_t n, uint32_t K, const uint32_t* id_i,
+                                  const uint32_t* id_j, const float* dt3,
+                                  const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
+                                  uint32_t* flags) {
+  int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= m) return;
+  const uint32_t a = id_i[e];
+  if (a >= (uint64_t)n) { atomicOr(flags, 1u); return; }
+  const uint32_t s = slot_of_id[a];
+  const uint32_t k = atomicAdd(&cnt[s], 1u);
+  if (k >= K) { atomicOr(flags, 2u); return; }
+  hist[(size_t)k * n + s] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
+                                        __uint_as_float(id_j[e]));
+}
+
+__global__ void k_cnt_stats(int64_t n, const uint32_t* cnt, unsigned long long* sum_max) {
+  unsigned long long s = 0;
+  uint32_t mx = 0;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    s += cnt[i];
+    mx = max(mx, cnt[i]);
+  }
+  for (int d = 16; d > 0; d >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, d);
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, d));
+  }
+  if (lane_id() == 0) {
+    atomicAdd(&sum_max[0], s);
+    atomicMax(&sum_max[1], (unsigned long long)mx);
+  }
+}
+
+// ------------------------------------------------------------ launchers ----
+
+static inline unsigned blocks_for(int64_t n, int threads) {
+  return (unsigned)((n + threads - 1) / threads);
+}
+
+int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out) {
+  if (n <= 0) return K_OTHER;
+  k_probe<<<blocks_for(n, 256), 256, 0, st>>>(n, in, g, out);
+  return K_OTHER;
+}
+
+int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
+                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank) {
+  if (n <= 0) return K_HASH;
+  k_pack<<<blocks_for(n, 256), 256, 0, st>>>(n, in, g, pos, vel, omg, key, count, prank);
+  return K_HASH;
+}
+
+int launch_count(cudaStream_t st, int64_t n, const uint32_t* key, uint32_t* count,
+                 uint32_t* prank) {
+  if (n <= 0) return K_HASH;
+  k_count<<<blocks_for(n, 256), 256, 0, st>>>(n, key, count, prank);
+  return K_HASH;
+}
+
+int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen,
+                   uint32_t* dup_flag) {
+  if (n <= 0) return K_OTHER;
+  k_idcheck<<<blocks_for(n, 256), 256, 0, st>>>(n, omg, seen, dup_flag);
+  return K_OTHER;
+}
+
+int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
+                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
+  const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
+  k_scan<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, out, n, zero, status, ctr, err,
+                                                         count_step);
+  return K_SCAN;
+}
+
+int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next) {
+  const int64_t work = n > (int64_t)ntiles_next ? n : (int64_t)ntiles_next;
+  k_scatter<<<blocks_for(work > 0 ? work : 1, 256), 256, 0, st>>>(
+      n, b.key_in, b.prank, b.off, b.tmp, b.scan_status_next, b.scan_ctr_next, ntiles_next,
+      b.err);
+  return K_SCATTER;
+}
+
+int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
+  if (n <= 0) return K_RANK;
+  k_rank<<<blocks_for(n, 256), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm, b.err);
+  return K_RANK;
+}
+
+int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
+                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph) {
+  if (n <= 0) return K_SWEEP;
+  const unsigned blocks = blocks_for(n, 128);
+  const uint32_t N = (uint32_t)n;
+  if (model == 0) {
+    if (diag)
+      k_sweep<0, true><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+    else
+      k_sweep<0, false><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+  } else {
+    if (diag)
+      k_sweep<1, true><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+    else
+      k_sweep<1, false><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+  }
+  return K_SWEEP;
+}
+
+int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
+                  const float4* omg, const float4* F, const float4* T, float* o_pos,
+                  float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
+                  float* o_F, float* o_T) {
+  if (n <= 0) return K_OTHER;
+  k_unpack<<<blocks_for(n, 256), 256, 0, st>>>(n, by_id, pos, vel, omg, F, T, o_pos, o_vel,
+                                               o_omg, o_r, o_m, o_id, o_F, o_T);
+  return K_OTHER;
+}
+
+int launch_emit_contacts(cudaStream_t st, int64_t n, uint32_t K, const float4* hist,
+                         const uint32_t* cnt, const uint32_t* base, const float4* omg,
+                         uint32_t* id_i, uint32_t* id_j, float* dt3) {
+  if (n <= 0) return K_OTHER;
+  k_emit_contacts<<<blocks_for(n, 256), 256, 0, st>>>(n, K, hist, cnt, base, omg, id_i, id_j,
+                                                      dt3);
+  return K_OTHER;
+}
+
+int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* slot_of_id) {
+  if (n <= 0) return K_OTHER;
+  k_slot_of_id<<<blocks_for(n, 256), 256, 0, st>>>(n, omg, slot_of_id);
+  return K_OTHER;
+}
+
+int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, uint32_t K,
+                           const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
+                           const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
+                           uint32_t* flags) {
+  if (m <= 0) return K_OTHER;
+  k_insert_contacts<<<blocks_for(m, 256), 256, 0, st>>>(m, n, K, id_i, id_j, dt3, slot_of_id,
+                                                        hist, cnt, flags);
+  return K_OTHER;
+}
+
+int launch_cnt_stats(cudaStream_t st, int64_t n, const uint32_t* cnt,
+                     unsigned long long* sum_max) {
+  if (n <= 0) return K_OTHER;
+  k_cnt_stats<<<296, 256, 0, st>>>(n, cnt, sum_max);
+  return K_OTHER;
+}
+
+}  // namespace dem

@@ -1,0 +1,327 @@
+"""GPU parity: the CUDA path (through the C ABI) against the fp64 oracle on the
+same seeded inputs. Run on a B200 via gpurun:
+    python -m pytest tests -m gpu -x -q
+"""
+import math
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1301_1714_b200 import scenes as S
+from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_NO_GRAPH,
+                                      DEM_ORDER_ID, Dem, DemError)
+
+from .parity import assert_T2_forces, assert_T2_history, contacts_dict, oracle_inputs
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch
+
+
+def make(sc, flags=DEM_F_DIAG, **kw) -> Dem:
+    d = Dem(sc.params, flags=flags, **kw)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    return d
+
+
+def scenes_small():
+    return [S.C1(), S.random_gas(3000, 14.0, 5, r_range=(0.25e-3, 0.5e-3), v_sigma=0.05,
+                                 params=S.SimParams(max_contacts=32))]
+
+
+# --------------------------------------------------------- T1 bit-exact ----
+
+@pytest.mark.parametrize("name", ["C1", "C2", "C3"])
+def test_hash_sort_offsets_bit_exact(name):
+    sc = S.CONFIGS[name]()
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc, flags=0)
+    key0, _, _ = d.get_grid()
+    s0 = d.get_state()
+    CM = orc.hash_cells(p, s0["pos"].astype(np.float64))
+    assert np.array_equal(key0, CM)
+    d.step(1)
+    key1, perm, off = d.get_grid()
+    SCM, SCCM = orc.sort_map(CM)
+    assert np.array_equal(perm, SCCM)  # Eq. 11, stable
+    assert np.array_equal(off, orc.cell_offsets(SCM, off.shape[0] - 1))
+    s1 = d.get_state()
+    assert np.array_equal(s1["id"], s0["id"][SCCM])  # the reorder of step 4
+    assert np.array_equal(key1, orc.hash_cells(p, s1["pos"].astype(np.float64)))
+
+
+# ------------------------------------------------------ T2 one step -------
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_one_step_T2(idx):
+    sc = scenes_small()[idx]
+    K = sc.params.max_contacts
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc)
+    for k in range(4):  # steps 1..4 each from the GPU's own state + history
+        st, h = oracle_inputs(d, K)
+        d.step(1)
+        g = d.get_state(forces=True)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        assert np.array_equal(g["id"], st.id)  # same sorted order
+        assert_T2_forces(g["force"], g["torque"], res, what=f"{sc.name} step {k + 1}")
+        assert_T2_history(contacts_dict(d), h.as_dict(st.id))
+        # integrated state: within the force tolerance carried through Δt, plus fp32 rounding
+        dt = p.dt
+        tolF = 1e-4 * np.linalg.norm(res.F, axis=1) + 1e-5 * res.Fabs
+        dv = np.linalg.norm(g["vel"] - st.vel, axis=1)
+        assert np.all(dv <= tolF / st.mass * dt + 3e-7 * np.linalg.norm(st.vel, axis=1) + 1e-12)
+        dx = np.abs(g["pos"] - st.pos).max(axis=1)
+        assert np.all(dx <= dv * dt + 2 * np.spacing(np.abs(st.pos).astype(np.float32)).max(axis=1))
+
+
+def test_one_step_T2_C2_both_models():
+    for model in ("practical", "simple"):
+        sc = S.C2(S.SimParams(model=model))
+        p = orc.make_params(sc.params, sc.radius)
+        d = make(sc)
+        d.step(3)
+        st, h = oracle_inputs(d, 16)
+        d.step(1)
+        g = d.get_state(forces=True)
+        res = orc.step(p, st, h)
+        assert np.array_equal(g["id"], st.id)
+        assert_T2_forces(g["force"], g["torque"], res, what=f"C2 {model}")
+        if model == "practical":
+            assert_T2_history(contacts_dict(d), h.as_dict(st.id))
+
+
+def test_one_step_T2_C3_full():
+    sc = S.C3()
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc)
+    d.step(2)
+    st, h = oracle_inputs(d, 16)
+    d.step(1)
+    g = d.get_state(forces=True)
+    res = orc.step(p, st, h)
+    assert np.array_equal(g["id"], st.id)
+    assert_T2_forces(g["force"], g["torque"], res, what="C3")
+    assert_T2_history(contacts_dict(d), h.as_dict(st.id))
+
+
+def test_full_size_C4_sampled():
+    """4M-particle settling bed in the bench's launch configuration (graph
+    replay): grid bit-exact for every particle; forces, torques and histories
+    of ~300 sampled particles against the oracle evaluated one by one."""
+    sc = S.C4()
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc)
+    d.step(20)
+    K = int(d.stats()["max_contacts_seen"]) + 2
+    st, h = oracle_inputs(d, K)
+    key0, _, _ = d.get_grid()
+    CM = orc.hash_cells(p, st.pos)
+    assert np.array_equal(key0, CM)
+    d.step(1)
+    key1, perm, off = d.get_grid()
+    SCM, SCCM = orc.sort_map(CM)
+    assert np.array_equal(perm, SCCM)
+    assert np.array_equal(off, orc.cell_offsets(SCM, off.shape[0] - 1))
+    g = d.get_state(forces=True)
+    rng = np.random.default_rng(44)
+    mask = np.zeros(sc.n, bool)
+    mask[rng.choice(sc.n, 256, replace=False)] = True
+    near = np.nonzero(g["pos"][:, 1] < 0.6e-3)[0]  # floor contacts too
+    mask[near[:32]] = True
+    res = orc.step(p, st, h, only=mask)
+    assert np.array_equal(g["id"], st.id)
+    assert_T2_forces(g["force"], g["torque"], res, mask=mask, what="C4 sampled")
+    sample_ids = st.id[mask]
+    id_i, id_j, dt3 = d.get_contacts()
+    keep = np.isin(id_i, sample_ids)
+    gc = {(int(a), int(b)): v.astype(np.float64)
+          for a, b, v in zip(id_i[keep], id_j[keep], dt3[keep])}
+    oc = {}
+    for s in np.nonzero(mask)[0]:
+        for k in range(int(h.cnt[s])):
+            oc[(int(st.id[s]), int(h.pid[s, k]))] = h.dt[s, k].copy()
+    assert_T2_history(gc, oc)
+
+
+# ------------------------------------------- T3 shadow bound, 100 steps ----
+
+def test_shadow_bound_100_steps():
+    sc = S.C1()
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc, flags=0)
+    st = orc.State.from_scene(sc)
+    hx = orc.History.empty(sc.n, 16)
+    st_r = st.copy()
+    hr = orc.History.empty(sc.n, 16)
+    for _ in range(100):
+        assert orc.step(p, st, hx).rc == 0
+        assert orc.step(p, st_r, hr).rc == 0
+        r = st_r.rounded_fp32()
+        st_r.pos, st_r.vel, st_r.omega = r.pos, r.vel, r.omega
+        hr.dt = hr.dt.astype(np.float32).astype(np.float64)
+    d.step(100)
+    g = d.get_state(order=DEM_ORDER_ID)
+    o = np.argsort(st.id)
+    o_r = np.argsort(st_r.id)
+    shadow = np.abs(st.pos[o] - st_r.pos[o_r]).max()
+    err = np.abs(g["pos"] - st.pos[o]).max()
+    L = max(abs(x) for x in sc.params.box_hi)
+    bound = max(10 * shadow, 8 * 100 * np.spacing(np.float32(L)))
+    assert err <= bound, (err, shadow, bound)
+    vshadow = np.abs(st.vel[o] - st_r.vel[o_r]).max()
+    verr = np.abs(g["vel"] - st.vel[o]).max()
+    assert verr <= max(10 * vshadow, 8 * 100 * np.spacing(np.float32(np.abs(st.vel).max()))), (
+        verr, vshadow)
+
+
+# ------------------------------------------------- invariants ------------
+
+def test_third_law_bitwise_history():
+    """P11 on the GPU: δ_t,ij = -δ_t,ji bitwise for every pair contact."""
+    sc = S.C2()
+    d = make(sc, flags=0)
+    d.step(30)
+    c = contacts_dict(d)
+    pairs = [(a, b) for (a, b) in c if b < S_WALL]
+    assert len(pairs) > 10000
+    for a, b in pairs:
+        assert np.array_equal(c[(a, b)].astype(np.float32), -c[(b, a)].astype(np.float32))
+
+
+S_WALL = 0xFFFFFFF0
+
+
+def test_kissing_bound_and_contact_symmetry():
+    sc = S.C3()
+    d = make(sc, flags=0)
+    for _ in range(3):
+        d.step(10)
+        id_i, id_j, _ = d.get_contacts()
+        pair = id_j < S_WALL
+        per = np.bincount(id_i[pair], minlength=sc.n)
+        assert per.max() <= 12
+        st = d.stats()
+        assert st["contacts"] == len(id_i)
+        assert st["max_contacts_seen"] <= 16
+
+
+def test_momentum_conservation_gpu():
+    """T4/P12: g = 0, no walls touched: |ΔΣmv| within fp32 accumulation."""
+    c1 = S.C1()
+    sp = S.SimParams(gravity=(0.0, 0.0, 0.0), box_hi=(0.016, 0.02, 0.016))
+    sc = S.make_scene("free", sp, c1.pos + np.float32(2e-3), c1.vel, c1.omega)
+    d = make(sc, flags=0)
+    s0 = d.get_state()
+    P0 = (s0["mass"][:, None].astype(np.float64) * s0["vel"]).sum(0)
+    A = (s0["mass"][:, None].astype(np.float64) * np.abs(s0["vel"])).sum()
+    d.step(2000)
+    s1 = d.get_state()
+    P1 = (s1["mass"][:, None].astype(np.float64) * s1["vel"]).sum(0)
+    assert np.abs(P1 - P0).max() <= 1e-4 * A
+
+
+def test_determinism_and_graph_equivalence():
+    sc = S.C2()
+    outs = []
+    for flags in (0, 0, DEM_F_NO_GRAPH):
+        d = make(sc, flags=flags)
+        d.step(41)
+        s = d.get_state()
+        outs.append((s, d.get_contacts()))
+    for s, c in outs[1:]:
+        for k in ("pos", "vel", "omega", "id"):
+            assert np.array_equal(s[k], outs[0][0][k])
+        for a, b in zip(c, outs[0][1]):
+            assert np.array_equal(a, b)
+
+
+def test_checkpoint_roundtrip_bitwise():
+    sc = S.C1()
+    d1 = make(sc, flags=0)
+    d1.step(25)
+    s = d1.get_state()
+    id_i, id_j, dt3 = d1.get_contacts()
+    d2 = Dem(sc.params)
+    d2.set_particles(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"], s["id"])
+    d2.set_contacts(id_i, id_j, dt3)
+    d1.step(15)
+    d2.step(15)
+    a, b = d1.get_state(), d2.get_state()
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(a[k], b[k])
+
+
+@pytest.mark.parametrize("K", [6, 9])
+def test_overflow_rejects_step_and_keeps_last_good_state(K):
+    sc = S.C1(S.SimParams(max_contacts=K))
+    d = make(sc, flags=0)
+    with pytest.raises(DemError) as e:
+        for _ in range(200):
+            d.step(1)
+    assert e.value.code == DEM_EOVERFLOW
+    done = d.stats()["steps"]
+    ref = make(sc, flags=0)
+    if done:
+        ref.step(done)
+    a, b = d.get_state(), ref.get_state()
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(a[k], b[k])
+    # the same failure happens inside a multi-step graph replay
+    d3 = make(sc, flags=0)
+    with pytest.raises(DemError):
+        d3.step(200)
+    assert d3.stats()["steps"] == done
+    assert np.array_equal(d3.get_state()["pos"], a["pos"])
+
+
+def test_escape_is_reported():
+    sc = S.C1()
+    vel = sc.vel.copy()
+    vel[0] = (0.0, -4000.0, 0.0)  # crosses the floor within a step
+    sc2 = S.make_scene("esc", sc.params, sc.pos, vel, sc.omega)
+    d = make(sc2, flags=0)
+    with pytest.raises(DemError) as e:
+        d.step(5)
+    assert e.value.code == DEM_EESCAPED
+    assert "particle id 0" in str(e.value)
+
+
+def test_device_tensors_and_order_id(cuda):
+    torch = cuda
+    sc = S.C1()
+    d = Dem(sc.params)
+    t = lambda a: torch.as_tensor(a).cuda()  # noqa: E731
+    d.set_particles(t(sc.pos), t(sc.vel), t(sc.omega), t(sc.radius), t(sc.mass),
+                    t(sc.id.astype(np.int32)))
+    d.step(3)
+    out = {k: torch.empty(v, dtype=torch.float32, device="cuda")
+           for k, v in (("pos", (sc.n, 3)), ("vel", (sc.n, 3)), ("omega", (sc.n, 3)))}
+    out["id"] = torch.empty(sc.n, dtype=torch.int32, device="cuda")
+    d.get_state(order=DEM_ORDER_ID, out=out)
+    torch.cuda.synchronize()
+    assert torch.equal(out["id"].cpu(), torch.arange(sc.n, dtype=torch.int32))
+    h = make(sc, flags=0)
+    h.step(3)
+    ref = h.get_state(order=DEM_ORDER_ID)
+    assert np.array_equal(out["pos"].cpu().numpy(), ref["pos"])
+
+
+def test_profile_mode_times_every_kernel():
+    sc = S.C2()
+    d = make(sc, flags=0)
+    d.profile(True)
+    d.step(10)
+    st = d.stats()
+    for k in ("scan", "scatter", "rank", "sweep"):
+        assert st["kernel_count"][k] == 10
+        assert st["kernel_ms"][k] > 0
+    assert st["steps"] == 10
