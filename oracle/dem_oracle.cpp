@@ -294,7 +294,7 @@ int orc_friction_cap(double* Ft, double fn_mag, double mu) {
 void orc_pair_practical(const double* n, double delta, double Rstar, double mstar,
                         const double* v, const double* rw, const double* dt_old,
                         double Cn, double Ct, double alpha, double mu, double dt,
-                        uint32_t flags, double* F, double* Tc, double* dt_new) {
+                        uint32_t flags, double* F, double* Tc, double* dt_new, double* mag) {
   double kn, kt;
   orc_stiffness(Cn, Ct, delta, Rstar, &kn, &kt);          /* Eqs. 8-9 */
   double eta = orc_damping(alpha, kn, mstar);             /* Eq. 10   */
@@ -321,18 +321,27 @@ void orc_pair_practical(const double* n, double delta, double Rstar, double msta
   }
   for (int a = 0; a < 3; ++a) F[a] = Fn[a] + Ft[a]; /* Eq. 2 */
   cross3(n, Ft, Tc);                                /* Eq. 3 without r_i */
+  if (mag) {
+    /* magnitudes of the terms Eq. 4 sums (the cancellation scale of a
+     * floating-point evaluation of F and of F_t): |k_n δ|, |η v_n|, |k_t δ_t|, |η v_t| */
+    double tt = kt * norm3(dt_new) + eta * norm3(vt);
+    mag[0] = kn * delta + eta * std::fabs(vnm) + tt;
+    mag[1] = tt;
+  }
 }
 
 /* Eq. 1 with the SDK sign convention (reading R1):
  *   F_i = -k_sp δ n + k_da u + k_sh (u - (u·n) n),  u = v_j - v_i.
  * Gravity is applied once per particle in the integrator (reading R2). */
 void orc_pair_simple(const double* n, double delta, const double* u, double ksp,
-                     double kda, double ksh, double* F) {
+                     double kda, double ksh, double* F, double* mag) {
   double un = dot3(u, n);
+  double ut[3];
   for (int a = 0; a < 3; ++a) {
-    double ut = u[a] - un * n[a];
-    F[a] = (-ksp * delta * n[a] + kda * u[a]) + ksh * ut;
+    ut[a] = u[a] - un * n[a];
+    F[a] = (-ksp * delta * n[a] + kda * u[a]) + ksh * ut[a];
   }
+  if (mag) mag[0] = ksp * delta + kda * norm3(u) + ksh * norm3(ut); /* term magnitudes */
 }
 
 /* ---------------------------------------------------------------- step ---- */
@@ -359,9 +368,10 @@ typedef struct {
   uint32_t* off;   /* [ncells+1]; may be NULL */
   double* F;       /* [3n]  total contact force on each sorted particle (no gravity); may be NULL */
   double* T;       /* [3n]  total contact torque; may be NULL */
-  double* Fabs;    /* [n]   Σ_j |F_ij| over the contacts of each particle (incl. walls);
-                      the summation-cancellation scale of the T2 tolerance; may be NULL */
-  double* Tabs;    /* [n]   Σ_j |T_ij|; may be NULL */
+  double* Fabs;    /* [n]   Σ over the contacts of each particle (incl. walls) of the
+                      magnitudes of the terms Eq. 4 (Eq. 1) sums: the cancellation scale
+                      of the T2 tolerance's absolute floor; may be NULL */
+  double* Tabs;    /* [n]   the same for r_i (n × F_t): Σ r_i (|k_t δ_t| + |η v_t|) */
   int64_t err[3];  /* code, sorted slot, particle id of the first error */
   int64_t n_pair_contacts;  /* ordered (i,j) particle contacts found (each pair twice) */
   int64_t n_wall_contacts;
@@ -464,7 +474,7 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
       double nrm[3], delta = (r[j] + r[t]) - D;
       if (delta < 0.0) delta = 0.0;
       for (int a = 0; a < 3; ++a) nrm[a] = (x[3 * t + a] - x[3 * j + a]) / D;
-      double Fc[3];
+      double Fc[3], mag[2] = {0.0, 0.0};
       if (practical) {
         double Rstar = 1.0 / (1.0 / r[j] + 1.0 / r[t]);
         double mstar = 1.0 / (1.0 / m[j] + 1.0 / m[t]);
@@ -475,17 +485,17 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
         }
         lookup(j, id[t], dold);
         orc_pair_practical(nrm, delta, Rstar, mstar, vrel, rw, dold, p->Cn, p->Ct, p->alpha,
-                           p->mu, p->dt, p->flags, Fc, Tc, dnew);
+                           p->mu, p->dt, p->flags, Fc, Tc, dnew, mag);
         for (int a = 0; a < 3; ++a) Ti[a] += r[j] * Tc[a];
-        Tabs[j] += r[j] * norm3(Tc);
+        Tabs[j] += r[j] * mag[1];
         if (!push_hist(id[t], dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
       } else {
         double u[3];
         for (int a = 0; a < 3; ++a) u[a] = v[3 * t + a] - v[3 * j + a];
-        orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc);
+        orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc, mag);
       }
       for (int a = 0; a < 3; ++a) Fi[a] += Fc[a];
-      Fabs[j] += norm3(Fc);
+      Fabs[j] += mag[0];
     };
     if (brute) {
       for (size_t t = 0; t < N; ++t)
@@ -509,7 +519,7 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
       double nrm[3] = {0.0, 0.0, 0.0};
       nrm[a] = hi_side ? 1.0 : -1.0;
       double delta = r[j] - dist;
-      double Fc[3];
+      double Fc[3], mag[2] = {0.0, 0.0};
       if (practical) {
         double rw[3], dold[3], dnew[3], Tc[3];
         for (int b = 0; b < 3; ++b) rw[b] = r[j] * w[3 * j + b]; /* r_w ω_w := 0 */
@@ -517,17 +527,17 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
         lookup(j, pid, dold);
         /* R* = r_i, m* = m_i, v_j = ω_j = 0: the limits r_j, m_j -> ∞ */
         orc_pair_practical(nrm, delta, r[j], m[j], &v[3 * j], rw, dold, p->wCn, p->wCt,
-                           p->walpha, p->wmu, p->dt, p->flags, Fc, Tc, dnew);
+                           p->walpha, p->wmu, p->dt, p->flags, Fc, Tc, dnew, mag);
         for (int b = 0; b < 3; ++b) Ti[b] += r[j] * Tc[b];
-        Tabs[j] += r[j] * norm3(Tc);
+        Tabs[j] += r[j] * mag[1];
         if (!push_hist(pid, dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
       } else {
         double u[3];
         for (int b = 0; b < 3; ++b) u[b] = -v[3 * j + b]; /* v_wall = 0 */
-        orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc);
+        orc_pair_simple(nrm, delta, u, p->ksp, p->kda, p->ksh, Fc, mag);
       }
       for (int b = 0; b < 3; ++b) Fi[b] += Fc[b];
-      Fabs[j] += norm3(Fc);
+      Fabs[j] += mag[0];
     }
   }
 

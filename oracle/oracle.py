@@ -70,8 +70,8 @@ def lib():
         L.orc_tangential_displacement.argtypes = [_P, _P, _P, _D, _P]
         L.orc_friction_cap.argtypes = [_P, _D, _D]
         L.orc_pair_practical.argtypes = [_P, _D, _D, _D, _P, _P, _P, _D, _D, _D, _D, _D,
-                                         C.c_uint32, _P, _P, _P]
-        L.orc_pair_simple.argtypes = [_P, _D, _P, _D, _D, _D, _P]
+                                         C.c_uint32, _P, _P, _P, _P]
+        L.orc_pair_simple.argtypes = [_P, _D, _P, _D, _D, _D, _P, _P]
         L.orc_step.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(OrcState),
                                C.POINTER(OrcHist), C.POINTER(OrcOut)]
         L.orc_step_sampled.argtypes = [C.POINTER(OrcParams), C.c_int64, C.POINTER(OrcState),
@@ -230,14 +230,14 @@ def pair_practical(n, delta, Rstar, mstar, v, rw, dt_old, Cn, Ct, alpha, mu, dt,
     n, v, rw, d0 = _v(n), _v(v), _v(rw), _v(dt_old)
     F, Tc, d1 = np.empty(3), np.empty(3), np.empty(3)
     lib().orc_pair_practical(_ptr(n), delta, Rstar, mstar, _ptr(v), _ptr(rw), _ptr(d0), Cn, Ct,
-                             alpha, mu, dt, flags, _ptr(F), _ptr(Tc), _ptr(d1))
+                             alpha, mu, dt, flags, _ptr(F), _ptr(Tc), _ptr(d1), None)
     return F, Tc, d1
 
 
 def pair_simple(n, delta, u, ksp, kda, ksh):
     n, u = _v(n), _v(u)
     F = np.empty(3)
-    lib().orc_pair_simple(_ptr(n), delta, _ptr(u), ksp, kda, ksh, _ptr(F))
+    lib().orc_pair_simple(_ptr(n), delta, _ptr(u), ksp, kda, ksh, _ptr(F), None)
     return F
 
 
