@@ -246,7 +246,9 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        d = Dem(sc.params, device=local, stream=stream)
+        from paper_1301_1714_b200.dem import DEM_F_THREAD_PER_PARTICLE
+        d = Dem(sc.params, device=local, stream=stream,
+                flags=DEM_F_THREAD_PER_PARTICLE if args.sweep == "tpp" else 0)
         d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
         d.step(max(args.warmup, 3))
         stats0 = d.stats()
@@ -309,7 +311,7 @@ def run_ours(args):
             "grid": list(stats0["dims"]), "rho_c": rho_c, "c_bar": c_bar,
             "parallelism": f"replicas{world}" if world > 1 else "single-gpu",
             "l2": "working set > 1 GB per step >> 126 MB L2; no flush needed",
-            "dt": sc.params.dt,
+            "dt": sc.params.dt, "sweep": args.sweep,
         },
         "roofline": {
             "bound": "hbm", "kernel": "k_sweep", "achieved": achieved, "peak": peak_gbs,
@@ -399,6 +401,8 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--sweep", default="warp", choices=["warp", "tpp"],
+                    help="warp-cooperative sweep (default) or the paper's thread-per-particle")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

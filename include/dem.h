@@ -75,6 +75,8 @@ enum dem_flags {
   DEM_F_ASYNC = 1u << 3,       /* dem_step does not synchronise; errors surface at the next
                                   synchronising call */
   DEM_F_NO_GRAPH = 1u << 4,    /* launch kernels eagerly instead of replaying a CUDA graph */
+  DEM_F_THREAD_PER_PARTICLE = 1u << 5, /* ablation: the paper's one-thread-per-particle sweep
+                                           instead of the warp-cooperative one */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };

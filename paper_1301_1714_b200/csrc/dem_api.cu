@@ -52,6 +52,7 @@ struct dem_handle {
   float4* hist[2] = {};
   uint32_t* cnt[2] = {};
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
+  float4* pos_sorted = nullptr;
   float4 *F = nullptr, *T = nullptr;
   unsigned long long* scan_status[2] = {};
   uint32_t* scan_ctr = nullptr;  // [2]
@@ -150,6 +151,7 @@ void free_buffers(dem_handle* h) {
     h->scan_status[b] = nullptr;
   }
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
+  h->pos_sorted = nullptr;
   h->F = h->T = nullptr;
   h->err = nullptr;
   h->cap_n = h->cap_cells = -1;
@@ -170,6 +172,7 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.off = h->off;
   s.tmp = h->tmp;
   s.perm = h->perm;
+  s.pos_sorted = h->pos_sorted;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -221,7 +224,8 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   launch_rank(h->stream, h->n, s);
   rec(K_RANK, false);
   rec(K_SWEEP, true);
-  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph);
+  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph,
+               (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : 0);
   rec(K_SWEEP, false);
   h->launches += 4;
   cudaError_t e = cudaGetLastError();
@@ -512,7 +516,8 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     }
     ok &= dalloc(h, &h->prank, N) && dalloc(h, &h->count, (size_t)ncells + 1) &&
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
-          dalloc(h, &h->perm, N) && dalloc(h, &h->scan_ctr, 2) && dalloc(h, &h->err, 1);
+          dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->scan_ctr, 2) &&
+          dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
     if (!ok) {
       unstage();

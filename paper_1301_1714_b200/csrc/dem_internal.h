@@ -65,6 +65,7 @@ struct StepBuffers {
   uint32_t* off;
   uint32_t* tmp;
   uint32_t* perm;
+  float4* pos_sorted;  // (x,y,z,r) gathered into SCM order by k_rank (step 4 for positions)
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;
@@ -110,8 +111,10 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
+// variant 0: warp-cooperative two-phase sweep (default); 1: one thread per
+// particle for the whole step (the paper's mapping; ablation)
 int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
-                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph);
+                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph, int variant);
 
 // Introspection / state movement.
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,

@@ -282,32 +282,74 @@ __global__ void __launch_bounds__(kScanThreads)
 }
 
 // --------------------------------------------------------- k_scatter -------
-__global__ void k_scatter(int64_t n, const uint32_t* __restrict__ key,
-                          const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
-                          uint32_t* __restrict__ tmp, unsigned long long* status_next,
-                          uint32_t* ctr_next, uint32_t ntiles_next, const DevErr* err) {
+// Four slots per thread, loads batched ahead of the dependent off[] gathers so
+// every thread keeps several independent memory requests in flight.
+constexpr int kItems = 4;
+
+__global__ void __launch_bounds__(256)
+    k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ prank,
+              const uint32_t* __restrict__ off, uint32_t* __restrict__ tmp,
+              unsigned long long* status_next, uint32_t* ctr_next, uint32_t ntiles_next,
+              const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
-  int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // reset the other parity's scan state for the next step
-  for (int64_t t = i; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
-  if (i == 0) *ctr_next = 0u;
-  if (i >= n) return;
-  tmp[off[key[i]] + prank[i]] = (uint32_t)i;
+  for (int64_t t = tid; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
+  if (tid == 0) *ctr_next = 0u;
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
+  uint32_t k[kItems], r[kItems], o[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t i = base + (int64_t)u * blockDim.x;
+    k[u] = i < n ? __ldg(&key[i]) : 0u;
+    r[u] = i < n ? __ldg(&prank[i]) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) o[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&off[k[u]]) : 0u;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t i = base + (int64_t)u * blockDim.x;
+    if (i < n) tmp[o[u] + r[u]] = (uint32_t)i;
+  }
 }
 
 // ------------------------------------------------------------ k_rank -------
-__global__ void k_rank(int64_t n, const uint32_t* __restrict__ key,
-                       const uint32_t* __restrict__ off, const uint32_t* __restrict__ tmp,
-                       uint32_t* __restrict__ perm, const DevErr* err) {
+// perm[off[c] + #{t in cell c: tmp[t] < s}] = s, and the position of that
+// particle gathered into sorted order (PAPER.md:125 step 4, for the field the
+// 27-cell candidate loop reads).
+__global__ void __launch_bounds__(256)
+    k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
+           const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
+           const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
+           const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
-  int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  const uint32_t s = tmp[j];
-  const uint32_t c = key[s];
-  const uint32_t a = off[c], b = off[c + 1];
-  uint32_t r = 0;
-  for (uint32_t t = a; t < b; ++t) r += (tmp[t] < s) ? 1u : 0u;
-  perm[a + r] = s;
+  const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
+  uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const int64_t j = base + (int64_t)u * blockDim.x;
+    s[u] = j < n ? __ldg(&tmp[j]) : 0u;
+  }
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) c[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&key[s[u]]) : 0u;
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    const bool ok = base + (int64_t)u * blockDim.x < n;
+    a[u] = ok ? __ldg(&off[c[u]]) : 0u;
+    e[u] = ok ? __ldg(&off[c[u] + 1]) : 0u;
+  }
+  float4 P[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u)
+    P[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&pos_in[s[u]]) : make_float4(0.f, 0.f, 0.f, 0.f);
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (base + (int64_t)u * blockDim.x >= n) continue;
+    uint32_t r = 0;
+    for (uint32_t t = a[u]; t < e[u]; ++t) r += (__ldg(&tmp[t]) < s[u]) ? 1u : 0u;
+    perm[a[u] + r] = s[u];
+    pos_sorted[a[u] + r] = P[u];
+  }
 }
 
 // ----------------------------------------------------------- k_sweep -------
@@ -366,116 +408,66 @@ __device__ __forceinline__ double exact_d2(float4 P, float4 Q) {
   return __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
 }
 
-template <int MODEL, bool DIAG>
-__global__ void __launch_bounds__(128) k_sweep(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
-                                               uint32_t K) {
-  if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
+// Contact predicate (R14): fp32 decides outside a ±16u band around S², the
+// exact fp64 expression inside it (|d²₃₂ - d²| <= 5u d², |S²₃₂ - S²| <= 3u S²).
+__device__ __forceinline__ bool in_contact(float4 P, float4 Q) {
+  const float dxf = Q.x - P.x, dyf = Q.y - P.y, dzf = Q.z - P.z;
+  const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
+  const float Sf = P.w + Q.w;
+  const float S2f = Sf * Sf;
+  if (fabsf(d2f - S2f) > 9.5367431640625e-07f * S2f) return d2f < S2f;  // 16 * 2^-24
+  const double S = (double)P.w + (double)Q.w;
+  return exact_d2(P, Q) < __dmul_rn(S, S);
+}
 
-  // step 4 + 5: the particle of sorted slot j, gathered through SCCM
-  const uint32_t s = __ldg(&b.perm[j]);
-  const float4 P = __ldg(&b.pos_in[s]);
-  const float4 V = __ldg(&b.vel_in[s]);
-  const float4 W = __ldg(&b.omg_in[s]);
-  const uint32_t my_id = __float_as_uint(W.w);
-  const uint32_t c = __ldg(&b.key_in[s]);
-  const int cx = (int)(c % (uint32_t)g.nx);
-  const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
-  const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
-  const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
+// Geometry of a contact from the fp32 values: n (fp32, i -> j) and the
+// overlap δ = S - D evaluated as (S² - d²)/(S + D) with the numerator in fp64
+// (S² is exact in fp64; d² has the fixed order of R14) — the cancellation of
+// S - D is in exact-ish fp64, the division in fp32. Symmetric in (i, j).
+// Returns false for coincident centres (d² = 0, R18).
+__device__ __forceinline__ bool contact_geometry(float4 P, float4 Q, f3& n, float& delta) {
+  const double d2 = exact_d2(P, Q);
+  if (d2 == 0.0) return false;
+  const double S = (double)P.w + (double)Q.w;
+  const float num = (float)__dsub_rn(__dmul_rn(S, S), d2);
+  const float D = sqrtf((float)d2);
+  delta = fmaxf(num / __fadd_rn((float)S, D), 0.f);
+  const float invD = 1.0f / D;
+  n = mk((Q.x - P.x) * invD, (Q.y - P.y) * invD, (Q.z - P.z) * invD);
+  return true;
+}
 
-  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
-  uint32_t ncnt = 0;
-  bool overflow = false;
+struct Own {  // the particle of a sorted slot, as one contact evaluation needs it
+  float4 P, V, W;  // (x, r), (v, m), (ω, id bits)
+};
 
-  const float ri = P.w, mi = V.w;
-  const float inv_ri = __frcp_rn(ri), inv_mi = __frcp_rn(mi);
-  const f3 rwi = mk(__fmul_rn(ri, W.x), __fmul_rn(ri, W.y), __fmul_rn(ri, W.z));
+// Steps 7 for one particle pair (i owner, j partner): practical model with
+// history. `dold` is δ_t,old of the pair (0 if new). Returns F on i, Tc.
+__device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, float4 VQ, float4 WQ,
+                                                    f3 n, float delta, f3 dold, const DevPhys& ph,
+                                                    f3& Fc, f3& Tc, f3& dnew) {
+  const float Rs = __frcp_rn(__fadd_rn(__frcp_rn(o.P.w), __frcp_rn(Q.w)));
+  const float ms = __frcp_rn(__fadd_rn(__frcp_rn(o.V.w), __frcp_rn(VQ.w)));
+  const f3 v = mk(o.V.x - VQ.x, o.V.y - VQ.y, o.V.z - VQ.z);
+  // r_i ω_i + r_j ω_j with no contraction, so both sides round it identically (P11)
+  const f3 rw = mk(__fadd_rn(__fmul_rn(o.P.w, o.W.x), __fmul_rn(Q.w, WQ.x)),
+                   __fadd_rn(__fmul_rn(o.P.w, o.W.y), __fmul_rn(Q.w, WQ.y)),
+                   __fadd_rn(__fmul_rn(o.P.w, o.W.z), __fmul_rn(Q.w, WQ.z)));
+  pair_practical(n, delta, Rs, ms, v, rw, dold, ph.Cn, ph.Ct, ph.alpha, ph.mu, ph.dt, ph.flags,
+                 Fc, Tc, dnew);
+}
 
-  auto lookup = [&](uint32_t pid) -> f3 {
-    for (uint32_t k = 0; k < n_old; ++k) {
-      const float4 h = __ldg(&b.hist_in[(size_t)k * N + s]);
-      if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
-    }
-    return mk(0.f, 0.f, 0.f);
-  };
-  auto push = [&](f3 d, uint32_t pid) {
-    if (ncnt < K) {
-      b.hist_out[(size_t)ncnt * N + j] = make_float4(d.x, d.y, d.z, __uint_as_float(pid));
-      ++ncnt;
-    } else {
-      overflow = true;
-    }
-  };
-
-  // steps 6-7: the 27 cells of Eq. 12 in ascending cell index; a row of 3 cells
-  // along x is one contiguous slot range
-  const int xa = cx > 0 ? cx - 1 : 0;
-  const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
-  for (int dz = -1; dz <= 1; ++dz) {
-    const int z = cz + dz;
-    if (z < 0 || z >= g.nz) continue;
-    for (int dy = -1; dy <= 1; ++dy) {
-      const int y = cy + dy;
-      if (y < 0 || y >= g.ny) continue;
-      const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
-      const uint32_t t0 = __ldg(&b.off[row + xa]);
-      const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
-      for (uint32_t t = t0; t < t1; ++t) {
-        if (t == j) continue;
-        const uint32_t q = __ldg(&b.perm[t]);
-        const float4 Q = __ldg(&b.pos_in[q]);
-        // contact predicate (R14): fp32 decides outside a ±16u band, else fp64
-        const float dxf = Q.x - P.x, dyf = Q.y - P.y, dzf = Q.z - P.z;
-        const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
-        const float Sf = ri + Q.w;
-        const float S2f = Sf * Sf;
-        bool contact;
-        if (fabsf(d2f - S2f) > 9.5367431640625e-07f * S2f) {  // 16 * 2^-24
-          contact = d2f < S2f;
-        } else {
-          const double S = (double)ri + (double)Q.w;
-          contact = exact_d2(P, Q) < __dmul_rn(S, S);
-        }
-        if (!contact) continue;
-        // geometry in fp64 from the fp32 values: Δ exact, d² fixed order, δ = S - D
-        const double d2 = exact_d2(P, Q);
-        if (d2 == 0.0) {
-          raise_error(b.err, 9u, j, my_id);
-          continue;
-        }
-        const double D = sqrt(d2);
-        const float delta = fmaxf((float)(((double)ri + (double)Q.w) - D), 0.f);
-        const float invD = (float)(1.0 / D);
-        const f3 n = mk(dxf * invD, dyf * invD, dzf * invD);
-        const float4 VQ = __ldg(&b.vel_in[q]);
-        if (MODEL == 0) {
-          const float4 WQ = __ldg(&b.omg_in[q]);
-          const uint32_t pid = __float_as_uint(WQ.w);
-          const float Rs = __frcp_rn(__fadd_rn(inv_ri, __frcp_rn(Q.w)));
-          const float ms = __frcp_rn(__fadd_rn(inv_mi, __frcp_rn(VQ.w)));
-          const f3 v = mk(V.x - VQ.x, V.y - VQ.y, V.z - VQ.z);
-          const f3 rw = mk(__fadd_rn(rwi.x, __fmul_rn(Q.w, WQ.x)),
-                           __fadd_rn(rwi.y, __fmul_rn(Q.w, WQ.y)),
-                           __fadd_rn(rwi.z, __fmul_rn(Q.w, WQ.z)));
-          f3 Fc, Tc, dnew;
-          pair_practical(n, delta, Rs, ms, v, rw, lookup(pid), ph.Cn, ph.Ct, ph.alpha, ph.mu,
-                         ph.dt, ph.flags, Fc, Tc, dnew);
-          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
-          T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
-          push(dnew, pid);
-        } else {
-          const f3 u = mk(VQ.x - V.x, VQ.y - V.y, VQ.z - V.z);
-          const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
-          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
-        }
-      }
-    }
-  }
-
+// Step 8 + step 1 + next step 2 for one particle (shared by both sweeps):
+// walls, integration, state write at slot j, next CM and its counting rank.
+template <int MODEL, bool DIAG, class LookupFn>
+__device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevGrid& g,
+                                                const DevPhys& ph, uint32_t N, uint32_t K,
+                                                uint32_t j, const Own& o, f3 F, f3 T,
+                                                uint32_t ncnt, bool overflow, LookupFn lookup) {
+  const float ri = o.P.w, mi = o.V.w;
+  const uint32_t my_id = __float_as_uint(o.W.w);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
-  const float xs[3] = {P.x, P.y, P.z};
+  const float xs[3] = {o.P.x, o.P.y, o.P.z};
 #pragma unroll
   for (int w = 0; w < 6; ++w) {
     const int a = w >> 1;
@@ -489,14 +481,20 @@ __global__ void __launch_bounds__(128) k_sweep(StepBuffers b, DevGrid g, DevPhys
     if (a == 2) n.z = hi ? 1.f : -1.f;
     if (MODEL == 0) {
       const uint32_t pid = kWallPid0 + (uint32_t)w;
+      const f3 rwi = mk(__fmul_rn(ri, o.W.x), __fmul_rn(ri, o.W.y), __fmul_rn(ri, o.W.z));
       f3 Fc, Tc, dnew;
-      pair_practical(n, delta, ri, mi, mk(V.x, V.y, V.z), rwi, lookup(pid), ph.wCn, ph.wCt,
+      pair_practical(n, delta, ri, mi, mk(o.V.x, o.V.y, o.V.z), rwi, lookup(pid), ph.wCn, ph.wCt,
                      ph.walpha, ph.wmu, ph.dt, ph.flags, Fc, Tc, dnew);
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
       T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
-      push(dnew, pid);
+      if (ncnt < K) {
+        b.hist_out[(size_t)ncnt * N + j] = make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
+        ++ncnt;
+      } else {
+        overflow = true;
+      }
     } else {
-      const f3 Fc = pair_simple(n, delta, mk(-V.x, -V.y, -V.z), ph.ksp, ph.kda, ph.ksh);
+      const f3 Fc = pair_simple(n, delta, mk(-o.V.x, -o.V.y, -o.V.z), ph.ksp, ph.kda, ph.ksh);
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
     }
   }
@@ -506,39 +504,309 @@ __global__ void __launch_bounds__(128) k_sweep(StepBuffers b, DevGrid g, DevPhys
     b.F_out[j] = make_float4(F.x, F.y, F.z, 0.f);
     b.T_out[j] = make_float4(T.x, T.y, T.z, 0.f);
   }
-
   // step 1 (next iteration): semi-implicit Euler (R9)
   const float dt = ph.dt;
   const float ax = F.x / mi + ph.g[0], ay = F.y / mi + ph.g[1], az = F.z / mi + ph.g[2];
-  const float vx = V.x + ax * dt, vy = V.y + ay * dt, vz = V.z + az * dt;
-  const float x = P.x + vx * dt, y = P.y + vy * dt, z = P.z + vz * dt;
-  float wx = W.x, wy = W.y, wz = W.z;
+  const float vx = o.V.x + ax * dt, vy = o.V.y + ay * dt, vz = o.V.z + az * dt;
+  const float x = o.P.x + vx * dt, y = o.P.y + vy * dt, z = o.P.z + vz * dt;
+  float wx = o.W.x, wy = o.W.y, wz = o.W.z;
   if (MODEL == 0) {
     const float I = 0.4f * mi * ri * ri;
-    wx = W.x + (T.x / I) * dt;
-    wy = W.y + (T.y / I) * dt;
-    wz = W.z + (T.z / I) * dt;
+    wx = o.W.x + (T.x / I) * dt;
+    wy = o.W.y + (T.y / I) * dt;
+    wz = o.W.z + (T.z / I) * dt;
   }
   b.pos_out[j] = make_float4(x, y, z, ri);
   b.vel_out[j] = make_float4(vx, vy, vz, mi);
-  b.omg_out[j] = make_float4(wx, wy, wz, W.w);
-
+  b.omg_out[j] = make_float4(wx, wy, wz, o.W.w);
   const bool finite = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(vx) &&
                       isfinite(vy) && isfinite(vz) && isfinite(wx) && isfinite(wy) &&
                       isfinite(wz);
+  uint32_t k2 = 0;
   if (!finite) {
     raise_error(b.err, 7u, j, my_id);
-    b.key_out[j] = 0u;
-    return;
+  } else {
+    const double rd = (double)ri;
+    if ((double)x < g.lo[0] - rd || (double)x > g.hi[0] + rd || (double)y < g.lo[1] - rd ||
+        (double)y > g.hi[1] + rd || (double)z < g.lo[2] - rd || (double)z > g.hi[2] + rd)
+      raise_error(b.err, 8u, j, my_id);
+    k2 = cell_key(g, x, y, z);  // step 2 of the next step: CM of the new position
   }
-  const double rd = (double)ri;
-  if ((double)x < g.lo[0] - rd || (double)x > g.hi[0] + rd || (double)y < g.lo[1] - rd ||
-      (double)y > g.hi[1] + rd || (double)z < g.lo[2] - rd || (double)z > g.hi[2] + rd)
-    raise_error(b.err, 8u, j, my_id);
-  // step 2 of the next step: CM of the new position, counted into its cell
-  const uint32_t k2 = cell_key(g, x, y, z);
   b.key_out[j] = k2;
-  b.prank[j] = count_into_cell(b.count, k2);
+  b.prank[j] = count_into_cell(b.count, k2);  // counted into its cell for the next sort
+}
+
+// ---- variant 1: one thread per sorted particle for the whole step ---------
+// The paper's mapping ("Assign the i-th thread to the SCM[i]-th
+// particle"): each thread loops over its candidates and evaluates its own
+// contacts, so a warp idles on the lanes without a contact (§6's "quarter").
+template <int MODEL, bool DIAG>
+__global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, DevPhys ph,
+                                                   uint32_t N, uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const uint32_t s = __ldg(&b.perm[j]);
+  Own o;
+  o.P = __ldg(&b.pos_sorted[j]);
+  o.V = __ldg(&b.vel_in[s]);
+  o.W = __ldg(&b.omg_in[s]);
+  const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
+  auto lookup = [&](uint32_t pid) -> f3 {
+    for (uint32_t k = 0; k < n_old; ++k) {
+      const float4 h = __ldg(&b.hist_in[(size_t)k * N + s]);
+      if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
+    }
+    return mk(0.f, 0.f, 0.f);
+  };
+  const int cx = cell_coord(o.P.x, g.lo[0], g.inv_h, g.nx);
+  const int cy = cell_coord(o.P.y, g.lo[1], g.inv_h, g.ny);
+  const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz);
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  uint32_t ncnt = 0;
+  bool overflow = false;
+  const int xa = cx > 0 ? cx - 1 : 0;
+  const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int z = cz + dz;
+    if (z < 0 || z >= g.nz) continue;
+    for (int dy = -1; dy <= 1; ++dy) {
+      const int y = cy + dy;
+      if (y < 0 || y >= g.ny) continue;
+      const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
+      const uint32_t t0 = __ldg(&b.off[row + xa]);
+      const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
+      for (uint32_t t = t0; t < t1; ++t) {
+        if (t == j) continue;
+        const float4 Q = __ldg(&b.pos_sorted[t]);
+        if (!in_contact(o.P, Q)) continue;
+        f3 n;
+        float delta;
+        if (!contact_geometry(o.P, Q, n, delta)) {
+          raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
+          continue;
+        }
+        const uint32_t q = __ldg(&b.perm[t]);
+        const float4 VQ = __ldg(&b.vel_in[q]);
+        if (MODEL == 0) {
+          const float4 WQ = __ldg(&b.omg_in[q]);
+          const uint32_t pid = __float_as_uint(WQ.w);
+          f3 Fc, Tc, dnew;
+          eval_pair_practical(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
+          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+          T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
+          if (ncnt < K) {
+            b.hist_out[(size_t)ncnt * N + j] =
+                make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
+            ++ncnt;
+          } else {
+            overflow = true;
+          }
+        } else {
+          const f3 u = mk(VQ.x - o.V.x, VQ.y - o.V.y, VQ.z - o.V.z);
+          const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+          F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+        }
+      }
+    }
+  }
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, ncnt, overflow, lookup);
+}
+
+// ---- variant 0: warp-cooperative two-phase sweep (default) ----------------
+// Phase A: each lane scans its own 27-cell candidates (sorted positions, one
+// load each) and queues its contacts in shared memory, in candidate order.
+// Phase B: the warp's contacts are flattened and dealt round-robin to all 32
+// lanes, so a round evaluates 32 contacts regardless of which particles own
+// them — the divergence of §6 (~12 contacts among ~47
+// candidates leaves 3/4 of a thread-per-particle warp idle) is removed from
+// the expensive part. Each round's results go to shared memory and every
+// owner adds its own contacts in candidate order (deterministic, the oracle's
+// order). Old-history partner ids are staged in shared memory up front.
+struct WarpSmemLayout {
+  uint32_t bytes, oldpid, cq, res, base, slot, nold;
+  __host__ __device__ static WarpSmemLayout make(uint32_t K) {
+    WarpSmemLayout L;
+    uint32_t o = 3 * 32 * 16;  // own P, V, W
+    L.oldpid = o;
+    o += K * 32 * 4;
+    L.cq = o;
+    o += K * 32 * 4;
+    L.res = o;
+    o += 32 * 6 * 4;
+    L.base = o;
+    o += 36 * 4;
+    L.slot = o;
+    o += 32 * 4;
+    L.nold = o;
+    o += 32 * 4;
+    L.bytes = (o + 15u) & ~15u;
+    return L;
+  }
+};
+constexpr int kSweepWarps = 4;
+
+template <int MODEL, bool DIAG>
+__global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, DevGrid g,
+                                                                 DevPhys ph, uint32_t N,
+                                                                 uint32_t K) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const WarpSmemLayout L = WarpSmemLayout::make(K);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
+  float4* sP = reinterpret_cast<float4*>(ws);
+  float4* sV = sP + 32;
+  float4* sW = sV + 32;
+  uint32_t* s_oldpid = reinterpret_cast<uint32_t*>(ws + L.oldpid);  // [k*32 + lane]
+  uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);          // [k*32 + lane]
+  float* s_res = reinterpret_cast<float*>(ws + L.res);              // [6][32]
+  uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);      // [33]
+  uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
+  uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
+
+  const uint32_t j0 = (blockIdx.x * kSweepWarps + warp) * 32u;
+  const uint32_t j = j0 + lane;
+  const bool valid = j < N;
+  if (j0 >= N) return;  // whole warp past the end
+
+  // ---- phase 0: own particle (step 4 gather through SCCM) and old history ids
+  const uint32_t s = valid ? __ldg(&b.perm[j]) : 0u;
+  Own o;
+  o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
+  o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
+  o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldg(&b.cnt_in[s]), K) : 0u;
+  sP[lane] = o.P;
+  sV[lane] = o.V;
+  sW[lane] = o.W;
+  s_slot[lane] = s;
+  s_nold[lane] = n_old;
+  if (MODEL == 0) {
+    for (uint32_t k = 0; k < n_old; ++k)
+      s_oldpid[k * 32 + lane] = __float_as_uint(__ldg(&b.hist_in[(size_t)k * N + s]).w);
+  }
+
+  // ---- phase A: candidates of the 27 cells (Eq. 12), ascending cell and slot
+  uint32_t npair = 0;
+  bool overflow = false;
+  if (valid) {
+    const int cx = cell_coord(o.P.x, g.lo[0], g.inv_h, g.nx);
+    const int cy = cell_coord(o.P.y, g.lo[1], g.inv_h, g.ny);
+    const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz);
+    const int xa = cx > 0 ? cx - 1 : 0;
+    const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int z = cz + dz;
+      if (z < 0 || z >= g.nz) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int y = cy + dy;
+        if (y < 0 || y >= g.ny) continue;
+        const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
+        const uint32_t t0 = __ldg(&b.off[row + xa]);
+        const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
+        float4 Qn = t0 < t1 ? __ldg(&b.pos_sorted[t0]) : o.P;
+        for (uint32_t t = t0; t < t1; ++t) {
+          const float4 Q = Qn;
+          if (t + 1 < t1) Qn = __ldg(&b.pos_sorted[t + 1]);  // one candidate ahead
+          if (t == j || !in_contact(o.P, Q)) continue;
+          if (npair < K) {
+            s_cq[npair * 32 + lane] = t;
+            ++npair;
+          } else {
+            overflow = true;
+          }
+        }
+      }
+    }
+  }
+  // exclusive warp scan of the per-lane contact counts
+  uint32_t incl = npair;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += v;
+  }
+  const uint32_t mybase = incl - npair;
+  const uint32_t M = __shfl_sync(0xffffffffu, incl, 31);
+  s_base[lane] = mybase;
+  if (lane == 31) s_base[32] = M;
+  __syncwarp();
+
+  // ---- phase B: the warp's M contacts, 32 per round
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  for (uint32_t r0 = 0; r0 < M; r0 += 32) {
+    const uint32_t m = r0 + lane;
+    f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
+    if (m < M) {
+      // owner = last lane whose base <= m
+      uint32_t ow = 0;
+#pragma unroll
+      for (uint32_t step = 16; step > 0; step >>= 1)
+        if (s_base[ow + step] <= m) ow += step;
+      const uint32_t k = m - s_base[ow];
+      const uint32_t t = s_cq[k * 32 + ow];
+      Own po;
+      po.P = sP[ow];
+      po.V = sV[ow];
+      po.W = sW[ow];
+      const float4 Q = __ldg(&b.pos_sorted[t]);
+      f3 n;
+      float delta;
+      if (!contact_geometry(po.P, Q, n, delta)) {
+        raise_error(b.err, 9u, j0 + ow, __float_as_uint(po.W.w));
+      } else {
+        const uint32_t q = __ldg(&b.perm[t]);
+        const float4 VQ = __ldg(&b.vel_in[q]);
+        if (MODEL == 0) {
+          const float4 WQ = __ldg(&b.omg_in[q]);
+          const uint32_t pid = __float_as_uint(WQ.w);
+          f3 dold = mk(0.f, 0.f, 0.f);
+          const uint32_t no = s_nold[ow];
+          for (uint32_t kk = 0; kk < no; ++kk)
+            if (s_oldpid[kk * 32 + ow] == pid) {
+              const float4 h = __ldg(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
+              dold = mk(h.x, h.y, h.z);
+              break;
+            }
+          f3 dnew;
+          eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+          b.hist_out[(size_t)k * N + j0 + ow] =
+              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
+        } else {
+          const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
+          Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+        }
+      }
+    }
+    s_res[0 * 32 + lane] = Fc.x;
+    s_res[1 * 32 + lane] = Fc.y;
+    s_res[2 * 32 + lane] = Fc.z;
+    s_res[3 * 32 + lane] = Tc.x;
+    s_res[4 * 32 + lane] = Tc.y;
+    s_res[5 * 32 + lane] = Tc.z;
+    __syncwarp();
+    // each owner adds its contacts of this round, in candidate order
+    const uint32_t lo = max(mybase, r0), hi = min(mybase + npair, r0 + 32);
+    for (uint32_t x = lo; x < hi; ++x) {
+      const uint32_t l = x - r0;
+      F = mk(F.x + s_res[l], F.y + s_res[32 + l], F.z + s_res[64 + l]);
+      if (MODEL == 0)
+        T = mk(T.x + o.P.w * s_res[96 + l], T.y + o.P.w * s_res[128 + l],
+               T.z + o.P.w * s_res[160 + l]);
+    }
+    __syncwarp();
+  }
+  if (!valid) return;
+  auto lookup = [&](uint32_t pid) -> f3 {
+    for (uint32_t kk = 0; kk < n_old; ++kk)
+      if (s_oldpid[kk * 32 + lane] == pid) {
+        const float4 h = __ldg(&b.hist_in[(size_t)kk * N + s]);
+        return mk(h.x, h.y, h.z);
+      }
+    return mk(0.f, 0.f, 0.f);
+  };
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
 }
 
 // --------------------------------------------------- introspection ---------
@@ -659,34 +927,57 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
 }
 
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next) {
-  const int64_t work = n > (int64_t)ntiles_next ? n : (int64_t)ntiles_next;
-  k_scatter<<<blocks_for(work > 0 ? work : 1, 256), 256, 0, st>>>(
-      n, b.key_in, b.prank, b.off, b.tmp, b.scan_status_next, b.scan_ctr_next, ntiles_next,
-      b.err);
+  const int64_t per = 256 * kItems;
+  int64_t blocks = (n + per - 1) / per;
+  const int64_t need = ((int64_t)ntiles_next + 255) / 256;
+  if (blocks < need) blocks = need;
+  if (blocks < 1) blocks = 1;
+  k_scatter<<<(unsigned)blocks, 256, 0, st>>>(n, b.key_in, b.prank, b.off, b.tmp,
+                                              b.scan_status_next, b.scan_ctr_next, ntiles_next,
+                                              b.err);
   return K_SCATTER;
 }
 
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
-  k_rank<<<blocks_for(n, 256), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm, b.err);
+  const int64_t per = 256 * kItems;
+  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm,
+                                                           b.pos_in, b.pos_sorted, b.err);
   return K_RANK;
 }
 
-int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
-                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph) {
-  if (n <= 0) return K_SWEEP;
-  const unsigned blocks = blocks_for(n, 128);
+template <int MODEL, bool DIAG>
+static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
+                           const DevGrid& g, const DevPhys& ph, int variant) {
   const uint32_t N = (uint32_t)n;
+  if (variant == 1) {
+    k_sweep_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    return;
+  }
+  const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
+  static bool attr_set[2][2] = {{false, false}, {false, false}};
+  if (smem > 48 * 1024 && !attr_set[MODEL][DIAG]) {
+    cudaFuncSetAttribute(k_sweep_warp<MODEL, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)smem);
+    attr_set[MODEL][DIAG] = true;
+  }
+  k_sweep_warp<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
+      b, g, ph, N, K);
+}
+
+int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
+                 const StepBuffers& b, const DevGrid& g, const DevPhys& ph, int variant) {
+  if (n <= 0) return K_SWEEP;
   if (model == 0) {
     if (diag)
-      k_sweep<0, true><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+      sweep_dispatch<0, true>(st, n, K, b, g, ph, variant);
     else
-      k_sweep<0, false><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+      sweep_dispatch<0, false>(st, n, K, b, g, ph, variant);
   } else {
     if (diag)
-      k_sweep<1, true><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+      sweep_dispatch<1, true>(st, n, K, b, g, ph, variant);
     else
-      k_sweep<1, false><<<blocks, 128, 0, st>>>(b, g, ph, N, K);
+      sweep_dispatch<1, false>(st, n, K, b, g, ph, variant);
   }
   return K_SWEEP;
 }

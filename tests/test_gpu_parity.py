@@ -10,7 +10,7 @@ import pytest
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
 from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_NO_GRAPH,
-                                      DEM_ORDER_ID, Dem, DemError)
+                                      DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID, Dem, DemError)
 
 from .parity import assert_T2_forces, assert_T2_history, contacts_dict, oracle_inputs
 
@@ -59,12 +59,13 @@ def test_hash_sort_offsets_bit_exact(name):
 
 # ------------------------------------------------------ T2 one step -------
 
+@pytest.mark.parametrize("variant", [0, DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
-def test_one_step_T2(idx):
+def test_one_step_T2(idx, variant):
     sc = scenes_small()[idx]
     K = sc.params.max_contacts
     p = orc.make_params(sc.params, sc.radius)
-    d = make(sc)
+    d = make(sc, flags=DEM_F_DIAG | variant)
     for k in range(4):  # steps 1..4 each from the GPU's own state + history
         st, h = oracle_inputs(d, K)
         d.step(1)
@@ -242,6 +243,19 @@ def test_determinism_and_graph_equivalence():
             assert np.array_equal(s[k], outs[0][0][k])
         for a, b in zip(c, outs[0][1]):
             assert np.array_equal(a, b)
+
+
+def test_sweep_variants_agree():
+    """The warp-cooperative sweep and the paper's thread-per-particle sweep
+    sum each particle's contacts in the same order: bitwise equal steps."""
+    sc = S.C2()
+    a = make(sc, flags=0)
+    b = make(sc, flags=DEM_F_THREAD_PER_PARTICLE)
+    a.step(20)
+    b.step(20)
+    sa, sb = a.get_state(), b.get_state()
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(sa[k], sb[k])
 
 
 def test_checkpoint_roundtrip_bitwise():
