@@ -325,8 +325,11 @@ void orc_pair_practical(const double* n, double delta, double Rstar, double msta
     /* magnitudes of the terms Eq. 4 sums (the cancellation scale of a
      * floating-point evaluation of F and of F_t): |k_n δ|, |η v_n|, |k_t δ_t|, |η v_t| */
     double tt = kt * norm3(dt_new) + eta * norm3(vt);
-    mag[0] = kn * delta + eta * std::fabs(vnm) + tt;
-    mag[1] = tt;
+    double nn = kn * delta + eta * std::fabs(vnm);
+    mag[0] = nn + tt;
+    /* F_t is bounded by μ|F_n| (Eq. 5): when capped it inherits the
+     * cancellation of |F_n|, so its scale includes μ(|k_n δ| + |η v_n|) */
+    mag[1] = tt + mu * nn;
   }
 }
 
@@ -371,7 +374,8 @@ typedef struct {
   double* Fabs;    /* [n]   Σ over the contacts of each particle (incl. walls) of the
                       magnitudes of the terms Eq. 4 (Eq. 1) sums: the cancellation scale
                       of the T2 tolerance's absolute floor; may be NULL */
-  double* Tabs;    /* [n]   the same for r_i (n × F_t): Σ r_i (|k_t δ_t| + |η v_t|) */
+  double* Tabs;    /* [n]   the same for r_i (n × F_t):
+                      Σ r_i (|k_t δ_t| + |η v_t| + μ(|k_n δ| + |η v_n|)) */
   int64_t err[3];  /* code, sorted slot, particle id of the first error */
   int64_t n_pair_contacts;  /* ordered (i,j) particle contacts found (each pair twice) */
   int64_t n_wall_contacts;

@@ -30,7 +30,8 @@ def assert_T2_forces(F_gpu, T_gpu, res, rel=1e-4, floor=1e-5, mask=None, what=""
     the absolute floor's scale Fabs is the oracle's cancellation scale: the sum
     over the particle's contacts of the magnitudes of the terms Eq. 4 adds
     (|k_n δ| + |η v_n| + |k_t δ_t| + |η v_t|; Eq. 1's for the simple model).
-    The same for T with Σ r_i (|k_t δ_t| + |η v_t|). See DESIGN.md §3."""
+    The same for T with Σ r_i (|k_t δ_t| + |η v_t| + μ(|k_n δ| + |η v_n|)) —
+    Eq. 5 makes a capped F_t inherit the cancellation of |F_n|. DESIGN.md §3."""
     F_gpu = np.asarray(F_gpu, np.float64)
     T_gpu = np.asarray(T_gpu, np.float64)
     sel = slice(None) if mask is None else mask
