@@ -88,6 +88,21 @@ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
+// Approximate MUFU reciprocal / square root (|rel. error| ~ 2^-22): the
+// force arithmetic is fp32 with a 1e-4 parity tolerance, and IEEE div/sqrt
+// expand into slow-path subroutines. Deterministic, so the pair evaluation
+// stays bitwise antisymmetric (P11).
+__device__ __forceinline__ float frcp(float x) {
+  float y;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+__device__ __forceinline__ float fsqrt(float x) {
+  float y;
+  asm("sqrt.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+  return y;
+}
+
 // ------------------------------------------------ set_particles kernels ----
 
 __global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
@@ -360,9 +375,9 @@ __device__ __forceinline__ void pair_practical(f3 n, float delta, float Rs, floa
                                                f3 rw, f3 dold, float Cn, float Ct, float alpha,
                                                float mu, float dt, uint32_t flags, f3& F, f3& Tc,
                                                f3& dnew) {
-  const float s = sqrtf(delta * Rs);  // Eqs. 8-9 share sqrt(|δ_n| / (r_i^-1 + r_j^-1))
+  const float s = fsqrt(delta * Rs);  // Eqs. 8-9 share sqrt(|δ_n| / (r_i^-1 + r_j^-1))
   const float kn = Cn * s, kt = Ct * s;
-  const float eta = alpha * sqrtf(kn * ms);  // Eq. 10
+  const float eta = alpha * fsqrt(kn * ms);  // Eq. 10
   const float vn = dot(v, n);
   const f3 c = cross(rw, n);
   const f3 vt = mk((v.x - vn * n.x) + c.x, (v.y - vn * n.y) + c.y, (v.z - vn * n.z) + c.z);  // Eq. 6
@@ -374,18 +389,20 @@ __device__ __forceinline__ void pair_practical(f3 n, float delta, float Rs, floa
              -knd * n.z - eta * (vn * n.z));  // Eq. 4, normal
   f3 Ft = mk(-kt * dnew.x - eta * vt.x, -kt * dnew.y - eta * vt.y,
              -kt * dnew.z - eta * vt.z);  // Eq. 4, tangential
-  float fn = sqrtf(dot(Fn, Fn));
+  float fn = fsqrt(dot(Fn, Fn));
   if (flags & 2u) {  // DEM_F_CLAMP_FN (R3)
     float rep = -dot(Fn, n);
     fn = rep > 0.f ? rep : 0.f;
   }
-  const float ft = sqrtf(dot(Ft, Ft));
+  const float ft2 = dot(Ft, Ft);
   const float lim = mu * fn;
-  if (ft > lim) {  // Eq. 5
-    const float sc = lim / ft;
+  if (ft2 > lim * lim) {  // Eq. 5: |F_t| > μ|F_n|
+    const float sc = lim * frcp(fsqrt(ft2));
     Ft = mk(Ft.x * sc, Ft.y * sc, Ft.z * sc);
-    if ((flags & 1u) && kt > 0.f)  // DEM_F_TRUNCATE_DT (R4)
-      dnew = mk(-(Ft.x + eta * vt.x) / kt, -(Ft.y + eta * vt.y) / kt, -(Ft.z + eta * vt.z) / kt);
+    if ((flags & 1u) && kt > 0.f) {  // DEM_F_TRUNCATE_DT (R4)
+      const float ik = frcp(kt);
+      dnew = mk(-(Ft.x + eta * vt.x) * ik, -(Ft.y + eta * vt.y) * ik, -(Ft.z + eta * vt.z) * ik);
+    }
   }
   F = mk(Fn.x + Ft.x, Fn.y + Ft.y, Fn.z + Ft.z);  // Eq. 2
   Tc = cross(n, Ft);                               // Eq. 3 (without r_i)
@@ -415,7 +432,8 @@ __device__ __forceinline__ bool in_contact(float4 P, float4 Q) {
   const float d2f = dxf * dxf + dyf * dyf + dzf * dzf;
   const float Sf = P.w + Q.w;
   const float S2f = Sf * Sf;
-  if (fabsf(d2f - S2f) > 9.5367431640625e-07f * S2f) return d2f < S2f;  // 16 * 2^-24
+  if (d2f >= S2f * 1.00000095367431640625f) return false;  // (1 + 16u) S²: clearly apart
+  if (d2f <= S2f * 0.99999904632568359375f) return true;   // (1 - 16u) S²: clearly touching
   const double S = (double)P.w + (double)Q.w;
   return exact_d2(P, Q) < __dmul_rn(S, S);
 }
@@ -430,9 +448,9 @@ __device__ __forceinline__ bool contact_geometry(float4 P, float4 Q, f3& n, floa
   if (d2 == 0.0) return false;
   const double S = (double)P.w + (double)Q.w;
   const float num = (float)__dsub_rn(__dmul_rn(S, S), d2);
-  const float D = sqrtf((float)d2);
-  delta = fmaxf(num / __fadd_rn((float)S, D), 0.f);
-  const float invD = 1.0f / D;
+  const float D = fsqrt((float)d2);
+  delta = fmaxf(num * frcp(__fadd_rn((float)S, D)), 0.f);
+  const float invD = frcp(D);
   n = mk((Q.x - P.x) * invD, (Q.y - P.y) * invD, (Q.z - P.z) * invD);
   return true;
 }
@@ -446,8 +464,8 @@ struct Own {  // the particle of a sorted slot, as one contact evaluation needs 
 __device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, float4 VQ, float4 WQ,
                                                     f3 n, float delta, f3 dold, const DevPhys& ph,
                                                     f3& Fc, f3& Tc, f3& dnew) {
-  const float Rs = __frcp_rn(__fadd_rn(__frcp_rn(o.P.w), __frcp_rn(Q.w)));
-  const float ms = __frcp_rn(__fadd_rn(__frcp_rn(o.V.w), __frcp_rn(VQ.w)));
+  const float Rs = frcp(__fadd_rn(frcp(o.P.w), frcp(Q.w)));
+  const float ms = frcp(__fadd_rn(frcp(o.V.w), frcp(VQ.w)));
   const f3 v = mk(o.V.x - VQ.x, o.V.y - VQ.y, o.V.z - VQ.z);
   // r_i ω_i + r_j ω_j with no contraction, so both sides round it identically (P11)
   const f3 rw = mk(__fadd_rn(__fmul_rn(o.P.w, o.W.x), __fmul_rn(Q.w, WQ.x)),
@@ -468,8 +486,17 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
   const uint32_t my_id = __float_as_uint(o.W.w);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
   const float xs[3] = {o.P.x, o.P.y, o.P.z};
+  // conservative fp32 prefilter: only particles within r (+ rounding margin)
+  // of a face evaluate the exact fp64 wall predicate
+  bool near_wall = false;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    const float m = ri + 1e-6f * (fabsf(xs[a]) + ri) + 1e-30f;
+    near_wall |= (xs[a] - (float)g.lo[a] < m) | ((float)g.hi[a] - xs[a] < m);
+  }
 #pragma unroll
   for (int w = 0; w < 6; ++w) {
+    if (!near_wall) break;
     const int a = w >> 1;
     const bool hi = (w & 1) != 0;
     const double dist = hi ? (g.hi[a] - (double)xs[a]) : ((double)xs[a] - g.lo[a]);
@@ -506,15 +533,16 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
   }
   // step 1 (next iteration): semi-implicit Euler (R9)
   const float dt = ph.dt;
-  const float ax = F.x / mi + ph.g[0], ay = F.y / mi + ph.g[1], az = F.z / mi + ph.g[2];
+  const float im = frcp(mi);
+  const float ax = F.x * im + ph.g[0], ay = F.y * im + ph.g[1], az = F.z * im + ph.g[2];
   const float vx = o.V.x + ax * dt, vy = o.V.y + ay * dt, vz = o.V.z + az * dt;
   const float x = o.P.x + vx * dt, y = o.P.y + vy * dt, z = o.P.z + vz * dt;
   float wx = o.W.x, wy = o.W.y, wz = o.W.z;
   if (MODEL == 0) {
-    const float I = 0.4f * mi * ri * ri;
-    wx = o.W.x + (T.x / I) * dt;
-    wy = o.W.y + (T.y / I) * dt;
-    wz = o.W.z + (T.z / I) * dt;
+    const float iI = frcp(0.4f * mi * ri * ri);
+    wx = o.W.x + (T.x * iI) * dt;
+    wy = o.W.y + (T.y * iI) * dt;
+    wz = o.W.z + (T.z * iI) * dt;
   }
   b.pos_out[j] = make_float4(x, y, z, ri);
   b.vel_out[j] = make_float4(vx, vy, vz, mi);
@@ -624,7 +652,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 // owner adds its own contacts in candidate order (deterministic, the oracle's
 // order). Old-history partner ids are staged in shared memory up front.
 struct WarpSmemLayout {
-  uint32_t bytes, oldpid, cq, res, base, slot, nold;
+  uint32_t bytes, oldpid, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
     uint32_t o = 3 * 32 * 16;  // own P, V, W
@@ -634,6 +662,8 @@ struct WarpSmemLayout {
     o += K * 32 * 4;
     L.res = o;
     o += 32 * 6 * 4;
+    L.own = o;
+    o += ((K * 32 + 15u) & ~15u);
     L.base = o;
     o += 36 * 4;
     L.slot = o;
@@ -664,6 +694,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);      // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
+  uint8_t* s_own = ws + L.own;  // owner lane of each flattened contact
 
   const uint32_t j0 = (blockIdx.x * kSweepWarps + warp) * 32u;
   const uint32_t j = j0 + lane;
@@ -676,26 +707,43 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldg(&b.cnt_in[s]), K) : 0u;
+  const uint32_t c = valid ? __ldcg(&b.key_in[s]) : 0u;
+  const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcg(&b.cnt_in[s]), K) : 0u;
   sP[lane] = o.P;
   sV[lane] = o.V;
   sW[lane] = o.W;
   s_slot[lane] = s;
   s_nold[lane] = n_old;
   if (MODEL == 0) {
-    for (uint32_t k = 0; k < n_old; ++k)
-      s_oldpid[k * 32 + lane] = __float_as_uint(__ldg(&b.hist_in[(size_t)k * N + s]).w);
+    for (uint32_t k0 = 0; k0 < n_old; k0 += 4) {  // four loads in flight per lane
+      float w4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        w4[u] = (k0 + u < n_old) ? __ldcg(&b.hist_in[(size_t)(k0 + u) * N + s].w) : 0.f;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < n_old) s_oldpid[(k0 + u) * 32 + lane] = __float_as_uint(w4[u]);
+    }
   }
 
   // ---- phase A: candidates of the 27 cells (Eq. 12), ascending cell and slot
   uint32_t npair = 0;
   bool overflow = false;
   if (valid) {
-    const int cx = cell_coord(o.P.x, g.lo[0], g.inv_h, g.nx);
-    const int cy = cell_coord(o.P.y, g.lo[1], g.inv_h, g.ny);
-    const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz);
+    const int cx = (int)(c % (uint32_t)g.nx);
+    const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
+    const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
     const int xa = cx > 0 ? cx - 1 : 0;
     const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
+    const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+    auto push = [&](uint32_t t) {
+      if (npair < K) {
+        s_cq[npair * 32 + lane] = t;
+        ++npair;
+      } else {
+        overflow = true;
+      }
+    };
     for (int dz = -1; dz <= 1; ++dz) {
       const int z = cz + dz;
       if (z < 0 || z >= g.nz) continue;
@@ -705,17 +753,13 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
         const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
         const uint32_t t0 = __ldg(&b.off[row + xa]);
         const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
-        float4 Qn = t0 < t1 ? __ldg(&b.pos_sorted[t0]) : o.P;
-        for (uint32_t t = t0; t < t1; ++t) {
-          const float4 Q = Qn;
-          if (t + 1 < t1) Qn = __ldg(&b.pos_sorted[t + 1]);  // one candidate ahead
-          if (t == j || !in_contact(o.P, Q)) continue;
-          if (npair < K) {
-            s_cq[npair * 32 + lane] = t;
-            ++npair;
-          } else {
-            overflow = true;
-          }
+        for (uint32_t t = t0; t < t1; t += 2) {  // two candidates per iteration
+          const float4 Q0 = __ldg(&b.pos_sorted[t]);
+          const float4 Q1 = t + 1 < t1 ? __ldg(&b.pos_sorted[t + 1]) : far;
+          const bool c0 = in_contact(o.P, Q0);
+          const bool c1 = in_contact(o.P, Q1);
+          if (c0 && t != j) push(t);
+          if (c1 && t + 1 != j) push(t + 1);
         }
       }
     }
@@ -731,6 +775,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   const uint32_t M = __shfl_sync(0xffffffffu, incl, 31);
   s_base[lane] = mybase;
   if (lane == 31) s_base[32] = M;
+  for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
   __syncwarp();
 
   // ---- phase B: the warp's M contacts, 32 per round
@@ -739,11 +784,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
     const uint32_t m = r0 + lane;
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (m < M) {
-      // owner = last lane whose base <= m
-      uint32_t ow = 0;
-#pragma unroll
-      for (uint32_t step = 16; step > 0; step >>= 1)
-        if (s_base[ow + step] <= m) ow += step;
+      const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
       const uint32_t t = s_cq[k * 32 + ow];
       Own po;
@@ -763,12 +804,14 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
           const uint32_t pid = __float_as_uint(WQ.w);
           f3 dold = mk(0.f, 0.f, 0.f);
           const uint32_t no = s_nold[ow];
-          for (uint32_t kk = 0; kk < no; ++kk)
-            if (s_oldpid[kk * 32 + ow] == pid) {
-              const float4 h = __ldg(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
-              dold = mk(h.x, h.y, h.z);
-              break;
-            }
+          // persisting contacts usually keep their list position: try k first
+          uint32_t kk = (k < no && s_oldpid[k * 32 + ow] == pid) ? k : 0xFFFFFFFFu;
+          for (uint32_t x = 0; kk == 0xFFFFFFFFu && x < no; ++x)
+            if (s_oldpid[x * 32 + ow] == pid) kk = x;
+          if (kk != 0xFFFFFFFFu) {
+            const float4 h = __ldcg(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
+            dold = mk(h.x, h.y, h.z);
+          }
           f3 dnew;
           eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
           b.hist_out[(size_t)k * N + j0 + ow] =
@@ -801,7 +844,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   auto lookup = [&](uint32_t pid) -> f3 {
     for (uint32_t kk = 0; kk < n_old; ++kk)
       if (s_oldpid[kk * 32 + lane] == pid) {
-        const float4 h = __ldg(&b.hist_in[(size_t)kk * N + s]);
+        const float4 h = __ldcg(&b.hist_in[(size_t)kk * N + s]);
         return mk(h.x, h.y, h.z);
       }
     return mk(0.f, 0.f, 0.f);
