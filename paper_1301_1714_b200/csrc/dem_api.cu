@@ -52,7 +52,7 @@ struct dem_handle {
   float4* hist[2] = {};
   uint32_t* cnt[2] = {};
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
-  float4* pos_sorted = nullptr;
+  float4 *pos_sorted = nullptr, *vel_sorted = nullptr, *omg_sorted = nullptr;
   float4 *F = nullptr, *T = nullptr;
   unsigned long long* scan_status[2] = {};
   uint32_t* scan_ctr = nullptr;  // [2]
@@ -151,7 +151,7 @@ void free_buffers(dem_handle* h) {
     h->scan_status[b] = nullptr;
   }
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
-  h->pos_sorted = nullptr;
+  h->pos_sorted = h->vel_sorted = h->omg_sorted = nullptr;
   h->F = h->T = nullptr;
   h->err = nullptr;
   h->cap_n = h->cap_cells = -1;
@@ -173,6 +173,8 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.tmp = h->tmp;
   s.perm = h->perm;
   s.pos_sorted = h->pos_sorted;
+  s.vel_sorted = h->vel_sorted;
+  s.omg_sorted = h->omg_sorted;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -516,7 +518,8 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     }
     ok &= dalloc(h, &h->prank, N) && dalloc(h, &h->count, (size_t)ncells + 1) &&
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
-          dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->scan_ctr, 2) &&
+          dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->vel_sorted, N) &&
+          dalloc(h, &h->omg_sorted, N) && dalloc(h, &h->scan_ctr, 2) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
     if (!ok) {

@@ -65,7 +65,9 @@ struct StepBuffers {
   uint32_t* off;
   uint32_t* tmp;
   uint32_t* perm;
-  float4* pos_sorted;  // (x,y,z,r) gathered into SCM order by k_rank (step 4 for positions)
+  float4* pos_sorted;  // state gathered into SCM order by k_rank: the paper's step 4
+  float4* vel_sorted;  // "reorder all the properties along SCM"
+  float4* omg_sorted;
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;

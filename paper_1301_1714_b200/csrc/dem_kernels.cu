@@ -329,14 +329,16 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------ k_rank -------
-// perm[off[c] + #{t in cell c: tmp[t] < s}] = s, and the position of that
-// particle gathered into sorted order (PAPER.md:125 step 4, for the field the
-// 27-cell candidate loop reads).
+// perm[off[c] + #{t in cell c: tmp[t] < s}] = s, and the particle's properties
+// gathered into sorted order: step 4, "reorder all the properties along SCM"
+// (PAPER.md:125). The sweep then reads its own and its partners' state
+// directly (coalesced), with no SCCM indirection on the candidate path.
 __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
-           const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const DevErr* err) {
+           const float4* __restrict__ pos_in, const float4* __restrict__ vel_in,
+           const float4* __restrict__ omg_in, float4* __restrict__ pos_sorted,
+           float4* __restrict__ vel_sorted, float4* __restrict__ omg_sorted, const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
@@ -353,17 +355,20 @@ __global__ void __launch_bounds__(256)
     a[u] = ok ? __ldg(&off[c[u]]) : 0u;
     e[u] = ok ? __ldg(&off[c[u] + 1]) : 0u;
   }
-  float4 P[kItems];
-#pragma unroll
-  for (int u = 0; u < kItems; ++u)
-    P[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&pos_in[s[u]]) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
     if (base + (int64_t)u * blockDim.x >= n) continue;
     uint32_t r = 0;
     for (uint32_t t = a[u]; t < e[u]; ++t) r += (__ldg(&tmp[t]) < s[u]) ? 1u : 0u;
-    perm[a[u] + r] = s[u];
-    pos_sorted[a[u] + r] = P[u];
+    a[u] += r;  // the sorted slot of s[u]
+  }
+#pragma unroll
+  for (int u = 0; u < kItems; ++u) {
+    if (base + (int64_t)u * blockDim.x >= n) continue;
+    perm[a[u]] = s[u];
+    pos_sorted[a[u]] = __ldcs(&pos_in[s[u]]);
+    vel_sorted[a[u]] = __ldcs(&vel_in[s[u]]);
+    omg_sorted[a[u]] = __ldcs(&omg_in[s[u]]);
   }
 }
 
@@ -577,8 +582,8 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   const uint32_t s = __ldg(&b.perm[j]);
   Own o;
   o.P = __ldg(&b.pos_sorted[j]);
-  o.V = __ldg(&b.vel_in[s]);
-  o.W = __ldg(&b.omg_in[s]);
+  o.V = __ldg(&b.vel_sorted[j]);
+  o.W = __ldg(&b.omg_sorted[j]);
   const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
   auto lookup = [&](uint32_t pid) -> f3 {
     for (uint32_t k = 0; k < n_old; ++k) {
@@ -614,10 +619,9 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
           raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
           continue;
         }
-        const uint32_t q = __ldg(&b.perm[t]);
-        const float4 VQ = __ldg(&b.vel_in[q]);
+        const float4 VQ = __ldg(&b.vel_sorted[t]);
         if (MODEL == 0) {
-          const float4 WQ = __ldg(&b.omg_in[q]);
+          const float4 WQ = __ldg(&b.omg_sorted[t]);
           const uint32_t pid = __float_as_uint(WQ.w);
           f3 Fc, Tc, dnew;
           eval_pair_practical(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
@@ -642,20 +646,33 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 }
 
 // ---- variant 0: warp-cooperative two-phase sweep (default) ----------------
-// Phase A: each lane scans its own 27-cell candidates (sorted positions, one
-// load each) and queues its contacts in shared memory, in candidate order.
+// Staging: the 32 consecutive sorted particles of a warp lie in R (usually 1
+// or 2) rows of the CDG; the union of their 27-cell candidates is 9 contiguous
+// slot ranges per row ([x_min - 1, x_max + 1] of each neighbour row). One lane
+// per row issues those ranges as TMA 1D bulk copies (cp.async.bulk, completion
+// on an mbarrier) into shared memory, so phase A runs from shared memory.
+// Phase A: each lane scans its own candidates (the paper's steps 5-6) and
+// queues its contacts in candidate order.
 // Phase B: the warp's contacts are flattened and dealt round-robin to all 32
 // lanes, so a round evaluates 32 contacts regardless of which particles own
 // them — the divergence of §6 (~12 contacts among ~47
 // candidates leaves 3/4 of a thread-per-particle warp idle) is removed from
 // the expensive part. Each round's results go to shared memory and every
-// owner adds its own contacts in candidate order (deterministic, the oracle's
-// order). Old-history partner ids are staged in shared memory up front.
+// owner adds its own contacts in candidate order (deterministic; the
+// oracle's order). Old-history partner ids are staged in shared memory.
+constexpr uint32_t kStageCap = 512;  // staged candidate positions per warp
+constexpr uint32_t kMaxRows = 4;     // rows per warp that staging handles (else: L1/L2 path)
+
 struct WarpSmemLayout {
-  uint32_t bytes, oldpid, cq, res, own, base, slot, nold;
+  uint32_t bytes, stage, own_state, oldpid, cq, res, own, base, slot, nold, seg_t0, seg_base,
+      mbar;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
-    uint32_t o = 3 * 32 * 16;  // own P, V, W
+    uint32_t o = 0;
+    L.stage = o;
+    o += kStageCap * 16;
+    L.own_state = o;
+    o += 3 * 32 * 16;  // own P, V, W
     L.oldpid = o;
     o += K * 32 * 4;
     L.cq = o;
@@ -670,45 +687,134 @@ struct WarpSmemLayout {
     o += 32 * 4;
     L.nold = o;
     o += 32 * 4;
-    L.bytes = (o + 15u) & ~15u;
+    L.seg_t0 = o;
+    o += kMaxRows * 9 * 4;
+    L.seg_base = o;
+    o += kMaxRows * 9 * 4;
+    L.mbar = o;
+    o += 16;
+    L.bytes = (o + 127u) & ~127u;
     return L;
   }
 };
 constexpr int kSweepWarps = 4;
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
+               : "memory");
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  uint32_t done = 0;
+  while (!done) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
+        "selp.u32 %0, 1, 0, p;\n\t}"
+        : "=r"(done)
+        : "r"(smem_u32(bar)), "r"(parity)
+        : "memory");
+  }
+}
+// TMA 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
+                                         uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// Phase A for one lane: its 27-cell candidates (Eq. 12), ascending cell and
+// slot; STAGED reads positions from the warp's shared-memory copy.
+template <bool STAGED>
+__device__ __forceinline__ void scan_candidates(const StepBuffers& b, const DevGrid& g,
+                                                uint32_t K, uint32_t j, uint32_t c, float4 P,
+                                                const float4* stage, const uint32_t* seg_t0,
+                                                const uint32_t* seg_base, uint32_t myrow,
+                                                uint32_t* s_cq, uint32_t lane, uint32_t& npair,
+                                                bool& overflow) {
+  const int cx = (int)(c % (uint32_t)g.nx);
+  const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
+  const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
+  const int xa = cx > 0 ? cx - 1 : 0;
+  const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
+  const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+  auto push = [&](uint32_t t) {
+    if (npair < K) {
+      s_cq[npair * 32 + lane] = t;
+      ++npair;
+    } else {
+      overflow = true;
+    }
+  };
+#pragma unroll 1
+  for (int q9 = 0; q9 < 9; ++q9) {
+    const int dz = q9 / 3 - 1, dy = q9 % 3 - 1;
+    const int z = cz + dz, y = cy + dy;
+    if (z < 0 || z >= g.nz || y < 0 || y >= g.ny) continue;
+    const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
+    const uint32_t t0 = __ldg(&b.off[row + xa]);
+    const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
+    const float4* src = b.pos_sorted;
+    if (STAGED) src = stage + seg_base[myrow * 9 + q9] - seg_t0[myrow * 9 + q9];
+    for (uint32_t t = t0; t < t1; t += 2) {  // two candidates per iteration
+      const float4 Q0 = STAGED ? src[t] : __ldg(&src[t]);
+      const float4 Q1 = t + 1 < t1 ? (STAGED ? src[t + 1] : __ldg(&src[t + 1])) : far;
+      const bool c0 = in_contact(P, Q0);
+      const bool c1 = in_contact(P, Q1);
+      if (c0 && t != j) push(t);
+      if (c1 && t + 1 != j) push(t + 1);
+    }
+  }
+}
+
 template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, DevGrid g,
                                                                  DevPhys ph, uint32_t N,
                                                                  uint32_t K) {
-  extern __shared__ __align__(16) uint8_t smem_raw[];
+  extern __shared__ __align__(128) uint8_t smem_raw[];
   if (ld_volatile(&b.err->code) != 0u) return;
   const WarpSmemLayout L = WarpSmemLayout::make(K);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
-  float4* sP = reinterpret_cast<float4*>(ws);
+  float4* stage = reinterpret_cast<float4*>(ws + L.stage);
+  float4* sP = reinterpret_cast<float4*>(ws + L.own_state);
   float4* sV = sP + 32;
   float4* sW = sV + 32;
   uint32_t* s_oldpid = reinterpret_cast<uint32_t*>(ws + L.oldpid);  // [k*32 + lane]
   uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);          // [k*32 + lane]
   float* s_res = reinterpret_cast<float*>(ws + L.res);              // [6][32]
+  uint8_t* s_own = ws + L.own;                                      // owner of each contact
   uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);      // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
-  uint8_t* s_own = ws + L.own;  // owner lane of each flattened contact
+  uint32_t* seg_t0 = reinterpret_cast<uint32_t*>(ws + L.seg_t0);
+  uint32_t* seg_base = reinterpret_cast<uint32_t*>(ws + L.seg_base);
+  uint64_t* mbar = reinterpret_cast<uint64_t*>(ws + L.mbar);
 
   const uint32_t j0 = (blockIdx.x * kSweepWarps + warp) * 32u;
   const uint32_t j = j0 + lane;
   const bool valid = j < N;
   if (j0 >= N) return;  // whole warp past the end
 
-  // ---- phase 0: own particle (step 4 gather through SCCM) and old history ids
-  const uint32_t s = valid ? __ldg(&b.perm[j]) : 0u;
+  // ---- phase 0: own particle (already in sorted order) and old history ids
+  const uint32_t s = valid ? __ldcs(&b.perm[j]) : 0u;
   Own o;
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const uint32_t c = valid ? __ldcg(&b.key_in[s]) : 0u;
-  const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcg(&b.cnt_in[s]), K) : 0u;
+  o.V = valid ? __ldg(&b.vel_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
+  o.W = valid ? __ldg(&b.omg_sorted[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  const uint32_t c = valid ? __ldcs(&b.key_in[s]) : 0u;
+  const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
   sP[lane] = o.P;
   sV[lane] = o.V;
   sW[lane] = o.W;
@@ -726,43 +832,82 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
     }
   }
 
-  // ---- phase A: candidates of the 27 cells (Eq. 12), ascending cell and slot
+  // ---- staging: rows of the warp, their 9 neighbour slot ranges, TMA copies
+  const uint32_t cxu = c % (uint32_t)g.nx;
+  const uint32_t rowkey = valid ? c / (uint32_t)g.nx : 0xFFFFFFFFu;  // (y, z) row id
+  const uint32_t prevkey = __shfl_up_sync(0xffffffffu, rowkey, 1);
+  const bool row_start = valid && (lane == 0 || rowkey != prevkey);
+  const uint32_t starts = __ballot_sync(0xffffffffu, row_start);
+  const uint32_t R = __popc(starts);
+  const uint32_t myrow = valid ? (uint32_t)__popc(starts & (lanemask_lt() | (1u << lane))) - 1u : 0u;
+  const uint32_t nextkey = __shfl_down_sync(0xffffffffu, rowkey, 1);
+  const bool row_end = valid && (lane == 31 || nextkey != rowkey);
+  // x extent of each row: start lane has x_min, end lane has x_max
+  const uint32_t endmask = __ballot_sync(0xffffffffu, row_end);
+  uint32_t stage_bytes_row = 0;
+  bool staged = R <= kMaxRows;
+  // x_max per lane via shuffle from the end lane of its row (all lanes participate)
+  const uint32_t my_end = valid ? (uint32_t)(__ffs(endmask & ~((1u << lane) - 1u)) - 1) : lane;
+  const uint32_t xmax_row = __shfl_sync(0xffffffffu, cxu, my_end);
+  uint32_t seglen[9];
+  if (staged && row_start) {
+    const int ry = (int)(rowkey % (uint32_t)g.ny), rz = (int)(rowkey / (uint32_t)g.ny);
+    const int xa = cxu > 0 ? (int)cxu - 1 : 0;
+    const int xb = (int)xmax_row < g.nx - 1 ? (int)xmax_row + 1 : g.nx - 1;
+#pragma unroll
+    for (int q9 = 0; q9 < 9; ++q9) {
+      const int z = rz + q9 / 3 - 1, y = ry + q9 % 3 - 1;
+      uint32_t t0 = 0, t1 = 0;
+      if (z >= 0 && z < g.nz && y >= 0 && y < g.ny) {
+        const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
+        t0 = __ldg(&b.off[row + xa]);
+        t1 = __ldg(&b.off[row + xb + 1]);
+      }
+      seg_t0[myrow * 9 + q9] = t0;
+      seglen[q9] = t1 - t0;
+      stage_bytes_row += (t1 - t0) * 16u;
+    }
+  }
+  // exclusive scan of the rows' staged bytes -> base of each row in `stage`
+  uint32_t incl_b = stage_bytes_row;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl_b, d);
+    if (lane >= (uint32_t)d) incl_b += v;
+  }
+  const uint32_t total_bytes = __shfl_sync(0xffffffffu, incl_b, 31);
+  staged = staged && total_bytes <= kStageCap * 16u;
+  if (staged) {
+    if (lane == 0) {
+      mbar_init(mbar, 1);
+      mbar_arrive_expect_tx(mbar, total_bytes);
+    }
+    __syncwarp();
+    if (row_start) {
+      uint32_t off_b = incl_b - stage_bytes_row;
+#pragma unroll
+      for (int q9 = 0; q9 < 9; ++q9) {
+        seg_base[myrow * 9 + q9] = off_b / 16u;
+        if (seglen[q9])
+          bulk_g2s(reinterpret_cast<uint8_t*>(stage) + off_b,
+                   b.pos_sorted + seg_t0[myrow * 9 + q9], seglen[q9] * 16u, mbar);
+        off_b += seglen[q9] * 16u;
+      }
+    }
+    __syncwarp();
+    mbar_wait(mbar, 0);
+  }
+
+  // ---- phase A: candidates -> per-lane contact queue
   uint32_t npair = 0;
   bool overflow = false;
   if (valid) {
-    const int cx = (int)(c % (uint32_t)g.nx);
-    const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
-    const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
-    const int xa = cx > 0 ? cx - 1 : 0;
-    const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
-    const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
-    auto push = [&](uint32_t t) {
-      if (npair < K) {
-        s_cq[npair * 32 + lane] = t;
-        ++npair;
-      } else {
-        overflow = true;
-      }
-    };
-    for (int dz = -1; dz <= 1; ++dz) {
-      const int z = cz + dz;
-      if (z < 0 || z >= g.nz) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int y = cy + dy;
-        if (y < 0 || y >= g.ny) continue;
-        const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
-        const uint32_t t0 = __ldg(&b.off[row + xa]);
-        const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
-        for (uint32_t t = t0; t < t1; t += 2) {  // two candidates per iteration
-          const float4 Q0 = __ldg(&b.pos_sorted[t]);
-          const float4 Q1 = t + 1 < t1 ? __ldg(&b.pos_sorted[t + 1]) : far;
-          const bool c0 = in_contact(o.P, Q0);
-          const bool c1 = in_contact(o.P, Q1);
-          if (c0 && t != j) push(t);
-          if (c1 && t + 1 != j) push(t + 1);
-        }
-      }
-    }
+    if (staged)
+      scan_candidates<true>(b, g, K, j, c, o.P, stage, seg_t0, seg_base, myrow, s_cq, lane, npair,
+                            overflow);
+    else
+      scan_candidates<false>(b, g, K, j, c, o.P, stage, seg_t0, seg_base, myrow, s_cq, lane,
+                             npair, overflow);
   }
   // exclusive warp scan of the per-lane contact counts
   uint32_t incl = npair;
@@ -792,34 +937,31 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
       po.V = sV[ow];
       po.W = sW[ow];
       const float4 Q = __ldg(&b.pos_sorted[t]);
+      const float4 VQ = __ldg(&b.vel_sorted[t]);
+      const float4 WQ = MODEL == 0 ? __ldg(&b.omg_sorted[t]) : make_float4(0.f, 0.f, 0.f, 0.f);
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
         raise_error(b.err, 9u, j0 + ow, __float_as_uint(po.W.w));
-      } else {
-        const uint32_t q = __ldg(&b.perm[t]);
-        const float4 VQ = __ldg(&b.vel_in[q]);
-        if (MODEL == 0) {
-          const float4 WQ = __ldg(&b.omg_in[q]);
-          const uint32_t pid = __float_as_uint(WQ.w);
-          f3 dold = mk(0.f, 0.f, 0.f);
-          const uint32_t no = s_nold[ow];
-          // persisting contacts usually keep their list position: try k first
-          uint32_t kk = (k < no && s_oldpid[k * 32 + ow] == pid) ? k : 0xFFFFFFFFu;
-          for (uint32_t x = 0; kk == 0xFFFFFFFFu && x < no; ++x)
-            if (s_oldpid[x * 32 + ow] == pid) kk = x;
-          if (kk != 0xFFFFFFFFu) {
-            const float4 h = __ldcg(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
-            dold = mk(h.x, h.y, h.z);
-          }
-          f3 dnew;
-          eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
-          b.hist_out[(size_t)k * N + j0 + ow] =
-              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
-        } else {
-          const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
-          Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+      } else if (MODEL == 0) {
+        const uint32_t pid = __float_as_uint(WQ.w);
+        f3 dold = mk(0.f, 0.f, 0.f);
+        const uint32_t no = s_nold[ow];
+        // persisting contacts usually keep their list position: try k first
+        uint32_t kk = (k < no && s_oldpid[k * 32 + ow] == pid) ? k : 0xFFFFFFFFu;
+        for (uint32_t x = 0; kk == 0xFFFFFFFFu && x < no; ++x)
+          if (s_oldpid[x * 32 + ow] == pid) kk = x;
+        if (kk != 0xFFFFFFFFu) {
+          const float4 h = __ldcs(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
+          dold = mk(h.x, h.y, h.z);
         }
+        f3 dnew;
+        eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+        __stcs(&b.hist_out[(size_t)k * N + j0 + ow],
+               make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
+      } else {
+        const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
+        Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
       }
     }
     s_res[0 * 32 + lane] = Fc.x;
@@ -844,7 +986,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   auto lookup = [&](uint32_t pid) -> f3 {
     for (uint32_t kk = 0; kk < n_old; ++kk)
       if (s_oldpid[kk * 32 + lane] == pid) {
-        const float4 h = __ldcg(&b.hist_in[(size_t)kk * N + s]);
+        const float4 h = __ldcs(&b.hist_in[(size_t)kk * N + s]);
         return mk(h.x, h.y, h.z);
       }
     return mk(0.f, 0.f, 0.f);
@@ -984,8 +1126,9 @@ int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t nt
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
-  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm,
-                                                           b.pos_in, b.pos_sorted, b.err);
+  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(
+      n, b.key_in, b.off, b.tmp, b.perm, b.pos_in, b.vel_in, b.omg_in, b.pos_sorted, b.vel_sorted,
+      b.omg_sorted, b.err);
   return K_RANK;
 }
 
