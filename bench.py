@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-steps/sec (ms/step) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "particle-steps/s"
-KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other")
+KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect")
 
 
 def load_peaks():

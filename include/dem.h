@@ -160,7 +160,8 @@ typedef struct {
 
 /* Kernel indices of dem_stats.kernel_ms. */
 enum dem_kernel { DEM_K_HASH = 0, DEM_K_SCAN = 1, DEM_K_SCATTER = 2, DEM_K_RANK = 3,
-                  DEM_K_SWEEP = 4, DEM_K_OTHER = 5 };
+                  DEM_K_SWEEP = 4 /* force + integrate */, DEM_K_OTHER = 5,
+                  DEM_K_DETECT = 6 /* candidates -> contact lists */ };
 
 /* Create a handle: validates params (DEM_EINVAL/DEM_EABI), selects the device
  * and stream. Grid and buffers are sized by dem_set_particles. *out = NULL on

@@ -52,7 +52,8 @@ struct dem_handle {
   float4* hist[2] = {};
   uint32_t* cnt[2] = {};
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
-  float4 *pos_sorted = nullptr, *vel_sorted = nullptr, *omg_sorted = nullptr;
+  float4* pos_sorted = nullptr;
+  uint32_t *clist = nullptr, *ccount = nullptr;
   float4 *F = nullptr, *T = nullptr;
   unsigned long long* scan_status[2] = {};
   uint32_t* scan_ctr = nullptr;  // [2]
@@ -151,7 +152,8 @@ void free_buffers(dem_handle* h) {
     h->scan_status[b] = nullptr;
   }
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
-  h->pos_sorted = h->vel_sorted = h->omg_sorted = nullptr;
+  h->pos_sorted = nullptr;
+  h->clist = h->ccount = nullptr;
   h->F = h->T = nullptr;
   h->err = nullptr;
   h->cap_n = h->cap_cells = -1;
@@ -173,8 +175,8 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.tmp = h->tmp;
   s.perm = h->perm;
   s.pos_sorted = h->pos_sorted;
-  s.vel_sorted = h->vel_sorted;
-  s.omg_sorted = h->omg_sorted;
+  s.clist = h->clist;
+  s.ccount = h->ccount;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -189,7 +191,11 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   return s;
 }
 
-// Enqueue one step from parity b: scan, scatter, rank, sweep.
+int kernels_per_step(const dem_handle* h) {
+  return (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 4 : 5;
+}
+
+// Enqueue one step from parity b: scan, scatter, rank, (detect,) sweep.
 // `ev` (profiling) receives an event pair around each kernel.
 int enqueue_step(dem_handle* h, int b, bool profile) {
   const StepBuffers s = step_buffers(h, b);
@@ -225,9 +231,15 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   rec(K_RANK, true);
   launch_rank(h->stream, h->n, s);
   rec(K_RANK, false);
+  const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : 0;
+  if (variant == 0) {
+    rec(K_DETECT, true);
+    launch_detect(h->stream, h->n, h->K, s, h->g);
+    rec(K_DETECT, false);
+    h->launches += 1;
+  }
   rec(K_SWEEP, true);
-  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph,
-               (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : 0);
+  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph, variant);
   rec(K_SWEEP, false);
   h->launches += 4;
   cudaError_t e = cudaGetLastError();
@@ -518,8 +530,8 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     }
     ok &= dalloc(h, &h->prank, N) && dalloc(h, &h->count, (size_t)ncells + 1) &&
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
-          dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->vel_sorted, N) &&
-          dalloc(h, &h->omg_sorted, N) && dalloc(h, &h->scan_ctr, 2) &&
+          dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->clist, N * h->K) &&
+          dalloc(h, &h->ccount, N) && dalloc(h, &h->scan_ctr, 2) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
     if (!ok) {
@@ -554,6 +566,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   launch_pack(st, n, in, g, h->pos[0], h->vel[0], h->omg[0], h->key[0], h->count, h->prank);
   h->launches += (n > 0) ? 2 : 1;
   // 6. ids: unique; dense (a permutation of 0..n-1) enables ORDER_ID and set_contacts
+  sweep_prepare(h->K);
   h->ids_dense = false;
   if (n > 0) {
     uint32_t* seen = nullptr;
@@ -643,13 +656,13 @@ int dem_step(dem_handle* h, int64_t nsteps) {
     while (left >= 2) {
       CUDA_TRY(h, cudaGraphLaunch(h->g2[h->cur], h->stream));
       h->graph_launches++;
-      h->launches += 8;
+      h->launches += 2 * kernels_per_step(h);
       left -= 2;
     }
     if (left) {
       CUDA_TRY(h, cudaGraphLaunch(h->g1[h->cur], h->stream));
       h->graph_launches++;
-      h->launches += 4;
+      h->launches += kernels_per_step(h);
       h->cur ^= 1;
     }
   }

@@ -65,9 +65,9 @@ struct StepBuffers {
   uint32_t* off;
   uint32_t* tmp;
   uint32_t* perm;
-  float4* pos_sorted;  // state gathered into SCM order by k_rank: the paper's step 4
-  float4* vel_sorted;  // "reorder all the properties along SCM"
-  float4* omg_sorted;
+  float4* pos_sorted;  // (x,y,z,r) gathered into SCM order by k_rank (step 4, positions)
+  uint32_t* clist;     // contacts found by k_detect: clist[k*N + j] = partner's sorted slot
+  uint32_t* ccount;    // number of pair contacts of sorted slot j (K+1: overflow)
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;
@@ -81,7 +81,8 @@ struct StepBuffers {
   DevErr* err;
 };
 
-enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5 };
+enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5,
+                K_DETECT = 6 };
 
 // ---- launchers (dem_kernels.cu) -------------------------------------------
 // Every launcher enqueues exactly one kernel on `st` and returns its id.
@@ -113,8 +114,12 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
-// variant 0: warp-cooperative two-phase sweep (default); 1: one thread per
-// particle for the whole step (the paper's mapping; ablation)
+// Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
+// warp-cooperative). Variant 1 (ablation): one thread per particle for the
+// whole step (the paper's mapping) in a single kernel.
+void sweep_prepare(uint32_t K);  // host: kernel attributes (call outside stream capture)
+int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
+                  const DevGrid& g);
 int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
                  const StepBuffers& b, const DevGrid& g, const DevPhys& ph, int variant);
 

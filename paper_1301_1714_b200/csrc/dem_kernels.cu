@@ -329,16 +329,14 @@ __global__ void __launch_bounds__(256)
 }
 
 // ------------------------------------------------------------ k_rank -------
-// perm[off[c] + #{t in cell c: tmp[t] < s}] = s, and the particle's properties
-// gathered into sorted order: step 4, "reorder all the properties along SCM"
-// (PAPER.md:125). The sweep then reads its own and its partners' state
-// directly (coalesced), with no SCCM indirection on the candidate path.
+// perm[off[c] + #{t in cell c: tmp[t] < s}] = s, and the particle's position
+// gathered into sorted order (PAPER.md:125 step 4, for the field the 27-cell
+// candidate loop reads; velocities and spins are read through SCCM).
 __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
-           const float4* __restrict__ pos_in, const float4* __restrict__ vel_in,
-           const float4* __restrict__ omg_in, float4* __restrict__ pos_sorted,
-           float4* __restrict__ vel_sorted, float4* __restrict__ omg_sorted, const DevErr* err) {
+           const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
+           const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
@@ -355,20 +353,17 @@ __global__ void __launch_bounds__(256)
     a[u] = ok ? __ldg(&off[c[u]]) : 0u;
     e[u] = ok ? __ldg(&off[c[u] + 1]) : 0u;
   }
+  float4 P[kItems];
+#pragma unroll
+  for (int u = 0; u < kItems; ++u)
+    P[u] = base + (int64_t)u * blockDim.x < n ? __ldcs(&pos_in[s[u]]) : make_float4(0.f, 0.f, 0.f, 0.f);
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
     if (base + (int64_t)u * blockDim.x >= n) continue;
     uint32_t r = 0;
     for (uint32_t t = a[u]; t < e[u]; ++t) r += (__ldg(&tmp[t]) < s[u]) ? 1u : 0u;
-    a[u] += r;  // the sorted slot of s[u]
-  }
-#pragma unroll
-  for (int u = 0; u < kItems; ++u) {
-    if (base + (int64_t)u * blockDim.x >= n) continue;
-    perm[a[u]] = s[u];
-    pos_sorted[a[u]] = __ldcs(&pos_in[s[u]]);
-    vel_sorted[a[u]] = __ldcs(&vel_in[s[u]]);
-    omg_sorted[a[u]] = __ldcs(&omg_in[s[u]]);
+    perm[a[u] + r] = s[u];
+    pos_sorted[a[u] + r] = P[u];
   }
 }
 
@@ -582,8 +577,8 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   const uint32_t s = __ldg(&b.perm[j]);
   Own o;
   o.P = __ldg(&b.pos_sorted[j]);
-  o.V = __ldg(&b.vel_sorted[j]);
-  o.W = __ldg(&b.omg_sorted[j]);
+  o.V = __ldg(&b.vel_in[s]);
+  o.W = __ldg(&b.omg_in[s]);
   const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
   auto lookup = [&](uint32_t pid) -> f3 {
     for (uint32_t k = 0; k < n_old; ++k) {
@@ -619,9 +614,10 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
           raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
           continue;
         }
-        const float4 VQ = __ldg(&b.vel_sorted[t]);
+        const uint32_t q = __ldg(&b.perm[t]);
+        const float4 VQ = __ldg(&b.vel_in[q]);
         if (MODEL == 0) {
-          const float4 WQ = __ldg(&b.omg_sorted[t]);
+          const float4 WQ = __ldg(&b.omg_in[q]);
           const uint32_t pid = __float_as_uint(WQ.w);
           f3 Fc, Tc, dnew;
           eval_pair_practical(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
@@ -645,38 +641,75 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, ncnt, overflow, lookup);
 }
 
-// ---- variant 0: warp-cooperative two-phase sweep (default) ----------------
-// Staging: the 32 consecutive sorted particles of a warp lie in R (usually 1
-// or 2) rows of the CDG; the union of their 27-cell candidates is 9 contiguous
-// slot ranges per row ([x_min - 1, x_max + 1] of each neighbour row). One lane
-// per row issues those ranges as TMA 1D bulk copies (cp.async.bulk, completion
-// on an mbarrier) into shared memory, so phase A runs from shared memory.
-// Phase A: each lane scans its own candidates (the paper's steps 5-6) and
-// queues its contacts in candidate order.
-// Phase B: the warp's contacts are flattened and dealt round-robin to all 32
-// lanes, so a round evaluates 32 contacts regardless of which particles own
-// them — the divergence of §6 (~12 contacts among ~47
-// candidates leaves 3/4 of a thread-per-particle warp idle) is removed from
-// the expensive part. Each round's results go to shared memory and every
-// owner adds its own contacts in candidate order (deterministic; the
-// oracle's order). Old-history partner ids are staged in shared memory.
-constexpr uint32_t kStageCap = 512;  // staged candidate positions per warp
-constexpr uint32_t kMaxRows = 4;     // rows per warp that staging handles (else: L1/L2 path)
+// ---- default path: k_detect (steps 5-6) then k_force (steps 7-8, 1) -------
+// k_detect: one light thread per sorted particle scans its 27-cell candidates
+// (Eq. 12: 9 contiguous slot ranges of sorted positions, the 18 row bounds
+// loaded up front) with the exact predicate (R14) and writes its contact list
+// clist[k*N + j] (partner sorted slots, candidate order). Few registers, so
+// the SM keeps many warps in flight to hide the neighbour-row latency.
+#ifndef DEM_DETECT_UNROLL
+#define DEM_DETECT_UNROLL 2
+#endif
+__global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32_t N, uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const float4 P = __ldg(&b.pos_sorted[j]);
+  // own cell: the step-2 hash of the own position (identical to CM by construction)
+  const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
+  const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
+  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz);
+  const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
+  const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
+  uint32_t t0[9], t1[9];
+#pragma unroll
+  for (int q9 = 0; q9 < 9; ++q9) {  // all 18 row bounds in flight at once
+    const int z = cz + q9 / 3 - 1, y = cy + q9 % 3 - 1;
+    const bool in = z >= 0 && z < g.nz && y >= 0 && y < g.ny;
+    const uint32_t row = in ? ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx : 0u;
+    t0[q9] = in ? __ldg(&b.off[row + xa]) : 0u;
+    t1[q9] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
+  }
+  const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+  uint32_t npair = 0;
+#pragma unroll
+  for (int q9 = 0; q9 < 9; ++q9) {
+    for (uint32_t t = t0[q9]; t < t1[q9]; t += DEM_DETECT_UNROLL) {
+      float4 Q[DEM_DETECT_UNROLL];
+#pragma unroll
+      for (int u = 0; u < DEM_DETECT_UNROLL; ++u)
+        Q[u] = t + u < t1[q9] ? __ldg(&b.pos_sorted[t + u]) : far;
+#pragma unroll
+      for (int u = 0; u < DEM_DETECT_UNROLL; ++u) {
+        if (in_contact(P, Q[u]) && t + u != j) {
+          if (npair < K) __stcg(&b.clist[(size_t)npair * N + j], t + u);
+          ++npair;
+        }
+      }
+    }
+  }
+  __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
+}
 
+// k_force: warp per 32 consecutive sorted particles. The warp's contacts are
+// flattened and dealt round-robin to all 32 lanes, so a round evaluates 32
+// contacts (Eqs. 2-10) regardless of which particles own them — the
+// divergence of §6 (~12 contacts among ~47 candidates
+// leaves 3/4 of a thread-per-particle warp idle) is removed from the
+// expensive part. Each round's results go to shared memory and every owner
+// adds its own contacts in candidate order (deterministic; the oracle's
+// order). Partner slots are translated to old slots once per warp, so a round
+// issues its partner-state and history loads together. δ_t,old is read at the
+// contact's own list index first (persisting contacts keep their position).
 struct WarpSmemLayout {
-  uint32_t bytes, stage, own_state, oldpid, cq, res, own, base, slot, nold, seg_t0, seg_base,
-      mbar;
+  uint32_t bytes, own_state, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
     uint32_t o = 0;
-    L.stage = o;
-    o += kStageCap * 16;
     L.own_state = o;
     o += 3 * 32 * 16;  // own P, V, W
-    L.oldpid = o;
-    o += K * 32 * 4;
     L.cq = o;
-    o += K * 32 * 4;
+    o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
     o += 32 * 6 * 4;
     L.own = o;
@@ -687,227 +720,79 @@ struct WarpSmemLayout {
     o += 32 * 4;
     L.nold = o;
     o += 32 * 4;
-    L.seg_t0 = o;
-    o += kMaxRows * 9 * 4;
-    L.seg_base = o;
-    o += kMaxRows * 9 * 4;
-    L.mbar = o;
-    o += 16;
-    L.bytes = (o + 127u) & ~127u;
+    L.bytes = (o + 15u) & ~15u;
     return L;
   }
 };
 constexpr int kSweepWarps = 4;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return (uint32_t)__cvta_generic_to_shared(p);
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count)
-               : "memory");
-  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-}
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  uint32_t done = 0;
-  while (!done) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n\t"
-        "selp.u32 %0, 1, 0, p;\n\t}"
-        : "=r"(done)
-        : "r"(smem_u32(bar)), "r"(parity)
-        : "memory");
+// δ_t,old of partner `pid` in the old list of old slot s (n entries): try
+// index k first, then scan (R10: absent -> 0).
+__device__ __forceinline__ f3 old_history(const float4* __restrict__ hist_in, uint32_t N,
+                                          uint32_t s, uint32_t n, uint32_t k, uint32_t pid) {
+  if (k < n) {
+    const float4 h = __ldcs(&hist_in[(size_t)k * N + s]);
+    if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
   }
-}
-// TMA 1D bulk copy global -> shared, completion counted on `bar` (bytes % 16 == 0)
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes,
-                                         uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
+  for (uint32_t x = 0; x < n; ++x) {
+    if (x == k) continue;
+    const float4 h = __ldcs(&hist_in[(size_t)x * N + s]);
+    if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
+  }
+  return mk(0.f, 0.f, 0.f);
 }
 
-// Phase A for one lane: its 27-cell candidates (Eq. 12), ascending cell and
-// slot; STAGED reads positions from the warp's shared-memory copy.
-template <bool STAGED>
-__device__ __forceinline__ void scan_candidates(const StepBuffers& b, const DevGrid& g,
-                                                uint32_t K, uint32_t j, uint32_t c, float4 P,
-                                                const float4* stage, const uint32_t* seg_t0,
-                                                const uint32_t* seg_base, uint32_t myrow,
-                                                uint32_t* s_cq, uint32_t lane, uint32_t& npair,
-                                                bool& overflow) {
-  const int cx = (int)(c % (uint32_t)g.nx);
-  const int cy = (int)((c / (uint32_t)g.nx) % (uint32_t)g.ny);
-  const int cz = (int)(c / ((uint32_t)g.nx * (uint32_t)g.ny));
-  const int xa = cx > 0 ? cx - 1 : 0;
-  const int xb = cx < g.nx - 1 ? cx + 1 : g.nx - 1;
-  const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
-  auto push = [&](uint32_t t) {
-    if (npair < K) {
-      s_cq[npair * 32 + lane] = t;
-      ++npair;
-    } else {
-      overflow = true;
-    }
-  };
-#pragma unroll 1
-  for (int q9 = 0; q9 < 9; ++q9) {
-    const int dz = q9 / 3 - 1, dy = q9 % 3 - 1;
-    const int z = cz + dz, y = cy + dy;
-    if (z < 0 || z >= g.nz || y < 0 || y >= g.ny) continue;
-    const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
-    const uint32_t t0 = __ldg(&b.off[row + xa]);
-    const uint32_t t1 = __ldg(&b.off[row + xb + 1]);
-    const float4* src = b.pos_sorted;
-    if (STAGED) src = stage + seg_base[myrow * 9 + q9] - seg_t0[myrow * 9 + q9];
-    for (uint32_t t = t0; t < t1; t += 2) {  // two candidates per iteration
-      const float4 Q0 = STAGED ? src[t] : __ldg(&src[t]);
-      const float4 Q1 = t + 1 < t1 ? (STAGED ? src[t + 1] : __ldg(&src[t + 1])) : far;
-      const bool c0 = in_contact(P, Q0);
-      const bool c1 = in_contact(P, Q1);
-      if (c0 && t != j) push(t);
-      if (c1 && t + 1 != j) push(t + 1);
-    }
-  }
-}
-
+#ifndef DEM_SWEEP_MINB
+#define DEM_SWEEP_MINB 8
+#endif
 template <int MODEL, bool DIAG>
-__global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, DevGrid g,
-                                                                 DevPhys ph, uint32_t N,
-                                                                 uint32_t K) {
-  extern __shared__ __align__(128) uint8_t smem_raw[];
+__global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
+    k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+  extern __shared__ __align__(16) uint8_t smem_raw[];
   if (ld_volatile(&b.err->code) != 0u) return;
   const WarpSmemLayout L = WarpSmemLayout::make(K);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
-  float4* stage = reinterpret_cast<float4*>(ws + L.stage);
   float4* sP = reinterpret_cast<float4*>(ws + L.own_state);
   float4* sV = sP + 32;
   float4* sW = sV + 32;
-  uint32_t* s_oldpid = reinterpret_cast<uint32_t*>(ws + L.oldpid);  // [k*32 + lane]
-  uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);          // [k*32 + lane]
-  float* s_res = reinterpret_cast<float*>(ws + L.res);              // [6][32]
-  uint8_t* s_own = ws + L.own;                                      // owner of each contact
-  uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);      // [33]
+  uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
+  float* s_res = reinterpret_cast<float*>(ws + L.res);          // [6][32]
+  uint8_t* s_own = ws + L.own;                                  // owner of each contact
+  uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);  // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
-  uint32_t* seg_t0 = reinterpret_cast<uint32_t*>(ws + L.seg_t0);
-  uint32_t* seg_base = reinterpret_cast<uint32_t*>(ws + L.seg_base);
-  uint64_t* mbar = reinterpret_cast<uint64_t*>(ws + L.mbar);
 
   const uint32_t j0 = (blockIdx.x * kSweepWarps + warp) * 32u;
   const uint32_t j = j0 + lane;
   const bool valid = j < N;
   if (j0 >= N) return;  // whole warp past the end
 
-  // ---- phase 0: own particle (already in sorted order) and old history ids
+  // ---- own particle (step 4 gather through SCCM) and its contact list
   const uint32_t s = valid ? __ldcs(&b.perm[j]) : 0u;
+  const uint32_t nc = valid ? __ldcs(&b.ccount[j]) : 0u;
+  const bool overflow = nc > K;
+  const uint32_t npair = min(nc, K);
   Own o;
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  o.V = valid ? __ldg(&b.vel_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  o.W = valid ? __ldg(&b.omg_sorted[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
-  const uint32_t c = valid ? __ldcs(&b.key_in[s]) : 0u;
+  o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
+  o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
   sP[lane] = o.P;
   sV[lane] = o.V;
   sW[lane] = o.W;
   s_slot[lane] = s;
   s_nold[lane] = n_old;
-  if (MODEL == 0) {
-    for (uint32_t k0 = 0; k0 < n_old; k0 += 4) {  // four loads in flight per lane
-      float w4[4];
+  // partner sorted slots -> old slots (SCCM), four lookups in flight per lane
+  for (uint32_t k0 = 0; k0 < npair; k0 += 4) {
+    uint32_t t4[4], q4[4];
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        w4[u] = (k0 + u < n_old) ? __ldcg(&b.hist_in[(size_t)(k0 + u) * N + s].w) : 0.f;
+    for (int u = 0; u < 4; ++u) t4[u] = k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u;
 #pragma unroll
-      for (int u = 0; u < 4; ++u)
-        if (k0 + u < n_old) s_oldpid[(k0 + u) * 32 + lane] = __float_as_uint(w4[u]);
-    }
-  }
-
-  // ---- staging: rows of the warp, their 9 neighbour slot ranges, TMA copies
-  const uint32_t cxu = c % (uint32_t)g.nx;
-  const uint32_t rowkey = valid ? c / (uint32_t)g.nx : 0xFFFFFFFFu;  // (y, z) row id
-  const uint32_t prevkey = __shfl_up_sync(0xffffffffu, rowkey, 1);
-  const bool row_start = valid && (lane == 0 || rowkey != prevkey);
-  const uint32_t starts = __ballot_sync(0xffffffffu, row_start);
-  const uint32_t R = __popc(starts);
-  const uint32_t myrow = valid ? (uint32_t)__popc(starts & (lanemask_lt() | (1u << lane))) - 1u : 0u;
-  const uint32_t nextkey = __shfl_down_sync(0xffffffffu, rowkey, 1);
-  const bool row_end = valid && (lane == 31 || nextkey != rowkey);
-  // x extent of each row: start lane has x_min, end lane has x_max
-  const uint32_t endmask = __ballot_sync(0xffffffffu, row_end);
-  uint32_t stage_bytes_row = 0;
-  bool staged = R <= kMaxRows;
-  // x_max per lane via shuffle from the end lane of its row (all lanes participate)
-  const uint32_t my_end = valid ? (uint32_t)(__ffs(endmask & ~((1u << lane) - 1u)) - 1) : lane;
-  const uint32_t xmax_row = __shfl_sync(0xffffffffu, cxu, my_end);
-  uint32_t seglen[9];
-  if (staged && row_start) {
-    const int ry = (int)(rowkey % (uint32_t)g.ny), rz = (int)(rowkey / (uint32_t)g.ny);
-    const int xa = cxu > 0 ? (int)cxu - 1 : 0;
-    const int xb = (int)xmax_row < g.nx - 1 ? (int)xmax_row + 1 : g.nx - 1;
+    for (int u = 0; u < 4; ++u) q4[u] = k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u;
 #pragma unroll
-    for (int q9 = 0; q9 < 9; ++q9) {
-      const int z = rz + q9 / 3 - 1, y = ry + q9 % 3 - 1;
-      uint32_t t0 = 0, t1 = 0;
-      if (z >= 0 && z < g.nz && y >= 0 && y < g.ny) {
-        const uint32_t row = ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx;
-        t0 = __ldg(&b.off[row + xa]);
-        t1 = __ldg(&b.off[row + xb + 1]);
-      }
-      seg_t0[myrow * 9 + q9] = t0;
-      seglen[q9] = t1 - t0;
-      stage_bytes_row += (t1 - t0) * 16u;
-    }
-  }
-  // exclusive scan of the rows' staged bytes -> base of each row in `stage`
-  uint32_t incl_b = stage_bytes_row;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl_b, d);
-    if (lane >= (uint32_t)d) incl_b += v;
-  }
-  const uint32_t total_bytes = __shfl_sync(0xffffffffu, incl_b, 31);
-  staged = staged && total_bytes <= kStageCap * 16u;
-  if (staged) {
-    if (lane == 0) {
-      mbar_init(mbar, 1);
-      mbar_arrive_expect_tx(mbar, total_bytes);
-    }
-    __syncwarp();
-    if (row_start) {
-      uint32_t off_b = incl_b - stage_bytes_row;
-#pragma unroll
-      for (int q9 = 0; q9 < 9; ++q9) {
-        seg_base[myrow * 9 + q9] = off_b / 16u;
-        if (seglen[q9])
-          bulk_g2s(reinterpret_cast<uint8_t*>(stage) + off_b,
-                   b.pos_sorted + seg_t0[myrow * 9 + q9], seglen[q9] * 16u, mbar);
-        off_b += seglen[q9] * 16u;
-      }
-    }
-    __syncwarp();
-    mbar_wait(mbar, 0);
-  }
-
-  // ---- phase A: candidates -> per-lane contact queue
-  uint32_t npair = 0;
-  bool overflow = false;
-  if (valid) {
-    if (staged)
-      scan_candidates<true>(b, g, K, j, c, o.P, stage, seg_t0, seg_base, myrow, s_cq, lane, npair,
-                            overflow);
-    else
-      scan_candidates<false>(b, g, K, j, c, o.P, stage, seg_t0, seg_base, myrow, s_cq, lane,
-                             npair, overflow);
+    for (int u = 0; u < 4; ++u)
+      if (k0 + u < npair) s_cq[(k0 + u) * 32 + lane] = q4[u];
   }
   // exclusive warp scan of the per-lane contact counts
   uint32_t incl = npair;
@@ -923,7 +808,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
   for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
   __syncwarp();
 
-  // ---- phase B: the warp's M contacts, 32 per round
+  // ---- the warp's M contacts, 32 per round (step 7)
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
   for (uint32_t r0 = 0; r0 < M; r0 += 32) {
     const uint32_t m = r0 + lane;
@@ -931,30 +816,28 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
     if (m < M) {
       const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
-      const uint32_t t = s_cq[k * 32 + ow];
+      const uint32_t q = s_cq[k * 32 + ow];
+      const uint32_t so = s_slot[ow];
+      const uint32_t no = s_nold[ow];
+      // partner state and the predicted history entry: independent loads
+      const float4 Q = __ldg(&b.pos_in[q]);
+      const float4 VQ = __ldg(&b.vel_in[q]);
+      const float4 WQ = MODEL == 0 ? __ldg(&b.omg_in[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 hk = (MODEL == 0 && k < no) ? __ldcs(&b.hist_in[(size_t)k * N + so])
+                                               : make_float4(0.f, 0.f, 0.f, 0.f);
       Own po;
       po.P = sP[ow];
       po.V = sV[ow];
       po.W = sW[ow];
-      const float4 Q = __ldg(&b.pos_sorted[t]);
-      const float4 VQ = __ldg(&b.vel_sorted[t]);
-      const float4 WQ = MODEL == 0 ? __ldg(&b.omg_sorted[t]) : make_float4(0.f, 0.f, 0.f, 0.f);
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
         raise_error(b.err, 9u, j0 + ow, __float_as_uint(po.W.w));
       } else if (MODEL == 0) {
         const uint32_t pid = __float_as_uint(WQ.w);
-        f3 dold = mk(0.f, 0.f, 0.f);
-        const uint32_t no = s_nold[ow];
-        // persisting contacts usually keep their list position: try k first
-        uint32_t kk = (k < no && s_oldpid[k * 32 + ow] == pid) ? k : 0xFFFFFFFFu;
-        for (uint32_t x = 0; kk == 0xFFFFFFFFu && x < no; ++x)
-          if (s_oldpid[x * 32 + ow] == pid) kk = x;
-        if (kk != 0xFFFFFFFFu) {
-          const float4 h = __ldcs(&b.hist_in[(size_t)kk * N + s_slot[ow]]);
-          dold = mk(h.x, h.y, h.z);
-        }
+        const f3 dold = (k < no && __float_as_uint(hk.w) == pid)
+                            ? mk(hk.x, hk.y, hk.z)
+                            : old_history(b.hist_in, N, so, no, 0xFFFFFFFFu, pid);
         f3 dnew;
         eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
         __stcs(&b.hist_out[(size_t)k * N + j0 + ow],
@@ -983,15 +866,20 @@ __global__ void __launch_bounds__(32 * kSweepWarps) k_sweep_warp(StepBuffers b, 
     __syncwarp();
   }
   if (!valid) return;
-  auto lookup = [&](uint32_t pid) -> f3 {
-    for (uint32_t kk = 0; kk < n_old; ++kk)
-      if (s_oldpid[kk * 32 + lane] == pid) {
-        const float4 h = __ldcs(&b.hist_in[(size_t)kk * N + s]);
-        return mk(h.x, h.y, h.z);
-      }
-    return mk(0.f, 0.f, 0.f);
+  auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
+    return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
   finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
+}
+
+// Set the dynamic shared-memory limit of every k_force instantiation once,
+// outside any stream capture (cudaFuncSetAttribute is not capturable).
+void sweep_prepare(uint32_t K) {
+  const int smem = (int)(WarpSmemLayout::make(K).bytes * kSweepWarps);
+  cudaFuncSetAttribute(k_force<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_force<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_force<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  cudaFuncSetAttribute(k_force<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
 // --------------------------------------------------- introspection ---------
@@ -1126,9 +1014,8 @@ int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t nt
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
-  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(
-      n, b.key_in, b.off, b.tmp, b.perm, b.pos_in, b.vel_in, b.omg_in, b.pos_sorted, b.vel_sorted,
-      b.omg_sorted, b.err);
+  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm,
+                                                           b.pos_in, b.pos_sorted, b.err);
   return K_RANK;
 }
 
@@ -1141,14 +1028,15 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     return;
   }
   const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
-  static bool attr_set[2][2] = {{false, false}, {false, false}};
-  if (smem > 48 * 1024 && !attr_set[MODEL][DIAG]) {
-    cudaFuncSetAttribute(k_sweep_warp<MODEL, DIAG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         (int)smem);
-    attr_set[MODEL][DIAG] = true;
-  }
-  k_sweep_warp<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
+  k_force<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
       b, g, ph, N, K);
+}
+
+int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
+                  const DevGrid& g) {
+  if (n <= 0) return K_DETECT;
+  k_detect<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, K);
+  return K_DETECT;
 }
 
 int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,

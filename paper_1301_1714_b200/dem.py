@@ -18,7 +18,7 @@ from typing import Optional
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libdem.so")
+LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
 
 DEM_ABI_VERSION = 1
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
@@ -28,7 +28,7 @@ DEM_F_TRUNCATE_DT, DEM_F_CLAMP_FN, DEM_F_DIAG, DEM_F_ASYNC, DEM_F_NO_GRAPH = 1, 
 DEM_F_THREAD_PER_PARTICLE = 32
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
-KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other")
+KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect")
 WALL_PID0 = 0xFFFFFFF0
 
 _f = C.c_float
