@@ -647,8 +647,8 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 // loaded up front) with the exact predicate (R14) and writes its contact list
 // clist[k*N + j] (partner sorted slots, candidate order). Few registers, so
 // the SM keeps many warps in flight to hide the neighbour-row latency.
-#ifndef DEM_DETECT_UNROLL
-#define DEM_DETECT_UNROLL 2
+#ifndef DEM_DETECT_PLANES
+#define DEM_DETECT_PLANES 1  // 1: row bounds loaded per z-plane (6 at a time); 0: all 18
 #endif
 __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32_t N, uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
@@ -661,28 +661,38 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
   const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz);
   const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
   const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
-  uint32_t t0[9], t1[9];
-#pragma unroll
-  for (int q9 = 0; q9 < 9; ++q9) {  // all 18 row bounds in flight at once
-    const int z = cz + q9 / 3 - 1, y = cy + q9 % 3 - 1;
-    const bool in = z >= 0 && z < g.nz && y >= 0 && y < g.ny;
-    const uint32_t row = in ? ((uint32_t)z * (uint32_t)g.ny + (uint32_t)y) * (uint32_t)g.nx : 0u;
-    t0[q9] = in ? __ldg(&b.off[row + xa]) : 0u;
-    t1[q9] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
-  }
-  const float4 far = make_float4(1e30f, 1e30f, 1e30f, 0.f);
+  const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
   uint32_t npair = 0;
+  uint32_t* out = b.clist + j;
+#pragma unroll 1
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int z = cz + dz;
+    if (z < 0 || z >= g.nz) continue;
+    uint32_t t0[3], t1[3];
 #pragma unroll
-  for (int q9 = 0; q9 < 9; ++q9) {
-    for (uint32_t t = t0[q9]; t < t1[q9]; t += DEM_DETECT_UNROLL) {
-      float4 Q[DEM_DETECT_UNROLL];
+    for (int r = 0; r < 3; ++r) {  // the plane's 6 row bounds in flight together
+      const int y = cy + r - 1;
+      const bool in = y >= 0 && y < g.ny;
+      const uint32_t row = (uint32_t)z * nxy + (uint32_t)(in ? y : 0) * (uint32_t)g.nx;
+      t0[r] = in ? __ldg(&b.off[row + xa]) : 0u;
+      t1[r] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
+    }
 #pragma unroll
-      for (int u = 0; u < DEM_DETECT_UNROLL; ++u)
-        Q[u] = t + u < t1[q9] ? __ldg(&b.pos_sorted[t + u]) : far;
-#pragma unroll
-      for (int u = 0; u < DEM_DETECT_UNROLL; ++u) {
-        if (in_contact(P, Q[u]) && t + u != j) {
-          if (npair < K) __stcg(&b.clist[(size_t)npair * N + j], t + u);
+    for (int r = 0; r < 3; ++r) {
+#pragma unroll 1
+      for (uint32_t t = t0[r]; t < t1[r]; ++t) {
+        const float4 Q = __ldg(&b.pos_sorted[t]);
+        const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
+        const float d2 = dx * dx + dy * dy + dz2 * dz2;
+        const float S = P.w + Q.w;
+        const float S2 = S * S;
+        bool hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
+        if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
+          const double Sd = (double)P.w + (double)Q.w;
+          hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
+        }
+        if (hit && t != j) {
+          if (npair < K) __stcg(out + (size_t)npair * N, t);
           ++npair;
         }
       }
