@@ -712,12 +712,12 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
 // issues its partner-state and history loads together. δ_t,old is read at the
 // contact's own list index first (persisting contacts keep their position).
 struct WarpSmemLayout {
-  uint32_t bytes, own_state, cq, res, own, base, slot, nold;
+  uint32_t bytes, pf, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
     uint32_t o = 0;
-    L.own_state = o;
-    o += 3 * 32 * 16;  // own P, V, W
+    L.pf = o;
+    o += 2 * 4 * 32 * 16;  // double-buffered prefetch: partner pos, vel, omg, old δ_t entry
     L.cq = o;
     o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
@@ -752,8 +752,26 @@ __device__ __forceinline__ f3 old_history(const float4* __restrict__ hist_in, ui
   return mk(0.f, 0.f, 0.f);
 }
 
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return (uint32_t)__cvta_generic_to_shared(p);
+}
+
+// 16-byte global -> shared asynchronous copy (LDGSTS), L2 only.
+__device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() {
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+template <int N_PENDING>
+__device__ __forceinline__ void cp_async_wait() {
+  asm volatile("cp.async.wait_group %0;" ::"n"(N_PENDING) : "memory");
+}
+
 #ifndef DEM_SWEEP_MINB
-#define DEM_SWEEP_MINB 8
+#define DEM_SWEEP_MINB 7
 #endif
 template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
@@ -763,9 +781,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   const WarpSmemLayout L = WarpSmemLayout::make(K);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
-  float4* sP = reinterpret_cast<float4*>(ws + L.own_state);
-  float4* sV = sP + 32;
-  float4* sW = sV + 32;
+  float4* pf = reinterpret_cast<float4*>(ws + L.pf);            // [buf][field][lane]
   uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
   float* s_res = reinterpret_cast<float*>(ws + L.res);          // [6][32]
   uint8_t* s_own = ws + L.own;                                  // owner of each contact
@@ -788,9 +804,6 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
-  sP[lane] = o.P;
-  sV[lane] = o.V;
-  sW[lane] = o.W;
   s_slot[lane] = s;
   s_nold[lane] = n_old;
   // partner sorted slots -> old slots (SCCM), four lookups in flight per lane
@@ -818,36 +831,71 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
   __syncwarp();
 
-  // ---- the warp's M contacts, 32 per round (step 7)
-  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
-  for (uint32_t r0 = 0; r0 < M; r0 += 32) {
+  // prefetch of round r0's partner state + predicted old δ_t entry into buffer `buf`
+  auto prefetch = [&](uint32_t r0, uint32_t buf) {
     const uint32_t m = r0 + lane;
-    f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (m < M) {
       const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
       const uint32_t q = s_cq[k * 32 + ow];
-      const uint32_t so = s_slot[ow];
-      const uint32_t no = s_nold[ow];
-      // partner state and the predicted history entry: independent loads
-      const float4 Q = __ldg(&b.pos_in[q]);
-      const float4 VQ = __ldg(&b.vel_in[q]);
-      const float4 WQ = MODEL == 0 ? __ldg(&b.omg_in[q]) : make_float4(0.f, 0.f, 0.f, 0.f);
-      const float4 hk = (MODEL == 0 && k < no) ? __ldcs(&b.hist_in[(size_t)k * N + so])
-                                               : make_float4(0.f, 0.f, 0.f, 0.f);
-      Own po;
-      po.P = sP[ow];
-      po.V = sV[ow];
-      po.W = sW[ow];
+      float4* d = pf + buf * 128;
+      cp_async16(&d[lane], &b.pos_in[q]);
+      cp_async16(&d[32 + lane], &b.vel_in[q]);
+      if (MODEL == 0) {
+        cp_async16(&d[64 + lane], &b.omg_in[q]);
+        if (k < s_nold[ow]) cp_async16(&d[96 + lane], &b.hist_in[(size_t)k * N + s_slot[ow]]);
+      }
+    }
+    cp_async_commit();
+  };
+
+  // ---- the warp's M contacts, 32 per round (step 7), next round in flight
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  if (M > 0) prefetch(0, 0);
+  uint32_t buf = 0;
+  for (uint32_t r0 = 0; r0 < M; r0 += 32, buf ^= 1u) {
+    if (r0 + 32 < M) {
+      prefetch(r0 + 32, buf ^ 1u);
+      cp_async_wait<1>();
+    } else {
+      cp_async_wait<0>();
+    }
+    const uint32_t m = r0 + lane;
+    const uint32_t ow = m < M ? s_own[m] : 0u;
+    // owner state from the owner lane's registers (all lanes take part)
+    Own po;
+    po.P.x = __shfl_sync(0xffffffffu, o.P.x, ow);
+    po.P.y = __shfl_sync(0xffffffffu, o.P.y, ow);
+    po.P.z = __shfl_sync(0xffffffffu, o.P.z, ow);
+    po.P.w = __shfl_sync(0xffffffffu, o.P.w, ow);
+    po.V.x = __shfl_sync(0xffffffffu, o.V.x, ow);
+    po.V.y = __shfl_sync(0xffffffffu, o.V.y, ow);
+    po.V.z = __shfl_sync(0xffffffffu, o.V.z, ow);
+    po.V.w = __shfl_sync(0xffffffffu, o.V.w, ow);
+    po.W.x = __shfl_sync(0xffffffffu, o.W.x, ow);
+    po.W.y = __shfl_sync(0xffffffffu, o.W.y, ow);
+    po.W.z = __shfl_sync(0xffffffffu, o.W.z, ow);
+    po.W.w = __shfl_sync(0xffffffffu, o.W.w, ow);
+    f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
+    if (m < M) {
+      const uint32_t k = m - s_base[ow];
+      const float4* d = pf + buf * 128;
+      const float4 Q = d[lane];
+      const float4 VQ = d[32 + lane];
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
         raise_error(b.err, 9u, j0 + ow, __float_as_uint(po.W.w));
       } else if (MODEL == 0) {
+        const float4 WQ = d[64 + lane];
         const uint32_t pid = __float_as_uint(WQ.w);
-        const f3 dold = (k < no && __float_as_uint(hk.w) == pid)
-                            ? mk(hk.x, hk.y, hk.z)
-                            : old_history(b.hist_in, N, so, no, 0xFFFFFFFFu, pid);
+        const uint32_t no = s_nold[ow];
+        f3 dold;
+        const float4 hk = k < no ? d[96 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        if (k < no && __float_as_uint(hk.w) == pid)
+          dold = mk(hk.x, hk.y, hk.z);
+        else
+          dold = old_history(b.hist_in, N, s_slot[ow], no, 0xFFFFFFFFu, pid);
         f3 dnew;
         eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
         __stcs(&b.hist_out[(size_t)k * N + j0 + ow],
