@@ -132,13 +132,18 @@ def describe(sc) -> str:
 
 # ------------------------------------------------- algorithmic bytes -------
 def alg_bytes(model: str, rho_c: float, c_bar: float):
-    """Per particle-step. Sweep kernel: state read+write 96,
-    SCCM read 4, next CM write 4, offsets read 4 rho_c, history counts r+w 8,
-    history entries r+w 32 c_bar. Whole step: 120 + 8 rho_c +
-    32 c_bar (practical), 88 + 8 rho_c (simple)."""
+    """Algorithmic bytes per particle-step.
+
+    k_force (steps 7-8 and 1, the dominant kernel): state read + write 96,
+    SCCM read 4, next CM write 4, history counts r+w 8, history entries r+w
+    32 c_bar -> 112 + 32 c_bar (practical); simple model (no history, no spin
+    update): position + velocity r+w 64, radius/mass/id carried 16, SCCM 4,
+    CM 4 -> 88.
+    Whole step: 120 + 8 rho_c + 32 c_bar (practical),
+    88 + 8 rho_c (simple)."""
     if model == "practical":
-        return 112 + 4 * rho_c + 32 * c_bar, 120 + 8 * rho_c + 32 * c_bar
-    return 80 + 4 * rho_c, 88 + 8 * rho_c
+        return 112 + 32 * c_bar, 120 + 8 * rho_c + 32 * c_bar
+    return 88.0, 88 + 8 * rho_c
 
 
 # ------------------------------------------------------- reference arm -----
@@ -298,7 +303,7 @@ def run_ours(args):
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.model}.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("sweep_dram_bytes_per_launch")
+            traffic = json.load(open(tr_path)).get("force_dram_bytes_per_launch")
         except Exception:
             traffic = None
     line = {
@@ -314,10 +319,10 @@ def run_ours(args):
             "dt": sc.params.dt, "sweep": args.sweep,
         },
         "roofline": {
-            "bound": "hbm", "kernel": "k_sweep", "achieved": achieved, "peak": peak_gbs,
+            "bound": "hbm", "kernel": "k_force", "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
             "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
-            "sweep_ms_avg": sweep_ms, "sweep_share_of_step": kernel_avg["sweep"] / step_kernel_ms
+            "kernel_ms_avg": sweep_ms, "kernel_share_of_step": kernel_avg["sweep"] / step_kernel_ms
             if step_kernel_ms else None,
             "step_alg_bytes_per_particle": b_step,
             "step_frac": b_step * sc.n / (ms_step * 1e-3) / 1e9 / peak_gbs,
@@ -325,8 +330,7 @@ def run_ours(args):
         },
         "kernel_ms_avg": kernel_avg,
         "ms_per_step_graph": ms_graph_max / args.steps,
-        "gpu_launches": int(st["kernel_count"]["sweep"] + st["kernel_count"]["scan"]
-                            + st["kernel_count"]["scatter"] + st["kernel_count"]["rank"]),
+        "gpu_launches": int(sum(st["kernel_count"].values())),
         "clocks": clk.summary(),
     }
     # end to end through the public API with pinned host buffers
