@@ -28,12 +28,18 @@ def raw(rep):
     return res
 
 
-def stalls(rep, top=25):
-    out = subprocess.check_output(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source",
-                                   "sass"], text=True, stderr=subprocess.DEVNULL)
+def stalls(rep, top=25, kernel=None):
+    cmd = ["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"]
+    if kernel:
+        cmd += ["-k", kernel]
+    out = subprocess.check_output(cmd, text=True, stderr=subprocess.DEVNULL)
     rows = list(csv.reader(io.StringIO(out)))
+    # multi-kernel reports: keep the first kernel's table
+    starts = [i for i, r in enumerate(rows) if r and r[0] == "Kernel Name"]
+    if len(starts) > 1:
+        rows = rows[starts[0]:starts[1]]
     hdr = rows[1]
-    data = rows[2:]
+    data = [r for r in rows[2:] if len(r) == len(hdr)]
     i_s = hdr.index("Warp Stall Sampling (All Samples)")
     i_src = hdr.index("Source")
     i_th = hdr.index("Avg. Threads Executed")
@@ -55,4 +61,5 @@ if __name__ == "__main__":
             if key in k:
                 print(f"   {key:70s} {k[key][0]:>16} {k[key][1]}")
     if "--stalls" in sys.argv:
-        print(stalls(rep))
+        kern = sys.argv[sys.argv.index("--stalls") + 1] if len(sys.argv) > sys.argv.index("--stalls") + 1 else None
+        print(stalls(rep, kernel=kern))
