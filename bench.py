@@ -251,9 +251,10 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        from paper_1301_1714_b200.dem import DEM_F_THREAD_PER_PARTICLE
+        from paper_1301_1714_b200.dem import DEM_F_FORCE_LISTS_TPP, DEM_F_THREAD_PER_PARTICLE
         d = Dem(sc.params, device=local, stream=stream,
-                flags=DEM_F_THREAD_PER_PARTICLE if args.sweep == "tpp" else 0)
+                flags={"warp": 0, "lists": DEM_F_FORCE_LISTS_TPP,
+                       "tpp": DEM_F_THREAD_PER_PARTICLE}[args.sweep])
         d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
         d.step(max(args.warmup, 3))
         stats0 = d.stats()
@@ -405,8 +406,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="warp", choices=["warp", "tpp"],
-                    help="warp-cooperative sweep (default) or the paper's thread-per-particle")
+    ap.add_argument("--sweep", default="warp", choices=["warp", "lists", "tpp"],
+                    help="detect + warp-flattened force rounds (default), detect + thread-per-"
+                         "particle force over the lists, or the paper's fused thread-per-particle")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

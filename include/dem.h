@@ -75,8 +75,10 @@ enum dem_flags {
   DEM_F_ASYNC = 1u << 3,       /* dem_step does not synchronise; errors surface at the next
                                   synchronising call */
   DEM_F_NO_GRAPH = 1u << 4,    /* launch kernels eagerly instead of replaying a CUDA graph */
-  DEM_F_THREAD_PER_PARTICLE = 1u << 5, /* ablation: the paper's one-thread-per-particle sweep
-                                           instead of the warp-cooperative one */
+  DEM_F_THREAD_PER_PARTICLE = 1u << 5, /* ablation: the paper's mapping, detection and forces
+                                          in one thread-per-particle kernel */
+  DEM_F_FORCE_LISTS_TPP = 1u << 6, /* ablation: the force kernel with one thread per particle
+                                      over its contact list (default: warp-flattened rounds) */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };

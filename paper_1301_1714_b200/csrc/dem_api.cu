@@ -231,8 +231,10 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   rec(K_RANK, true);
   launch_rank(h->stream, h->n, s);
   rec(K_RANK, false);
-  const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : 0;
-  if (variant == 0) {
+  const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
+                      : (h->p.flags & DEM_F_FORCE_LISTS_TPP)   ? 2
+                                                               : 0;
+  if (variant != 1) {
     rec(K_DETECT, true);
     launch_detect(h->stream, h->n, h->K, s, h->g);
     rec(K_DETECT, false);

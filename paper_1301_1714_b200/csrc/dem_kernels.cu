@@ -643,10 +643,11 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 
 // ---- default path: k_detect (steps 5-6) then k_force (steps 7-8, 1) -------
 // k_detect: one light thread per sorted particle scans its 27-cell candidates
-// (Eq. 12: 9 contiguous slot ranges of sorted positions, the 18 row bounds
-// loaded up front) with the exact predicate (R14) and writes its contact list
-// clist[k*N + j] (partner sorted slots, candidate order). Few registers, so
-// the SM keeps many warps in flight to hide the neighbour-row latency.
+// (Eq. 12: 9 contiguous slot ranges of sorted positions, row bounds loaded per
+// z-plane) with the exact predicate (R14) and writes its contact list
+// clist[k*N + j] = t (each partner's sorted slot, in candidate order =
+// ascending sorted slot). Few registers, so the SM keeps many warps in flight
+// to hide the neighbour-row latency.
 #ifndef DEM_DETECT_PLANES
 #define DEM_DETECT_PLANES 1  // 1: row bounds loaded per z-plane (6 at a time); 0: all 18
 #endif
@@ -930,6 +931,84 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
 }
 
+// k_force_tpp: one thread per sorted particle evaluates its own contacts from
+// the contact list (the paper's particle-per-thread mapping for step 7, but
+// without the candidate loop: divergence only from unequal contact counts),
+// accumulating F and T in registers in candidate order. No shared memory, so
+// the SM's 228 KB stay L1 for the neighbours' state, which the block's
+// consecutive particles share. The next contact's partner state and predicted
+// history entry are loaded while the current one is evaluated.
+#ifndef DEM_FTPP_MINB
+#define DEM_FTPP_MINB 8
+#endif
+template <int MODEL, bool DIAG>
+__global__ void __launch_bounds__(128, DEM_FTPP_MINB)
+    k_force_tpp(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= N) return;
+  const uint32_t s = __ldcs(&b.perm[j]);
+  const uint32_t nc = __ldcs(&b.ccount[j]);
+  const bool overflow = nc > K;
+  const uint32_t npair = min(nc, K);
+  Own o;
+  o.P = __ldg(&b.pos_sorted[j]);
+  o.V = __ldg(&b.vel_in[s]);
+  o.W = __ldg(&b.omg_in[s]);
+  const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  // loads of contact k: partner position, velocity, spin, predicted old entry
+  float4 Q = z4, VQ = z4, WQ = z4, H = z4;
+  if (npair > 0) {
+    const uint32_t q = __ldg(&b.perm[__ldcs(&b.clist[j])]);
+    Q = __ldg(&b.pos_in[q]);
+    VQ = __ldg(&b.vel_in[q]);
+    if (MODEL == 0) {
+      WQ = __ldg(&b.omg_in[q]);
+      if (n_old > 0) H = __ldcs(&b.hist_in[s]);
+    }
+  }
+  for (uint32_t k = 0; k < npair; ++k) {
+    const float4 Qc = Q, VQc = VQ, WQc = WQ, Hc = H;
+    if (k + 1 < npair) {  // next contact's loads in flight during this one's arithmetic
+      const uint32_t q = __ldg(&b.perm[__ldcs(&b.clist[(size_t)(k + 1) * N + j])]);
+      Q = __ldg(&b.pos_in[q]);
+      VQ = __ldg(&b.vel_in[q]);
+      if (MODEL == 0) {
+        WQ = __ldg(&b.omg_in[q]);
+        H = k + 1 < n_old ? __ldcs(&b.hist_in[(size_t)(k + 1) * N + s]) : z4;
+      }
+    }
+    f3 n;
+    float delta;
+    if (!contact_geometry(o.P, Qc, n, delta)) {
+      raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
+      continue;
+    }
+    if (MODEL == 0) {
+      const uint32_t pid = __float_as_uint(WQc.w);
+      const f3 dold = (k < n_old && __float_as_uint(Hc.w) == pid)
+                          ? mk(Hc.x, Hc.y, Hc.z)
+                          : old_history(b.hist_in, N, s, n_old, 0xFFFFFFFFu, pid);
+      f3 Fc, Tc, dnew;
+      eval_pair_practical(o, Qc, VQc, WQc, n, delta, dold, ph, Fc, Tc, dnew);
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+      T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
+      __stcs(&b.hist_out[(size_t)k * N + j],
+             make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
+    } else {
+      const f3 u = mk(VQc.x - o.V.x, VQc.y - o.V.y, VQc.z - o.V.z);
+      const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+    }
+  }
+  auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
+    return old_history(b.hist_in, N, s, n_old, n_old, pid);
+  };
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
+}
+
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
 void sweep_prepare(uint32_t K) {
@@ -1081,13 +1160,15 @@ template <int MODEL, bool DIAG>
 static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                            const DevGrid& g, const DevPhys& ph, int variant) {
   const uint32_t N = (uint32_t)n;
-  if (variant == 1) {
+  if (variant == 1) {  // the paper's mapping, one fused kernel
     k_sweep_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
-    return;
+  } else if (variant == 2) {  // thread per particle over the contact lists
+    k_force_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+  } else {  // warp-flattened contact rounds (default)
+    const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
+    k_force<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
+        b, g, ph, N, K);
   }
-  const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
-  k_force<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
-      b, g, ph, N, K);
 }
 
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,

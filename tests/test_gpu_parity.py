@@ -9,8 +9,9 @@ import pytest
 
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
-from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_NO_GRAPH,
-                                      DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID, Dem, DemError)
+from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_LISTS_TPP,
+                                      DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
+                                      Dem, DemError)
 
 from .parity import assert_T2_forces, assert_T2_history, contacts_dict, oracle_inputs
 
@@ -59,7 +60,7 @@ def test_hash_sort_offsets_bit_exact(name):
 
 # ------------------------------------------------------ T2 one step -------
 
-@pytest.mark.parametrize("variant", [0, DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_LISTS_TPP, DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
     sc = scenes_small()[idx]
@@ -245,14 +246,16 @@ def test_determinism_and_graph_equivalence():
             assert np.array_equal(a, b)
 
 
-def test_sweep_variants_agree():
-    """The warp-cooperative sweep and the paper's thread-per-particle sweep
-    evaluate the same contacts with the same arithmetic and summation order;
-    only the compiler's FMA contraction may differ between the two kernels, so
-    one step agrees to fp32 rounding, and the contact sets bit-exactly."""
+@pytest.mark.parametrize("other", [DEM_F_FORCE_LISTS_TPP, DEM_F_THREAD_PER_PARTICLE])
+def test_sweep_variants_agree(other):
+    """The force-kernel mappings (contact lists, warp-flattened rounds, the
+    paper's fused thread per particle) evaluate the same contacts with the
+    same arithmetic and summation order; only the compiler's FMA contraction
+    may differ between kernels, so one step agrees to fp32 rounding and the
+    contact sets bit-exactly."""
     sc = S.C2()
     a = make(sc, flags=DEM_F_DIAG)
-    b = make(sc, flags=DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE)
+    b = make(sc, flags=DEM_F_DIAG | other)
     a.step(5)
     b.step(5)
     sa, sb = a.get_state(forces=True), b.get_state(forces=True)
