@@ -192,7 +192,7 @@ StepBuffers step_buffers(dem_handle* h, int b) {
 }
 
 int kernels_per_step(const dem_handle* h) {
-  return (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 4 : 5;
+  return (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : 6;
 }
 
 // Enqueue one step from parity b: scan, scatter, rank, (detect,) sweep.
@@ -243,7 +243,7 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   rec(K_SWEEP, true);
   launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph, variant);
   rec(K_SWEEP, false);
-  h->launches += 4;
+  h->launches += 5;  // scan is two kernels
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
   return DEM_OK;

@@ -163,42 +163,21 @@ __global__ void k_idcheck(int64_t n, const float4* omg, uint32_t* seen, uint32_t
 }
 
 // ------------------------------------------------------------ k_scan -------
-// Exclusive scan out[0..n] of in[0..n) (out[n] = total), one pass with
-// dynamic tile ids and decoupled look-back over 64-bit status words
-// [flag:2 | value:32] (flag 1 = tile aggregate, 2 = inclusive prefix).
-// Optionally zeroes `zero` (the per-cell counts, ready for the next step's
-// atomics) and advances the step counter.
+// Exclusive scan out[0..n] of in[0..n) (out[n] = total) in two passes of
+// 4,096-element tiles: k_tile_sum writes one sum per tile; k_scan_apply adds
+// the sums of all preceding tiles (a block-wide reduction over at most a few
+// thousand L2-resident words) to the tile's own block scan. No inter-block
+// waiting, so every tile streams at full bandwidth. Optionally zeroes `zero`
+// (the per-cell counts, ready for the next step's atomics) and advances the
+// step counter. `in` and `zero` may alias.
 
-__device__ __forceinline__ unsigned long long ld_status(const unsigned long long* p) {
-  unsigned long long v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-__device__ __forceinline__ void st_status(unsigned long long* p, unsigned long long v) {
-  asm volatile("st.relaxed.gpu.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
-}
-
-__global__ void __launch_bounds__(kScanThreads)
-    k_scan(const uint32_t* in, uint32_t* __restrict__ out, uint32_t n, uint32_t* zero,
-           unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
-  // `in` and `zero` may alias (the per-cell counts are read, then cleared)
-  __shared__ uint32_t s_tile, s_prefix;
-  __shared__ uint32_t s_warp[kScanThreads / 32];
-  if (err && ld_volatile(&err->code) != 0u) return;
-  if (threadIdx.x == 0) {
-    s_tile = atomicAdd(ctr, 1u);
-    if (s_tile == 0 && count_step && err) atomicAdd(&err->step_ctr, 1u);
-  }
-  __syncthreads();
-  const uint32_t tile = s_tile;
-  const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
-
-  uint32_t v[kScanItems];
+__device__ __forceinline__ void load_tile(const uint32_t* in, uint32_t n, uint64_t base,
+                                          uint32_t (&v)[kScanItems]) {
   if (base + kScanItems <= n) {
     const uint4* p = reinterpret_cast<const uint4*>(in + base);
 #pragma unroll
     for (int q = 0; q < kScanItems / 4; ++q) {
-      uint4 w = p[q];
+      const uint4 w = __ldcs(&p[q]);
       v[4 * q] = w.x;
       v[4 * q + 1] = w.y;
       v[4 * q + 2] = w.z;
@@ -208,63 +187,80 @@ __global__ void __launch_bounds__(kScanThreads)
 #pragma unroll
     for (int q = 0; q < kScanItems; ++q) v[q] = (base + q < n) ? in[base + q] : 0u;
   }
+}
+
+__device__ __forceinline__ uint32_t block_sum(uint32_t x, uint32_t* s_warp) {
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) x += __shfl_xor_sync(0xffffffffu, x, d);
+  __syncthreads();
+  if (lane == 0) s_warp[warp] = x;
+  __syncthreads();
+  uint32_t t = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) t += __shfl_xor_sync(0xffffffffu, t, d);
+  return t;
+}
+
+__global__ void __launch_bounds__(kScanThreads)
+    k_tile_sum(const uint32_t* in, uint32_t n, uint32_t* tsum, DevErr* err, int count_step) {
+  __shared__ uint32_t s_warp[kScanThreads / 32];
+  if (err && ld_volatile(&err->code) != 0u) return;
+  const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  load_tile(in, n, base, v);
   uint32_t local = 0;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) local += v[q];
+  const uint32_t tot = block_sum(local, s_warp);
+  if (threadIdx.x == 0) {
+    tsum[blockIdx.x] = tot;
+    if (blockIdx.x == 0 && count_step && err) atomicAdd(&err->step_ctr, 1u);
+  }
+}
 
+__global__ void __launch_bounds__(kScanThreads)
+    k_scan_apply(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
+                 const uint32_t* __restrict__ tsum, DevErr* err) {
+  __shared__ uint32_t s_warp[kScanThreads / 32];
+  __shared__ uint32_t s_excl[kScanThreads / 32];
+  if (err && ld_volatile(&err->code) != 0u) return;
+  const uint32_t tile = blockIdx.x;
+  // prefix of all preceding tiles
+  uint32_t acc = 0;
+  for (uint32_t t = threadIdx.x; t < tile; t += kScanThreads) acc += __ldg(&tsum[t]);
+  const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
+  uint32_t v[kScanItems];
+  load_tile(in, n, base, v);
+  const uint32_t prefix = block_sum(acc, s_warp);
+  uint32_t local = 0;
+#pragma unroll
+  for (int q = 0; q < kScanItems; ++q) local += v[q];
   // block exclusive scan of `local`
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint32_t incl = local;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
-    uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
+    const uint32_t t = __shfl_up_sync(0xffffffffu, incl, d);
     if (lane >= (uint32_t)d) incl += t;
   }
+  __syncthreads();
   if (lane == 31) s_warp[warp] = incl;
   __syncthreads();
   if (warp == 0) {
-    uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
+    const uint32_t w = lane < kScanThreads / 32 ? s_warp[lane] : 0u;
     uint32_t wi = w;
 #pragma unroll
     for (int d = 1; d < kScanThreads / 32; d <<= 1) {
-      uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
+      const uint32_t t = __shfl_up_sync(0xffffffffu, wi, d);
       if (lane >= (uint32_t)d) wi += t;
     }
-    if (lane < kScanThreads / 32) s_warp[lane] = wi - w;  // exclusive warp offsets
-    const uint32_t aggregate = __shfl_sync(0xffffffffu, wi, kScanThreads / 32 - 1);
-    // decoupled look-back (warp 0)
-    uint32_t prefix = 0;
-    if (tile == 0) {
-      if (lane == 0) st_status(&status[0], (2ull << 32) | aggregate);
-    } else {
-      if (lane == 0) st_status(&status[tile], (1ull << 32) | aggregate);
-      int64_t look = (int64_t)tile - 1;
-      while (true) {
-        int64_t t = look - (int64_t)lane;
-        unsigned long long s = 0;
-        uint32_t flag;
-        do {  // spin until this lane's predecessor has published something
-          s = t >= 0 ? ld_status(&status[t]) : (2ull << 32);
-          flag = (uint32_t)(s >> 32) & 3u;
-        } while (__any_sync(0xffffffffu, flag == 0u));
-        const uint32_t val = (uint32_t)s;
-        const uint32_t pmask = __ballot_sync(0xffffffffu, flag == 2u);
-        // lanes up to (and including) the nearest inclusive prefix contribute
-        const uint32_t stop = pmask ? (uint32_t)(__ffs(pmask) - 1) : 32u;
-        uint32_t contrib = lane <= stop ? val : 0u;
-#pragma unroll
-        for (int d = 16; d > 0; d >>= 1) contrib += __shfl_xor_sync(0xffffffffu, contrib, d);
-        prefix += contrib;
-        if (pmask) break;
-        look -= 32;
-      }
-      if (lane == 0) st_status(&status[tile], (2ull << 32) | (prefix + aggregate));
-    }
-    if (lane == 0) s_prefix = prefix;
-    if (lane == 0 && (uint64_t)(tile + 1) * kScanTile >= n) out[n] = prefix + aggregate;
+    if (lane < kScanThreads / 32) s_excl[lane] = wi - w;
+    if (lane == kScanThreads / 32 - 1 && (uint64_t)(tile + 1) * kScanTile >= n)
+      out[n] = prefix + wi;  // total
   }
   __syncthreads();
-  uint32_t run = s_prefix + s_warp[warp] + (incl - local);
+  uint32_t run = prefix + s_excl[warp] + (incl - local);
   if (base + kScanItems <= n) {
     uint4* p = reinterpret_cast<uint4*>(out + base);
 #pragma unroll
@@ -283,7 +279,7 @@ __global__ void __launch_bounds__(kScanThreads)
     if (zero) {
       uint4* z = reinterpret_cast<uint4*>(zero + base);
 #pragma unroll
-      for (int q = 0; q < kScanItems / 4; ++q) z[q] = make_uint4(0u, 0u, 0u, 0u);
+      for (int q = 0; q < kScanItems / 4; ++q) __stcs(&z[q], make_uint4(0u, 0u, 0u, 0u));
     }
   } else {
 #pragma unroll
@@ -1130,9 +1126,12 @@ int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen
 
 int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
+  // `status` holds at least ceil(n / kScanTile) words: used as the tile sums
+  (void)ctr;
   const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
-  k_scan<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, out, n, zero, status, ctr, err,
-                                                         count_step);
+  uint32_t* tsum = reinterpret_cast<uint32_t*>(status);
+  k_tile_sum<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, n, tsum, err, count_step);
+  k_scan_apply<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, out, n, zero, tsum, err);
   return K_SCAN;
 }
 
