@@ -54,6 +54,8 @@ struct dem_handle {
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
   float4* pos_sorted = nullptr;
   uint32_t *clist = nullptr, *ccount = nullptr;
+  uint32_t* nslots = nullptr;  // device: input slots of the next step
+  uint32_t* flags = nullptr;   // slab mode
   float4 *F = nullptr, *T = nullptr;
   unsigned long long* scan_status[2] = {};
   uint32_t* scan_ctr = nullptr;  // [2]
@@ -153,7 +155,7 @@ void free_buffers(dem_handle* h) {
   }
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
-  h->clist = h->ccount = nullptr;
+  h->clist = h->ccount = h->nslots = h->flags = nullptr;
   h->F = h->T = nullptr;
   h->err = nullptr;
   h->cap_n = h->cap_cells = -1;
@@ -177,6 +179,8 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.pos_sorted = h->pos_sorted;
   s.clist = h->clist;
   s.ccount = h->ccount;
+  s.nslots = h->nslots;
+  s.flags = h->flags;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -513,6 +517,14 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   g.nz = (int)dims[2];
   g.ncells = (uint32_t)ncells;
   g.inv_h = 1.0 / hc;
+  g.nz_global = g.nz;
+  g.zlo = 0;
+  g.z0 = 0;
+  g.z1 = g.nz;
+  g.own_c0 = 0;
+  g.own_c1 = g.ncells;
+  g.trash = g.ncells;
+  g.slab = 0;
   // 4. buffers (reallocated when n or the grid changes)
   CUDA_TRY(h, cudaStreamSynchronize(st));
   if (h->cap_n != n || h->cap_cells != ncells) {
@@ -533,7 +545,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     ok &= dalloc(h, &h->prank, N) && dalloc(h, &h->count, (size_t)ncells + 1) &&
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
           dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->clist, N * h->K) &&
-          dalloc(h, &h->ccount, N) && dalloc(h, &h->scan_ctr, 2) &&
+          dalloc(h, &h->ccount, N) && dalloc(h, &h->nslots, 1) && dalloc(h, &h->scan_ctr, 2) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
     if (!ok) {
@@ -562,6 +574,11 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     CUDA_TRY(h, cudaMemsetAsync(h->scan_status[b], 0, sizeof(unsigned long long) * h->ntiles, st));
   CUDA_TRY(h, cudaMemsetAsync(h->scan_ctr, 0, 2 * sizeof(uint32_t), st));
   CUDA_TRY(h, cudaMemsetAsync(h->err, 0, sizeof(DevErr), st));
+  {
+    const uint32_t nn = (uint32_t)n;
+    CUDA_TRY(h, cudaMemcpyAsync(h->nslots, &nn, 4, cudaMemcpyHostToDevice, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+  }
   if (h->F) CUDA_TRY(h, cudaMemsetAsync(h->F, 0, sizeof(float4) * N, st));
   if (h->T) CUDA_TRY(h, cudaMemsetAsync(h->T, 0, sizeof(float4) * N, st));
   // 5. pack + hash (step 2 for the first step) + counting ranks

@@ -21,10 +21,17 @@ namespace dem {
 constexpr uint32_t kWallPid0 = 0xFFFFFFF0u;
 
 struct DevGrid {
-  int nx, ny, nz;
-  uint32_t ncells;
+  int nx, ny, nz;    // local grid (nz = planes held by this rank, ghosts included)
+  uint32_t ncells;   // local cells (+1 trash cell for departed particles in slab mode)
   double lo[3], hi[3];
-  double inv_h;  // 1/h, correctly rounded on the host (R15)
+  double inv_h;      // 1/h, correctly rounded on the host (R15)
+  int nz_global;     // global planes along z
+  int zlo;           // global z of local plane 0
+  int z0, z1;        // global z range [z0, z1) owned by this rank (single GPU: [0, nz))
+  uint32_t own_c0, own_c1;  // local cells of the owned planes: owned sorted slots are
+                            // [off[own_c0], off[own_c1])
+  uint32_t trash;    // key of particles that left the slab (slab mode), else ncells
+  int slab;          // 1: slab decomposition active
 };
 
 struct DevPhys {
@@ -68,6 +75,9 @@ struct StepBuffers {
   float4* pos_sorted;  // (x,y,z,r) gathered into SCM order by k_rank (step 4, positions)
   uint32_t* clist;     // contacts found by k_detect: clist[k*N + j] = partner's sorted slot
   uint32_t* ccount;    // number of pair contacts of sorted slot j (K+1: overflow)
+  const uint32_t* nslots;  // device: input slots of this step (owned + appended)
+  uint32_t* flags;     // slab mode: per output slot, bit0/1 migrate to left/right neighbour,
+                       // bit2/3 ghost for left/right neighbour
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;

@@ -59,10 +59,14 @@ __device__ __forceinline__ int cell_coord(float x, double lo, double inv_h, int 
   return (int)t;
 }
 
+// Local cell key of a position: global (cx, cy, cz) of R15, z shifted to the
+// rank's local planes. Returns the trash key for a z outside the local grid
+// (only reachable in slab mode; the caller flags it).
 __device__ __forceinline__ uint32_t cell_key(const DevGrid& g, float x, float y, float z) {
   int cx = cell_coord(x, g.lo[0], g.inv_h, g.nx);
   int cy = cell_coord(y, g.lo[1], g.inv_h, g.ny);
-  int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz);
+  int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+  if (cz < 0 || cz >= g.nz) return g.trash;
   return (uint32_t)cx + (uint32_t)g.nx * ((uint32_t)cy + (uint32_t)g.ny * (uint32_t)cz);
 }
 
@@ -298,15 +302,16 @@ __global__ void __launch_bounds__(kScanThreads)
 constexpr int kItems = 4;
 
 __global__ void __launch_bounds__(256)
-    k_scatter(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ prank,
-              const uint32_t* __restrict__ off, uint32_t* __restrict__ tmp,
-              unsigned long long* status_next, uint32_t* ctr_next, uint32_t ntiles_next,
-              const DevErr* err) {
+    k_scatter(int64_t n, const uint32_t* __restrict__ nslots, const uint32_t* __restrict__ key,
+              const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
+              uint32_t* __restrict__ tmp, unsigned long long* status_next, uint32_t* ctr_next,
+              uint32_t ntiles_next, const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   // reset the other parity's scan state for the next step
   for (int64_t t = tid; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
   if (tid == 0) *ctr_next = 0u;
+  n = min(n, (int64_t)__ldg(nslots));  // this step's input slots
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t k[kItems], r[kItems], o[kItems];
 #pragma unroll
@@ -332,8 +337,9 @@ __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const DevErr* err) {
+           const uint32_t* __restrict__ nslots, const DevErr* err) {
   if (ld_volatile(&err->code) != 0u) return;
+  n = min(n, (int64_t)__ldg(nslots));
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
 #pragma unroll
@@ -473,11 +479,14 @@ __device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, floa
 
 // Step 8 + step 1 + next step 2 for one particle (shared by both sweeps):
 // walls, integration, state write at slot j, next CM and its counting rank.
+// The outputs go to slot oj = j - (first owned sorted slot): the owned
+// particles of the next step are dense from 0.
 template <int MODEL, bool DIAG, class LookupFn>
 __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevGrid& g,
                                                 const DevPhys& ph, uint32_t N, uint32_t K,
-                                                uint32_t j, const Own& o, f3 F, f3 T,
+                                                uint32_t oj, const Own& o, f3 F, f3 T,
                                                 uint32_t ncnt, bool overflow, LookupFn lookup) {
+  const uint32_t j = oj;  // output slot
   const float ri = o.P.w, mi = o.V.w;
   const uint32_t my_id = __float_as_uint(o.W.w);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
@@ -555,6 +564,18 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
         (double)y > g.hi[1] + rd || (double)z < g.lo[2] - rd || (double)z > g.hi[2] + rd)
       raise_error(b.err, 8u, j, my_id);
     k2 = cell_key(g, x, y, z);  // step 2 of the next step: CM of the new position
+    if (g.slab) {
+      // slab exchange flags: leaving the owned planes = migrant
+      // (its key becomes the trash cell); on a boundary plane = ghost for the neighbour
+      const int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz_global);
+      uint32_t f = 0;
+      if (cz < g.z0) f |= 1u;
+      if (cz >= g.z1) f |= 2u;
+      if (cz == g.z0) f |= 4u;
+      if (cz == g.z1 - 1) f |= 8u;
+      if (f & 3u) k2 = g.trash;
+      b.flags[j] = f;
+    }
   }
   b.key_out[j] = k2;
   b.prank[j] = count_into_cell(b.count, k2);  // counted into its cell for the next sort
@@ -568,8 +589,9 @@ template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, DevPhys ph,
                                                    uint32_t N, uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jhi) return;
   const uint32_t s = __ldg(&b.perm[j]);
   Own o;
   o.P = __ldg(&b.pos_sorted[j]);
@@ -585,7 +607,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   };
   const int cx = cell_coord(o.P.x, g.lo[0], g.inv_h, g.nx);
   const int cy = cell_coord(o.P.y, g.lo[1], g.inv_h, g.ny);
-  const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz);
+  const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
   uint32_t ncnt = 0;
   bool overflow = false;
@@ -620,7 +642,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
           F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
           T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
           if (ncnt < K) {
-            b.hist_out[(size_t)ncnt * N + j] =
+            b.hist_out[(size_t)ncnt * N + (j - jlo)] =
                 make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
             ++ncnt;
           } else {
@@ -634,7 +656,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
       }
     }
   }
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, ncnt, overflow, lookup);
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, ncnt, overflow, lookup);
 }
 
 // ---- default path: k_detect (steps 5-6) then k_force (steps 7-8, 1) -------
@@ -649,13 +671,14 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 #endif
 __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32_t N, uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jhi) return;
   const float4 P = __ldg(&b.pos_sorted[j]);
   // own cell: the step-2 hash of the own position (identical to CM by construction)
   const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
   const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
-  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz);
+  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
   const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
   const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
   const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
@@ -786,10 +809,11 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
 
-  const uint32_t j0 = (blockIdx.x * kSweepWarps + warp) * 32u;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j0 = jlo + (blockIdx.x * kSweepWarps + warp) * 32u;
   const uint32_t j = j0 + lane;
-  const bool valid = j < N;
-  if (j0 >= N) return;  // whole warp past the end
+  const bool valid = j < jhi;
+  if (j0 >= jhi) return;  // whole warp past the end
 
   // ---- own particle (step 4 gather through SCCM) and its contact list
   const uint32_t s = valid ? __ldcs(&b.perm[j]) : 0u;
@@ -882,7 +906,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
-        raise_error(b.err, 9u, j0 + ow, __float_as_uint(po.W.w));
+        raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w));
       } else if (MODEL == 0) {
         const float4 WQ = d[64 + lane];
         const uint32_t pid = __float_as_uint(WQ.w);
@@ -895,7 +919,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
           dold = old_history(b.hist_in, N, s_slot[ow], no, 0xFFFFFFFFu, pid);
         f3 dnew;
         eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
-        __stcs(&b.hist_out[(size_t)k * N + j0 + ow],
+        __stcs(&b.hist_out[(size_t)k * N + (j0 - jlo) + ow],
                make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
       } else {
         const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
@@ -924,7 +948,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
 // k_force_tpp: one thread per sorted particle evaluates its own contacts from
@@ -941,8 +965,9 @@ template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(128, DEM_FTPP_MINB)
     k_force_tpp(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= N) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jhi) return;
   const uint32_t s = __ldcs(&b.perm[j]);
   const uint32_t nc = __ldcs(&b.ccount[j]);
   const bool overflow = nc > K;
@@ -979,7 +1004,7 @@ __global__ void __launch_bounds__(128, DEM_FTPP_MINB)
     f3 n;
     float delta;
     if (!contact_geometry(o.P, Qc, n, delta)) {
-      raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
+      raise_error(b.err, 9u, j - jlo, __float_as_uint(o.W.w));
       continue;
     }
     if (MODEL == 0) {
@@ -991,7 +1016,7 @@ __global__ void __launch_bounds__(128, DEM_FTPP_MINB)
       eval_pair_practical(o, Qc, VQc, WQc, n, delta, dold, ph, Fc, Tc, dnew);
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
       T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
-      __stcs(&b.hist_out[(size_t)k * N + j],
+      __stcs(&b.hist_out[(size_t)k * N + (j - jlo)],
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
     } else {
       const f3 u = mk(VQc.x - o.V.x, VQc.y - o.V.y, VQc.z - o.V.z);
@@ -1002,7 +1027,7 @@ __global__ void __launch_bounds__(128, DEM_FTPP_MINB)
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j, o, F, T, npair, overflow, lookup);
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
 // Set the dynamic shared-memory limit of every k_force instantiation once,
@@ -1141,7 +1166,7 @@ int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t nt
   const int64_t need = ((int64_t)ntiles_next + 255) / 256;
   if (blocks < need) blocks = need;
   if (blocks < 1) blocks = 1;
-  k_scatter<<<(unsigned)blocks, 256, 0, st>>>(n, b.key_in, b.prank, b.off, b.tmp,
+  k_scatter<<<(unsigned)blocks, 256, 0, st>>>(n, b.nslots, b.key_in, b.prank, b.off, b.tmp,
                                               b.scan_status_next, b.scan_ctr_next, ntiles_next,
                                               b.err);
   return K_SCATTER;
@@ -1151,7 +1176,8 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
   k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm,
-                                                           b.pos_in, b.pos_sorted, b.err);
+                                                           b.pos_in, b.pos_sorted, b.nslots,
+                                                           b.err);
   return K_RANK;
 }
 
