@@ -60,6 +60,8 @@ enum dem_error {
                            (tunnelling); state = last completed step */
   DEM_ECOINCIDENT = -9, /* two centres coincide while in contact (n undefined, R18) */
   DEM_ESTATE = -10,     /* call out of order (e.g. dem_step before dem_set_particles) */
+  DEM_EPEER = -11,      /* slab exchange failed: a neighbour did not publish in time, or a
+                           particle moved more than one cell plane across a slab boundary */
 };
 
 enum dem_model {
@@ -123,8 +125,8 @@ typedef struct {
   int32_t device;            /* CUDA ordinal; -1 -> current device */
   void* stream;              /* cudaStream_t; NULL -> a stream owned by the handle */
   const dem_allocator* allocator; /* NULL -> cudaMallocAsync on the stream */
-  int32_t rank, world_size;  /* world_size <= 1: single GPU (z-slabs otherwise) */
-  const void* nccl_id;       /* 128-byte ncclUniqueId when world_size > 1 */
+  int32_t rank, world_size;  /* world_size <= 1: single GPU; > 1: z-slab rank */
+  const void* nccl_id;       /* unused (slab exchange is over CUDA IPC peer memory) */
 } dem_params;
 
 /* Particle arrays, all host or all device (mem_kind). Layout: pos/vel/omega
@@ -224,7 +226,30 @@ int dem_get_stats(dem_handle* h, dem_stats* out);
  * resets the accumulated times. */
 int dem_profile(dem_handle* h, int32_t enable);
 
-/* Fill out128 with a new ncclUniqueId (rank 0 of a multi-GPU run). */
+/* ---- Slab decomposition (world_size > 1) ---------------------
+ * Rank r of P owns the cell planes z in [floor(r nz/P), floor((r+1) nz/P)) of
+ * the global grid (nz >= 2P). dem_set_particles takes the full set (or any
+ * superset of the rank's slab) and keeps the rank's particles. Every step
+ * starts by reading the neighbours' migrants and ghost planes from their
+ * exchange regions (peer memory over NVLink via CUDA IPC) and ends by
+ * publishing this rank's. Ranks must be connected before dem_step, and step
+ * in lockstep (a rank waits for its neighbours' previous step). After a step,
+ * dem_get_state / dem_get_contacts return the particles this rank advanced;
+ * the union over ranks is the whole set, each particle exactly once. Errors
+ * in slab mode are not rolled back (set the particles again). */
+
+/* 64-byte cudaIpcMemHandle_t of this rank's exchange region (after
+ * dem_set_particles); the caller distributes it to the neighbours. */
+int dem_exchange_handle(dem_handle* h, void* out64);
+/* Device pointer of the exchange region (same-process neighbours). */
+int dem_exchange_ptr(dem_handle* h, void** out);
+/* Open the neighbours' handles (NULL for rank 0's left / rank P-1's right). */
+int dem_connect(dem_handle* h, const void* left64, const void* right64);
+/* Same-process neighbours: their dem_exchange_ptr values (NULL at the ends). */
+int dem_connect_ptrs(dem_handle* h, void* left, void* right);
+
+/* Fill out128 with a new ncclUniqueId (unused: the slab exchange uses CUDA IPC
+ * peer memory; returns DEM_ENCCL). */
 int dem_nccl_unique_id(void* out128);
 
 const char* dem_strerror(int code);

@@ -64,6 +64,20 @@ struct dem_handle {
   DevErr* err_host = nullptr;  // pinned
   int64_t cap_n = -1, cap_cells = -1;
 
+  int64_t cap = 0;  // slot capacity = stride of the K-major arrays (single GPU: n)
+
+  // slab decomposition (world_size > 1), DESIGN.md §7
+  bool slab = false;
+  int rank = 0, world = 1;
+  uint8_t* xregion = nullptr;  // this rank's exchange region (cudaMalloc: IPC-shareable)
+  XLayout xl{};
+  const uint8_t* xleft = nullptr;   // neighbours' regions (peer pointers)
+  const uint8_t* xright = nullptr;
+  bool xleft_ipc = false, xright_ipc = false;
+  bool connected = false;
+  XState* xs = nullptr;
+  uint32_t* xtiles = nullptr;  // pack tile counts [4][ntiles]
+
   int cur = 0;
   int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
 
@@ -156,6 +170,8 @@ void free_buffers(dem_handle* h) {
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
+  h->xs = nullptr;
+  h->xtiles = nullptr;
   h->F = h->T = nullptr;
   h->err = nullptr;
   h->cap_n = h->cap_cells = -1;
@@ -196,7 +212,7 @@ StepBuffers step_buffers(dem_handle* h, int b) {
 }
 
 int kernels_per_step(const dem_handle* h) {
-  return (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : 6;
+  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : 6) + (h->slab ? 5 : 0);
 }
 
 // Enqueue one step from parity b: scan, scatter, rank, (detect,) sweep.
@@ -225,29 +241,42 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
       h->prof.push_back({evb, e, k});
     }
   };
+  if (h->slab) {  // this step's migrants and ghosts from the neighbours (peer memory)
+    rec(K_OTHER, true);
+    launch_xunpack(h->stream, h->cap, s, h->g, h->K, h->xleft, h->xright, h->xl, h->xs,
+                   h->nslots);
+    rec(K_OTHER, false);
+    h->launches += 2;
+  }
   rec(K_SCAN, true);
   launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, s.scan_ctr,
               h->err, 1);
   rec(K_SCAN, false);
   rec(K_SCATTER, true);
-  launch_scatter(h->stream, h->n, s, h->ntiles);
+  launch_scatter(h->stream, h->cap, s, h->ntiles);
   rec(K_SCATTER, false);
   rec(K_RANK, true);
-  launch_rank(h->stream, h->n, s);
+  launch_rank(h->stream, h->cap, s);
   rec(K_RANK, false);
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
                       : (h->p.flags & DEM_F_FORCE_LISTS_TPP)   ? 2
                                                                : 0;
   if (variant != 1) {
     rec(K_DETECT, true);
-    launch_detect(h->stream, h->n, h->K, s, h->g);
+    launch_detect(h->stream, h->cap, h->K, s, h->g);
     rec(K_DETECT, false);
     h->launches += 1;
   }
   rec(K_SWEEP, true);
-  launch_sweep(h->stream, h->n, h->K, h->p.model, diag, s, h->g, h->ph, variant);
+  launch_sweep(h->stream, h->cap, h->K, h->p.model, diag, s, h->g, h->ph, variant);
   rec(K_SWEEP, false);
   h->launches += 5;  // scan is two kernels
+  if (h->slab) {  // pack and publish the next step's migrants and ghosts
+    rec(K_OTHER, true);
+    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion, h->xl, h->xtiles, h->xs, 0);
+    rec(K_OTHER, false);
+    h->launches += 3;
+  }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
   return DEM_OK;
@@ -289,7 +318,21 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
   const DevErr e = *h->err_host;
   if (e.code == 0) {
     h->steps = ctr0 + nsteps;
+    if (h->slab) {  // particles this rank advanced in its last step
+      XState x{};
+      CUDA_TRY(h, cudaMemcpy(&x, h->xs, sizeof x, cudaMemcpyDeviceToHost));
+      h->n = x.n_out;
+    }
     return DEM_OK;
+  }
+  if (h->slab) {  // no roll-back across ranks: the handle must be set again
+    char buf[200];
+    snprintf(buf, sizeof buf, "%s (slab rank %d): particle id %u in step %u; set the particles again",
+             e.code == 11u ? "slab exchange failed (peer timeout or a migrant skipped a plane)"
+                           : err_name(e.code),
+             h->rank, e.id, e.step);
+    h->n = -1;
+    return fail(h, e.code == 11u ? DEM_EPEER : -(int)e.code, buf);
   }
   const int64_t failed = (int64_t)e.step;  // 1-based counter value of the failing step
   const int64_t done = std::max<int64_t>(0, failed - 1 - ctr0);
@@ -328,7 +371,7 @@ int validate_params(const dem_params* p) {
   for (float v : nonneg)
     if (!(v >= 0.0f) || !std::isfinite(v)) return DEM_EINVAL;
   if (p->cell_edge < 0.0f || !std::isfinite(p->cell_edge)) return DEM_EINVAL;
-  if (p->world_size > 1) return DEM_EINVAL;  // slab decomposition: see DESIGN.md §7
+  if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
   return DEM_OK;
 }
 
@@ -365,6 +408,9 @@ int dem_create(const dem_params* p, dem_handle** out) {
   dem_handle* h = new dem_handle();
   h->p = *p;
   h->K = p->max_contacts ? p->max_contacts : 16u;
+  h->slab = p->world_size > 1;
+  h->rank = h->slab ? p->rank : 0;
+  h->world = h->slab ? p->world_size : 1;
   if (p->device >= 0) {
     if (cudaSetDevice(p->device) != cudaSuccess) {
       delete h;
@@ -416,6 +462,9 @@ int dem_create(const dem_params* p, dem_handle** out) {
 int dem_destroy(dem_handle* h) {
   if (!h) return DEM_OK;
   cudaStreamSynchronize(h->stream);
+  if (h->xleft_ipc && h->xleft) cudaIpcCloseMemHandle((void*)h->xleft);
+  if (h->xright_ipc && h->xright) cudaIpcCloseMemHandle((void*)h->xright);
+  if (h->xregion) cudaFree(h->xregion);
   free_buffers(h);
   for (auto& pr : h->prof) {
     cudaEventDestroy(pr.b);
@@ -525,17 +574,68 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   g.own_c1 = g.ncells;
   g.trash = g.ncells;
   g.slab = 0;
-  // 4. buffers (reallocated when n or the grid changes)
+  int64_t n_own = n;    // particles this rank keeps
+  int64_t cap = n;      // slot capacity
+  uint32_t *keep = nullptr, *dst = nullptr;
+  if (h->slab) {
+    // 3b. slabs along z (the slowest axis of the cell index): rank r owns the
+    // planes [z0, z1); its local grid adds one ghost plane on each side
+    const int P = h->world, r = h->rank;
+    const int z0 = (int)((int64_t)r * g.nz_global / P), z1 = (int)((int64_t)(r + 1) * g.nz_global / P);
+    if (z1 - z0 < 2) {
+      unstage();
+      return fail(h, DEM_EINVAL, "slab thinner than 2 cell planes: fewer ranks or smaller cells");
+    }
+    g.z0 = z0;
+    g.z1 = z1;
+    g.zlo = std::max(z0 - 1, 0);
+    const int zhi = std::min(z1 + 1, g.nz_global);
+    g.nz = zhi - g.zlo;
+    const uint32_t plane = (uint32_t)g.nx * (uint32_t)g.ny;
+    g.trash = plane * (uint32_t)g.nz;
+    g.ncells = g.trash + 1u;  // + the trash cell that collects departed particles
+    g.own_c0 = (uint32_t)(z0 - g.zlo) * plane;
+    g.own_c1 = (uint32_t)(z1 - g.zlo) * plane;
+    g.slab = 1;
+    // this rank's particles, compacted in input order (deterministic)
+    unsigned long long* st_tiles = nullptr;
+    uint32_t* ctr = nullptr;
+    const uint32_t kt = (uint32_t)((n + kScanTile - 1) / kScanTile) + 1;
+    if (!dalloc(h, &keep, (size_t)std::max<int64_t>(n, 1)) ||
+        !dalloc(h, &dst, (size_t)std::max<int64_t>(n, 1) + 1) || !dalloc(h, &st_tiles, kt) ||
+        !dalloc(h, &ctr, 1)) {
+      unstage();
+      return fail(h, DEM_ENOMEM, "allocation failed");
+    }
+    launch_keep(st, n, in.pos, g, keep);
+    launch_scan(st, keep, dst, (uint32_t)n, nullptr, st_tiles, ctr, nullptr, 0);
+    uint32_t kept = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&kept, dst + n, 4, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    dev_free(h, st_tiles);
+    dev_free(h, ctr);
+    n_own = kept;
+    const int64_t per_plane = n_own / std::max(1, z1 - z0) + 1;
+    const uint32_t gcap = (uint32_t)std::max<int64_t>(4096, 2 * per_plane + 1024);
+    const uint32_t mcap = std::max<uint32_t>(1024, gcap / 4);
+    cap = n_own + n_own / 4 + 2 * (int64_t)gcap + 2 * (int64_t)mcap;
+    h->xl = XLayout::make(mcap, gcap, h->K);
+  }
+  const int64_t ncl = g.ncells;  // cells the scan covers (local + trash in slab mode)
+  // 4. buffers (reallocated when the capacity or the grid changes)
   CUDA_TRY(h, cudaStreamSynchronize(st));
-  if (h->cap_n != n || h->cap_cells != ncells) {
+  if (h->cap_n != cap || h->cap_cells != ncl) {
     // keep staged inputs alive: free only the persistent buffers
-    std::vector<void*> keep(staged);
+    std::vector<void*> keepalive(staged);
+    keepalive.push_back(keep);
+    keepalive.push_back(dst);
     destroy_graphs(h);
     std::vector<Alloc> all = h->allocs;
     for (auto& a : all)
-      if (std::find(keep.begin(), keep.end(), a.p) == keep.end()) dev_free(h, a.p);
-    const size_t N = (size_t)(n > 0 ? n : 1);
-    const uint32_t ntiles = (uint32_t)((ncells + kScanTile - 1) / kScanTile) + 1;
+      if (std::find(keepalive.begin(), keepalive.end(), a.p) == keepalive.end()) dev_free(h, a.p);
+    const size_t N = (size_t)(cap > 0 ? cap : 1);
+    const int64_t ncells = ncl;
+    const uint32_t ntiles = (uint32_t)((std::max<int64_t>(ncells, cap) + kScanTile - 1) / kScanTile) + 1;
     bool ok = true;
     for (int b = 0; b < 2; ++b) {
       ok &= dalloc(h, &h->pos[b], N) && dalloc(h, &h->vel[b], N) && dalloc(h, &h->omg[b], N) &&
@@ -548,6 +648,14 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
           dalloc(h, &h->ccount, N) && dalloc(h, &h->nslots, 1) && dalloc(h, &h->scan_ctr, 2) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
+    if (h->slab) {
+      ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
+            dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
+      if (h->xregion) cudaFree(h->xregion);
+      h->xregion = nullptr;
+      if (cudaMalloc((void**)&h->xregion, 4 * h->xl.bytes) != cudaSuccess) ok = false;
+      else cudaMemset(h->xregion, 0, 4 * h->xl.bytes);
+    }
     if (!ok) {
       unstage();
       free_buffers(h);
@@ -555,18 +663,20 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
       return fail(h, DEM_ENOMEM, "device allocation failed");
     }
     h->ntiles = ntiles;
-    h->cap_n = n;
-    h->cap_cells = ncells;
+    h->cap_n = cap;
+    h->cap_cells = ncl;
   }
   h->g = g;
   h->h = hc;
-  h->n = n;
+  h->n = n_own;
+  h->cap = cap;
   h->cur = 0;
   h->steps = 0;
   destroy_graphs(h);
-  const size_t N = (size_t)(n > 0 ? n : 1);
-  CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells + 1), st));
-  CUDA_TRY(h, cudaMemsetAsync(h->off, 0, sizeof(uint32_t) * ((size_t)ncells + 1), st));
+  const size_t N = (size_t)(cap > 0 ? cap : 1);
+  const int64_t ncells_a = ncl;
+  CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
+  CUDA_TRY(h, cudaMemsetAsync(h->off, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
   CUDA_TRY(h, cudaMemsetAsync(h->perm, 0, sizeof(uint32_t) * N, st));
   CUDA_TRY(h, cudaMemsetAsync(h->cnt[0], 0, sizeof(uint32_t) * N, st));
   CUDA_TRY(h, cudaMemsetAsync(h->cnt[1], 0, sizeof(uint32_t) * N, st));
@@ -575,17 +685,43 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   CUDA_TRY(h, cudaMemsetAsync(h->scan_ctr, 0, 2 * sizeof(uint32_t), st));
   CUDA_TRY(h, cudaMemsetAsync(h->err, 0, sizeof(DevErr), st));
   {
-    const uint32_t nn = (uint32_t)n;
+    const uint32_t nn = (uint32_t)n_own;
     CUDA_TRY(h, cudaMemcpyAsync(h->nslots, &nn, 4, cudaMemcpyHostToDevice, st));
+    if (h->slab) {
+      XState x{};
+      x.n_out = nn;
+      CUDA_TRY(h, cudaMemcpyAsync(h->xs, &x, sizeof x, cudaMemcpyHostToDevice, st));
+    }
     CUDA_TRY(h, cudaStreamSynchronize(st));
   }
   if (h->F) CUDA_TRY(h, cudaMemsetAsync(h->F, 0, sizeof(float4) * N, st));
   if (h->T) CUDA_TRY(h, cudaMemsetAsync(h->T, 0, sizeof(float4) * N, st));
   // 5. pack + hash (step 2 for the first step) + counting ranks
-  launch_pack(st, n, in, g, h->pos[0], h->vel[0], h->omg[0], h->key[0], h->count, h->prank);
+  launch_pack(st, n, in, g, h->pos[0], h->vel[0], h->omg[0], h->key[0], h->count, h->prank, dst,
+              keep);
   h->launches += (n > 0) ? 2 : 1;
-  // 6. ids: unique; dense (a permutation of 0..n-1) enables ORDER_ID and set_contacts
   sweep_prepare(h->K);
+  if (h->slab) {
+    // 5b. publish the ghosts of the set state for the neighbours' first step
+    dev_free(h, keep);
+    dev_free(h, dst);
+    launch_flags(st, n_own, h->pos[0], g, h->flags);
+    StepBuffers sb{};
+    sb.pos_out = h->pos[0];
+    sb.vel_out = h->vel[0];
+    sb.omg_out = h->omg[0];
+    sb.cnt_out = h->cnt[0];
+    sb.hist_out = h->hist[0];
+    sb.flags = h->flags;
+    sb.off = h->off;
+    sb.err = h->err;
+    launch_xpack(st, cap, sb, g, h->K, h->xregion, h->xl, h->xtiles, h->xs, 1);
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    unstage();
+    h->ids_dense = false;  // ids are global: ORDER_ID / set_contacts are single-GPU only
+    return DEM_OK;
+  }
+  // 6. ids: unique; dense (a permutation of 0..n-1) enables ORDER_ID and set_contacts
   h->ids_dense = false;
   if (n > 0) {
     uint32_t* seen = nullptr;
@@ -635,7 +771,8 @@ int dem_step(dem_handle* h, int64_t nsteps) {
   if (!h) return DEM_EINVAL;
   if (nsteps < 0) return fail(h, DEM_EINVAL, "nsteps < 0");
   if (h->n < 0) return fail(h, DEM_ESTATE, "dem_step before dem_set_particles");
-  if (nsteps == 0 || h->n == 0) {
+  if (h->slab && !h->connected) return fail(h, DEM_ESTATE, "slab rank not connected (dem_connect)");
+  if (nsteps == 0 || (h->n == 0 && !h->slab)) {
     h->steps += (h->n == 0) ? nsteps : 0;
     return DEM_OK;
   }
@@ -793,8 +930,8 @@ int dem_get_contacts(dem_handle* h, int32_t mem_kind, int64_t cap, uint32_t* id_
       dj = id_j ? (uint32_t*)dev_alloc(h, 4ull * m) : nullptr;
       dd = dt3 ? (float*)dev_alloc(h, 12ull * m) : nullptr;
     }
-    launch_emit_contacts(st, n, h->K, h->hist[h->cur], h->cnt[h->cur], base, h->omg[h->cur], di,
-                         dj, dd);
+    launch_emit_contacts(st, n, h->cap, h->K, h->hist[h->cur], h->cnt[h->cur], base,
+                         h->omg[h->cur], di, dj, dd);
     h->launches++;
     if (!dev) {
       if (id_i) CUDA_TRY(h, cudaMemcpyAsync(id_i, di, 4ull * m, cudaMemcpyDeviceToHost, st));
@@ -856,7 +993,7 @@ int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t*
   }
   CUDA_TRY(h, cudaMemsetAsync(flags, 0, 4, st));
   launch_slot_of_id(st, n, h->omg[h->cur], slot);
-  launch_insert_contacts(st, m, n, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
+  launch_insert_contacts(st, m, n, h->cap, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
                          flags);
   h->launches += 2;
   uint32_t hf = 0;
@@ -940,6 +1077,61 @@ int dem_profile(dem_handle* h, int32_t enable) {
       h->kernel_count[k] = 0;
     }
   }
+  return DEM_OK;
+}
+
+int dem_exchange_handle(dem_handle* h, void* out64) {
+  if (!h || !out64) return DEM_EINVAL;
+  if (!h->slab || !h->xregion) return fail(h, DEM_ESTATE, "no exchange region (set particles first)");
+  cudaIpcMemHandle_t m;
+  CUDA_TRY(h, cudaIpcGetMemHandle(&m, h->xregion));
+  memcpy(out64, &m, sizeof m);
+  return DEM_OK;
+}
+
+int dem_exchange_ptr(dem_handle* h, void** out) {
+  if (!h || !out) return DEM_EINVAL;
+  if (!h->slab || !h->xregion) return fail(h, DEM_ESTATE, "no exchange region (set particles first)");
+  *out = h->xregion;
+  return DEM_OK;
+}
+
+int dem_connect(dem_handle* h, const void* left64, const void* right64) {
+  if (!h) return DEM_EINVAL;
+  if (!h->slab) return fail(h, DEM_ESTATE, "not a slab rank");
+  const void* in[2] = {left64, right64};
+  const uint8_t** outp[2] = {&h->xleft, &h->xright};
+  bool* ipc[2] = {&h->xleft_ipc, &h->xright_ipc};
+  for (int k = 0; k < 2; ++k) {
+    if (!in[k]) {
+      *outp[k] = nullptr;
+      continue;
+    }
+    cudaIpcMemHandle_t m;
+    memcpy(&m, in[k], sizeof m);
+    void* p = nullptr;
+    cudaError_t e = cudaIpcOpenMemHandle(&p, m, cudaIpcMemLazyEnablePeerAccess);
+    if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("cudaIpcOpenMemHandle: ") + cudaGetErrorString(e));
+    *outp[k] = (const uint8_t*)p;
+    *ipc[k] = true;
+  }
+  if ((h->rank > 0) != (h->xleft != nullptr) || (h->rank < h->world - 1) != (h->xright != nullptr))
+    return fail(h, DEM_EINVAL, "a rank needs exactly its existing neighbours");
+  h->connected = true;
+  destroy_graphs(h);
+  return DEM_OK;
+}
+
+int dem_connect_ptrs(dem_handle* h, void* left, void* right) {
+  if (!h) return DEM_EINVAL;
+  if (!h->slab) return fail(h, DEM_ESTATE, "not a slab rank");
+  h->xleft = (const uint8_t*)left;
+  h->xright = (const uint8_t*)right;
+  h->xleft_ipc = h->xright_ipc = false;
+  if ((h->rank > 0) != (h->xleft != nullptr) || (h->rank < h->world - 1) != (h->xright != nullptr))
+    return fail(h, DEM_EINVAL, "a rank needs exactly its existing neighbours");
+  h->connected = true;
+  destroy_graphs(h);
   return DEM_OK;
 }
 

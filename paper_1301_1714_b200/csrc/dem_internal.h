@@ -91,6 +91,54 @@ struct StepBuffers {
   DevErr* err;
 };
 
+// ---- slab exchange ------------------------------------------
+// Per rank an exchange region (cudaMalloc, shareable by CUDA IPC) holding, for
+// each direction d (0 = to the left neighbour, 1 = to the right) and step
+// parity p, a header and the packed migrants (state + history) and ghosts
+// (state) of that step. The neighbour reads it directly (peer memory).
+struct XHeader {
+  uint32_t tag;     // step number the data is for (published last, release/acquire)
+  uint32_t n_mig;   // migrants packed
+  uint32_t n_ghost; // ghosts packed
+  uint32_t pad;
+};
+struct XLayout {  // byte offsets inside one (direction, parity) block
+  uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, bytes;
+  uint32_t mig_cap, ghost_cap, K;
+  __host__ __device__ static XLayout make(uint32_t mig_cap, uint32_t ghost_cap, uint32_t K) {
+    XLayout L;
+    L.mig_cap = mig_cap;
+    L.ghost_cap = ghost_cap;
+    L.K = K;
+    uint64_t o = 0;
+    L.header = o;
+    o += 256;
+    L.mig_pos = o;
+    o += (uint64_t)mig_cap * 16;
+    L.mig_vel = o;
+    o += (uint64_t)mig_cap * 16;
+    L.mig_omg = o;
+    o += (uint64_t)mig_cap * 16;
+    L.mig_cnt = o;
+    o += ((uint64_t)mig_cap * 4 + 255) & ~255ull;
+    L.mig_hist = o;  // entry-major: [m * K + k]
+    o += (uint64_t)mig_cap * K * 16;
+    L.gh_pos = o;
+    o += (uint64_t)ghost_cap * 16;
+    L.gh_vel = o;
+    o += (uint64_t)ghost_cap * 16;
+    L.gh_omg = o;
+    o += (uint64_t)ghost_cap * 16;
+    L.bytes = (o + 4095) & ~4095ull;
+    return L;
+  }
+};
+struct XState {  // device scratch of the exchange of one step
+  uint32_t n_out;      // output slots of the last step (base of the appended slots)
+  uint32_t appended[4];  // migrants from left, right; ghosts from left, right
+  uint32_t pad[3];
+};
+
 enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5,
                 K_DETECT = 6 };
 
@@ -113,7 +161,10 @@ struct Probe {  // validation results of k_probe
 };
 int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out);
 int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
-                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank);
+                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank,
+                const uint32_t* dst = nullptr, const uint32_t* keep = nullptr);
+// initial exchange flags of the set state (slab mode)
+int launch_flags(cudaStream_t st, int64_t n, const float4* pos, DevGrid g, uint32_t* flags);
 int launch_count(cudaStream_t st, int64_t n, const uint32_t* key, uint32_t* count,
                  uint32_t* prank);
 int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen,
@@ -133,16 +184,26 @@ int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
 int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
                  const StepBuffers& b, const DevGrid& g, const DevPhys& ph, int variant);
 
+// Slab exchange. `mine` = this rank's exchange region; `left`/`right` = the
+// neighbours' regions (peer pointers, NULL at the ends of the domain).
+int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
+                 uint8_t* mine, XLayout L, uint32_t* tile_counts, XState* xs, int initial);
+int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
+                   uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
+                   uint32_t* nslots_out);
+// set_particles in slab mode: keep[i] = particle i's z-cell is owned by this rank.
+int launch_keep(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* keep);
+
 // Introspection / state movement.
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
                   const float4* omg, const float4* F, const float4* T, float* o_pos,
                   float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
                   float* o_F, float* o_T);
-int launch_emit_contacts(cudaStream_t st, int64_t n, uint32_t K, const float4* hist,
-                         const uint32_t* cnt, const uint32_t* base, const float4* omg,
-                         uint32_t* id_i, uint32_t* id_j, float* dt3);
+int launch_emit_contacts(cudaStream_t st, int64_t n, int64_t stride, uint32_t K,
+                         const float4* hist, const uint32_t* cnt, const uint32_t* base,
+                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3);
 int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* slot_of_id);
-int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, uint32_t K,
+int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride, uint32_t K,
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
                            uint32_t* flags);

@@ -133,18 +133,25 @@ __global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
 }
 
 __global__ void k_pack(int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel, float4* omg,
-                       uint32_t* key, uint32_t* count, uint32_t* prank) {
+                       uint32_t* key, uint32_t* count, uint32_t* prank, const uint32_t* dst,
+                       const uint32_t* keep) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  float r = in.radius ? in.radius[i] : in.def_radius;
-  float m = in.mass ? in.mass[i] : in.def_mass_coef * r * r * r;
-  float x = in.pos[3 * i], y = in.pos[3 * i + 1], z = in.pos[3 * i + 2];
+  const int64_t src = i;
+  if (keep) {  // slab mode: only this rank's particles, compacted in input order
+    if (!keep[i]) return;
+    i = dst[i];
+  }
+  const int64_t q = src;
+  float r = in.radius ? in.radius[q] : in.def_radius;
+  float m = in.mass ? in.mass[q] : in.def_mass_coef * r * r * r;
+  float x = in.pos[3 * q], y = in.pos[3 * q + 1], z = in.pos[3 * q + 2];
   pos[i] = make_float4(x, y, z, r);
-  vel[i] = in.vel ? make_float4(in.vel[3 * i], in.vel[3 * i + 1], in.vel[3 * i + 2], m)
+  vel[i] = in.vel ? make_float4(in.vel[3 * q], in.vel[3 * q + 1], in.vel[3 * q + 2], m)
                   : make_float4(0.f, 0.f, 0.f, m);
-  uint32_t id = in.id ? in.id[i] : (uint32_t)i;
+  uint32_t id = in.id ? in.id[q] : (uint32_t)q;
   omg[i] = in.omega
-               ? make_float4(in.omega[3 * i], in.omega[3 * i + 1], in.omega[3 * i + 2],
+               ? make_float4(in.omega[3 * q], in.omega[3 * q + 1], in.omega[3 * q + 2],
                              __uint_as_float(id))
                : make_float4(0.f, 0.f, 0.f, __uint_as_float(id));
   uint32_t k = cell_key(g, x, y, z);
@@ -1040,6 +1047,274 @@ void sweep_prepare(uint32_t K) {
   cudaFuncSetAttribute(k_force<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
 }
 
+// --------------------------------------------------------- slab exchange --
+// DESIGN.md §7. Slabs along z; each step ends with a deterministic pack of the
+// output slots flagged by the integrator (migrants with their history, and the
+// particles of the two boundary planes as the neighbours' ghosts) into this
+// rank's exchange region, published with a system-scope release of the step
+// tag; the next step starts by acquiring the neighbours' tags and appending
+// their migrants and ghosts straight from peer memory (CUDA IPC over
+// NVLink/NVSwitch, or the same device), in a fixed order (migrants from the
+// left, from the right, ghosts from the left, from the right) so the stable
+// sort that follows is deterministic.
+
+__device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
+  uint32_t v;
+  asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
+  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ int global_cz(const DevGrid& g, float z) {
+  return cell_coord(z, g.lo[2], g.inv_h, g.nz_global);
+}
+
+__global__ void k_keep(int64_t n, const float* pos, DevGrid g, uint32_t* keep) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cz = global_cz(g, pos[3 * i + 2]);
+  keep[i] = (cz >= g.z0 && cz < g.z1) ? 1u : 0u;
+}
+
+__global__ void k_flags(int64_t n, const float4* pos, DevGrid g, uint32_t* flags) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int cz = global_cz(g, pos[i].z);
+  flags[i] = (cz == g.z0 ? 4u : 0u) | (cz == g.z1 - 1 ? 8u : 0u);
+}
+
+constexpr int kXTile = 1024;  // output slots per pack tile (256 threads x 4)
+
+__device__ __forceinline__ uint32_t owned_out(const StepBuffers& b, const DevGrid& g) {
+  return __ldg(&b.off[g.own_c1]) - __ldg(&b.off[g.own_c0]);
+}
+
+// counts of the four categories per tile; also records n_out for the next unpack
+__global__ void __launch_bounds__(256) k_xpack_count(StepBuffers b, DevGrid g, uint32_t* tc,
+                                                     uint32_t ntiles, XState* xs, int initial) {
+  __shared__ uint32_t s_c[4];
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t n_out = initial ? xs->n_out : owned_out(b, g);
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !initial) xs->n_out = n_out;
+  if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
+  __syncthreads();
+  uint32_t c[4] = {0, 0, 0, 0};
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
+    if (o < n_out) {
+      const uint32_t f = b.flags[o];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) c[q] += (f >> q) & 1u;
+    }
+  }
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    uint32_t v = c[q];
+    for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+    if (lane_id() == 0) atomicAdd(&s_c[q], v);
+  }
+  __syncthreads();
+  if (threadIdx.x < 4) tc[threadIdx.x * ntiles + blockIdx.x] = s_c[threadIdx.x];
+}
+
+// deterministic placement: prefix over earlier tiles + in-tile rank (slot order)
+__global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, uint32_t K,
+                                                     uint32_t N, uint8_t* mine, XLayout L,
+                                                     const uint32_t* tc, uint32_t ntiles,
+                                                     XState* xs) {
+  __shared__ uint32_t s_base[4];
+  __shared__ uint32_t s_warp[4][8];
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t n_out = xs->n_out;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u;  // the step that will read it
+  const uint32_t par = tag & 1u;
+  if (threadIdx.x < 4) {
+    uint32_t acc = 0;
+    for (uint32_t t = 0; t < blockIdx.x; ++t) acc += tc[threadIdx.x * ntiles + t];
+    s_base[threadIdx.x] = acc;
+  }
+  __syncthreads();
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  for (int u = 0; u < 4; ++u) {
+    const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
+    const uint32_t f = o < n_out ? b.flags[o] : 0u;
+    uint32_t rank[4];
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t m = __ballot_sync(0xffffffffu, (f >> q) & 1u);
+      rank[q] = __popc(m & lanemask_lt());
+      if (lane == 0) s_warp[q][warp] = __popc(m);
+    }
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      uint32_t before = s_base[q];
+      for (uint32_t w = 0; w < warp; ++w) before += s_warp[q][w];
+      rank[q] += before;
+    }
+    if (f) {
+      const float4 P = b.pos_out[o], V = b.vel_out[o], W = b.omg_out[o];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!((f >> q) & 1u)) continue;
+        const int dir = q & 1;  // 0: to the left neighbour, 1: to the right
+        uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
+        const uint32_t e = rank[q];
+        if (q < 2) {  // migrant: state + history
+          if (e >= L.mig_cap) {
+            raise_error(b.err, 6u, o, __float_as_uint(W.w));
+            continue;
+          }
+          reinterpret_cast<float4*>(blk + L.mig_pos)[e] = P;
+          reinterpret_cast<float4*>(blk + L.mig_vel)[e] = V;
+          reinterpret_cast<float4*>(blk + L.mig_omg)[e] = W;
+          const uint32_t nc = b.cnt_out[o];
+          reinterpret_cast<uint32_t*>(blk + L.mig_cnt)[e] = nc;
+          float4* h = reinterpret_cast<float4*>(blk + L.mig_hist) + (size_t)e * K;
+          for (uint32_t k = 0; k < nc; ++k) h[k] = b.hist_out[(size_t)k * N + o];
+        } else {  // ghost: state only
+          if (e >= L.ghost_cap) {
+            raise_error(b.err, 6u, o, __float_as_uint(W.w));
+            continue;
+          }
+          reinterpret_cast<float4*>(blk + L.gh_pos)[e] = P;
+          reinterpret_cast<float4*>(blk + L.gh_vel)[e] = V;
+          reinterpret_cast<float4*>(blk + L.gh_omg)[e] = W;
+        }
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x < 4) {
+      uint32_t tot = 0;
+      for (int w = 0; w < 8; ++w) tot += s_warp[threadIdx.x][w];
+      s_base[threadIdx.x] += tot;
+    }
+    __syncthreads();
+  }
+}
+
+// header counts, then the tag with a system-scope release (the data above is
+// complete: this kernel starts after k_xpack_write finished)
+__global__ void k_xpublish(uint8_t* mine, XLayout L, const uint32_t* tc, uint32_t ntiles,
+                           DevErr* err) {
+  if (ld_volatile(&err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u;
+  const uint32_t par = tag & 1u;
+  uint32_t tot[4] = {0, 0, 0, 0};
+  for (int q = 0; q < 4; ++q)
+    for (uint32_t t = 0; t < ntiles; ++t) tot[q] += tc[q * ntiles + t];
+  for (int dir = 0; dir < 2; ++dir) {
+    XHeader* h = reinterpret_cast<XHeader*>(mine + (size_t)(dir * 2 + par) * L.bytes + L.header);
+    h->n_mig = tot[dir];
+    h->n_ghost = tot[2 + dir];
+    __threadfence_system();
+    st_release_sys(&h->tag, tag);
+  }
+}
+
+// acquire the neighbours' tags for this step; the base and counts of the
+// appended slots; capacity check
+__global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
+                        uint32_t* nslots, uint32_t cap, DevErr* err) {
+  __shared__ uint32_t s_cnt[4];
+  __shared__ uint32_t s_ok;
+  if (ld_volatile(&err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u;
+  const uint32_t par = tag & 1u;
+  if (threadIdx.x == 0) s_ok = 1u;
+  __syncthreads();
+  if (threadIdx.x < 2) {
+    // lane 0: the left neighbour's block "to the right"; lane 1: the right one's "to the left"
+    const uint8_t* peer = threadIdx.x == 0 ? left : right;
+    const int dir = threadIdx.x == 0 ? 1 : 0;
+    uint32_t nm = 0, ng = 0;
+    if (peer) {
+      const XHeader* h =
+          reinterpret_cast<const XHeader*>(peer + (size_t)(dir * 2 + par) * L.bytes + L.header);
+      unsigned long long spins = 0;
+      while (ld_acquire_sys(&h->tag) != tag) {
+        if (++spins > (1ull << 27)) {  // peer never published (~30 s): fail, do not hang
+          s_ok = 0u;
+          break;
+        }
+        __nanosleep(200);
+      }
+      nm = ld_volatile(&h->n_mig);
+      ng = ld_volatile(&h->n_ghost);
+    }
+    s_cnt[threadIdx.x] = nm;
+    s_cnt[2 + threadIdx.x] = ng;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    if (!s_ok) {
+      raise_error(err, 11u, 0u, 0u);
+      return;
+    }
+    const uint32_t base = xs->n_out;
+    const uint32_t tot = s_cnt[0] + s_cnt[1] + s_cnt[2] + s_cnt[3];
+    for (int q = 0; q < 4; ++q) xs->appended[q] = s_cnt[q];
+    if ((uint64_t)base + tot > cap) {
+      raise_error(err, 6u, base, 0u);
+      return;
+    }
+    *nslots = base + tot;
+  }
+}
+
+// append migrants (with history) and ghosts at slots n_out.., compute their
+// cell keys and count them into their cells for this step's sort
+__global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint32_t K, uint32_t N,
+                                                 const uint8_t* left, const uint8_t* right,
+                                                 XLayout L, const XState* xs) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u;
+  const uint32_t par = tag & 1u;
+  const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
+  const uint32_t c0 = xs->appended[0], c1 = xs->appended[1], c2 = xs->appended[2],
+                 c3 = xs->appended[3];
+  const uint32_t tot = c0 + c1 + c2 + c3;
+  if (i >= tot) return;
+  uint32_t q, e;
+  if (i < c0) { q = 0; e = i; }
+  else if (i < c0 + c1) { q = 1; e = i - c0; }
+  else if (i < c0 + c1 + c2) { q = 2; e = i - c0 - c1; }
+  else { q = 3; e = i - c0 - c1 - c2; }
+  const bool from_left = (q & 1u) == 0u;
+  const uint8_t* peer = from_left ? left : right;
+  const int dir = from_left ? 1 : 0;
+  const uint8_t* blk = peer + (size_t)(dir * 2 + par) * L.bytes;
+  const uint32_t slot = xs->n_out + i;
+  float4 P, V, W;
+  if (q < 2) {
+    P = __ldcv(reinterpret_cast<const float4*>(blk + L.mig_pos) + e);
+    V = __ldcv(reinterpret_cast<const float4*>(blk + L.mig_vel) + e);
+    W = __ldcv(reinterpret_cast<const float4*>(blk + L.mig_omg) + e);
+    const uint32_t nc = min(__ldcv(reinterpret_cast<const uint32_t*>(blk + L.mig_cnt) + e), K);
+    const float4* h = reinterpret_cast<const float4*>(blk + L.mig_hist) + (size_t)e * K;
+    float4* hist = const_cast<float4*>(b.hist_in);
+    for (uint32_t k = 0; k < nc; ++k) hist[(size_t)k * N + slot] = __ldcv(h + k);
+    const_cast<uint32_t*>(b.cnt_in)[slot] = nc;
+  } else {
+    P = __ldcv(reinterpret_cast<const float4*>(blk + L.gh_pos) + e);
+    V = __ldcv(reinterpret_cast<const float4*>(blk + L.gh_vel) + e);
+    W = __ldcv(reinterpret_cast<const float4*>(blk + L.gh_omg) + e);
+    const_cast<uint32_t*>(b.cnt_in)[slot] = 0u;
+  }
+  const_cast<float4*>(b.pos_in)[slot] = P;
+  const_cast<float4*>(b.vel_in)[slot] = V;
+  const_cast<float4*>(b.omg_in)[slot] = W;
+  uint32_t k2 = cell_key(g, P.x, P.y, P.z);
+  if (q < 2) {  // a migrant must land in this rank's owned planes (one plane per step)
+    const int cz = global_cz(g, P.z);
+    if (cz < g.z0 || cz >= g.z1) raise_error(b.err, 11u, slot, __float_as_uint(W.w));
+  }
+  const_cast<uint32_t*>(b.key_in)[slot] = k2;
+  b.prank[slot] = count_into_cell(b.count, k2);
+}
+
 // --------------------------------------------------- introspection ---------
 
 __global__ void k_unpack(int64_t n, bool by_id, const float4* pos, const float4* vel,
@@ -1061,15 +1336,15 @@ __global__ void k_unpack(int64_t n, bool by_id, const float4* pos, const float4*
   if (o_T && T) { float4 t = T[i]; o_T[3 * d] = t.x; o_T[3 * d + 1] = t.y; o_T[3 * d + 2] = t.z; }
 }
 
-__global__ void k_emit_contacts(int64_t n, uint32_t K, const float4* hist, const uint32_t* cnt,
-                                const uint32_t* base, const float4* omg, uint32_t* id_i,
-                                uint32_t* id_j, float* dt3) {
+__global__ void k_emit_contacts(int64_t n, int64_t stride, uint32_t K, const float4* hist,
+                                const uint32_t* cnt, const uint32_t* base, const float4* omg,
+                                uint32_t* id_i, uint32_t* id_j, float* dt3) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t c = cnt[i], o = base[i];
   const uint32_t me = __float_as_uint(omg[i].w);
   for (uint32_t k = 0; k < c && k < K; ++k) {
-    const float4 h = hist[(size_t)k * n + i];
+    const float4 h = hist[(size_t)k * stride + i];
     if (id_i) id_i[o + k] = me;
     if (id_j) id_j[o + k] = __float_as_uint(h.w);
     if (dt3) { dt3[3 * (o + k)] = h.x; dt3[3 * (o + k) + 1] = h.y; dt3[3 * (o + k) + 2] = h.z; }
@@ -1083,7 +1358,8 @@ __global__ void k_slot_of_id(int64_t n, const float4* omg, uint32_t* slot_of_id)
 }
 
 // flags[0] |= 1: id out of range, |= 2: capacity overflow
-__global__ void k_insert_contacts(int64_t m, int64_t n, uint32_t K, const uint32_t* id_i,
+__global__ void k_insert_contacts(int64_t m, int64_t n, int64_t stride, uint32_t K,
+                                  const uint32_t* id_i,
                                   const uint32_t* id_j, const float* dt3,
                                   const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
                                   uint32_t* flags) {
@@ -1094,7 +1370,7 @@ __global__ void k_insert_contacts(int64_t m, int64_t n, uint32_t K, const uint32
   const uint32_t s = slot_of_id[a];
   const uint32_t k = atomicAdd(&cnt[s], 1u);
   if (k >= K) { atomicOr(flags, 2u); return; }
-  hist[(size_t)k * n + s] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
+  hist[(size_t)k * stride + s] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
                                         __uint_as_float(id_j[e]));
 }
 
@@ -1129,9 +1405,11 @@ int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out) {
 }
 
 int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
-                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank) {
+                float4* omg, uint32_t* key, uint32_t* count, uint32_t* prank, const uint32_t* dst,
+                const uint32_t* keep) {
   if (n <= 0) return K_HASH;
-  k_pack<<<blocks_for(n, 256), 256, 0, st>>>(n, in, g, pos, vel, omg, key, count, prank);
+  k_pack<<<blocks_for(n, 256), 256, 0, st>>>(n, in, g, pos, vel, omg, key, count, prank, dst,
+                                              keep);
   return K_HASH;
 }
 
@@ -1220,6 +1498,37 @@ int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
   return K_SWEEP;
 }
 
+int launch_keep(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* keep) {
+  if (n <= 0) return K_OTHER;
+  k_keep<<<blocks_for(n, 256), 256, 0, st>>>(n, pos, g, keep);
+  return K_OTHER;
+}
+
+int launch_flags(cudaStream_t st, int64_t n, const float4* pos, DevGrid g, uint32_t* flags) {
+  if (n <= 0) return K_OTHER;
+  k_flags<<<blocks_for(n, 256), 256, 0, st>>>(n, pos, g, flags);
+  return K_OTHER;
+}
+
+// initial = 1: publish the state set by dem_set_particles (xs->n_out preset)
+int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
+                 uint8_t* mine, XLayout L, uint32_t* tile_counts, XState* xs, int initial) {
+  const uint32_t ntiles = (uint32_t)((cap + kXTile - 1) / kXTile);
+  k_xpack_count<<<ntiles, 256, 0, st>>>(b, g, tile_counts, ntiles, xs, initial);
+  k_xpack_write<<<ntiles, 256, 0, st>>>(b, g, K, (uint32_t)cap, mine, L, tile_counts, ntiles, xs);
+  k_xpublish<<<1, 1, 0, st>>>(mine, L, tile_counts, ntiles, b.err);
+  return K_OTHER;
+}
+
+int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
+                   uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
+                   uint32_t* nslots_out) {
+  k_xwait<<<1, 32, 0, st>>>(left, right, L, xs, nslots_out, (uint32_t)cap, b.err);
+  const uint32_t most = 2 * L.mig_cap + 2 * L.ghost_cap;
+  k_xappend<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs);
+  return K_OTHER;
+}
+
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
                   const float4* omg, const float4* F, const float4* T, float* o_pos,
                   float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
@@ -1230,12 +1539,12 @@ int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, con
   return K_OTHER;
 }
 
-int launch_emit_contacts(cudaStream_t st, int64_t n, uint32_t K, const float4* hist,
-                         const uint32_t* cnt, const uint32_t* base, const float4* omg,
-                         uint32_t* id_i, uint32_t* id_j, float* dt3) {
+int launch_emit_contacts(cudaStream_t st, int64_t n, int64_t stride, uint32_t K,
+                         const float4* hist, const uint32_t* cnt, const uint32_t* base,
+                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3) {
   if (n <= 0) return K_OTHER;
-  k_emit_contacts<<<blocks_for(n, 256), 256, 0, st>>>(n, K, hist, cnt, base, omg, id_i, id_j,
-                                                      dt3);
+  k_emit_contacts<<<blocks_for(n, 256), 256, 0, st>>>(n, stride, K, hist, cnt, base, omg, id_i,
+                                                      id_j, dt3);
   return K_OTHER;
 }
 
@@ -1245,13 +1554,13 @@ int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* s
   return K_OTHER;
 }
 
-int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, uint32_t K,
+int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride, uint32_t K,
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
                            uint32_t* flags) {
   if (m <= 0) return K_OTHER;
-  k_insert_contacts<<<blocks_for(m, 256), 256, 0, st>>>(m, n, K, id_i, id_j, dt3, slot_of_id,
-                                                        hist, cnt, flags);
+  k_insert_contacts<<<blocks_for(m, 256), 256, 0, st>>>(m, n, stride, K, id_i, id_j, dt3,
+                                                        slot_of_id, hist, cnt, flags);
   return K_OTHER;
 }
 

@@ -23,6 +23,7 @@ LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
 DEM_ABI_VERSION = 1
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
 DEM_EOVERFLOW, DEM_ENONFINITE, DEM_EESCAPED, DEM_ECOINCIDENT, DEM_ESTATE = -6, -7, -8, -9, -10
+DEM_EPEER = -11
 DEM_MODEL_PRACTICAL, DEM_MODEL_SIMPLE = 0, 1
 DEM_F_TRUNCATE_DT, DEM_F_CLAMP_FN, DEM_F_DIAG, DEM_F_ASYNC, DEM_F_NO_GRAPH = 1, 2, 4, 8, 16
 DEM_F_THREAD_PER_PARTICLE = 32
@@ -98,6 +99,10 @@ def lib() -> C.CDLL:
         L.dem_get_stats.argtypes = [VP, C.POINTER(DemStats)]
         L.dem_profile.argtypes = [VP, I32]
         L.dem_nccl_unique_id.argtypes = [VP]
+        L.dem_exchange_handle.argtypes = [VP, P]
+        L.dem_exchange_ptr.argtypes = [VP, C.POINTER(VP)]
+        L.dem_connect.argtypes = [VP, P, P]
+        L.dem_connect_ptrs.argtypes = [VP, VP, VP]
         L.dem_strerror.argtypes = [C.c_int]
         L.dem_strerror.restype = C.c_char_p
         L.dem_last_error.argtypes = [VP]
@@ -111,7 +116,8 @@ def _f32(x) -> float:
 
 
 def params_from(sp, *, flags: int = 0, device: int = -1, stream=None, allocator=None,
-                radius: Optional[float] = None, density: float = 2500.0) -> DemParams:
+                radius: Optional[float] = None, density: float = 2500.0, rank: int = 0,
+                world: int = 1) -> DemParams:
     """dem_params from a scenes.SimParams-like object."""
     p = DemParams()
     p.abi_version = DEM_ABI_VERSION
@@ -135,7 +141,7 @@ def params_from(sp, *, flags: int = 0, device: int = -1, stream=None, allocator=
     p.device = device
     p.stream = stream
     p.allocator = allocator
-    p.rank, p.world_size = 0, 1
+    p.rank, p.world_size = rank, world
     return p
 
 
@@ -179,7 +185,7 @@ class Dem:
 
     def __init__(self, sp, *, flags: int = 0, device: int = 0, stream=None,
                  torch_allocator: bool = True, radius: Optional[float] = None,
-                 density: float = 2500.0):
+                 density: float = 2500.0, rank: int = 0, world: int = 1):
         L = lib()
         self._keep = []
         alloc_p = None
@@ -205,7 +211,9 @@ class Dem:
             self._keep += [A, _alloc, _free]
             alloc_p = C.pointer(A)
         self.params = params_from(sp, flags=flags, device=device, stream=stream_ptr,
-                                  allocator=alloc_p, radius=radius, density=density)
+                                  allocator=alloc_p, radius=radius, density=density, rank=rank,
+                                  world=world)
+        self.rank, self.world = rank, world
         self.flags = self.params.flags
         h = C.c_void_p()
         rc = L.dem_create(C.byref(self.params), C.byref(h))
@@ -238,7 +246,8 @@ class Dem:
 
     # ---------------------------------------------------------- set ----
     def set_particles(self, pos, vel=None, omega=None, radius=None, mass=None, id=None):
-        """dem_set_particles: numpy arrays (host) or CUDA tensors (device)."""
+        """dem_set_particles: numpy arrays (host) or CUDA tensors (device). A slab
+        rank keeps its own particles of the given set."""
         device = _is_torch(pos) and pos.is_cuda
         n = int(pos.shape[0]) if pos is not None else 0
         args = [_Arg(pos, np.float32, device=device), _Arg(vel, np.float32, device=device),
@@ -247,7 +256,7 @@ class Dem:
         P = DemParticles(DEM_MEM_DEVICE if device else DEM_MEM_HOST, *(a.ptr for a in args),
                          None, None)
         self._check(lib().dem_set_particles(self.h, n, C.byref(P)), "dem_set_particles")
-        self.n = n
+        self.n = n if self.world == 1 else int(self.stats()["n"])
 
     def set_contacts(self, id_i, id_j, dt3):
         """dem_set_contacts: (id_i, id_j, δ_t) triples (Eq. 7's δ_t,old)."""
@@ -263,12 +272,43 @@ class Dem:
     def step(self, nsteps: int = 1):
         """dem_step: advance nsteps timesteps."""
         self._check(lib().dem_step(self.h, int(nsteps)), "dem_step")
+        if self.world > 1:
+            self.n = int(self.stats()["n"])
 
     def sync(self):
         self._check(lib().dem_sync(self.h), "dem_sync")
 
     def profile(self, enable: bool = True):
         self._check(lib().dem_profile(self.h, 1 if enable else 0), "dem_profile")
+
+    # -------------------------------------------------------- slabs ----
+    def exchange_handle(self) -> bytes:
+        """dem_exchange_handle: 64-byte CUDA IPC handle of this rank's exchange region."""
+        buf = C.create_string_buffer(64)
+        self._check(lib().dem_exchange_handle(self.h, buf), "dem_exchange_handle")
+        return buf.raw
+
+    def exchange_ptr(self) -> int:
+        p = C.c_void_p()
+        self._check(lib().dem_exchange_ptr(self.h, C.byref(p)), "dem_exchange_ptr")
+        return p.value
+
+    def connect(self, left: Optional[bytes], right: Optional[bytes]):
+        """dem_connect: the neighbours' IPC handles (None at the domain ends)."""
+        lb = C.create_string_buffer(left, 64) if left else None
+        rb = C.create_string_buffer(right, 64) if right else None
+        self._check(lib().dem_connect(self.h, lb, rb), "dem_connect")
+
+    def connect_local(self, left: Optional["Dem"], right: Optional["Dem"]):
+        """dem_connect_ptrs: same-process neighbours."""
+        self._check(lib().dem_connect_ptrs(self.h, left.exchange_ptr() if left else None,
+                                           right.exchange_ptr() if right else None),
+                    "dem_connect_ptrs")
+
+    def connect_group(self, group=None):
+        """Exchange IPC handles over torch.distributed (any backend) and connect."""
+        from .slabs import neighbour_handles
+        self.connect(*neighbour_handles(self.rank, self.world, self.exchange_handle(), group))
 
     # ---------------------------------------------------------- get ----
     def get_state(self, order: int = DEM_ORDER_INTERNAL, forces: bool = False,

@@ -1,0 +1,180 @@
+"""GPU tests of the slab decomposition on one B200:
+P slab ranks as separate handles — in one process (neighbours connected by
+device pointer) and in two processes (connected by CUDA IPC handles, the
+multi-GPU transport) — against the fp64 oracle on the gathered state, and
+against the single-GPU path. Run via gpurun: python -m pytest tests -m gpu."""
+import multiprocessing as mp
+
+import numpy as np
+import pytest
+
+from oracle import oracle as orc
+from paper_1301_1714_b200 import scenes as S
+from paper_1301_1714_b200.dem import DEM_F_DIAG, Dem
+
+from .parity import assert_T2_forces, assert_T2_history
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def cuda():
+    torch = pytest.importorskip("torch")
+    if not torch.cuda.is_available():
+        pytest.fail("CUDA device required for -m gpu tests")
+    return torch
+
+
+def fast_gas(seed=3, n=6000):
+    """Dense polydisperse gas with fast particles: migrations every step."""
+    return S.random_gas(n, 18.0, seed, r_range=(0.3e-3, 0.5e-3), v_sigma=3.0, w_sigma=50.0,
+                        params=S.SimParams(max_contacts=32, gravity=(0.0, -9.81, 0.0)))
+
+
+def make_slabs(sc, P, flags=DEM_F_DIAG):
+    ds = [Dem(sc.params, flags=flags, rank=r, world=P) for r in range(P)]
+    for d in ds:
+        d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    for r, d in enumerate(ds):
+        d.connect_local(ds[r - 1] if r > 0 else None, ds[r + 1] if r < P - 1 else None)
+    return ds
+
+
+def step_all(ds, n=1):
+    for _ in range(n):
+        for d in ds:
+            d.step(1)
+
+
+def union_state(ds, forces=False):
+    parts = [d.get_state(forces=forces) for d in ds]
+    cat = {k: np.concatenate([p[k] for p in parts]) for k in parts[0]}
+    o = np.argsort(cat["id"], kind="stable")
+    return {k: v[o] for k, v in cat.items()}
+
+
+def union_contacts(ds):
+    out = {}
+    for d in ds:
+        a, b, v = d.get_contacts()
+        for x, y, z in zip(a, b, v):
+            key = (int(x), int(y))
+            assert key not in out  # each particle is reported by exactly one rank
+            out[key] = z.astype(np.float64)
+    return out
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_partition_is_exact(P):
+    sc = S.C2()
+    ds = make_slabs(sc, P)
+    ns = [d.n for d in ds]
+    assert sum(ns) == sc.n and min(ns) > 0
+    u = union_state(ds)
+    assert np.array_equal(u["id"], np.sort(sc.id))
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_slab_steps_match_oracle(P):
+    """Every step, the union of the ranks' outputs equals one oracle step of the
+    union of their inputs: same contact pairs bit-exactly, T2 forces/torques,
+    with particles migrating between slabs."""
+    sc = fast_gas()
+    p = orc.make_params(sc.params, sc.radius)
+    ds = make_slabs(sc, P)
+    migrated = 0
+    owner = {int(i): r for r, d in enumerate(ds) for i in d.get_state()["id"]}
+    for k in range(6):
+        u = union_state(ds)
+        st = orc.State.from_arrays(u["pos"], u["vel"], u["omega"], u["radius"], u["mass"], u["id"])
+        c = union_contacts(ds) if k else {}
+        if c:
+            keys = sorted(c)
+            h = orc.History.from_pairs(st.id, 32, [a for a, _ in keys], [b for _, b in keys],
+                                       np.array([c[x] for x in keys]))
+        else:
+            h = orc.History.empty(st.n, 32)
+        step_all(ds)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        g = union_state(ds, forces=True)
+        o = np.argsort(st.id)  # oracle output (its sorted order) -> id order
+        assert np.array_equal(g["id"], st.id[o])
+
+        class R:  # the oracle result in id order
+            F, T, Fabs, Tabs = res.F[o], res.T[o], res.Fabs[o], res.Tabs[o]
+        assert_T2_forces(g["force"], g["torque"], R, what=f"P={P} step {k + 1}")
+        assert_T2_history(union_contacts(ds), h.as_dict(st.id))
+        now = {int(i): r for r, d in enumerate(ds) for i in d.get_state()["id"]}
+        migrated += sum(1 for i in now if now[i] != owner[i])
+        owner = now
+    assert migrated > 0  # the test exercised migration
+
+
+def test_slabs_agree_with_single_gpu():
+    sc = S.C2()
+    one = Dem(sc.params, flags=DEM_F_DIAG)
+    one.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    ds = make_slabs(sc, 3)
+    one.step(1)
+    step_all(ds)
+    a = one.get_state(forces=True)
+    o = np.argsort(a["id"])
+    a = {k: v[o] for k, v in a.items()}
+    b = union_state(ds, forces=True)
+    assert np.array_equal(a["id"], b["id"])
+    scale = np.abs(a["force"]).max()
+    assert np.abs(a["force"] - b["force"]).max() <= 1e-5 * scale
+    ca = {}
+    for x, y, z in zip(*one.get_contacts()):
+        ca[(int(x), int(y))] = z
+    assert ca.keys() == union_contacts(ds).keys()
+
+
+def test_slab_run_is_deterministic():
+    sc = fast_gas(seed=9, n=4000)
+    runs = []
+    for _ in range(2):
+        ds = make_slabs(sc, 2, flags=0)
+        step_all(ds, 15)
+        runs.append(union_state(ds))
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(runs[0][k], runs[1][k])
+
+
+def _ipc_rank(rank, world, q_out, q_in, steps, result):
+    import torch  # noqa: F401  (CUDA context in the child)
+    sc = fast_gas(seed=9, n=4000)
+    d = Dem(sc.params, flags=0, rank=rank, world=world, torch_allocator=False)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    q_out.put((rank, d.exchange_handle()))
+    handles = dict([q_in.get() for _ in range(world - 1)])
+    d.connect(handles.get(rank - 1), handles.get(rank + 1))
+    d.step(steps)
+    s = d.get_state()
+    result.put((rank, {k: v.copy() for k, v in s.items()}))
+
+
+def test_two_process_ipc_matches_single_process():
+    """The CUDA IPC transport (two processes sharing the GPU, as two GPUs
+    would over NVLink) reproduces the in-process slab run bitwise."""
+    ctx = mp.get_context("spawn")
+    q0, q1, res = ctx.Queue(), ctx.Queue(), ctx.Queue()
+    steps = 15
+    # rank r publishes on q_r and reads the other's
+    procs = [ctx.Process(target=_ipc_rank, args=(0, 2, q0, q1, steps, res)),
+             ctx.Process(target=_ipc_rank, args=(1, 2, q1, q0, steps, res))]
+    for p in procs:
+        p.start()
+    parts = dict(res.get(timeout=600) for _ in procs)
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    cat = {k: np.concatenate([parts[0][k], parts[1][k]]) for k in parts[0]}
+    o = np.argsort(cat["id"], kind="stable")
+    ipc = {k: v[o] for k, v in cat.items()}
+    ds = make_slabs(fast_gas(seed=9, n=4000), 2, flags=0)
+    step_all(ds, steps)
+    ref = union_state(ds)
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(ipc[k], ref[k])
