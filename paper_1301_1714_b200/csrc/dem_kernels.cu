@@ -572,15 +572,17 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       raise_error(b.err, 8u, j, my_id);
     k2 = cell_key(g, x, y, z);  // step 2 of the next step: CM of the new position
     if (g.slab) {
-      // slab exchange flags: leaving the owned planes = migrant
-      // (its key becomes the trash cell); on a boundary plane = ghost for the neighbour
+      // slab exchange flags: leaving the owned planes = migrant;
+      // on a boundary plane = ghost for the neighbour. A migrant keeps its key:
+      // it lands in this rank's ghost plane, where this rank's boundary
+      // particles need it as a neighbour next step (the receiver, which did
+      // not own it when it packed its ghosts, cannot send it back in time).
       const int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz_global);
       uint32_t f = 0;
       if (cz < g.z0) f |= 1u;
       if (cz >= g.z1) f |= 2u;
       if (cz == g.z0) f |= 4u;
       if (cz == g.z1 - 1) f |= 8u;
-      if (f & 3u) k2 = g.trash;
       b.flags[j] = f;
     }
   }
