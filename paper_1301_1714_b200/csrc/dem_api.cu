@@ -75,6 +75,8 @@ struct dem_handle {
   const uint8_t* xright = nullptr;
   bool xleft_ipc = false, xright_ipc = false;
   bool connected = false;
+  uint32_t xbase = 0;  // exchange tag offset of the current set (same sequence on every rank)
+  uint32_t nsets = 0;
   XState* xs = nullptr;
   uint32_t* xtiles = nullptr;  // pack tile counts [4][ntiles]
 
@@ -597,6 +599,10 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     g.own_c0 = (uint32_t)(z0 - g.zlo) * plane;
     g.own_c1 = (uint32_t)(z1 - g.zlo) * plane;
     g.slab = 1;
+    // tags continue across re-sets, so a neighbour never mistakes an old
+    // publication for the new one (every rank runs the same set/step sequence)
+    if (h->nsets++ > 0) h->xbase += (uint32_t)h->steps + 2u;
+    g.xbase = h->xbase;
     // this rank's particles, compacted in input order (deterministic)
     unsigned long long* st_tiles = nullptr;
     uint32_t* ctr = nullptr;
@@ -653,6 +659,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
       if (h->xregion) cudaFree(h->xregion);
       h->xregion = nullptr;
+      h->connected = false;  // the neighbours must reconnect to the new region
       if (cudaMalloc((void**)&h->xregion, 4 * h->xl.bytes) != cudaSuccess) ok = false;
       else cudaMemset(h->xregion, 0, 4 * h->xl.bytes);
     }

@@ -30,8 +30,9 @@ struct DevGrid {
   int z0, z1;        // global z range [z0, z1) owned by this rank (single GPU: [0, nz))
   uint32_t own_c0, own_c1;  // local cells of the owned planes: owned sorted slots are
                             // [off[own_c0], off[own_c1])
-  uint32_t trash;    // key of particles that left the slab (slab mode), else ncells
+  uint32_t trash;    // key of particles outside the local grid (slab mode), else ncells
   int slab;          // 1: slab decomposition active
+  uint32_t xbase;    // slab exchange tags = xbase + step number (distinct across re-sets)
 };
 
 struct DevPhys {

@@ -1130,7 +1130,7 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
   __shared__ uint32_t s_warp[4][8];
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t n_out = xs->n_out;
-  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u;  // the step that will read it
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
   const uint32_t par = tag & 1u;
   if (threadIdx.x < 4) {
     uint32_t acc = 0;
@@ -1200,9 +1200,9 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
 // header counts, then the tag with a system-scope release (the data above is
 // complete: this kernel starts after k_xpack_write finished)
 __global__ void k_xpublish(uint8_t* mine, XLayout L, const uint32_t* tc, uint32_t ntiles,
-                           DevErr* err) {
+                           DevErr* err, uint32_t xbase) {
   if (ld_volatile(&err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u;
+  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u + xbase;
   const uint32_t par = tag & 1u;
   uint32_t tot[4] = {0, 0, 0, 0};
   for (int q = 0; q < 4; ++q)
@@ -1219,11 +1219,11 @@ __global__ void k_xpublish(uint8_t* mine, XLayout L, const uint32_t* tc, uint32_
 // acquire the neighbours' tags for this step; the base and counts of the
 // appended slots; capacity check
 __global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
-                        uint32_t* nslots, uint32_t cap, DevErr* err) {
+                        uint32_t* nslots, uint32_t cap, DevErr* err, uint32_t xbase) {
   __shared__ uint32_t s_cnt[4];
   __shared__ uint32_t s_ok;
   if (ld_volatile(&err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u;
+  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u + xbase;
   const uint32_t par = tag & 1u;
   if (threadIdx.x == 0) s_ok = 1u;
   __syncthreads();
@@ -1272,7 +1272,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
                                                  const uint8_t* left, const uint8_t* right,
                                                  XLayout L, const XState* xs) {
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;
   const uint32_t par = tag & 1u;
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   const uint32_t c0 = xs->appended[0], c1 = xs->appended[1], c2 = xs->appended[2],
@@ -1518,14 +1518,14 @@ int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGr
   const uint32_t ntiles = (uint32_t)((cap + kXTile - 1) / kXTile);
   k_xpack_count<<<ntiles, 256, 0, st>>>(b, g, tile_counts, ntiles, xs, initial);
   k_xpack_write<<<ntiles, 256, 0, st>>>(b, g, K, (uint32_t)cap, mine, L, tile_counts, ntiles, xs);
-  k_xpublish<<<1, 1, 0, st>>>(mine, L, tile_counts, ntiles, b.err);
+  k_xpublish<<<1, 1, 0, st>>>(mine, L, tile_counts, ntiles, b.err, g.xbase);
   return K_OTHER;
 }
 
 int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
                    uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
                    uint32_t* nslots_out) {
-  k_xwait<<<1, 32, 0, st>>>(left, right, L, xs, nslots_out, (uint32_t)cap, b.err);
+  k_xwait<<<1, 32, 0, st>>>(left, right, L, xs, nslots_out, (uint32_t)cap, b.err, g.xbase);
   const uint32_t most = 2 * L.mig_cap + 2 * L.ghost_cap;
   k_xappend<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs);
   return K_OTHER;

@@ -178,3 +178,20 @@ def test_two_process_ipc_matches_single_process():
     ref = union_state(ds)
     for k in ("pos", "vel", "omega", "id"):
         assert np.array_equal(ipc[k], ref[k])
+
+
+def test_reset_particles_between_runs():
+    """Setting the particles again restarts every rank; stale publications of
+    the previous run are never taken for the new one (exchange tag epochs)."""
+    sc = fast_gas(seed=4, n=3000)
+    ds = make_slabs(sc, 2, flags=0)
+    step_all(ds, 3)
+    for d in ds:
+        d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    step_all(ds, 5)
+    a = union_state(ds)
+    fresh = make_slabs(sc, 2, flags=0)
+    step_all(fresh, 5)
+    b = union_state(fresh)
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(a[k], b[k])
