@@ -239,8 +239,13 @@ def run_ours(args):
     from paper_1301_1714_b200.dem import DEM_F_NO_GRAPH, Dem
 
     rank, world, local = dist_env()
+    # DEM_BENCH_SHARE_GPU=1: all ranks on cuda:0 with a gloo group — a functional
+    # check of the multi-rank path on a one-GPU box (timings are not meaningful)
+    share = os.environ.get("DEM_BENCH_SHARE_GPU") == "1"
+    if share:
+        local = 0
     if world > 1:
-        dist.init_process_group("nccl", init_method="env://")
+        dist.init_process_group("gloo" if share else "nccl", init_method="env://")
     torch.cuda.set_device(local)
     peak_gbs, peak_src = load_peaks()
     stream = torch.cuda.Stream()
@@ -290,7 +295,7 @@ def run_ours(args):
     ms_max = ms
     ms_graph_max = ms_graph
     if world > 1:
-        t = torch.tensor([ms, ms_graph], device="cuda")
+        t = torch.tensor([ms, ms_graph], device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms_max, ms_graph_max = float(t[0]), float(t[1])
 
