@@ -35,7 +35,7 @@ sys.path.insert(0, ROOT)
 
 METRIC = "particle-steps/sec (ms/step) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "particle-steps/s"
-KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect")
+KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
 
 
 def load_peaks():
@@ -134,16 +134,18 @@ def describe(sc) -> str:
 def alg_bytes(model: str, rho_c: float, c_bar: float):
     """Algorithmic bytes per particle-step.
 
-    k_force (steps 7-8 and 1, the dominant kernel): state read + write 96,
-    SCCM read 4, next CM write 4, history counts r+w 8, history entries r+w
-    32 c_bar -> 112 + 32 c_bar (practical); simple model (no history, no spin
-    update): position + velocity r+w 64, radius/mass/id carried 16, SCCM 4,
-    CM 4 -> 88.
+    The sweep (steps 5-8 and 1: detection, contact forces, walls, integration
+    — k_detect_half + k_pair + k_finish, the dominant part of the step): state
+    read + write 96, SCCM read 4, next CM write 4, cell offsets read 4 rho_c,
+    history counts r+w 8, history entries r+w 32 c_bar -> 112 + 4 rho_c +
+    32 c_bar (practical); simple model (no history, no spin update):
+    position + velocity r+w 64, radius/mass/id carried 16, SCCM 4, CM 4,
+    offsets 4 rho_c -> 88 + 4 rho_c.
     Whole step: 120 + 8 rho_c + 32 c_bar (practical),
     88 + 8 rho_c (simple)."""
     if model == "practical":
-        return 112 + 32 * c_bar, 120 + 8 * rho_c + 32 * c_bar
-    return 88.0, 88 + 8 * rho_c
+        return 112 + 4 * rho_c + 32 * c_bar, 120 + 8 * rho_c + 32 * c_bar
+    return 88 + 4 * rho_c, 88 + 8 * rho_c
 
 
 # ------------------------------------------------------- reference arm -----
@@ -256,9 +258,9 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        from paper_1301_1714_b200.dem import DEM_F_FORCE_LISTS_TPP, DEM_F_THREAD_PER_PARTICLE
+        from paper_1301_1714_b200.dem import DEM_F_FULL_LISTS, DEM_F_THREAD_PER_PARTICLE
         d = Dem(sc.params, device=local, stream=stream, rank=rank, world=world,
-                flags={"warp": 0, "lists": DEM_F_FORCE_LISTS_TPP,
+                flags={"half": 0, "full": DEM_F_FULL_LISTS,
                        "tpp": DEM_F_THREAD_PER_PARTICLE}[args.sweep])
         # every rank passes the whole set; a slab rank keeps its own planes
         d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
@@ -310,16 +312,16 @@ def run_ours(args):
     n_local = int(d.stats()["n"]) if world > 1 else sc.n
     rho_c = stats0["ncells"] / max(1, n_local)
     b_sweep, b_step = alg_bytes(sc.params.model, rho_c, c_bar)
-    sweep_ms = st["kernel_ms"]["sweep"] / max(1, st["kernel_count"]["sweep"])
-    achieved = b_sweep * n_local / (sweep_ms * 1e-3) / 1e9
     kernel_avg = {k: (st["kernel_ms"][k] / st["kernel_count"][k]) if st["kernel_count"][k] else 0.0
                   for k in KERNELS}
+    sweep_ms = kernel_avg["detect"] + kernel_avg["sweep"] + kernel_avg["finish"]
+    achieved = b_sweep * n_local / (sweep_ms * 1e-3) / 1e9
     step_kernel_ms = sum(kernel_avg.values())
     traffic = None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.model}.json")
     if os.path.exists(tr_path):
         try:
-            traffic = json.load(open(tr_path)).get("force_dram_bytes_per_launch")
+            traffic = json.load(open(tr_path)).get("sweep_dram_bytes_per_step")
         except Exception:
             traffic = None
     line = {
@@ -338,10 +340,14 @@ def run_ours(args):
             "dt": sc.params.dt, "sweep": args.sweep,
         },
         "roofline": {
-            "bound": "hbm", "kernel": "k_force", "achieved": achieved, "peak": peak_gbs,
+            "bound": "hbm",
+            "kernel": {"half": "sweep = k_detect_half + k_pair + k_finish",
+                       "full": "sweep = k_detect + k_force",
+                       "tpp": "sweep = k_sweep_tpp"}[args.sweep],
+            "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
             "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
-            "kernel_ms_avg": sweep_ms, "kernel_share_of_step": kernel_avg["sweep"] / step_kernel_ms
+            "kernel_ms_avg": sweep_ms, "kernel_share_of_step": sweep_ms / step_kernel_ms
             if step_kernel_ms else None,
             "step_alg_bytes_per_particle": b_step,
             "step_frac": b_step * n_local / (ms_step * 1e-3) / 1e9 / peak_gbs,
@@ -428,9 +434,9 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="warp", choices=["warp", "lists", "tpp"],
-                    help="detect + warp-flattened force rounds (default), detect + thread-per-"
-                         "particle force over the lists, or the paper's fused thread-per-particle")
+    ap.add_argument("--sweep", default="half", choices=["half", "full", "tpp"],
+                    help="half contact lists, each pair once (default); full lists with "
+                         "warp-flattened force rounds; or the paper's fused thread per particle")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

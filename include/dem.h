@@ -79,8 +79,9 @@ enum dem_flags {
   DEM_F_NO_GRAPH = 1u << 4,    /* launch kernels eagerly instead of replaying a CUDA graph */
   DEM_F_THREAD_PER_PARTICLE = 1u << 5, /* ablation: the paper's mapping, detection and forces
                                           in one thread-per-particle kernel */
-  DEM_F_FORCE_LISTS_TPP = 1u << 6, /* ablation: the force kernel with one thread per particle
-                                      over its contact list (default: warp-flattened rounds) */
+  DEM_F_FULL_LISTS = 1u << 6, /* ablation: every contact evaluated from both sides (full
+                                 contact lists, warp-flattened force rounds); default: half
+                                 lists, each pair evaluated once (Newton's third law) */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
@@ -164,8 +165,10 @@ typedef struct {
 
 /* Kernel indices of dem_stats.kernel_ms. */
 enum dem_kernel { DEM_K_HASH = 0, DEM_K_SCAN = 1, DEM_K_SCATTER = 2, DEM_K_RANK = 3,
-                  DEM_K_SWEEP = 4 /* force + integrate */, DEM_K_OTHER = 5,
-                  DEM_K_DETECT = 6 /* candidates -> contact lists */ };
+                  DEM_K_SWEEP = 4 /* contact forces (k_pair, or the fused sweep) */,
+                  DEM_K_OTHER = 5 /* slab exchange, introspection */,
+                  DEM_K_DETECT = 6 /* contact detection */,
+                  DEM_K_FINISH = 7 /* per-particle sums, walls, integration */ };
 
 /* Create a handle: validates params (DEM_EINVAL/DEM_EABI), selects the device
  * and stream. Grid and buffers are sized by dem_set_particles. *out = NULL on

@@ -54,6 +54,10 @@ struct dem_handle {
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
   float4* pos_sorted = nullptr;
   uint32_t *clist = nullptr, *ccount = nullptr;
+  uint8_t* cpos = nullptr;
+  uint32_t *lcount = nullptr, *llist = nullptr;
+  float4 *R0 = nullptr, *Fup = nullptr, *Tup = nullptr;
+  float2* R1 = nullptr;
   uint32_t* nslots = nullptr;  // device: input slots of the next step
   uint32_t* flags = nullptr;   // slab mode
   float4 *F = nullptr, *T = nullptr;
@@ -172,6 +176,10 @@ void free_buffers(dem_handle* h) {
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
+  h->cpos = nullptr;
+  h->lcount = h->llist = nullptr;
+  h->R0 = h->Fup = h->Tup = nullptr;
+  h->R1 = nullptr;
   h->xs = nullptr;
   h->xtiles = nullptr;
   h->F = h->T = nullptr;
@@ -199,6 +207,13 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.ccount = h->ccount;
   s.nslots = h->nslots;
   s.flags = h->flags;
+  s.cpos = h->cpos;
+  s.lcount = h->lcount;
+  s.llist = h->llist;
+  s.R0 = h->R0;
+  s.R1 = h->R1;
+  s.Fup = h->Fup;
+  s.Tup = h->Tup;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -214,7 +229,8 @@ StepBuffers step_buffers(dem_handle* h, int b) {
 }
 
 int kernels_per_step(const dem_handle* h) {
-  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : 6) + (h->slab ? 5 : 0);
+  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : (h->p.flags & DEM_F_FULL_LISTS) ? 6 : 7) +
+         (h->slab ? 5 : 0);
 }
 
 // Enqueue one step from parity b: scan, scatter, rank, (detect,) sweep.
@@ -261,17 +277,30 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   launch_rank(h->stream, h->cap, s);
   rec(K_RANK, false);
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
-                      : (h->p.flags & DEM_F_FORCE_LISTS_TPP)   ? 2
+                      : (h->p.flags & DEM_F_FULL_LISTS)        ? 2
                                                                : 0;
-  if (variant != 1) {
+  if (variant == 0) {  // half lists: detect, pair, finish
     rec(K_DETECT, true);
-    launch_detect(h->stream, h->cap, h->K, s, h->g);
+    launch_detect_half(h->stream, h->cap, h->K, s, h->g);
     rec(K_DETECT, false);
-    h->launches += 1;
+    rec(K_SWEEP, true);
+    launch_pair(h->stream, h->cap, h->K, h->p.model, s, h->g, h->ph);
+    rec(K_SWEEP, false);
+    rec(K_FINISH, true);
+    launch_finish(h->stream, h->cap, h->K, h->p.model, diag, s, h->g, h->ph);
+    rec(K_FINISH, false);
+    h->launches += 2;
+  } else {
+    if (variant == 2) {
+      rec(K_DETECT, true);
+      launch_detect(h->stream, h->cap, h->K, s, h->g);
+      rec(K_DETECT, false);
+      h->launches += 1;
+    }
+    rec(K_SWEEP, true);
+    launch_sweep(h->stream, h->cap, h->K, h->p.model, diag, s, h->g, h->ph, variant);
+    rec(K_SWEEP, false);
   }
-  rec(K_SWEEP, true);
-  launch_sweep(h->stream, h->cap, h->K, h->p.model, diag, s, h->g, h->ph, variant);
-  rec(K_SWEEP, false);
   h->launches += 5;  // scan is two kernels
   if (h->slab) {  // pack and publish the next step's migrants and ghosts
     rec(K_OTHER, true);
@@ -652,6 +681,9 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
           dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->clist, N * h->K) &&
           dalloc(h, &h->ccount, N) && dalloc(h, &h->nslots, 1) && dalloc(h, &h->scan_ctr, 2) &&
+          dalloc(h, &h->cpos, N * h->K) && dalloc(h, &h->lcount, N) &&
+          dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
+          dalloc(h, &h->R1, N * h->K) && dalloc(h, &h->Fup, N) && dalloc(h, &h->Tup, N) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
     if (h->slab) {

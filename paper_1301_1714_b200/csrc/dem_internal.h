@@ -79,6 +79,15 @@ struct StepBuffers {
   const uint32_t* nslots;  // device: input slots of this step (owned + appended)
   uint32_t* flags;     // slab mode: per output slot, bit0/1 migrate to left/right neighbour,
                        // bit2/3 ghost for left/right neighbour
+  // half-list path (Newton's third law): the pair (i, t) is
+  // evaluated once, by its lower sorted slot i ("upper" contact of i)
+  uint8_t* cpos;       // [k*N + i]: position of i in t's lower list
+  uint32_t* lcount;    // [t]: lower contacts appended to t (atomics in k_detect_half)
+  uint32_t* llist;     // [p*N + t] = i << 5 | k: t's lower contact p is i's upper contact k
+  float4* R0;          // [k*N + i]: (F_c on i, Tc.x) of i's upper contact k
+  float2* R1;          // [k*N + i]: (Tc.y, Tc.z)
+  float4* Fup;         // [i]: Σ F_c over i's upper contacts (candidate order)
+  float4* Tup;         // [i]: Σ r_i Tc over i's upper contacts
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;
@@ -141,7 +150,7 @@ struct XState {  // device scratch of the exchange of one step
 };
 
 enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5,
-                K_DETECT = 6 };
+                K_DETECT = 6, K_FINISH = 7 };
 
 // ---- launchers (dem_kernels.cu) -------------------------------------------
 // Every launcher enqueues exactly one kernel on `st` and returns its id.
@@ -182,6 +191,13 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
 void sweep_prepare(uint32_t K);  // host: kernel attributes (call outside stream capture)
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                   const DevGrid& g);
+// half-list path (default): k_detect_half, k_pair, k_finish
+int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
+                       const DevGrid& g);
+int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuffers& b,
+                const DevGrid& g, const DevPhys& ph);
+int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
+                  const StepBuffers& b, const DevGrid& g, const DevPhys& ph);
 int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
                  const StepBuffers& b, const DevGrid& g, const DevPhys& ph, int variant);
 

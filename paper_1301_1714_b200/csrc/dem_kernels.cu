@@ -960,50 +960,129 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
-// k_force_tpp: one thread per sorted particle evaluates its own contacts from
-// the contact list (the paper's particle-per-thread mapping for step 7, but
-// without the candidate loop: divergence only from unequal contact counts),
-// accumulating F and T in registers in candidate order. No shared memory, so
-// the SM's 228 KB stay L1 for the neighbours' state, which the block's
-// consecutive particles share. The next contact's partner state and predicted
-// history entry are loaded while the current one is evaluated.
-#ifndef DEM_FTPP_MINB
-#define DEM_FTPP_MINB 8
-#endif
-template <int MODEL, bool DIAG>
-__global__ void __launch_bounds__(128, DEM_FTPP_MINB)
-    k_force_tpp(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+// ---- half-list path (default): Newton's third law -------------------------
+// Eq. 3/Eq. 4 with the R1 orientation make the pair force antisymmetric and
+// the unscaled torque n x F_t symmetric, bitwise (P11): F_ji = -F_ij,
+// δ_t,ji = -δ_t,ij, T_j = r_j Tc, T_i = r_i Tc. So each contact pair is
+// evaluated once, by its lower sorted slot.
+//   k_detect_half  candidates t > i (4.5 of the 9 rows; in slab mode also the
+//                  low ghost rows), upper list of i, lower list of t (atomic
+//                  append: t learns who evaluates its contacts)
+//   k_pair         per upper contact: Eqs. 2-10, both history entries
+//                  (δ_t on i's side, -δ_t on t's), the pair result R for t
+//   k_finish       per particle: Σ over its lower contacts in ascending
+//                  partner slot (deterministic) + its upper partial sum, walls,
+//                  integration, next CM
+// Each particle's history list is [upper | lower (append order) | walls];
+// lookups are by partner id, so the order never changes a result.
+
+__global__ void __launch_bounds__(256) k_detect_half(StepBuffers b, DevGrid g, uint32_t N,
+                                                     uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
-  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= jhi) return;
-  const uint32_t s = __ldcs(&b.perm[j]);
-  const uint32_t nc = __ldcs(&b.ccount[j]);
-  const bool overflow = nc > K;
-  const uint32_t npair = min(nc, K);
+  const uint32_t i = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= jhi) return;
+  const float4 P = __ldg(&b.pos_sorted[i]);
+  const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
+  const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
+  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+  const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
+  const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
+  const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
+  uint32_t nup = 0;
+  bool overflow = false;
+#pragma unroll 1
+  for (int dz = -1; dz <= 1; ++dz) {
+    const int z = cz + dz;
+    if (z < 0 || z >= g.nz) continue;
+    uint32_t t0[3], t1[3];
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      const int y = cy + r - 1;
+      const bool in = y >= 0 && y < g.ny;
+      const uint32_t row = (uint32_t)z * nxy + (uint32_t)(in ? y : 0) * (uint32_t)g.nx;
+      t0[r] = in ? __ldg(&b.off[row + xa]) : 0u;
+      t1[r] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < 3; ++r) {
+      // this row's slots this particle evaluates: above i, or non-owned below jlo
+      uint32_t lo = t0[r], hi = t1[r];
+      if (lo <= i) lo = (hi > i) ? i + 1 : lo;  // the part above i
+      const bool low_ghosts = t0[r] < jlo;     // rows of the low ghost plane (slab mode)
+      if (!low_ghosts && lo >= hi) continue;
+      if (!low_ghosts && t0[r] < i && t1[r] <= i) continue;  // row entirely below i
+      const uint32_t ts = low_ghosts ? t0[r] : lo;
+#pragma unroll 1
+      for (uint32_t t = ts; t < hi; ++t) {
+        if (t <= i && t >= jlo) continue;
+        const float4 Q = __ldg(&b.pos_sorted[t]);
+        const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
+        const float d2 = dx * dx + dy * dy + dz2 * dz2;
+        const float S = P.w + Q.w;
+        const float S2 = S * S;
+        bool hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
+        if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
+          const double Sd = (double)P.w + (double)Q.w;
+          hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
+        }
+        if (!hit) continue;
+        if (nup >= K) {
+          overflow = true;
+          continue;
+        }
+        uint32_t p = 0xFFu;
+        if (t >= jlo && t < jhi) {  // an owned partner learns who evaluates its contact
+          p = atomicAdd(&b.lcount[t], 1u);
+          if (p < K) __stcg(&b.llist[(size_t)p * N + t], (i << 5) | nup);
+          else p = 0xFEu;  // partner overflow: raised by k_finish
+        }
+        __stcg(&b.clist[(size_t)nup * N + i], t);
+        b.cpos[(size_t)nup * N + i] = (uint8_t)min(p, 0xFFu);
+        ++nup;
+      }
+    }
+  }
+  __stcg(&b.ccount[i], overflow ? K + 1u : nup);
+}
+
+// one thread per particle over its upper contacts; next contact prefetched
+template <int MODEL>
+__global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
+                                              uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t i = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= jhi) return;
+  const uint32_t s = __ldcs(&b.perm[i]);
+  const uint32_t nup = min(__ldcs(&b.ccount[i]), K);
   Own o;
-  o.P = __ldg(&b.pos_sorted[j]);
+  o.P = __ldg(&b.pos_sorted[i]);
   o.V = __ldg(&b.vel_in[s]);
   o.W = __ldg(&b.omg_in[s]);
   const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+  const uint32_t oi = i - jlo;
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
   const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  // loads of contact k: partner position, velocity, spin, predicted old entry
+  uint32_t t = 0, q = 0;
   float4 Q = z4, VQ = z4, WQ = z4, H = z4;
-  if (npair > 0) {
-    const uint32_t q = __ldg(&b.perm[__ldcs(&b.clist[j])]);
-    Q = __ldg(&b.pos_in[q]);
+  if (nup > 0) {
+    t = __ldcs(&b.clist[i]);
+    q = __ldg(&b.perm[t]);
+    Q = __ldg(&b.pos_sorted[t]);
     VQ = __ldg(&b.vel_in[q]);
     if (MODEL == 0) {
       WQ = __ldg(&b.omg_in[q]);
       if (n_old > 0) H = __ldcs(&b.hist_in[s]);
     }
   }
-  for (uint32_t k = 0; k < npair; ++k) {
+  for (uint32_t k = 0; k < nup; ++k) {
+    const uint32_t tc = t;
     const float4 Qc = Q, VQc = VQ, WQc = WQ, Hc = H;
-    if (k + 1 < npair) {  // next contact's loads in flight during this one's arithmetic
-      const uint32_t q = __ldg(&b.perm[__ldcs(&b.clist[(size_t)(k + 1) * N + j])]);
-      Q = __ldg(&b.pos_in[q]);
+    if (k + 1 < nup) {  // the next contact's loads fly during this one's arithmetic
+      t = __ldcs(&b.clist[(size_t)(k + 1) * N + i]);
+      q = __ldg(&b.perm[t]);
+      Q = __ldg(&b.pos_sorted[t]);
       VQ = __ldg(&b.vel_in[q]);
       if (MODEL == 0) {
         WQ = __ldg(&b.omg_in[q]);
@@ -1012,31 +1091,89 @@ __global__ void __launch_bounds__(128, DEM_FTPP_MINB)
     }
     f3 n;
     float delta;
+    f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (!contact_geometry(o.P, Qc, n, delta)) {
-      raise_error(b.err, 9u, j - jlo, __float_as_uint(o.W.w));
-      continue;
-    }
-    if (MODEL == 0) {
+      raise_error(b.err, 9u, oi, __float_as_uint(o.W.w));
+    } else if (MODEL == 0) {
       const uint32_t pid = __float_as_uint(WQc.w);
       const f3 dold = (k < n_old && __float_as_uint(Hc.w) == pid)
                           ? mk(Hc.x, Hc.y, Hc.z)
                           : old_history(b.hist_in, N, s, n_old, 0xFFFFFFFFu, pid);
-      f3 Fc, Tc, dnew;
+      f3 dnew;
       eval_pair_practical(o, Qc, VQc, WQc, n, delta, dold, ph, Fc, Tc, dnew);
-      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
-      T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
-      __stcs(&b.hist_out[(size_t)k * N + (j - jlo)],
+      // this side's entry (upper part of i's list) and the partner's (lower part)
+      __stcs(&b.hist_out[(size_t)k * N + oi],
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
+      const uint32_t p = b.cpos[(size_t)k * N + i];
+      if (p < 0xFEu) {
+        const uint32_t nup_t = min(__ldcs(&b.ccount[tc]), K);
+        const uint32_t kt = nup_t + p;
+        if (kt < K)
+          __stcs(&b.hist_out[(size_t)kt * N + (tc - jlo)],
+                 make_float4(-dnew.x, -dnew.y, -dnew.z, o.W.w));
+      }
     } else {
       const f3 u = mk(VQc.x - o.V.x, VQc.y - o.V.y, VQc.z - o.V.z);
-      const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
-      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+      Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
     }
+    F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+    T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
+    __stcs(&b.R0[(size_t)k * N + i], make_float4(Fc.x, Fc.y, Fc.z, Tc.x));
+    if (MODEL == 0) __stcs(&b.R1[(size_t)k * N + i], make_float2(Tc.y, Tc.z));
+  }
+  __stcs(&b.Fup[i], make_float4(F.x, F.y, F.z, 0.f));
+  if (MODEL == 0) __stcs(&b.Tup[i], make_float4(T.x, T.y, T.z, 0.f));
+}
+
+// per particle: lower contacts in ascending partner slot, + the upper partial
+// sum, walls, integration (finish_particle)
+template <int MODEL, bool DIAG>
+__global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
+                                                uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jhi) return;
+  const uint32_t s = __ldcs(&b.perm[j]);
+  const uint32_t nc = __ldcs(&b.ccount[j]);
+  const uint32_t nlow_all = __ldcs(&b.lcount[j]);
+  const uint32_t nlow = min(nlow_all, K);
+  const uint32_t nup = min(nc, K);
+  bool overflow = nc > K || nlow_all > K || nup + nlow > K;
+  Own o;
+  o.P = __ldg(&b.pos_sorted[j]);
+  o.V = __ldg(&b.vel_in[s]);
+  o.W = __ldg(&b.omg_in[s]);
+  const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+  // lower contacts in ascending partner slot: entries (i << 5 | k) sort as i
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  uint32_t prev = 0u;
+  for (uint32_t r = 0; r < nlow; ++r) {
+    uint32_t best = 0xFFFFFFFFu;
+    for (uint32_t p = 0; p < nlow; ++p) {  // the smallest entry above the previous one
+      const uint32_t e = __ldcs(&b.llist[(size_t)p * N + j]);
+      if ((r == 0 || e > prev) && e < best) best = e;
+    }
+    prev = best;
+    const uint32_t i = best >> 5, k = best & 31u;
+    const float4 r0 = __ldcs(&b.R0[(size_t)k * N + i]);
+    F = mk(F.x - r0.x, F.y - r0.y, F.z - r0.z);
+    if (MODEL == 0) {
+      const float2 r1 = __ldcs(&b.R1[(size_t)k * N + i]);
+      T = mk(T.x + o.P.w * r0.w, T.y + o.P.w * r1.x, T.z + o.P.w * r1.y);
+    }
+  }
+  const float4 fu = __ldcs(&b.Fup[j]);
+  F = mk(F.x + fu.x, F.y + fu.y, F.z + fu.z);
+  if (MODEL == 0) {
+    const float4 tu = __ldcs(&b.Tup[j]);
+    T = mk(T.x + tu.x, T.y + tu.y, T.z + tu.z);
   }
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
+  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, min(nup + nlow, K), overflow,
+                               lookup);
 }
 
 // Set the dynamic shared-memory limit of every k_force instantiation once,
@@ -1467,13 +1604,47 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
   const uint32_t N = (uint32_t)n;
   if (variant == 1) {  // the paper's mapping, one fused kernel
     k_sweep_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
-  } else if (variant == 2) {  // thread per particle over the contact lists
-    k_force_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
-  } else {  // warp-flattened contact rounds (default)
+  } else {  // full contact lists, warp-flattened contact rounds
     const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
     k_force<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
         b, g, ph, N, K);
   }
+}
+
+int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
+                       const DevGrid& g) {
+  if (n <= 0) return K_DETECT;
+  cudaMemsetAsync(b.lcount, 0, sizeof(uint32_t) * n, st);
+  k_detect_half<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, K);
+  return K_DETECT;
+}
+
+int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuffers& b,
+                const DevGrid& g, const DevPhys& ph) {
+  if (n <= 0) return K_SWEEP;
+  if (model == 0)
+    k_pair<0><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  else
+    k_pair<1><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  return K_SWEEP;
+}
+
+int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
+                  const StepBuffers& b, const DevGrid& g, const DevPhys& ph) {
+  if (n <= 0) return K_FINISH;
+  const uint32_t N = (uint32_t)n;
+  if (model == 0) {
+    if (diag)
+      k_finish<0, true><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    else
+      k_finish<0, false><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+  } else {
+    if (diag)
+      k_finish<1, true><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    else
+      k_finish<1, false><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+  }
+  return K_FINISH;
 }
 
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
