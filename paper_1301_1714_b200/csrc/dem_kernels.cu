@@ -1046,87 +1046,86 @@ __global__ void __launch_bounds__(256) k_detect_half(StepBuffers b, DevGrid g, u
   __stcg(&b.ccount[i], overflow ? K + 1u : nup);
 }
 
-// one thread per particle over its upper contacts; next contact prefetched
+// k_pair: warp per 32 consecutive owned slots; the warp's upper contacts are
+// flattened across its lanes (~2.6 per particle at C4, so ~3 full rounds).
+// Each pair writes its result R (force on the lower particle, n x F_t) and
+// both history entries; no accumulation here, so no owner bookkeeping beyond
+// a shared-memory owner map.
 template <int MODEL>
 __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
                                               uint32_t K) {
+  __shared__ uint8_t s_own[4][32 * 32];
+  __shared__ uint32_t s_base[4][33];
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
-  const uint32_t i = jlo + blockIdx.x * blockDim.x + threadIdx.x;
-  if (i >= jhi) return;
-  const uint32_t s = __ldcs(&b.perm[i]);
-  const uint32_t nup = min(__ldcs(&b.ccount[i]), K);
-  Own o;
-  o.P = __ldg(&b.pos_sorted[i]);
-  o.V = __ldg(&b.vel_in[s]);
-  o.W = __ldg(&b.omg_in[s]);
-  const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
-  const uint32_t oi = i - jlo;
-  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
-  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
-  uint32_t t = 0, q = 0;
-  float4 Q = z4, VQ = z4, WQ = z4, H = z4;
-  if (nup > 0) {
-    t = __ldcs(&b.clist[i]);
-    q = __ldg(&b.perm[t]);
-    Q = __ldg(&b.pos_sorted[t]);
-    VQ = __ldg(&b.vel_in[q]);
-    if (MODEL == 0) {
-      WQ = __ldg(&b.omg_in[q]);
-      if (n_old > 0) H = __ldcs(&b.hist_in[s]);
-    }
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const uint32_t j0 = jlo + (blockIdx.x * 4u + warp) * 32u;
+  if (j0 >= jhi) return;
+  const uint32_t i_l = j0 + lane;
+  const uint32_t nup = i_l < jhi ? min(__ldcs(&b.ccount[i_l]), K) : 0u;
+  uint32_t incl = nup;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += v;
   }
-  for (uint32_t k = 0; k < nup; ++k) {
-    const uint32_t tc = t;
-    const float4 Qc = Q, VQc = VQ, WQc = WQ, Hc = H;
-    if (k + 1 < nup) {  // the next contact's loads fly during this one's arithmetic
-      t = __ldcs(&b.clist[(size_t)(k + 1) * N + i]);
-      q = __ldg(&b.perm[t]);
-      Q = __ldg(&b.pos_sorted[t]);
-      VQ = __ldg(&b.vel_in[q]);
-      if (MODEL == 0) {
-        WQ = __ldg(&b.omg_in[q]);
-        H = k + 1 < n_old ? __ldcs(&b.hist_in[(size_t)(k + 1) * N + s]) : z4;
-      }
-    }
+  const uint32_t mybase = incl - nup;
+  const uint32_t M = __shfl_sync(0xffffffffu, incl, 31);
+  s_base[warp][lane] = mybase;
+  for (uint32_t k = 0; k < nup; ++k) s_own[warp][mybase + k] = (uint8_t)lane;
+  __syncwarp();
+  const float4 z4 = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (uint32_t m = lane; m < M; m += 32) {
+    const uint32_t ow = s_own[warp][m];
+    const uint32_t k = m - s_base[warp][ow];
+    const uint32_t i = j0 + ow;
+    // first wave of independent loads
+    const uint32_t t = __ldcs(&b.clist[(size_t)k * N + i]);
+    const uint32_t cp = b.cpos[(size_t)k * N + i];
+    const uint32_t si = __ldg(&b.perm[i]);
+    Own o;
+    o.P = __ldg(&b.pos_sorted[i]);
+    const float4 Q = __ldg(&b.pos_sorted[t]);
+    // second wave: through SCCM
+    const uint32_t q = __ldg(&b.perm[t]);
+    o.V = __ldg(&b.vel_in[si]);
+    o.W = MODEL == 0 ? __ldg(&b.omg_in[si]) : z4;
+    const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[si]), K) : 0u;
+    const float4 Hk = (MODEL == 0 && k < K) ? __ldcs(&b.hist_in[(size_t)k * N + si]) : z4;
+    const uint32_t nup_t = (MODEL == 0 && cp < 0xFEu) ? min(__ldcs(&b.ccount[t]), K) : 0u;
+    const float4 VQ = __ldg(&b.vel_in[q]);
+    const float4 WQ = MODEL == 0 ? __ldg(&b.omg_in[q]) : z4;
     f3 n;
     float delta;
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
-    if (!contact_geometry(o.P, Qc, n, delta)) {
-      raise_error(b.err, 9u, oi, __float_as_uint(o.W.w));
+    if (!contact_geometry(o.P, Q, n, delta)) {
+      raise_error(b.err, 9u, i - jlo, __float_as_uint(o.W.w));
     } else if (MODEL == 0) {
-      const uint32_t pid = __float_as_uint(WQc.w);
-      const f3 dold = (k < n_old && __float_as_uint(Hc.w) == pid)
-                          ? mk(Hc.x, Hc.y, Hc.z)
-                          : old_history(b.hist_in, N, s, n_old, 0xFFFFFFFFu, pid);
+      const uint32_t pid = __float_as_uint(WQ.w);
+      const f3 dold = (k < n_old && __float_as_uint(Hk.w) == pid)
+                          ? mk(Hk.x, Hk.y, Hk.z)
+                          : old_history(b.hist_in, N, si, n_old, 0xFFFFFFFFu, pid);
       f3 dnew;
-      eval_pair_practical(o, Qc, VQc, WQc, n, delta, dold, ph, Fc, Tc, dnew);
+      eval_pair_practical(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
       // this side's entry (upper part of i's list) and the partner's (lower part)
-      __stcs(&b.hist_out[(size_t)k * N + oi],
+      __stcs(&b.hist_out[(size_t)k * N + (i - jlo)],
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
-      const uint32_t p = b.cpos[(size_t)k * N + i];
-      if (p < 0xFEu) {
-        const uint32_t nup_t = min(__ldcs(&b.ccount[tc]), K);
-        const uint32_t kt = nup_t + p;
-        if (kt < K)
-          __stcs(&b.hist_out[(size_t)kt * N + (tc - jlo)],
-                 make_float4(-dnew.x, -dnew.y, -dnew.z, o.W.w));
-      }
+      if (cp < 0xFEu && nup_t + cp < K)
+        __stcs(&b.hist_out[(size_t)(nup_t + cp) * N + (t - jlo)],
+               make_float4(-dnew.x, -dnew.y, -dnew.z, o.W.w));
     } else {
-      const f3 u = mk(VQc.x - o.V.x, VQc.y - o.V.y, VQc.z - o.V.z);
+      const f3 u = mk(VQ.x - o.V.x, VQ.y - o.V.y, VQ.z - o.V.z);
       Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
     }
-    F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
-    T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
     __stcs(&b.R0[(size_t)k * N + i], make_float4(Fc.x, Fc.y, Fc.z, Tc.x));
     if (MODEL == 0) __stcs(&b.R1[(size_t)k * N + i], make_float2(Tc.y, Tc.z));
   }
-  __stcs(&b.Fup[i], make_float4(F.x, F.y, F.z, 0.f));
-  if (MODEL == 0) __stcs(&b.Tup[i], make_float4(T.x, T.y, T.z, 0.f));
 }
 
-// per particle: lower contacts in ascending partner slot, + the upper partial
-// sum, walls, integration (finish_particle)
+// k_finish: per particle, every contact's result in the oracle's order —
+// lower partners ascending, then upper partners ascending (= ascending
+// partner slot) — then walls and integration (finish_particle).
+constexpr uint32_t kLowBatch = 8;  // lower-list entries sorted in registers
 template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
                                                 uint32_t K) {
@@ -1145,29 +1144,64 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
   o.V = __ldg(&b.vel_in[s]);
   o.W = __ldg(&b.omg_in[s]);
   const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
-  // lower contacts in ascending partner slot: entries (i << 5 | k) sort as i
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
-  uint32_t prev = 0u;
-  for (uint32_t r = 0; r < nlow; ++r) {
-    uint32_t best = 0xFFFFFFFFu;
-    for (uint32_t p = 0; p < nlow; ++p) {  // the smallest entry above the previous one
-      const uint32_t e = __ldcs(&b.llist[(size_t)p * N + j]);
-      if ((r == 0 || e > prev) && e < best) best = e;
+  auto add = [&](float4 r0, float2 r1, float sign) {
+    F = mk(F.x + sign * r0.x, F.y + sign * r0.y, F.z + sign * r0.z);
+    if (MODEL == 0) T = mk(T.x + o.P.w * r0.w, T.y + o.P.w * r1.x, T.z + o.P.w * r1.y);
+  };
+  // lower contacts: entries (i << 5 | k) sort as the partner slot i
+  uint32_t e[kLowBatch];
+#pragma unroll
+  for (uint32_t p = 0; p < kLowBatch; ++p)
+    e[p] = p < nlow ? __ldcs(&b.llist[(size_t)p * N + j]) : 0xFFFFFFFFu;
+#pragma unroll
+  for (uint32_t a = 1; a < kLowBatch; ++a)  // insertion sort, fully unrolled (registers)
+#pragma unroll
+    for (uint32_t c = a; c > 0; --c) {
+      const uint32_t lo = min(e[c - 1], e[c]), hi = max(e[c - 1], e[c]);
+      e[c - 1] = lo;
+      e[c] = hi;
     }
-    prev = best;
-    const uint32_t i = best >> 5, k = best & 31u;
-    const float4 r0 = __ldcs(&b.R0[(size_t)k * N + i]);
-    F = mk(F.x - r0.x, F.y - r0.y, F.z - r0.z);
-    if (MODEL == 0) {
-      const float2 r1 = __ldcs(&b.R1[(size_t)k * N + i]);
-      T = mk(T.x + o.P.w * r0.w, T.y + o.P.w * r1.x, T.z + o.P.w * r1.y);
+  if (nlow <= kLowBatch) {
+    float4 r0[kLowBatch];
+    float2 r1[kLowBatch];
+#pragma unroll
+    for (uint32_t p = 0; p < kLowBatch; ++p) {  // all loads in flight together
+      const bool ok = p < nlow;
+      const uint32_t i = e[p] >> 5, k = e[p] & 31u;
+      r0[p] = ok ? __ldcs(&b.R0[(size_t)k * N + i]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      r1[p] = (ok && MODEL == 0) ? __ldcs(&b.R1[(size_t)k * N + i]) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (uint32_t p = 0; p < kLowBatch; ++p)
+      if (p < nlow) add(r0[p], r1[p], -1.f);
+  } else {  // more than kLowBatch lower contacts: selection in ascending order
+    uint32_t prev = 0u;
+    for (uint32_t r = 0; r < nlow; ++r) {
+      uint32_t best = 0xFFFFFFFFu;
+      for (uint32_t p = 0; p < nlow; ++p) {
+        const uint32_t v = __ldcs(&b.llist[(size_t)p * N + j]);
+        if ((r == 0 || v > prev) && v < best) best = v;
+      }
+      prev = best;
+      const uint32_t i = best >> 5, k = best & 31u;
+      add(__ldcs(&b.R0[(size_t)k * N + i]),
+          MODEL == 0 ? __ldcs(&b.R1[(size_t)k * N + i]) : make_float2(0.f, 0.f), -1.f);
     }
   }
-  const float4 fu = __ldcs(&b.Fup[j]);
-  F = mk(F.x + fu.x, F.y + fu.y, F.z + fu.z);
-  if (MODEL == 0) {
-    const float4 tu = __ldcs(&b.Tup[j]);
-    T = mk(T.x + tu.x, T.y + tu.y, T.z + tu.z);
+  // upper contacts: this particle's own results, candidate order
+  for (uint32_t k0 = 0; k0 < nup; k0 += 4) {
+    float4 r0[4];
+    float2 r1[4];
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u) {
+      const bool ok = k0 + u < nup;
+      r0[u] = ok ? __ldcs(&b.R0[(size_t)(k0 + u) * N + j]) : make_float4(0.f, 0.f, 0.f, 0.f);
+      r1[u] = (ok && MODEL == 0) ? __ldcs(&b.R1[(size_t)(k0 + u) * N + j]) : make_float2(0.f, 0.f);
+    }
+#pragma unroll
+    for (uint32_t u = 0; u < 4; ++u)
+      if (k0 + u < nup) add(r0[u], r1[u], 1.f);
   }
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
@@ -1626,6 +1660,7 @@ int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuf
     k_pair<0><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
   else
     k_pair<1><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  // (one warp per 32 owned slots, 4 warps per block)
   return K_SWEEP;
 }
 
