@@ -258,9 +258,9 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        from paper_1301_1714_b200.dem import DEM_F_FULL_LISTS, DEM_F_THREAD_PER_PARTICLE
+        from paper_1301_1714_b200.dem import DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE
         d = Dem(sc.params, device=local, stream=stream, rank=rank, world=world,
-                flags={"half": 0, "full": DEM_F_FULL_LISTS,
+                flags={"full": 0, "half": DEM_F_HALF_LISTS,
                        "tpp": DEM_F_THREAD_PER_PARTICLE}[args.sweep])
         # every rank passes the whole set; a slab rank keeps its own planes
         d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
@@ -434,9 +434,10 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="half", choices=["half", "full", "tpp"],
-                    help="half contact lists, each pair once (default); full lists with "
-                         "warp-flattened force rounds; or the paper's fused thread per particle")
+    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp"],
+                    help="full contact lists + warp-flattened force rounds (default); half "
+                         "lists, each pair once (Newton's third law); or the paper's fused "
+                         "thread per particle")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

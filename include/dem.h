@@ -79,9 +79,9 @@ enum dem_flags {
   DEM_F_NO_GRAPH = 1u << 4,    /* launch kernels eagerly instead of replaying a CUDA graph */
   DEM_F_THREAD_PER_PARTICLE = 1u << 5, /* ablation: the paper's mapping, detection and forces
                                           in one thread-per-particle kernel */
-  DEM_F_FULL_LISTS = 1u << 6, /* ablation: every contact evaluated from both sides (full
-                                 contact lists, warp-flattened force rounds); default: half
-                                 lists, each pair evaluated once (Newton's third law) */
+  DEM_F_HALF_LISTS = 1u << 6, /* ablation: each contact pair evaluated once (Newton's third
+                                 law, half contact lists + a per-pair result buffer); default:
+                                 full lists, each side evaluated by its particle's warp */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };

@@ -229,7 +229,7 @@ StepBuffers step_buffers(dem_handle* h, int b) {
 }
 
 int kernels_per_step(const dem_handle* h) {
-  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : (h->p.flags & DEM_F_FULL_LISTS) ? 6 : 7) +
+  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : (h->p.flags & DEM_F_HALF_LISTS) ? 7 : 6) +
          (h->slab ? 5 : 0);
 }
 
@@ -276,9 +276,11 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   rec(K_RANK, true);
   launch_rank(h->stream, h->cap, s);
   rec(K_RANK, false);
+  // default: full contact lists (k_detect + warp-flattened k_force); the half
+  // lists (Newton's third law) and the paper's fused mapping are ablations
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
-                      : (h->p.flags & DEM_F_FULL_LISTS)        ? 2
-                                                               : 0;
+                      : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
+                                                               : 2;
   if (variant == 0) {  // half lists: detect, pair, finish
     rec(K_DETECT, true);
     launch_detect_half(h->stream, h->cap, h->K, s, h->g);

@@ -27,7 +27,7 @@ DEM_EPEER = -11
 DEM_MODEL_PRACTICAL, DEM_MODEL_SIMPLE = 0, 1
 DEM_F_TRUNCATE_DT, DEM_F_CLAMP_FN, DEM_F_DIAG, DEM_F_ASYNC, DEM_F_NO_GRAPH = 1, 2, 4, 8, 16
 DEM_F_THREAD_PER_PARTICLE = 32
-DEM_F_FULL_LISTS = 64
+DEM_F_HALF_LISTS = 64
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")

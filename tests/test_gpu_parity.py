@@ -9,7 +9,7 @@ import pytest
 
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
-from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FULL_LISTS,
+from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
                                       Dem, DemError)
 
@@ -60,7 +60,7 @@ def test_hash_sort_offsets_bit_exact(name):
 
 # ------------------------------------------------------ T2 one step -------
 
-@pytest.mark.parametrize("variant", [0, DEM_F_FULL_LISTS, DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("variant", [0, DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
     sc = scenes_small()[idx]
@@ -247,7 +247,7 @@ def test_determinism_and_graph_equivalence():
         assert as_dict(c) == as_dict(outs[0][1])  # bitwise δ_t per contact
 
 
-@pytest.mark.parametrize("other", [DEM_F_FULL_LISTS, DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("other", [DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
 def test_sweep_variants_agree(other):
     """The force-kernel mappings (contact lists, warp-flattened rounds, the
     paper's fused thread per particle) evaluate the same contacts with the
