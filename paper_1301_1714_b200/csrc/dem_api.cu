@@ -56,7 +56,7 @@ struct dem_handle {
   uint32_t *clist = nullptr, *ccount = nullptr;
   uint8_t* cpos = nullptr;
   uint32_t *lcount = nullptr, *llist = nullptr;
-  float4 *R0 = nullptr, *Fup = nullptr, *Tup = nullptr;
+  float4* R0 = nullptr;
   float2* R1 = nullptr;
   uint32_t* nslots = nullptr;  // device: input slots of the next step
   uint32_t* flags = nullptr;   // slab mode
@@ -178,7 +178,7 @@ void free_buffers(dem_handle* h) {
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
   h->cpos = nullptr;
   h->lcount = h->llist = nullptr;
-  h->R0 = h->Fup = h->Tup = nullptr;
+  h->R0 = nullptr;
   h->R1 = nullptr;
   h->xs = nullptr;
   h->xtiles = nullptr;
@@ -212,8 +212,6 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.llist = h->llist;
   s.R0 = h->R0;
   s.R1 = h->R1;
-  s.Fup = h->Fup;
-  s.Tup = h->Tup;
   s.hist_in = h->hist[b];
   s.cnt_in = h->cnt[b];
   s.hist_out = h->hist[b ^ 1];
@@ -683,11 +681,12 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
           dalloc(h, &h->off, (size_t)ncells + 1) && dalloc(h, &h->tmp, N) &&
           dalloc(h, &h->perm, N) && dalloc(h, &h->pos_sorted, N) && dalloc(h, &h->clist, N * h->K) &&
           dalloc(h, &h->ccount, N) && dalloc(h, &h->nslots, 1) && dalloc(h, &h->scan_ctr, 2) &&
-          dalloc(h, &h->cpos, N * h->K) && dalloc(h, &h->lcount, N) &&
-          dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
-          dalloc(h, &h->R1, N * h->K) && dalloc(h, &h->Fup, N) && dalloc(h, &h->Tup, N) &&
           dalloc(h, &h->err, 1);
     if (h->p.flags & DEM_F_DIAG) ok &= dalloc(h, &h->F, N) && dalloc(h, &h->T, N);
+    if (h->p.flags & DEM_F_HALF_LISTS)
+      ok &= dalloc(h, &h->cpos, N * h->K) && dalloc(h, &h->lcount, N) &&
+            dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
+            dalloc(h, &h->R1, N * h->K);
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);

@@ -86,8 +86,6 @@ struct StepBuffers {
   uint32_t* llist;     // [p*N + t] = i << 5 | k: t's lower contact p is i's upper contact k
   float4* R0;          // [k*N + i]: (F_c on i, Tc.x) of i's upper contact k
   float2* R1;          // [k*N + i]: (Tc.y, Tc.z)
-  float4* Fup;         // [i]: Σ F_c over i's upper contacts (candidate order)
-  float4* Tup;         // [i]: Σ r_i Tc over i's upper contacts
   const float4* hist_in;
   const uint32_t* cnt_in;
   float4* hist_out;
