@@ -706,31 +706,25 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
       t0[r] = in ? __ldg(&b.off[row + xa]) : 0u;
       t1[r] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
     }
-    auto test = [&](uint32_t t, float4 Q) {  // exact predicate (R14) and the push
-      const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
-      const float d2 = dx * dx + dy * dy + dz2 * dz2;
-      const float S = P.w + Q.w;
-      const float S2 = S * S;
-      bool hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
-      if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact
-        const double Sd = (double)P.w + (double)Q.w;
-        hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
-      }
-      const bool push = hit && t != j;
-      if (push && npair < K) __stcg(out + (size_t)npair * N, t);
-      npair += push ? 1u : 0u;
-    };
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-      uint32_t t = t0[r];
 #pragma unroll 1
-      for (; t + 1 < t1[r]; t += 2) {  // two candidates per iteration, both loads first
-        const float4 Q0 = __ldg(&b.pos_sorted[t]);
-        const float4 Q1 = __ldg(&b.pos_sorted[t + 1]);
-        test(t, Q0);
-        test(t + 1, Q1);
+      for (uint32_t t = t0[r]; t < t1[r]; ++t) {
+        const float4 Q = __ldg(&b.pos_sorted[t]);
+        const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
+        const float d2 = dx * dx + dy * dy + dz2 * dz2;
+        const float S = P.w + Q.w;
+        const float S2 = S * S;
+        bool hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
+        if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
+          const double Sd = (double)P.w + (double)Q.w;
+          hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
+        }
+        if (hit && t != j) {
+          if (npair < K) __stcg(out + (size_t)npair * N, t);
+          ++npair;
+        }
       }
-      if (t < t1[r]) test(t, __ldg(&b.pos_sorted[t]));
     }
   }
   __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
@@ -747,18 +741,16 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
 // issues its partner-state and history loads together. δ_t,old is read at the
 // contact's own list index first (persisting contacts keep their position).
 struct WarpSmemLayout {
-  uint32_t bytes, pf, ost, cq, res, own, base, slot, nold;
+  uint32_t bytes, pf, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
     uint32_t o = 0;
     L.pf = o;
     o += 2 * 4 * 32 * 16;  // double-buffered prefetch: partner pos, vel, omg, old δ_t entry
-    L.ost = o;
-    o += 3 * 32 * 16;  // own state P, V, W of each lane
     L.cq = o;
     o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
-    o += 32 * 8 * 4;  // round results: float4 (F_c, Tc.x) then float2 (Tc.y, Tc.z) per lane
+    o += 32 * 6 * 4;
     L.own = o;
     o += ((K * 32 + 15u) & ~15u);
     L.base = o;
@@ -820,11 +812,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
   float4* pf = reinterpret_cast<float4*>(ws + L.pf);            // [buf][field][lane]
   uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
-  float4* s_r4 = reinterpret_cast<float4*>(ws + L.res);        // [lane]: F_c, Tc.x
-  float2* s_r2 = reinterpret_cast<float2*>(ws + L.res + 512);  // [lane]: Tc.y, Tc.z
-  float4* sP = reinterpret_cast<float4*>(ws + L.ost);
-  float4* sV = sP + 32;
-  float4* sW = sV + 32;
+  float* s_res = reinterpret_cast<float*>(ws + L.res);          // [6][32]
   uint8_t* s_own = ws + L.own;                                  // owner of each contact
   uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);  // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
@@ -848,9 +836,6 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
   s_slot[lane] = s;
   s_nold[lane] = n_old;
-  sP[lane] = o.P;
-  sV[lane] = o.V;
-  sW[lane] = o.W;
   // partner sorted slots -> old slots (SCCM), four lookups in flight per lane
   for (uint32_t k0 = 0; k0 < npair; k0 += 4) {
     uint32_t t4[4], q4[4];
@@ -907,10 +892,20 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
     }
     const uint32_t m = r0 + lane;
     const uint32_t ow = m < M ? s_own[m] : 0u;
-    Own po;  // the contact's owner
-    po.P = sP[ow];
-    po.V = sV[ow];
-    po.W = sW[ow];
+    // owner state from the owner lane's registers (all lanes take part)
+    Own po;
+    po.P.x = __shfl_sync(0xffffffffu, o.P.x, ow);
+    po.P.y = __shfl_sync(0xffffffffu, o.P.y, ow);
+    po.P.z = __shfl_sync(0xffffffffu, o.P.z, ow);
+    po.P.w = __shfl_sync(0xffffffffu, o.P.w, ow);
+    po.V.x = __shfl_sync(0xffffffffu, o.V.x, ow);
+    po.V.y = __shfl_sync(0xffffffffu, o.V.y, ow);
+    po.V.z = __shfl_sync(0xffffffffu, o.V.z, ow);
+    po.V.w = __shfl_sync(0xffffffffu, o.V.w, ow);
+    po.W.x = __shfl_sync(0xffffffffu, o.W.x, ow);
+    po.W.y = __shfl_sync(0xffffffffu, o.W.y, ow);
+    po.W.z = __shfl_sync(0xffffffffu, o.W.z, ow);
+    po.W.w = __shfl_sync(0xffffffffu, o.W.w, ow);
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (m < M) {
       const uint32_t k = m - s_base[ow];
@@ -940,23 +935,25 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
         Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
       }
     }
-    s_r4[lane] = make_float4(Fc.x, Fc.y, Fc.z, Tc.x);
-    if (MODEL == 0) s_r2[lane] = make_float2(Tc.y, Tc.z);
+    s_res[0 * 32 + lane] = Fc.x;
+    s_res[1 * 32 + lane] = Fc.y;
+    s_res[2 * 32 + lane] = Fc.z;
+    s_res[3 * 32 + lane] = Tc.x;
+    s_res[4 * 32 + lane] = Tc.y;
+    s_res[5 * 32 + lane] = Tc.z;
     __syncwarp();
     // each owner adds its contacts of this round, in candidate order
     const uint32_t lo = max(mybase, r0), hi = min(mybase + npair, r0 + 32);
     for (uint32_t x = lo; x < hi; ++x) {
-      const float4 r4 = s_r4[x - r0];
-      F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
-      if (MODEL == 0) {
-        const float2 r2 = s_r2[x - r0];
-        T = mk(T.x + r4.w, T.y + r2.x, T.z + r2.y);  // Σ n x F_t; times r_i below
-      }
+      const uint32_t l = x - r0;
+      F = mk(F.x + s_res[l], F.y + s_res[32 + l], F.z + s_res[64 + l]);
+      if (MODEL == 0)
+        T = mk(T.x + o.P.w * s_res[96 + l], T.y + o.P.w * s_res[128 + l],
+               T.z + o.P.w * s_res[160 + l]);
     }
     __syncwarp();
   }
   if (!valid) return;
-  T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: T_i = r_i Σ (n x F_t)
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
