@@ -740,13 +740,17 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
 // order). Partner slots are translated to old slots once per warp, so a round
 // issues its partner-state and history loads together. δ_t,old is read at the
 // contact's own list index first (persisting contacts keep their position).
+#ifndef DEM_FORCE_PFBUFS
+#define DEM_FORCE_PFBUFS 1  // 1: single buffer (next round issued once the current is in registers)
+#endif
+constexpr uint32_t kPfBufs = DEM_FORCE_PFBUFS;
 struct WarpSmemLayout {
   uint32_t bytes, pf, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
     WarpSmemLayout L;
     uint32_t o = 0;
     L.pf = o;
-    o += 2 * 4 * 32 * 16;  // double-buffered prefetch: partner pos, vel, omg, old δ_t entry
+    o += kPfBufs * 4 * 32 * 16;  // prefetch buffer(s): partner pos, vel, omg, old δ_t entry
     L.cq = o;
     o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
@@ -883,12 +887,28 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
   if (M > 0) prefetch(0, 0);
   uint32_t buf = 0;
-  for (uint32_t r0 = 0; r0 < M; r0 += 32, buf ^= 1u) {
-    if (r0 + 32 < M) {
-      prefetch(r0 + 32, buf ^ 1u);
-      cp_async_wait<1>();
+  for (uint32_t r0 = 0; r0 < M; r0 += 32, buf ^= (kPfBufs - 1u)) {
+    float4 Qr, VQr, WQr, Hr;  // this lane's prefetched partner data, in registers
+    if (kPfBufs == 2) {
+      if (r0 + 32 < M) {
+        prefetch(r0 + 32, buf ^ 1u);
+        cp_async_wait<1>();
+      } else {
+        cp_async_wait<0>();
+      }
     } else {
       cp_async_wait<0>();
+    }
+    {
+      const float4* d = pf + buf * 128;
+      Qr = d[lane];
+      VQr = d[32 + lane];
+      WQr = d[64 + lane];
+      Hr = d[96 + lane];
+    }
+    if (kPfBufs == 1 && r0 + 32 < M) {
+      __syncwarp();
+      prefetch(r0 + 32, 0);  // overwrite the buffer: this round's data is in registers
     }
     const uint32_t m = r0 + lane;
     const uint32_t ow = m < M ? s_own[m] : 0u;
@@ -909,19 +929,18 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (m < M) {
       const uint32_t k = m - s_base[ow];
-      const float4* d = pf + buf * 128;
-      const float4 Q = d[lane];
-      const float4 VQ = d[32 + lane];
+      const float4 Q = Qr;
+      const float4 VQ = VQr;
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
         raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w));
       } else if (MODEL == 0) {
-        const float4 WQ = d[64 + lane];
+        const float4 WQ = WQr;
         const uint32_t pid = __float_as_uint(WQ.w);
         const uint32_t no = s_nold[ow];
         f3 dold;
-        const float4 hk = k < no ? d[96 + lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+        const float4 hk = k < no ? Hr : make_float4(0.f, 0.f, 0.f, 0.f);
         if (k < no && __float_as_uint(hk.w) == pid)
           dold = mk(hk.x, hk.y, hk.z);
         else
