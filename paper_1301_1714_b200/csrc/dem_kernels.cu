@@ -754,7 +754,7 @@ struct WarpSmemLayout {
     L.cq = o;
     o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
-    o += 32 * 6 * 4;
+    o += 32 * 8 * 4;  // round results: float4 (F_c, Tc.x) then float2 (Tc.y, Tc.z) per lane
     L.own = o;
     o += ((K * 32 + 15u) & ~15u);
     L.base = o;
@@ -816,7 +816,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
   float4* pf = reinterpret_cast<float4*>(ws + L.pf);            // [buf][field][lane]
   uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
-  float* s_res = reinterpret_cast<float*>(ws + L.res);          // [6][32]
+  float4* s_r4 = reinterpret_cast<float4*>(ws + L.res);        // [lane]: F_c, Tc.x
+  float2* s_r2 = reinterpret_cast<float2*>(ws + L.res + 512);  // [lane]: Tc.y, Tc.z
   uint8_t* s_own = ws + L.own;                                  // owner of each contact
   uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);  // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
@@ -954,21 +955,18 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
         Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
       }
     }
-    s_res[0 * 32 + lane] = Fc.x;
-    s_res[1 * 32 + lane] = Fc.y;
-    s_res[2 * 32 + lane] = Fc.z;
-    s_res[3 * 32 + lane] = Tc.x;
-    s_res[4 * 32 + lane] = Tc.y;
-    s_res[5 * 32 + lane] = Tc.z;
+    s_r4[lane] = make_float4(Fc.x, Fc.y, Fc.z, Tc.x);
+    if (MODEL == 0) s_r2[lane] = make_float2(Tc.y, Tc.z);
     __syncwarp();
     // each owner adds its contacts of this round, in candidate order
     const uint32_t lo = max(mybase, r0), hi = min(mybase + npair, r0 + 32);
     for (uint32_t x = lo; x < hi; ++x) {
-      const uint32_t l = x - r0;
-      F = mk(F.x + s_res[l], F.y + s_res[32 + l], F.z + s_res[64 + l]);
-      if (MODEL == 0)
-        T = mk(T.x + o.P.w * s_res[96 + l], T.y + o.P.w * s_res[128 + l],
-               T.z + o.P.w * s_res[160 + l]);
+      const float4 r4 = s_r4[x - r0];
+      F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
+      if (MODEL == 0) {
+        const float2 r2 = s_r2[x - r0];
+        T = mk(T.x + o.P.w * r4.w, T.y + o.P.w * r2.x, T.z + o.P.w * r2.y);
+      }
     }
     __syncwarp();
   }
