@@ -675,19 +675,16 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 // clist[k*N + j] = t (each partner's sorted slot, in candidate order =
 // ascending sorted slot). Few registers, so the SM keeps many warps in flight
 // to hide the neighbour-row latency.
-#ifndef DEM_DETECT_PLANES
-#define DEM_DETECT_PLANES 1  // 1: row bounds loaded per z-plane (6 at a time); 0: all 18
-#endif
-__global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32_t N, uint32_t K) {
-  if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
-  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= jhi) return;
-  const float4 P = __ldg(&b.pos_sorted[j]);
-  // own cell: the step-2 hash of the own position (identical to CM by construction)
-  const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
-  const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
-  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+// One scan of the 27-cell candidates of sorted slot j (9 row ranges, bounds
+// loaded per z-plane). FAST: the fp32 decision r = d² - S² < 0 only, with
+// `amb` raised (>= 0) when some candidate lies inside the ±16u band of R14 —
+// the caller then rescans with EXACT, which settles band candidates in fp64.
+// fl(d² - S²) keeps the sign of d² - S², and outside the band the fp32 and
+// exact decisions agree (in_contact's bound), so both scans give one list.
+template <bool EXACT>
+__device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
+                                                int cx, int cy, int cz, uint32_t j, uint32_t N,
+                                                uint32_t K, float& amb) {
   const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
   const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
   const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
@@ -715,18 +712,52 @@ __global__ void __launch_bounds__(256) k_detect(StepBuffers b, DevGrid g, uint32
         const float d2 = dx * dx + dy * dy + dz2 * dz2;
         const float S = P.w + Q.w;
         const float S2 = S * S;
-        bool hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
-        if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
-          const double Sd = (double)P.w + (double)Q.w;
-          hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
+        bool hit;
+        if (EXACT) {
+          hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
+          if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
+            const double Sd = (double)P.w + (double)Q.w;
+            hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
+          }
+        } else {
+          const float rr = d2 - S2;
+          hit = rr < 0.f;
+          amb = fmaxf(amb, fmaf(S2, 9.5367431640625e-7f, -fabsf(rr)));  // 16u S² - |r|
         }
         if (hit && t != j) {
-          if (npair < K) __stcg(out + (size_t)npair * N, t);
+          if (npair < K) __stcg(out, t);
+          out += N;
           ++npair;
         }
       }
     }
   }
+  return npair;
+}
+
+// k_detect: one light thread per sorted particle scans its 27-cell candidates
+// (Eq. 12) with the exact predicate (R14) and writes its contact list
+// clist[k*N + j] = t (each partner's sorted slot, in candidate order =
+// ascending sorted slot). Few registers, so the SM keeps many warps in flight
+// to hide the neighbour-row latency; the rare particle with a candidate in the
+// fp32 uncertainty band rescans exactly.
+#ifndef DEM_DETECT_MINB
+#define DEM_DETECT_MINB 6
+#endif
+__global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
+                                                                 uint32_t N, uint32_t K) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= jhi) return;
+  const float4 P = __ldg(&b.pos_sorted[j]);
+  // own cell: the step-2 hash of the own position (identical to CM by construction)
+  const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
+  const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
+  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+  float amb = -1.f;
+  uint32_t npair = detect_scan<false>(b, g, P, cx, cy, cz, j, N, K, amb);
+  if (amb >= 0.f) npair = detect_scan<true>(b, g, P, cx, cy, cz, j, N, K, amb);
   __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
 }
 
