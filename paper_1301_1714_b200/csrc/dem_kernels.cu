@@ -675,6 +675,9 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 // clist[k*N + j] = t (each partner's sorted slot, in candidate order =
 // ascending sorted slot). Few registers, so the SM keeps many warps in flight
 // to hide the neighbour-row latency.
+#ifndef DEM_DETECT_Q
+#define DEM_DETECT_Q 0  // 1: k_detect stores the partner's old slot perm[t] instead of t
+#endif
 // One scan of the 27-cell candidates of sorted slot j (9 row ranges, bounds
 // loaded per z-plane). FAST: the fp32 decision r = d² - S² < 0 only, with
 // `amb` raised (>= 0) when some candidate lies inside the ±16u band of R14 —
@@ -725,7 +728,11 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
           amb = fmaxf(amb, fmaf(S2, 9.5367431640625e-7f, -fabsf(rr)));  // 16u S² - |r|
         }
         if (hit && t != j) {
+#if DEM_DETECT_Q
+          if (npair < K) __stcg(out, __ldg(&b.perm[t]));  // the partner's old slot (SCCM)
+#else
           if (npair < K) __stcg(out, t);
+#endif
           out += N;
           ++npair;
         }
@@ -878,7 +885,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
 #pragma unroll
     for (int u = 0; u < 4; ++u) t4[u] = k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u;
 #pragma unroll
-    for (int u = 0; u < 4; ++u) q4[u] = k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u;
+    for (int u = 0; u < 4; ++u)
+      q4[u] = DEM_DETECT_Q ? t4[u] : (k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (k0 + u < npair) s_cq[(k0 + u) * 32 + lane] = q4[u];
@@ -996,12 +1004,13 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
       F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
       if (MODEL == 0) {
         const float2 r2 = s_r2[x - r0];
-        T = mk(T.x + o.P.w * r4.w, T.y + o.P.w * r2.x, T.z + o.P.w * r2.y);
+        T = mk(T.x + r4.w, T.y + r2.x, T.z + r2.y);
       }
     }
     __syncwarp();
   }
   if (!valid) return;
+  if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };

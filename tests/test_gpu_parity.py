@@ -115,6 +115,47 @@ def test_one_step_T2_C3_full():
     assert_T2_history(contacts_dict(d), h.as_dict(st.id))
 
 
+def band_pairs_scene(seed=11, m=8):
+    """m³ isolated pairs at separations S(1 + k 2⁻²³), |k| <= 40 (before the
+    fp32 rounding of the positions): ~60 pairs fall inside the ±16u fp32 band
+    of R14, where k_detect must rescan with the exact fp64 predicate."""
+    rng = np.random.default_rng(seed)
+    g = np.stack(np.meshgrid(*[np.arange(m)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    a = (g * 4.0 + 2.0) * S.D
+    u = rng.normal(size=a.shape)
+    u /= np.linalg.norm(u, axis=1, keepdims=True)
+    r = rng.choice([0.5 * S.R, 0.75 * S.R, S.R], size=(a.shape[0], 2))
+    sep = (r[:, 0] + r[:, 1]) * (1.0 + rng.integers(-40, 41, a.shape[0]) * 2.0 ** -23)
+    b = a + u * sep[:, None]
+    pos = np.concatenate([a, b]).astype(np.float32)
+    rad = np.concatenate([r[:, 0], r[:, 1]]).astype(np.float32)
+    L = (4.0 * m + 1.0) * S.D
+    p = S.SimParams(gravity=(0.0, 0.0, 0.0)).replace(box_lo=(0.0, 0.0, 0.0), box_hi=(L, L, L))
+    return S.make_scene("band_pairs", p, pos, radius=rad)
+
+
+def test_touching_pairs_in_fp32_band():
+    sc = band_pairs_scene()
+    p = orc.make_params(sc.params, sc.radius)
+    # the decisions the band has to settle: fp32 d², S² vs the exact fp64 predicate
+    n = sc.n // 2
+    A, B = sc.pos[:n].astype(np.float64), sc.pos[n:].astype(np.float64)
+    S2 = (sc.radius[:n].astype(np.float64) + sc.radius[n:]) ** 2
+    exact = ((B - A) ** 2).sum(1) < S2
+    d2f = ((sc.pos[n:] - sc.pos[:n]) ** 2).sum(1, dtype=np.float32)
+    in_band = np.abs(d2f.astype(np.float64) - S2) <= 16 * 2.0 ** -24 * S2
+    assert in_band.sum() >= 40 and exact[in_band].any() and not exact[in_band].all()
+    for flags in (DEM_F_DIAG, DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
+        d = make(sc, flags=flags)
+        st, h = oracle_inputs(d, 16)
+        d.step(1)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        got = contacts_dict(d)
+        assert got.keys() == h.as_dict(st.id).keys()
+        assert len(got) == 2 * int(exact.sum())  # each contact seen from both sides
+
+
 def test_full_size_C4_sampled():
     """4M-particle settling bed in the bench's launch configuration (graph
     replay): grid bit-exact for every particle; forces, torques and histories
