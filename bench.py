@@ -136,7 +136,7 @@ def alg_bytes(model: str, rho_c: float, c_bar: float):
     """Algorithmic bytes per particle-step.
 
     The sweep (steps 5-8 and 1: detection, contact forces, walls, integration
-    — k_detect_half + k_pair + k_finish, the dominant part of the step): state
+    — k_detect + k_force, the dominant part of the step): state
     read + write 96, SCCM read 4, next CM write 4, cell offsets read 4 rho_c,
     history counts r+w 8, history entries r+w 32 c_bar -> 112 + 4 rho_c +
     32 c_bar (practical); simple model (no history, no spin update):
