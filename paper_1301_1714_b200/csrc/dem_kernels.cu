@@ -782,6 +782,10 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
 #define DEM_FORCE_PFBUFS 1  // 1: single buffer (next round issued once the current is in registers)
 #endif
 constexpr uint32_t kPfBufs = DEM_FORCE_PFBUFS;
+#ifndef DEM_FORCE_RESW
+#define DEM_FORCE_RESW 2  // rounds per accumulation window (results kept in smem until then)
+#endif
+constexpr uint32_t kResW = 32 * DEM_FORCE_RESW;
 struct WarpSmemLayout {
   uint32_t bytes, pf, cq, res, own, base, slot, nold;
   __host__ __device__ static WarpSmemLayout make(uint32_t K) {
@@ -792,7 +796,7 @@ struct WarpSmemLayout {
     L.cq = o;
     o += K * 32 * 4;  // partner old slot of each (k, lane)
     L.res = o;
-    o += 32 * 8 * 4;  // round results: float4 (F_c, Tc.x) then float2 (Tc.y, Tc.z) per lane
+    o += kResW * 24;  // window of results: float4 (F_c, Tc.x) then float2 (Tc.y, Tc.z) per contact
     L.own = o;
     o += ((K * 32 + 15u) & ~15u);
     L.base = o;
@@ -827,11 +831,21 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// 16-byte global -> shared asynchronous copy (LDGSTS), L2 only.
+// 16-byte global -> shared asynchronous copy (LDGSTS); .ca allocates in L1
+// (partners are shared by neighbouring owners), .cg goes to L2 only.
+#ifndef DEM_CP_ASYNC_CA
+#define DEM_CP_ASYNC_CA 0
+#endif
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
+#if DEM_CP_ASYNC_CA
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
+               "l"(gmem_src)
+               : "memory");
+#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
                : "memory");
+#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -854,8 +868,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
   float4* pf = reinterpret_cast<float4*>(ws + L.pf);            // [buf][field][lane]
   uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
-  float4* s_r4 = reinterpret_cast<float4*>(ws + L.res);        // [lane]: F_c, Tc.x
-  float2* s_r2 = reinterpret_cast<float2*>(ws + L.res + 512);  // [lane]: Tc.y, Tc.z
+  float4* s_r4 = reinterpret_cast<float4*>(ws + L.res);              // [m % kResW]: F_c, Tc.x
+  float2* s_r2 = reinterpret_cast<float2*>(ws + L.res + kResW * 16);  // [m % kResW]: Tc.y, Tc.z
   uint8_t* s_own = ws + L.own;                                  // owner of each contact
   uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);  // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
@@ -994,20 +1008,23 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
         Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
       }
     }
-    s_r4[lane] = make_float4(Fc.x, Fc.y, Fc.z, Tc.x);
-    if (MODEL == 0) s_r2[lane] = make_float2(Tc.y, Tc.z);
-    __syncwarp();
-    // each owner adds its contacts of this round, in candidate order
-    const uint32_t lo = max(mybase, r0), hi = min(mybase + npair, r0 + 32);
-    for (uint32_t x = lo; x < hi; ++x) {
-      const float4 r4 = s_r4[x - r0];
-      F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
-      if (MODEL == 0) {
-        const float2 r2 = s_r2[x - r0];
-        T = mk(T.x + r4.w, T.y + r2.x, T.z + r2.y);
+    const uint32_t w0 = r0 - r0 % kResW;  // first contact of the current window
+    s_r4[r0 - w0 + lane] = make_float4(Fc.x, Fc.y, Fc.z, Tc.x);
+    if (MODEL == 0) s_r2[r0 - w0 + lane] = make_float2(Tc.y, Tc.z);
+    if (r0 + 32 - w0 == kResW || r0 + 32 >= M) {  // window full (or last round)
+      __syncwarp();
+      // each owner adds its contacts of this window, in candidate order
+      const uint32_t lo = max(mybase, w0), hi = min(mybase + npair, r0 + 32);
+      for (uint32_t x = lo; x < hi; ++x) {
+        const float4 r4 = s_r4[x - w0];
+        F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
+        if (MODEL == 0) {
+          const float2 r2 = s_r2[x - w0];
+          T = mk(T.x + r4.w, T.y + r2.x, T.z + r2.y);
+        }
       }
+      __syncwarp();
     }
-    __syncwarp();
   }
   if (!valid) return;
   if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
