@@ -216,10 +216,11 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, uint32_t* s_warp) {
 __global__ void __launch_bounds__(kScanThreads)
     k_tile_sum(const uint32_t* in, uint32_t n, uint32_t* tsum, DevErr* err, int count_step) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
-  if (err && ld_volatile(&err->code) != 0u) return;
+  const uint32_t e = err ? ld_volatile(&err->code) : 0u;  // checked once the loads are out
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   load_tile(in, n, base, v);
+  if (e != 0u) return;
   uint32_t local = 0;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) local += v[q];
@@ -235,14 +236,15 @@ __global__ void __launch_bounds__(kScanThreads)
                  const uint32_t* __restrict__ tsum, DevErr* err) {
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_excl[kScanThreads / 32];
-  if (err && ld_volatile(&err->code) != 0u) return;
+  const uint32_t e = err ? ld_volatile(&err->code) : 0u;  // checked once the loads are out
   const uint32_t tile = blockIdx.x;
-  // prefix of all preceding tiles
-  uint32_t acc = 0;
-  for (uint32_t t = threadIdx.x; t < tile; t += kScanThreads) acc += __ldg(&tsum[t]);
   const uint64_t base = (uint64_t)tile * kScanTile + (uint64_t)threadIdx.x * kScanItems;
   uint32_t v[kScanItems];
   load_tile(in, n, base, v);
+  // prefix of all preceding tiles
+  uint32_t acc = 0;
+  for (uint32_t t = threadIdx.x; t < tile; t += kScanThreads) acc += __ldg(&tsum[t]);
+  if (e != 0u) return;
   const uint32_t prefix = block_sum(acc, s_warp);
   uint32_t local = 0;
 #pragma unroll
@@ -313,12 +315,11 @@ __global__ void __launch_bounds__(256)
               const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
               uint32_t* __restrict__ tmp, unsigned long long* status_next, uint32_t* ctr_next,
               uint32_t ntiles_next, const DevErr* err) {
-  if (ld_volatile(&err->code) != 0u) return;
+  // error word, slot count and the first loads go out together (loads below
+  // the capacity n are always in bounds; entries past nslots are ignored)
+  const uint32_t e = ld_volatile(&err->code);
+  const int64_t ns = (int64_t)__ldg(nslots);  // this step's input slots
   const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  // reset the other parity's scan state for the next step
-  for (int64_t t = tid; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
-  if (tid == 0) *ctr_next = 0u;
-  n = min(n, (int64_t)__ldg(nslots));  // this step's input slots
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t k[kItems], r[kItems], o[kItems];
 #pragma unroll
@@ -327,6 +328,11 @@ __global__ void __launch_bounds__(256)
     k[u] = i < n ? __ldg(&key[i]) : 0u;
     r[u] = i < n ? __ldg(&prank[i]) : 0u;
   }
+  if (e != 0u) return;
+  // reset the other parity's scan state for the next step
+  for (int64_t t = tid; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
+  if (tid == 0) *ctr_next = 0u;
+  n = min(n, ns);
 #pragma unroll
   for (int u = 0; u < kItems; ++u) o[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&off[k[u]]) : 0u;
 #pragma unroll
@@ -345,8 +351,10 @@ __global__ void __launch_bounds__(256)
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
            const uint32_t* __restrict__ nslots, const DevErr* err) {
-  if (ld_volatile(&err->code) != 0u) return;
-  n = min(n, (int64_t)__ldg(nslots));
+  // error word, slot count and the first loads go out together (tmp below the
+  // capacity n is always in bounds; entries past nslots are ignored)
+  const uint32_t ecode = ld_volatile(&err->code);
+  const int64_t ns = (int64_t)__ldg(nslots);
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
 #pragma unroll
@@ -354,6 +362,8 @@ __global__ void __launch_bounds__(256)
     const int64_t j = base + (int64_t)u * blockDim.x;
     s[u] = j < n ? __ldg(&tmp[j]) : 0u;
   }
+  if (ecode != 0u) return;
+  n = min(n, ns);
 #pragma unroll
   for (int u = 0; u < kItems; ++u) c[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&key[s[u]]) : 0u;
 #pragma unroll
@@ -675,6 +685,19 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
 // clist[k*N + j] = t (each partner's sorted slot, in candidate order =
 // ascending sorted slot). Few registers, so the SM keeps many warps in flight
 // to hide the neighbour-row latency.
+// Owned sorted slots [jlo, jhi): single GPU all N slots (no memory access on
+// the critical path), slab mode [off[own_c0], off[own_c1]).
+__device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid& g, uint32_t N,
+                                            uint32_t& jlo, uint32_t& jhi) {
+  if (g.slab) {
+    jlo = __ldg(&b.off[g.own_c0]);
+    jhi = __ldg(&b.off[g.own_c1]);
+  } else {
+    jlo = 0u;
+    jhi = N;
+  }
+}
+
 #ifndef DEM_DETECT_Q
 #define DEM_DETECT_Q 0  // 1: k_detect stores the partner's old slot perm[t] instead of t
 #endif
@@ -753,11 +776,13 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
 #endif
 __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
                                                                  uint32_t N, uint32_t K) {
-  if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
+  uint32_t jlo, jhi;
+  owned_range(b, g, N, jlo, jhi);
   const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= jhi) return;
   const float4 P = __ldg(&b.pos_sorted[j]);
+  if (err != 0u) return;
   // own cell: the step-2 hash of the own position (identical to CM by construction)
   const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
   const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
@@ -862,7 +887,7 @@ template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
   extern __shared__ __align__(16) uint8_t smem_raw[];
-  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
   const WarpSmemLayout L = WarpSmemLayout::make(K);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
@@ -875,15 +900,22 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
 
-  const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
+  uint32_t jlo, jhi;
+  owned_range(b, g, N, jlo, jhi);
   const uint32_t j0 = jlo + (blockIdx.x * kSweepWarps + warp) * 32u;
   const uint32_t j = j0 + lane;
   const bool valid = j < jhi;
   if (j0 >= jhi) return;  // whole warp past the end
 
-  // ---- own particle (step 4 gather through SCCM) and its contact list
+  // ---- own particle (step 4 gather through SCCM) and its contact list. The
+  // first four list entries are read before the count is known (entries past
+  // the count are never used), so they do not wait for it.
   const uint32_t s = valid ? __ldcs(&b.perm[j]) : 0u;
   const uint32_t nc = valid ? __ldcs(&b.ccount[j]) : 0u;
+  uint32_t t_first[4];
+#pragma unroll
+  for (int u = 0; u < 4; ++u) t_first[u] = valid && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
+  if (err != 0u) return;  // warp-uniform (one load per warp instruction)
   const bool overflow = nc > K;
   const uint32_t npair = min(nc, K);
   Own o;
@@ -897,7 +929,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   for (uint32_t k0 = 0; k0 < npair; k0 += 4) {
     uint32_t t4[4], q4[4];
 #pragma unroll
-    for (int u = 0; u < 4; ++u) t4[u] = k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u;
+    for (int u = 0; u < 4; ++u)
+      t4[u] = k0 == 0 ? t_first[u]
+                      : (k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       q4[u] = DEM_DETECT_Q ? t4[u] : (k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u);
