@@ -698,9 +698,6 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
   }
 }
 
-#ifndef DEM_DETECT_Q
-#define DEM_DETECT_Q 0  // 1: k_detect stores the partner's old slot perm[t] instead of t
-#endif
 // One scan of the 27-cell candidates of sorted slot j (9 row ranges, bounds
 // loaded per z-plane). FAST: the fp32 decision r = d² - S² < 0 only, with
 // `amb` raised (>= 0) when some candidate lies inside the ±16u band of R14 —
@@ -751,11 +748,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
           amb = fmaxf(amb, fmaf(S2, 9.5367431640625e-7f, -fabsf(rr)));  // 16u S² - |r|
         }
         if (hit && t != j) {
-#if DEM_DETECT_Q
-          if (npair < K) __stcg(out, __ldg(&b.perm[t]));  // the partner's old slot (SCCM)
-#else
           if (npair < K) __stcg(out, t);
-#endif
           out += N;
           ++npair;
         }
@@ -934,7 +927,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
                       : (k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
 #pragma unroll
     for (int u = 0; u < 4; ++u)
-      q4[u] = DEM_DETECT_Q ? t4[u] : (k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u);
+      q4[u] = k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u;
 #pragma unroll
     for (int u = 0; u < 4; ++u)
       if (k0 + u < npair) s_cq[(k0 + u) * 32 + lane] = q4[u];
