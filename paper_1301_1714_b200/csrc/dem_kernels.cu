@@ -29,6 +29,20 @@ namespace dem {
 // ------------------------------------------------------------ helpers ------
 
 __device__ __forceinline__ uint32_t lane_id() { return threadIdx.x & 31u; }
+
+// Programmatic dependent launch (launch_pdl): let the next kernel of the step
+// be scheduled while this one drains, then wait here until the previous
+// kernel has completed and its writes are visible. No-ops when launched
+// without the attribute.
+#ifndef DEM_PDL
+#define DEM_PDL 0  // measured: no gain in the graph (profiles/r1_history.md #24)
+#endif
+__device__ __forceinline__ void pdl_enter() {
+#if DEM_PDL
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+  asm volatile("griddepcontrol.wait;" ::: "memory");
+#endif
+}
 __device__ __forceinline__ uint32_t lanemask_lt() {
   uint32_t m;
   asm("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
@@ -215,6 +229,7 @@ __device__ __forceinline__ uint32_t block_sum(uint32_t x, uint32_t* s_warp) {
 
 __global__ void __launch_bounds__(kScanThreads)
     k_tile_sum(const uint32_t* in, uint32_t n, uint32_t* tsum, DevErr* err, int count_step) {
+  pdl_enter();
   __shared__ uint32_t s_warp[kScanThreads / 32];
   const uint32_t e = err ? ld_volatile(&err->code) : 0u;  // checked once the loads are out
   const uint64_t base = (uint64_t)blockIdx.x * kScanTile + (uint64_t)threadIdx.x * kScanItems;
@@ -234,6 +249,7 @@ __global__ void __launch_bounds__(kScanThreads)
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_apply(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
                  const uint32_t* __restrict__ tsum, DevErr* err) {
+  pdl_enter();
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_excl[kScanThreads / 32];
   const uint32_t e = err ? ld_volatile(&err->code) : 0u;  // checked once the loads are out
@@ -315,6 +331,7 @@ __global__ void __launch_bounds__(256)
               const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
               uint32_t* __restrict__ tmp, unsigned long long* status_next, uint32_t* ctr_next,
               uint32_t ntiles_next, const DevErr* err) {
+  pdl_enter();
   // error word, slot count and the first loads go out together (loads below
   // the capacity n are always in bounds; entries past nslots are ignored)
   const uint32_t e = ld_volatile(&err->code);
@@ -351,6 +368,7 @@ __global__ void __launch_bounds__(256)
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
            const uint32_t* __restrict__ nslots, const DevErr* err) {
+  pdl_enter();
   // error word, slot count and the first loads go out together (tmp below the
   // capacity n is always in bounds; entries past nslots are ignored)
   const uint32_t ecode = ld_volatile(&err->code);
@@ -607,6 +625,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
 template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, DevPhys ph,
                                                    uint32_t N, uint32_t K) {
+  pdl_enter();
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t jlo = __ldg(&b.off[g.own_c0]), jhi = __ldg(&b.off[g.own_c1]);
   const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
@@ -769,6 +788,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
 #endif
 __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
                                                                  uint32_t N, uint32_t K) {
+  pdl_enter();
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
   uint32_t jlo, jhi;
   owned_range(b, g, N, jlo, jhi);
@@ -879,6 +899,7 @@ __device__ __forceinline__ void cp_async_wait() {
 template <int MODEL, bool DIAG>
 __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+  pdl_enter();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
   const WarpSmemLayout L = WarpSmemLayout::make(K);
@@ -1701,14 +1722,32 @@ int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen
   return K_OTHER;
 }
 
+// Launch with programmatic stream serialization (the kernel calls pdl_enter()).
+template <typename... KArgs, typename... Args>
+static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, size_t smem,
+                       cudaStream_t st, Args... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = DEM_PDL;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...);
+}
+
 int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
   // `status` holds at least ceil(n / kScanTile) words: used as the tile sums
   (void)ctr;
   const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
   uint32_t* tsum = reinterpret_cast<uint32_t*>(status);
-  k_tile_sum<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, n, tsum, err, count_step);
-  k_scan_apply<<<tiles > 0 ? tiles : 1, kScanThreads, 0, st>>>(in, out, n, zero, tsum, err);
+  launch_pdl(k_tile_sum, tiles > 0 ? tiles : 1, kScanThreads, 0, st, in, n, tsum, err, count_step);
+  launch_pdl(k_scan_apply, tiles > 0 ? tiles : 1, kScanThreads, 0, st, in, out, n, zero,
+             (const uint32_t*)tsum, err);
   return K_SCAN;
 }
 
@@ -1718,18 +1757,16 @@ int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t nt
   const int64_t need = ((int64_t)ntiles_next + 255) / 256;
   if (blocks < need) blocks = need;
   if (blocks < 1) blocks = 1;
-  k_scatter<<<(unsigned)blocks, 256, 0, st>>>(n, b.nslots, b.key_in, b.prank, b.off, b.tmp,
-                                              b.scan_status_next, b.scan_ctr_next, ntiles_next,
-                                              b.err);
+  launch_pdl(k_scatter, (unsigned)blocks, 256, 0, st, n, b.nslots, b.key_in, b.prank, b.off, b.tmp,
+             b.scan_status_next, b.scan_ctr_next, ntiles_next, b.err);
   return K_SCATTER;
 }
 
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
-  k_rank<<<(unsigned)((n + per - 1) / per), 256, 0, st>>>(n, b.key_in, b.off, b.tmp, b.perm,
-                                                           b.pos_in, b.pos_sorted, b.nslots,
-                                                           b.err);
+  launch_pdl(k_rank, (unsigned)((n + per - 1) / per), 256, 0, st, n, b.key_in, b.off, b.tmp, b.perm,
+             b.pos_in, b.pos_sorted, b.nslots, b.err);
   return K_RANK;
 }
 
@@ -1738,11 +1775,11 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
                            const DevGrid& g, const DevPhys& ph, int variant) {
   const uint32_t N = (uint32_t)n;
   if (variant == 1) {  // the paper's mapping, one fused kernel
-    k_sweep_tpp<MODEL, DIAG><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    launch_pdl(k_sweep_tpp<MODEL, DIAG>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
   } else {  // full contact lists, warp-flattened contact rounds
     const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
-    k_force<MODEL, DIAG><<<blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st>>>(
-        b, g, ph, N, K);
+    launch_pdl(k_force<MODEL, DIAG>, blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st,
+               b, g, ph, N, K);
   }
 }
 
@@ -1786,7 +1823,7 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                   const DevGrid& g) {
   if (n <= 0) return K_DETECT;
-  k_detect<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, K);
+  launch_pdl(k_detect, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K);
   return K_DETECT;
 }
 
