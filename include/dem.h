@@ -82,6 +82,11 @@ enum dem_flags {
   DEM_F_HALF_LISTS = 1u << 6, /* ablation: each contact pair evaluated once (Newton's third
                                  law, half contact lists + a per-pair result buffer); default:
                                  full lists, each side evaluated by its particle's warp */
+  DEM_F_FORCE_DENSE = 1u << 7, /* force-kernel configuration for many contacts per particle;
+                                  default: chosen after the first step from the measured
+                                  history entries per particle (> 7: dense). Both give
+                                  bitwise-identical results */
+  DEM_F_FORCE_LIGHT = 1u << 8, /* force-kernel configuration for few contacts per particle */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
@@ -161,6 +166,8 @@ typedef struct {
   /* per-kernel device time accumulated while profiling (dem_profile) */
   double kernel_ms[8];
   int64_t kernel_count[8];
+  int32_t force_cfg;     /* k_force configuration in use: 0 dense, 1 light, -1 not chosen yet */
+  int32_t reserved;
 } dem_stats;
 
 /* Kernel indices of dem_stats.kernel_ms. */

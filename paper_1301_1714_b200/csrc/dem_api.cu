@@ -86,6 +86,7 @@ struct dem_handle {
 
   int cur = 0;
   int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
+  int fcfg = -1;      // k_force configuration (0 dense, 1 light); -1: chosen at the first step
 
   // graphs: g2[b] = two steps starting at parity b; g1[b] = one step
   cudaGraphExec_t g2[2] = {nullptr, nullptr};
@@ -278,6 +279,7 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   // lists (Newton's third law) and the paper's fused mapping are ablations
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
                       : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
+                      : (h->fcfg == 1)                         ? 3
                                                                : 2;
   if (variant == 0) {  // half lists: detect, pair, finish
     rec(K_DETECT, true);
@@ -291,7 +293,7 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
     rec(K_FINISH, false);
     h->launches += 2;
   } else {
-    if (variant == 2) {
+    if (variant >= 2) {
       rec(K_DETECT, true);
       launch_detect(h->stream, h->cap, h->K, s, h->g);
       rec(K_DETECT, false);
@@ -712,6 +714,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   h->cap = cap;
   h->cur = 0;
   h->steps = 0;
+  h->fcfg = -1;
   destroy_graphs(h);
   const size_t N = (size_t)(cap > 0 ? cap : 1);
   const int64_t ncells_a = ncl;
@@ -807,6 +810,10 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   return DEM_OK;
 }
 
+// c̄ above which the dense k_force configuration wins (C2, C3: ~8-11 measured
+// faster dense; C4, C5: ~5 faster light; profiles/r1_history.md #25)
+constexpr double kDenseContacts = 7.0;
+
 int dem_step(dem_handle* h, int64_t nsteps) {
   if (!h) return DEM_EINVAL;
   if (nsteps < 0) return fail(h, DEM_EINVAL, "nsteps < 0");
@@ -815,6 +822,29 @@ int dem_step(dem_handle* h, int64_t nsteps) {
   if (nsteps == 0 || (h->n == 0 && !h->slab)) {
     h->steps += (h->n == 0) ? nsteps : 0;
     return DEM_OK;
+  }
+  if (h->fcfg < 0) {  // choose the k_force configuration
+    const uint32_t fl = h->p.flags;
+    if (fl & (DEM_F_FORCE_DENSE | DEM_F_FORCE_LIGHT) || h->p.model != DEM_MODEL_PRACTICAL) {
+      h->fcfg = (fl & DEM_F_FORCE_LIGHT) ? 1 : 0;
+    } else {
+      // one eager step in the dense configuration, then the history entries
+      // per particle it produced (c̄, walls included) decide the rest
+      h->fcfg = 0;
+      h->p.flags |= DEM_F_NO_GRAPH;
+      int rc = dem_step(h, 1);
+      h->p.flags = fl;
+      if (rc) return rc;
+      --nsteps;
+      if (h->n > 0) {
+        dem_stats st{};
+        rc = dem_get_stats(h, &st);
+        if (rc) return rc;
+        const double cbar = (double)st.contacts / (double)h->n;
+        h->fcfg = cbar > kDenseContacts ? 0 : 1;
+      }
+      if (nsteps == 0) return DEM_OK;
+    }
   }
   const int64_t ctr0 = h->pending ? h->pend_ctr0 + h->pend_steps : h->steps;
   const int cur0 = h->cur;
@@ -1089,6 +1119,7 @@ int dem_get_stats(dem_handle* h, dem_stats* out) {
   out->steps = h->steps;
   out->launches = h->launches;
   out->graph_launches = h->graph_launches;
+  out->force_cfg = h->fcfg;
   for (int k = 0; k < 8; ++k) {
     out->kernel_ms[k] = h->kernel_ms[k];
     out->kernel_count[k] = h->kernel_count[k];

@@ -816,27 +816,40 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
 // order). Partner slots are translated to old slots once per warp, so a round
 // issues its partner-state and history loads together. δ_t,old is read at the
 // contact's own list index first (persisting contacts keep their position).
-#ifndef DEM_FORCE_PFBUFS
-#define DEM_FORCE_PFBUFS 1  // 1: single buffer (next round issued once the current is in registers)
-#endif
-constexpr uint32_t kPfBufs = DEM_FORCE_PFBUFS;
-#ifndef DEM_FORCE_RESW
-#define DEM_FORCE_RESW 2  // rounds per accumulation window (results kept in smem until then)
-#endif
-constexpr uint32_t kResW = 32 * DEM_FORCE_RESW;
+// Two configurations of the same kernel, chosen per handle from the measured
+// contacts per particle (dem_api.cu, choose_force_cfg); identical arithmetic
+// and summation order, so their results are bitwise equal:
+//   kForceDense (0): owner state in registers, broadcast by 12 shuffles per
+//     round; partner old slots staged per (k, lane); 72 registers, 7 blocks/SM.
+//     Best when a warp has many rounds (c̄ ≳ 8: C2, C3).
+//   kForceLight (1): owner velocity and spin in shared memory (4 shuffles per
+//     round for the position), partner old slots staged in chunks of 256
+//     contacts; 64 registers, 8 blocks/SM. Best for c̄ ≲ 8 (C4, C5).
+// Both keep each window of two rounds' results in shared memory and let the
+// owners accumulate once per window.
+constexpr int kForceDense = 0, kForceLight = 1;
+template <int CFG>
+struct ForceCfg {
+  static constexpr bool kOwnSmem = CFG == kForceLight;
+  static constexpr uint32_t kChunk = CFG == kForceLight ? 256u : 0u;  // 0: per (k, lane)
+  static constexpr int kMinBlocks = CFG == kForceLight ? 8 : 7;
+};
+constexpr uint32_t kResW = 64;  // contacts per accumulation window (two rounds)
 struct WarpSmemLayout {
-  uint32_t bytes, pf, cq, res, own, base, slot, nold;
-  __host__ __device__ static WarpSmemLayout make(uint32_t K) {
+  uint32_t bytes, pf, cq, res, own, ost, base, slot, nold;
+  __host__ __device__ static WarpSmemLayout make(uint32_t K, int cfg) {
     WarpSmemLayout L;
     uint32_t o = 0;
     L.pf = o;
-    o += kPfBufs * 4 * 32 * 16;  // prefetch buffer(s): partner pos, vel, omg, old δ_t entry
+    o += 4 * 32 * 16;  // prefetch buffer: partner pos, vel, omg, predicted δ_t,old entry
     L.cq = o;
-    o += K * 32 * 4;  // partner old slot of each (k, lane)
+    o += (cfg == kForceLight ? ForceCfg<kForceLight>::kChunk : K * 32) * 4;  // partner old slots
     L.res = o;
-    o += kResW * 24;  // window of results: float4 (F_c, Tc.x) then float2 (Tc.y, Tc.z) per contact
+    o += kResW * 24;  // results window: float4 (F_c, Tc.x), then float2 (Tc.y, Tc.z)
     L.own = o;
-    o += ((K * 32 + 15u) & ~15u);
+    o += ((K * 32 + 15u) & ~15u);  // owner lane of each contact
+    L.ost = o;
+    if (cfg == kForceLight) o += 2 * 32 * 16;  // owner V, W per lane
     L.base = o;
     o += 36 * 4;
     L.slot = o;
@@ -869,21 +882,12 @@ __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return (uint32_t)__cvta_generic_to_shared(p);
 }
 
-// 16-byte global -> shared asynchronous copy (LDGSTS); .ca allocates in L1
-// (partners are shared by neighbouring owners), .cg goes to L2 only.
-#ifndef DEM_CP_ASYNC_CA
-#define DEM_CP_ASYNC_CA 0
-#endif
+// 16-byte global -> shared asynchronous copy (LDGSTS), L2 only (.cg; the
+// L1-allocating .ca measured slower, profiles/r1_history.md #18).
 __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src) {
-#if DEM_CP_ASYNC_CA
-  asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
-               "l"(gmem_src)
-               : "memory");
-#else
   asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(smem_dst)),
                "l"(gmem_src)
                : "memory");
-#endif
 }
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
@@ -893,24 +897,23 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N_PENDING) : "memory");
 }
 
-#ifndef DEM_SWEEP_MINB
-#define DEM_SWEEP_MINB 7
-#endif
-template <int MODEL, bool DIAG>
-__global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
+template <int MODEL, bool DIAG, int CFG>
+__global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+  using C = ForceCfg<CFG>;
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
-  const WarpSmemLayout L = WarpSmemLayout::make(K);
+  const WarpSmemLayout L = WarpSmemLayout::make(K, CFG);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
-  float4* pf = reinterpret_cast<float4*>(ws + L.pf);            // [buf][field][lane]
-  uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);      // [k*32 + lane]
+  float4* pf = reinterpret_cast<float4*>(ws + L.pf);                 // [field][lane]
+  uint32_t* s_cq = reinterpret_cast<uint32_t*>(ws + L.cq);           // partner old slots
   float4* s_r4 = reinterpret_cast<float4*>(ws + L.res);              // [m % kResW]: F_c, Tc.x
   float2* s_r2 = reinterpret_cast<float2*>(ws + L.res + kResW * 16);  // [m % kResW]: Tc.y, Tc.z
-  uint8_t* s_own = ws + L.own;                                  // owner of each contact
-  uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);  // [33]
+  uint8_t* s_own = ws + L.own;                                       // owner of each contact
+  float4* s_ost = reinterpret_cast<float4*>(ws + L.ost);             // light: [V | W][lane]
+  uint32_t* s_base = reinterpret_cast<uint32_t*>(ws + L.base);       // [33]
   uint32_t* s_slot = reinterpret_cast<uint32_t*>(ws + L.slot);
   uint32_t* s_nold = reinterpret_cast<uint32_t*>(ws + L.nold);
 
@@ -939,19 +942,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
   s_slot[lane] = s;
   s_nold[lane] = n_old;
-  // partner sorted slots -> old slots (SCCM), four lookups in flight per lane
-  for (uint32_t k0 = 0; k0 < npair; k0 += 4) {
-    uint32_t t4[4], q4[4];
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      t4[u] = k0 == 0 ? t_first[u]
-                      : (k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      q4[u] = k0 + u < npair ? __ldg(&b.perm[t4[u]]) : 0u;
-#pragma unroll
-    for (int u = 0; u < 4; ++u)
-      if (k0 + u < npair) s_cq[(k0 + u) * 32 + lane] = q4[u];
+  if (C::kOwnSmem) {
+    s_ost[lane] = o.V;
+    s_ost[32 + lane] = o.W;
   }
   // exclusive warp scan of the per-lane contact counts
   uint32_t incl = npair;
@@ -965,21 +958,42 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
   s_base[lane] = mybase;
   if (lane == 31) s_base[32] = M;
   for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
+  // partner sorted slots -> old slots (SCCM), four lookups in flight per lane:
+  // dense, all of them into s_cq[k*32 + lane]; light, those of the warp's
+  // contacts [c0, c0 + kChunk) into s_cq[m - c0]
+  auto translate = [&](uint32_t c0) {
+    const uint32_t klo = C::kChunk ? (c0 > mybase ? c0 - mybase : 0u) : 0u;
+    const uint32_t khi = C::kChunk ? min(npair, c0 + C::kChunk > mybase ? c0 + C::kChunk - mybase : 0u)
+                                   : npair;
+    for (uint32_t k0 = klo; k0 < khi; k0 += 4) {
+      uint32_t t4[4], q4[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        t4[u] = k0 == 0 ? t_first[u]
+                        : (k0 + u < khi ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) q4[u] = k0 + u < khi ? __ldg(&b.perm[t4[u]]) : 0u;
+#pragma unroll
+      for (int u = 0; u < 4; ++u)
+        if (k0 + u < khi) s_cq[C::kChunk ? mybase + k0 + u - c0 : (k0 + u) * 32 + lane] = q4[u];
+    }
+  };
+  translate(0);
   __syncwarp();
 
-  // prefetch of round r0's partner state + predicted old δ_t entry into buffer `buf`
-  auto prefetch = [&](uint32_t r0, uint32_t buf) {
+  // prefetch of round r0's partner state + predicted δ_t,old entry (the
+  // contact's own index in the owner's old list) into the buffer
+  auto prefetch = [&](uint32_t r0) {
     const uint32_t m = r0 + lane;
     if (m < M) {
       const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
-      const uint32_t q = s_cq[k * 32 + ow];
-      float4* d = pf + buf * 128;
-      cp_async16(&d[lane], &b.pos_in[q]);
-      cp_async16(&d[32 + lane], &b.vel_in[q]);
+      const uint32_t q = C::kChunk ? s_cq[m % C::kChunk] : s_cq[k * 32 + ow];
+      cp_async16(&pf[lane], &b.pos_in[q]);
+      cp_async16(&pf[32 + lane], &b.vel_in[q]);
       if (MODEL == 0) {
-        cp_async16(&d[64 + lane], &b.omg_in[q]);
-        if (k < s_nold[ow]) cp_async16(&d[96 + lane], &b.hist_in[(size_t)k * N + s_slot[ow]]);
+        cp_async16(&pf[64 + lane], &b.omg_in[q]);
+        if (k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[(size_t)k * N + s_slot[ow]]);
       }
     }
     cp_async_commit();
@@ -987,64 +1001,53 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
 
   // ---- the warp's M contacts, 32 per round (step 7), next round in flight
   f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
-  if (M > 0) prefetch(0, 0);
-  uint32_t buf = 0;
-  for (uint32_t r0 = 0; r0 < M; r0 += 32, buf ^= (kPfBufs - 1u)) {
-    float4 Qr, VQr, WQr, Hr;  // this lane's prefetched partner data, in registers
-    if (kPfBufs == 2) {
-      if (r0 + 32 < M) {
-        prefetch(r0 + 32, buf ^ 1u);
-        cp_async_wait<1>();
-      } else {
-        cp_async_wait<0>();
-      }
-    } else {
-      cp_async_wait<0>();
-    }
-    {
-      const float4* d = pf + buf * 128;
-      Qr = d[lane];
-      VQr = d[32 + lane];
-      WQr = d[64 + lane];
-      Hr = d[96 + lane];
-    }
-    if (kPfBufs == 1 && r0 + 32 < M) {
+  if (M > 0) prefetch(0);
+  for (uint32_t r0 = 0; r0 < M; r0 += 32) {
+    cp_async_wait<0>();
+    const float4 Q = pf[lane], VQ = pf[32 + lane], WQ = pf[64 + lane], Hr = pf[96 + lane];
+    if (r0 + 32 < M) {
       __syncwarp();
-      prefetch(r0 + 32, 0);  // overwrite the buffer: this round's data is in registers
+      if (C::kChunk && (r0 + 32) % C::kChunk == 0) {  // the next round opens a new chunk
+        translate(r0 + 32);
+        __syncwarp();
+      }
+      prefetch(r0 + 32);  // overwrite the buffer: this round's data is in registers
     }
     const uint32_t m = r0 + lane;
     const uint32_t ow = m < M ? s_own[m] : 0u;
-    // owner state from the owner lane's registers (all lanes take part)
+    // owner state: position from the owner lane's registers (all lanes take
+    // part), velocity and spin likewise (dense) or from shared memory (light)
     Own po;
     po.P.x = __shfl_sync(0xffffffffu, o.P.x, ow);
     po.P.y = __shfl_sync(0xffffffffu, o.P.y, ow);
     po.P.z = __shfl_sync(0xffffffffu, o.P.z, ow);
     po.P.w = __shfl_sync(0xffffffffu, o.P.w, ow);
-    po.V.x = __shfl_sync(0xffffffffu, o.V.x, ow);
-    po.V.y = __shfl_sync(0xffffffffu, o.V.y, ow);
-    po.V.z = __shfl_sync(0xffffffffu, o.V.z, ow);
-    po.V.w = __shfl_sync(0xffffffffu, o.V.w, ow);
-    po.W.x = __shfl_sync(0xffffffffu, o.W.x, ow);
-    po.W.y = __shfl_sync(0xffffffffu, o.W.y, ow);
-    po.W.z = __shfl_sync(0xffffffffu, o.W.z, ow);
-    po.W.w = __shfl_sync(0xffffffffu, o.W.w, ow);
+    if (C::kOwnSmem) {
+      po.V = s_ost[ow];
+      po.W = s_ost[32 + ow];
+    } else {
+      po.V.x = __shfl_sync(0xffffffffu, o.V.x, ow);
+      po.V.y = __shfl_sync(0xffffffffu, o.V.y, ow);
+      po.V.z = __shfl_sync(0xffffffffu, o.V.z, ow);
+      po.V.w = __shfl_sync(0xffffffffu, o.V.w, ow);
+      po.W.x = __shfl_sync(0xffffffffu, o.W.x, ow);
+      po.W.y = __shfl_sync(0xffffffffu, o.W.y, ow);
+      po.W.z = __shfl_sync(0xffffffffu, o.W.z, ow);
+      po.W.w = __shfl_sync(0xffffffffu, o.W.w, ow);
+    }
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (m < M) {
       const uint32_t k = m - s_base[ow];
-      const float4 Q = Qr;
-      const float4 VQ = VQr;
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
         raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w));
       } else if (MODEL == 0) {
-        const float4 WQ = WQr;
         const uint32_t pid = __float_as_uint(WQ.w);
         const uint32_t no = s_nold[ow];
         f3 dold;
-        const float4 hk = k < no ? Hr : make_float4(0.f, 0.f, 0.f, 0.f);
-        if (k < no && __float_as_uint(hk.w) == pid)
-          dold = mk(hk.x, hk.y, hk.z);
+        if (k < no && __float_as_uint(Hr.w) == pid)
+          dold = mk(Hr.x, Hr.y, Hr.z);
         else
           dold = old_history(b.hist_in, N, s_slot[ow], no, 0xFFFFFFFFu, pid);
         f3 dnew;
@@ -1075,6 +1078,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps, DEM_SWEEP_MINB)
     }
   }
   if (!valid) return;
+  if (C::kOwnSmem) {  // (those registers were free during the rounds)
+    o.V = s_ost[lane];
+    o.W = s_ost[32 + lane];
+  }
   if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
@@ -1335,11 +1342,17 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
 void sweep_prepare(uint32_t K) {
-  const int smem = (int)(WarpSmemLayout::make(K).bytes * kSweepWarps);
-  cudaFuncSetAttribute(k_force<0, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_force<0, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_force<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  cudaFuncSetAttribute(k_force<1, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
+  const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
+  const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
+  const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  cudaFuncSetAttribute(k_force<0, false, kForceDense>, A, sd);
+  cudaFuncSetAttribute(k_force<0, true, kForceDense>, A, sd);
+  cudaFuncSetAttribute(k_force<1, false, kForceDense>, A, sd);
+  cudaFuncSetAttribute(k_force<1, true, kForceDense>, A, sd);
+  cudaFuncSetAttribute(k_force<0, false, kForceLight>, A, sl);
+  cudaFuncSetAttribute(k_force<0, true, kForceLight>, A, sl);
+  cudaFuncSetAttribute(k_force<1, false, kForceLight>, A, sl);
+  cudaFuncSetAttribute(k_force<1, true, kForceLight>, A, sl);
 }
 
 // --------------------------------------------------------- slab exchange --
@@ -1776,10 +1789,15 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
   const uint32_t N = (uint32_t)n;
   if (variant == 1) {  // the paper's mapping, one fused kernel
     launch_pdl(k_sweep_tpp<MODEL, DIAG>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
-  } else {  // full contact lists, warp-flattened contact rounds
-    const uint32_t smem = WarpSmemLayout::make(K).bytes * kSweepWarps;
-    launch_pdl(k_force<MODEL, DIAG>, blocks_for(n, 32 * kSweepWarps), 32 * kSweepWarps, smem, st,
-               b, g, ph, N, K);
+  } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
+    const int cfg = variant == 3 ? kForceLight : kForceDense;
+    const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
+    if (cfg == kForceLight)
+      launch_pdl(k_force<MODEL, DIAG, kForceLight>, blocks_for(n, 32 * kSweepWarps),
+                 32 * kSweepWarps, smem, st, b, g, ph, N, K);
+    else
+      launch_pdl(k_force<MODEL, DIAG, kForceDense>, blocks_for(n, 32 * kSweepWarps),
+                 32 * kSweepWarps, smem, st, b, g, ph, N, K);
   }
 }
 

@@ -28,6 +28,8 @@ DEM_MODEL_PRACTICAL, DEM_MODEL_SIMPLE = 0, 1
 DEM_F_TRUNCATE_DT, DEM_F_CLAMP_FN, DEM_F_DIAG, DEM_F_ASYNC, DEM_F_NO_GRAPH = 1, 2, 4, 8, 16
 DEM_F_THREAD_PER_PARTICLE = 32
 DEM_F_HALF_LISTS = 64
+DEM_F_FORCE_DENSE = 128
+DEM_F_FORCE_LIGHT = 256
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
@@ -66,7 +68,8 @@ class DemStats(C.Structure):
                 ("cell_edge", C.c_double), ("steps", C.c_int64), ("contacts", C.c_int64),
                 ("max_contacts_seen", C.c_int64), ("launches", C.c_int64),
                 ("graph_launches", C.c_int64), ("kernel_ms", C.c_double * 8),
-                ("kernel_count", C.c_int64 * 8)]
+                ("kernel_count", C.c_int64 * 8), ("force_cfg", C.c_int32),
+                ("reserved", C.c_int32)]
 
 
 class DemError(RuntimeError):
@@ -377,7 +380,8 @@ class Dem:
                     steps=s.steps, contacts=s.contacts, max_contacts_seen=s.max_contacts_seen,
                     launches=s.launches, graph_launches=s.graph_launches,
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
-                    kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)})
+                    kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
+                    force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg])
 
 
 # C-ABI-named aliases ----------------------------------------------------------

@@ -9,7 +9,8 @@ import pytest
 
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
-from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_HALF_LISTS,
+from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
+                                      DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
                                       Dem, DemError)
 
@@ -60,7 +61,8 @@ def test_hash_sort_offsets_bit_exact(name):
 
 # ------------------------------------------------------ T2 one step -------
 
-@pytest.mark.parametrize("variant", [0, DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
+                                     DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
     sc = scenes_small()[idx]
@@ -145,7 +147,8 @@ def test_touching_pairs_in_fp32_band():
     d2f = ((sc.pos[n:] - sc.pos[:n]) ** 2).sum(1, dtype=np.float32)
     in_band = np.abs(d2f.astype(np.float64) - S2) <= 16 * 2.0 ** -24 * S2
     assert in_band.sum() >= 40 and exact[in_band].any() and not exact[in_band].all()
-    for flags in (DEM_F_DIAG, DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
+    for flags in (DEM_F_DIAG | DEM_F_FORCE_DENSE, DEM_F_DIAG | DEM_F_FORCE_LIGHT,
+                  DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
         d = make(sc, flags=flags)
         st, h = oracle_inputs(d, 16)
         d.step(1)
@@ -305,6 +308,36 @@ def test_sweep_variants_agree(other):
     scale = np.abs(sa["force"]).max()
     assert np.abs(sa["force"] - sb["force"]).max() <= 1e-5 * scale
     assert contacts_dict(a).keys() == contacts_dict(b).keys()
+
+
+@pytest.mark.parametrize("name", ["C2", "gas"])
+def test_force_configs_bitwise(name):
+    """The dense and light k_force configurations differ only in where the
+    owner state and partner slots are staged: same contacts, same arithmetic,
+    same summation order, so whole runs agree bitwise."""
+    sc = S.C2() if name == "C2" else scenes_small()[1]
+    runs = []
+    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT):
+        d = make(sc, flags=DEM_F_DIAG | f)
+        d.step(12)
+        runs.append((d.get_state(forces=True), contacts_dict(d), d.stats()["force_cfg"]))
+    assert [r[2] for r in runs] == ["dense", "light"]
+    for k in ("pos", "vel", "omega", "id", "force", "torque"):
+        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
+    assert runs[0][1].keys() == runs[1][1].keys()
+    assert all(np.array_equal(runs[0][1][x], runs[1][1][x]) for x in runs[0][1])
+
+
+def test_force_config_choice():
+    """Automatic choice after the first step: dense for the jittered FCC
+    packing (c̄ ≈ 11), light for the simple-cubic settling bed (c̄ ≈ 5)."""
+    fcc = make(S.C3(), flags=0)
+    assert fcc.stats()["force_cfg"] is None
+    fcc.step(2)
+    assert fcc.stats()["force_cfg"] == "dense"
+    bed = make(S.C4(scale=4), flags=0)
+    bed.step(2)
+    assert bed.stats()["force_cfg"] == "light"
 
 
 def test_checkpoint_roundtrip_bitwise():
