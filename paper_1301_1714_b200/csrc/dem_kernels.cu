@@ -837,17 +837,15 @@ struct ForceCfg {
 constexpr uint32_t kResW = 64;  // contacts per accumulation window (two rounds)
 struct WarpSmemLayout {
   uint32_t bytes, pf, cq, res, own, ost, base, slot, nold;
+  // fixed-size regions first, so their offsets are compile-time constants;
+  // the K-dependent ones (partner slots, owner map) last
   __host__ __device__ static WarpSmemLayout make(uint32_t K, int cfg) {
     WarpSmemLayout L;
     uint32_t o = 0;
     L.pf = o;
     o += 4 * 32 * 16;  // prefetch buffer: partner pos, vel, omg, predicted δ_t,old entry
-    L.cq = o;
-    o += (cfg == kForceLight ? ForceCfg<kForceLight>::kChunk : K * 32) * 4;  // partner old slots
     L.res = o;
     o += kResW * 24;  // results window: float4 (F_c, Tc.x), then float2 (Tc.y, Tc.z)
-    L.own = o;
-    o += ((K * 32 + 15u) & ~15u);  // owner lane of each contact
     L.ost = o;
     if (cfg == kForceLight) o += 2 * 32 * 16;  // owner V, W per lane
     L.base = o;
@@ -856,6 +854,10 @@ struct WarpSmemLayout {
     o += 32 * 4;
     L.nold = o;
     o += 32 * 4;
+    L.cq = o;
+    o += (cfg == kForceLight ? ForceCfg<kForceLight>::kChunk : K * 32) * 4;  // partner old slots
+    L.own = o;
+    o += ((K * 32 + 15u) & ~15u);  // owner lane of each contact
     L.bytes = (o + 15u) & ~15u;
     return L;
   }
