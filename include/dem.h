@@ -231,6 +231,29 @@ int dem_get_grid(dem_handle* h, int64_t cap, uint32_t* key, uint32_t* perm, uint
  * the current history with a small reduction kernel. */
 int dem_get_stats(dem_handle* h, dem_stats* out);
 
+/* The quantities of the paper's §6 analysis, measured on
+ * the input state of the last step (its sort, cell offsets and contact
+ * lists; owned slots only in slab mode). "Warp" = 32 consecutive sorted
+ * slots, the thread-per-particle mapping of the paper (and of k_detect). */
+typedef struct {
+  int64_t n;                 /* particles analysed */
+  int64_t candidates;        /* Σ_i particles j != i in i's 27 cells (Eq. 12; "about 47") */
+  int64_t max_candidates;
+  int64_t contacts;          /* Σ_i particle-particle contacts of i (walls excluded) */
+  int64_t max_contacts;      /* the kissing bound is 12 for equal spheres */
+  int64_t warp_candidate_slots; /* Σ_warps 32 · max_lanes candidates: lane-iterations of the
+                                   candidate loop under SIMT (divergence) */
+  int64_t warp_contact_slots;   /* Σ_warps 32 · max_lanes contacts: lane-iterations of the
+                                   contact-force evaluation if done per thread */
+  int64_t max_per_cell;      /* most particles in one cell (Eq. 13: √2 (h/d)³ at close packing) */
+  int64_t occupied_cells;
+  int64_t contact_hist[33];  /* particles with k contacts, k = 0..31; [32]: 32 or more */
+} dem_analysis;
+
+/* Fill *out from the last step (DEM_ESTATE before the first step).
+ * Synchronises; one small kernel. */
+int dem_analyze(dem_handle* h, dem_analysis* out);
+
 /* Per-kernel CUDA-event timing of subsequent dem_step calls (eager launches,
  * events around every kernel on the handle's stream); 0 disables. Enabling
  * resets the accumulated times. */

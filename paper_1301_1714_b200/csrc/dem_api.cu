@@ -12,6 +12,7 @@
 #include <algorithm>
 #include <cmath>
 #include <string>
+#include <cstring>
 #include <vector>
 
 #include "dem.h"
@@ -1136,6 +1137,35 @@ int dem_get_stats(dem_handle* h, dem_stats* out) {
     out->contacts = (int64_t)hs[0];
     out->max_contacts_seen = (int64_t)hs[1];
   }
+  return DEM_OK;
+}
+
+int dem_analyze(dem_handle* h, dem_analysis* out) {
+  if (!h || !out) return DEM_EINVAL;
+  if (h->n < 0 || h->steps == 0) return fail(h, DEM_ESTATE, "dem_analyze before the first step");
+  int rc = dem_sync(h);
+  if (rc) return rc;
+  std::memset(out, 0, sizeof(*out));
+  unsigned long long* acc = nullptr;
+  constexpr int kAcc = 9 + 33;
+  if (!dalloc(h, &acc, kAcc)) return fail(h, DEM_ENOMEM, "allocation failed");
+  CUDA_TRY(h, cudaMemsetAsync(acc, 0, sizeof(unsigned long long) * kAcc, h->stream));
+  // the last step read parity cur ^ 1; its sort, offsets and contact lists are intact
+  launch_analyze(h->stream, h->cap, step_buffers(h, h->cur ^ 1), h->g, acc);
+  unsigned long long a[kAcc];
+  CUDA_TRY(h, cudaMemcpyAsync(a, acc, sizeof(a), cudaMemcpyDeviceToHost, h->stream));
+  CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  dev_free(h, acc);
+  out->n = (int64_t)a[0];
+  out->candidates = (int64_t)a[1];
+  out->max_candidates = (int64_t)a[2];
+  out->contacts = (int64_t)a[3];
+  out->max_contacts = (int64_t)a[4];
+  out->warp_candidate_slots = (int64_t)a[5];
+  out->warp_contact_slots = (int64_t)a[6];
+  out->max_per_cell = (int64_t)a[7];
+  out->occupied_cells = (int64_t)a[8];
+  for (int k = 0; k < 33; ++k) out->contact_hist[k] = (int64_t)a[9 + k];
   return DEM_OK;
 }
 

@@ -222,6 +222,8 @@ int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
                            uint32_t* flags);
+int launch_analyze(cudaStream_t st, int64_t n, const StepBuffers& b, const DevGrid& g,
+                   unsigned long long* acc);
 int launch_cnt_stats(cudaStream_t st, int64_t n, const uint32_t* cnt,
                      unsigned long long* sum_max);
 

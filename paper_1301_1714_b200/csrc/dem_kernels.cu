@@ -1702,6 +1702,70 @@ __global__ void k_cnt_stats(int64_t n, const uint32_t* cnt, unsigned long long* 
   }
 }
 
+// §6 analysis (dem_analyze): per owned sorted slot of the last step, the
+// candidate count of its 9 rows (Eq. 12) and its contact count, reduced per
+// warp of 32 consecutive slots (the paper's mapping), plus the population of
+// its cell. acc: [0] n, [1] Σcand, [2] max cand, [3] Σcont, [4] max cont,
+// [5] Σ 32·warp-max cand, [6] Σ 32·warp-max cont, [7] max per cell,
+// [8] occupied cells, [9..41] contact histogram.
+__global__ void __launch_bounds__(256) k_analyze(StepBuffers b, DevGrid g, uint32_t N,
+                                                 unsigned long long* acc) {
+  __shared__ unsigned long long s_hist[33];
+  if (threadIdx.x < 33) s_hist[threadIdx.x] = 0ull;
+  __syncthreads();
+  uint32_t jlo, jhi;
+  owned_range(b, g, N, jlo, jhi);
+  const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
+  const bool valid = j < jhi;
+  uint32_t cand = 0, cont = 0, pop = 0, first = 0;
+  if (valid) {
+    const float4 P = __ldg(&b.pos_sorted[j]);
+    const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
+    const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
+    const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+    const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
+    const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
+    const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int z = cz + dz;
+      if (z < 0 || z >= g.nz) continue;
+      for (int dy = -1; dy <= 1; ++dy) {
+        const int y = cy + dy;
+        if (y < 0 || y >= g.ny) continue;
+        const uint32_t row = (uint32_t)z * nxy + (uint32_t)y * (uint32_t)g.nx;
+        cand += __ldg(&b.off[row + xb + 1]) - __ldg(&b.off[row + xa]);
+      }
+    }
+    cand -= 1u;  // itself
+    cont = __ldg(&b.ccount[j]);
+    const uint32_t c = (uint32_t)cz * nxy + (uint32_t)cy * (uint32_t)g.nx + (uint32_t)cx;
+    const uint32_t o0 = __ldg(&b.off[c]);
+    pop = __ldg(&b.off[c + 1]) - o0;
+    first = (j == o0) ? 1u : 0u;
+    atomicAdd(&s_hist[min(cont, 32u)], 1ull);
+  }
+  const uint32_t wmax_c = __reduce_max_sync(0xffffffffu, cand);
+  const uint32_t wmax_k = __reduce_max_sync(0xffffffffu, cont);
+  const uint32_t wpop = __reduce_max_sync(0xffffffffu, pop);
+  const uint32_t wn = __reduce_add_sync(0xffffffffu, valid ? 1u : 0u);
+  const uint32_t wcand = __reduce_add_sync(0xffffffffu, cand);
+  const uint32_t wcont = __reduce_add_sync(0xffffffffu, cont);
+  const uint32_t wfirst = __reduce_add_sync(0xffffffffu, first);
+  if (lane_id() == 0 && wn > 0) {
+    atomicAdd(&acc[0], (unsigned long long)wn);
+    atomicAdd(&acc[1], (unsigned long long)wcand);
+    atomicMax(&acc[2], (unsigned long long)wmax_c);
+    atomicAdd(&acc[3], (unsigned long long)wcont);
+    atomicMax(&acc[4], (unsigned long long)wmax_k);
+    atomicAdd(&acc[5], 32ull * wmax_c);
+    atomicAdd(&acc[6], 32ull * wmax_k);
+    atomicMax(&acc[7], (unsigned long long)wpop);
+    atomicAdd(&acc[8], (unsigned long long)wfirst);
+  }
+  __syncthreads();
+  if (threadIdx.x < 33 && s_hist[threadIdx.x]) atomicAdd(&acc[9 + threadIdx.x], s_hist[threadIdx.x]);
+}
+
 // ------------------------------------------------------------ launchers ----
 
 static inline unsigned blocks_for(int64_t n, int threads) {
@@ -1927,6 +1991,13 @@ int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride
   if (m <= 0) return K_OTHER;
   k_insert_contacts<<<blocks_for(m, 256), 256, 0, st>>>(m, n, stride, K, id_i, id_j, dt3,
                                                         slot_of_id, hist, cnt, flags);
+  return K_OTHER;
+}
+
+int launch_analyze(cudaStream_t st, int64_t n, const StepBuffers& b, const DevGrid& g,
+                   unsigned long long* acc) {
+  if (n <= 0) return K_OTHER;
+  k_analyze<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, acc);
   return K_OTHER;
 }
 

@@ -72,6 +72,14 @@ class DemStats(C.Structure):
                 ("reserved", C.c_int32)]
 
 
+class DemAnalysis(C.Structure):
+    _fields_ = [("n", C.c_int64), ("candidates", C.c_int64), ("max_candidates", C.c_int64),
+                ("contacts", C.c_int64), ("max_contacts", C.c_int64),
+                ("warp_candidate_slots", C.c_int64), ("warp_contact_slots", C.c_int64),
+                ("max_per_cell", C.c_int64), ("occupied_cells", C.c_int64),
+                ("contact_hist", C.c_int64 * 33)]
+
+
 class DemError(RuntimeError):
     def __init__(self, code: int, where: str, detail: str):
         super().__init__(f"{where}: {detail} (code {code})")
@@ -101,6 +109,7 @@ def lib() -> C.CDLL:
         L.dem_get_grid.argtypes = [VP, I64, P, P, P, C.POINTER(I64)]
         L.dem_get_stats.argtypes = [VP, C.POINTER(DemStats)]
         L.dem_profile.argtypes = [VP, I32]
+        L.dem_analyze.argtypes = [VP, C.POINTER(DemAnalysis)]
         L.dem_nccl_unique_id.argtypes = [VP]
         L.dem_exchange_handle.argtypes = [VP, P]
         L.dem_exchange_ptr.argtypes = [VP, C.POINTER(VP)]
@@ -384,6 +393,26 @@ class Dem:
                     force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg])
 
 
+    def analyze(self) -> dict:
+        """The paper's §6 quantities for the last step (dem_analyze), raw
+        counts plus the ratios the paper argues with."""
+        a = DemAnalysis()
+        self._check(lib().dem_analyze(self.h, C.byref(a)), "dem_analyze")
+        n = max(a.n, 1)
+        return dict(
+            n=a.n, candidates=a.candidates, max_candidates=a.max_candidates,
+            contacts=a.contacts, max_contacts=a.max_contacts,
+            warp_candidate_slots=a.warp_candidate_slots,
+            warp_contact_slots=a.warp_contact_slots, max_per_cell=a.max_per_cell,
+            occupied_cells=a.occupied_cells, contact_hist=list(a.contact_hist),
+            candidates_mean=a.candidates / n, contacts_mean=a.contacts / n,
+            # contacts among candidates: the paper's "about a quarter" (PAPER.md:155)
+            contact_fraction=a.contacts / max(a.candidates, 1),
+            # lane efficiency of the thread-per-particle mapping (SIMT divergence)
+            tpp_candidate_lane_efficiency=a.candidates / max(a.warp_candidate_slots, 1),
+            tpp_contact_lane_efficiency=a.contacts / max(a.warp_contact_slots, 1))
+
+
 # C-ABI-named aliases ----------------------------------------------------------
 def dem_create(sp, **kw) -> Dem:
     return Dem(sp, **kw)
@@ -415,6 +444,10 @@ def dem_get_contacts(h: Dem):
 
 def dem_get_grid(h: Dem):
     return h.get_grid()
+
+
+def dem_analyze(h: Dem):
+    return h.analyze()
 
 
 def dem_get_stats(h: Dem):

@@ -340,6 +340,53 @@ def test_force_config_choice():
     assert bed.stats()["force_cfg"] == "light"
 
 
+def analysis_from_oracle(p, s, K):
+    """The §6 quantities of dem_analyze, recomputed from the oracle's grid
+    (hash, stable sort, offsets, 27-cell neighbour sets) and its contact set
+    for the same input state."""
+    pos = s["pos"].astype(np.float64)
+    n = pos.shape[0]
+    nx, ny, nz = orc.grid_dims(p)
+    CM = orc.hash_cells(p, pos)
+    SCM, SCCM = orc.sort_map(CM)
+    off = orc.cell_offsets(SCM, nx * ny * nz).astype(np.int64)
+    pop = np.diff(off)
+    cand_cell = {}
+    cand = np.empty(n, np.int64)
+    for j in range(n):
+        c = int(SCM[j])
+        if c not in cand_cell:
+            cand_cell[c] = sum(int(pop[x]) for x in orc.neighbor_cells(p, c)) - 1
+        cand[j] = cand_cell[c]
+    pairs = orc.contacts_grid(p, pos, s["radius"])
+    cont = np.bincount(pairs.ravel().astype(np.int64), minlength=n)[SCCM]  # sorted order
+    w = lambda a: int(sum(32 * a[i:i + 32].max() for i in range(0, n, 32)))
+    return dict(n=n, candidates=int(cand.sum()), max_candidates=int(cand.max()),
+                contacts=int(cont.sum()), max_contacts=int(cont.max()),
+                warp_candidate_slots=w(cand), warp_contact_slots=w(cont),
+                max_per_cell=int(pop.max()), occupied_cells=int((pop > 0).sum()),
+                contact_hist=list(np.bincount(np.minimum(cont, 32), minlength=33)))
+
+
+@pytest.mark.parametrize("idx", [0, 1])
+def test_analysis_matches_oracle(idx):
+    """dem_analyze (the paper's §6 counts: candidates, contacts, SIMT lane
+    slots of the thread-per-particle mapping, cell populations) equals the
+    same counts taken from the oracle's grid and contact set, exactly."""
+    sc = [S.C2(), scenes_small()[1]][idx]
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc, flags=0)
+    d.step(3)
+    s = d.get_state()
+    d.step(1)
+    got = d.analyze()
+    want = analysis_from_oracle(p, s, sc.params.max_contacts)
+    for k, v in want.items():
+        assert got[k] == v, (k, got[k], v)
+    if idx == 0:  # equal spheres: the kissing bound of PAPER.md:155
+        assert got["max_contacts"] <= 12
+
+
 def test_checkpoint_roundtrip_bitwise():
     sc = S.C1()
     d1 = make(sc, flags=0)
