@@ -413,51 +413,59 @@ def run_ours(args):
 
 def run_e2e(d, sc, stream, steps, world, barrier):
     """Each step: dem_set_particles + dem_set_contacts from pinned host memory,
-    dem_step(1), dem_get_state + dem_get_contacts into pinned host memory."""
+    dem_step(1), dem_get_state + dem_get_contacts into pinned host memory. Two
+    pinned buffer sets alternate (a step's outputs are the next step's inputs),
+    as a host-driven user loop would run it."""
     import torch
 
     s = d.get_state()
     ci, cj, cd = d.get_contacts()
     n = sc.n
 
-    def pinned(a):
-        t = torch.empty(a.shape, dtype={np.float32: torch.float32, np.uint32: torch.int32}[
-            a.dtype.type], pin_memory=True)
-        out = t.numpy()
-        out[...] = a.view(out.dtype) if a.dtype == np.uint32 else a
-        return t, out.view(a.dtype)
+    def pinned(shape, dtype):
+        t = torch.empty(shape, dtype={np.float32: torch.float32, np.uint32: torch.int32}[dtype],
+                        pin_memory=True)
+        return t.numpy().view(dtype)
 
-    host = {k: pinned(v) for k, v in s.items()}
-    cap = max(len(ci) * 2, 1024)
-    hci = pinned(np.zeros(cap, np.uint32))
-    hcj = pinned(np.zeros(cap, np.uint32))
-    hcd = pinned(np.zeros((cap, 3), np.float32))
+    cap = max(2 * len(ci), 1024)
+    sets = []
+    for _ in range(2):
+        st = {k: pinned(v.shape, v.dtype.type) for k, v in s.items()}
+        ct = (pinned((cap,), np.uint32), pinned((cap,), np.uint32), pinned((cap, 3), np.float32))
+        sets.append((st, ct))
+    for k, v in s.items():
+        sets[0][0][k][...] = v
     m = len(ci)
-    hci[1][:m], hcj[1][:m], hcd[1][:m] = ci, cj, cd
-    out = {k: pinned(v)[1] for k, v in s.items()}
+    sets[0][1][0][:m], sets[0][1][1][:m], sets[0][1][2][:m] = ci, cj, cd
     h2d = d2h = 0
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
-    for _ in range(steps):
-        H = {k: v[1] for k, v in host.items()}
+    parts = np.zeros(5)
+    for k in range(steps):
+        (H, (hi, hj, hd)), (O, oc) = sets[k % 2], sets[(k + 1) % 2]
+        tt = [time.perf_counter()]
         d.set_particles(H["pos"], H["vel"], H["omega"], H["radius"], H["mass"], H["id"])
-        d.set_contacts(hci[1][:m], hcj[1][:m], hcd[1][:m])
+        tt.append(time.perf_counter())
+        d.set_contacts(hi[:m], hj[:m], hd[:m])
+        tt.append(time.perf_counter())
         d.step(1)
-        got = d.get_state(out=out)
-        a, b, c = d.get_contacts()
-        m = len(a)
-        hci[1][:m], hcj[1][:m], hcd[1][:m] = a, b, c
-        for k in host:
-            host[k][1][...] = got[k]
+        tt.append(time.perf_counter())
+        d.get_state(out=O)
+        tt.append(time.perf_counter())
         h2d += n * 48 + m * 20
+        m = len(d.get_contacts(out=oc)[0])
+        tt.append(time.perf_counter())
         d2h += n * 48 + m * 20
+        parts += np.diff(tt)
     barrier()
     t = time.perf_counter() - t0
     return {"value": world * n * steps / t, "unit": UNIT,
             "h2d_bytes_per_step": h2d // max(1, steps), "d2h_bytes_per_step": d2h // max(1, steps),
             "steps": steps, "api": "dem_set_particles+dem_set_contacts+dem_step(1)+"
-                                   "dem_get_state+dem_get_contacts per step, host buffers"}
+                                   "dem_get_state+dem_get_contacts per step, pinned host buffers",
+            "ms_per_call": dict(zip(("set_particles", "set_contacts", "step", "get_state",
+                                     "get_contacts"), (parts * 1e3 / max(1, steps)).round(2).tolist()))}
 
 
 def main():

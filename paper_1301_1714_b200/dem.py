@@ -214,7 +214,10 @@ class Dem:
                 return torch.cuda.caching_allocator_alloc(int(nbytes), dev, st or 0)
 
             def _free(ctx, ptr, nbytes, st):
-                torch.cuda.caching_allocator_delete(ptr)
+                try:
+                    torch.cuda.caching_allocator_delete(ptr)
+                except Exception:  # interpreter teardown: torch is already gone
+                    pass
 
             A = DemAllocator()
             A.ctx = None
@@ -352,9 +355,21 @@ class Dem:
                     "dem_get_state")
         return out
 
-    def get_contacts(self):
-        """dem_get_contacts -> (id_i, id_j, dt3) host arrays."""
+    def get_contacts(self, out=None):
+        """dem_get_contacts -> (id_i, id_j, dt3) host arrays. With `out` =
+        (id_i, id_j, dt3) caller buffers (e.g. pinned) of enough capacity, one
+        call fills them and views of the first m entries are returned."""
         m = C.c_int64()
+        if out is not None:
+            oi, oj, od = out
+            cap = min(len(oi), len(oj), len(od))
+            rc = lib().dem_get_contacts(self.h, DEM_MEM_HOST, cap, oi.ctypes.data, oj.ctypes.data,
+                                        od.ctypes.data, C.byref(m))
+            if rc == DEM_OK:
+                k = int(m.value)
+                return oi[:k], oj[:k], od[:k]
+            if rc != DEM_EINVAL:
+                self._check(rc, "dem_get_contacts")
         rc = lib().dem_get_contacts(self.h, DEM_MEM_HOST, 0, None, None, None, C.byref(m))
         if rc not in (DEM_OK, DEM_EINVAL):
             self._check(rc, "dem_get_contacts")
