@@ -187,7 +187,8 @@ int dem_destroy(dem_handle* h);
 
 /* Copy in n particles ("particle properties") and clear the
  * contact history. Validates radius > 0, mass > 0, finite values, centres
- * inside the box, ids < 0xFFFFFFF0 and unique, and the cell edge against
+ * at most r beyond a wall (R18: what a step may produce), ids < 0xFFFFFFF0
+ * and unique, and the cell edge against
  * 2 r_max (1 + 2^-10). Sizes the CDG: n_a = floor((hi_a - lo_a)/h) >= 3.
  * Computes CM for the next step (step 2). n == 0 is allowed. */
 int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src);
@@ -195,7 +196,11 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src);
 /* Replace the tangential-displacement history (Eq. 7's δ_t,old) with m
  * entries (id_i, id_j, dt3[3]): the displacement stored on particle id_i's
  * side for partner id_j (a wall w = 0..5 is id 0xFFFFFFF0 + w). Arrays are
- * host or device per mem_kind. Requires dense ids (a permutation of 0..n-1).
+ * host or device per mem_kind. Single GPU: requires dense ids (a permutation
+ * of 0..n-1; an id_i outside is DEM_EINVAL). Slab rank (world_size > 1): ids
+ * below 4 n + 2^20 of the set passed to dem_set_particles; entries whose
+ * id_i this rank does not own are skipped, so every rank may be given the
+ * same global list (or only its own, e.g. its dem_get_contacts output).
  * DEM_EOVERFLOW if a particle gets more than max_contacts entries. */
 int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t* id_i,
                      const uint32_t* id_j, const float* dt3);

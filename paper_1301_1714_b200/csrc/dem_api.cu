@@ -46,6 +46,7 @@ struct dem_handle {
   DevGrid g{};
   DevPhys ph{};
   bool ids_dense = false;
+  int64_t id_bound = 0;  // ids < id_bound (slot map size of dem_set_contacts); 0: sparse ids
 
   // device buffers (ping-pong b in {0,1})
   float4 *pos[2] = {}, *vel[2] = {}, *omg[2] = {};
@@ -762,11 +763,14 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     launch_xpack(st, cap, sb, g, h->K, h->xregion, h->xl, h->xtiles, h->xs, 1);
     CUDA_TRY(h, cudaStreamSynchronize(st));
     unstage();
-    h->ids_dense = false;  // ids are global: ORDER_ID / set_contacts are single-GPU only
+    h->ids_dense = false;  // ids are global: ORDER_ID is single-GPU only
+    // dem_set_contacts maps global ids through a table of id_max + 1 entries
+    h->id_bound = hp.id_max < (uint64_t)(4 * n + (1 << 20)) ? (int64_t)hp.id_max + 1 : 0;
     return DEM_OK;
   }
   // 6. ids: unique; dense (a permutation of 0..n-1) enables ORDER_ID and set_contacts
   h->ids_dense = false;
+  h->id_bound = 0;
   if (n > 0) {
     uint32_t* seen = nullptr;
     uint32_t* dup = nullptr;
@@ -789,6 +793,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
         return fail(h, DEM_EINVAL, "duplicate particle ids");
       }
       h->ids_dense = true;
+      h->id_bound = n;
     } else {
       // sparse ids: check uniqueness on the host (setup path only)
       std::vector<uint32_t> ids((size_t)n);
@@ -1026,7 +1031,9 @@ int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t*
                      const uint32_t* id_j, const float* dt3) {
   if (!h || m < 0 || (m > 0 && (!id_i || !id_j || !dt3))) return DEM_EINVAL;
   if (h->n < 0) return fail(h, DEM_ESTATE, "no particles set");
-  if (!h->ids_dense) return fail(h, DEM_EINVAL, "dem_set_contacts needs ids 0..n-1");
+  if (h->id_bound <= 0 && (h->n > 0 || h->slab))
+    return fail(h, DEM_EINVAL, h->slab ? "dem_set_contacts needs ids below 4 n + 2^20"
+                                       : "dem_set_contacts needs ids 0..n-1");
   if (h->p.model != DEM_MODEL_PRACTICAL) return m == 0 ? DEM_OK : fail(h, DEM_EINVAL, "simple model keeps no history");
   cudaStream_t st = h->stream;
   const int64_t n = h->n;
@@ -1057,15 +1064,19 @@ int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t*
   } else if (!h->own_stream) {
     cudaStreamSynchronize(nullptr);
   }
+  // id -> slot of this handle's particles (slab mode: the owned ones; contacts
+  // of particles owned by another rank are skipped)
   uint32_t *slot = nullptr, *flags = nullptr;
-  if (!dalloc(h, &slot, (size_t)n) || !dalloc(h, &flags, 1)) {
+  const int64_t nb = h->id_bound;
+  if (!dalloc(h, &slot, (size_t)nb) || !dalloc(h, &flags, 1)) {
     for (void* p : tmp) dev_free(h, p);
     return fail(h, DEM_ENOMEM, "allocation failed");
   }
   CUDA_TRY(h, cudaMemsetAsync(flags, 0, 4, st));
+  CUDA_TRY(h, cudaMemsetAsync(slot, 0xFF, sizeof(uint32_t) * nb, st));
   launch_slot_of_id(st, n, h->omg[h->cur], slot);
-  launch_insert_contacts(st, m, n, h->cap, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
-                         flags);
+  launch_insert_contacts(st, m, nb, h->cap, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
+                         flags, h->slab ? 1 : 0);
   h->launches += 2;
   uint32_t hf = 0;
   CUDA_TRY(h, cudaMemcpyAsync(&hf, flags, 4, cudaMemcpyDeviceToHost, st));

@@ -221,7 +221,7 @@ int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* s
 int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride, uint32_t K,
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
-                           uint32_t* flags);
+                           uint32_t* flags, int skip_unknown);
 int launch_analyze(cudaStream_t st, int64_t n, const StepBuffers& b, const DevGrid& g,
                    unsigned long long* acc);
 int launch_cnt_stats(cudaStream_t st, int64_t n, const uint32_t* cnt,

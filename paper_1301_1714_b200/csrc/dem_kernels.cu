@@ -136,7 +136,9 @@ __global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
     fin &= isfinite(x);
     if (in.vel) fin &= isfinite(in.vel[3 * i + a]);
     if (in.omega) fin &= isfinite(in.omega[3 * i + a]);
-    if (isfinite(x) && ((double)x < g.lo[a] || (double)x > g.hi[a]))
+    // a centre may lie up to r beyond a wall (in contact with it): the states
+    // a step produces (R18) must be loadable again
+    if (isfinite(x) && ((double)x < g.lo[a] - (double)r || (double)x > g.hi[a] + (double)r))
       atomicAdd(&out->outside, 1u);
   }
   if (!fin) atomicAdd(&out->nonfinite, 1u);
@@ -1667,17 +1669,23 @@ __global__ void k_slot_of_id(int64_t n, const float4* omg, uint32_t* slot_of_id)
   slot_of_id[__float_as_uint(omg[i].w)] = (uint32_t)i;
 }
 
-// flags[0] |= 1: id out of range, |= 2: capacity overflow
-__global__ void k_insert_contacts(int64_t m, int64_t n, int64_t stride, uint32_t K,
+// flags[0] |= 1: id out of range, |= 2: capacity overflow. slot_of_id has
+// id_bound entries; 0xFFFFFFFF marks an id this handle does not hold (a slab
+// rank skips the contacts of other ranks' particles).
+__global__ void k_insert_contacts(int64_t m, int64_t id_bound, int64_t stride, uint32_t K,
                                   const uint32_t* id_i,
                                   const uint32_t* id_j, const float* dt3,
                                   const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
-                                  uint32_t* flags) {
+                                  uint32_t* flags, int skip_unknown) {
   int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (e >= m) return;
   const uint32_t a = id_i[e];
-  if (a >= (uint64_t)n) { atomicOr(flags, 1u); return; }
+  if (a >= (uint64_t)id_bound) {
+    if (!skip_unknown) atomicOr(flags, 1u);
+    return;
+  }
   const uint32_t s = slot_of_id[a];
+  if (s == 0xFFFFFFFFu) return;
   const uint32_t k = atomicAdd(&cnt[s], 1u);
   if (k >= K) { atomicOr(flags, 2u); return; }
   hist[(size_t)k * stride + s] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
@@ -1987,10 +1995,11 @@ int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* s
 int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride, uint32_t K,
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,
-                           uint32_t* flags) {
+                           uint32_t* flags, int skip_unknown) {
   if (m <= 0) return K_OTHER;
   k_insert_contacts<<<blocks_for(m, 256), 256, 0, st>>>(m, n, stride, K, id_i, id_j, dt3,
-                                                        slot_of_id, hist, cnt, flags);
+                                                        slot_of_id, hist, cnt, flags,
+                                                        skip_unknown);
   return K_OTHER;
 }
 

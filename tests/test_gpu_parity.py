@@ -387,6 +387,22 @@ def test_analysis_matches_oracle(idx):
         assert got["max_contacts"] <= 12
 
 
+def test_set_particles_accepts_what_a_step_produces():
+    """dem_set_particles takes centres up to r beyond a wall (a particle in
+    contact with it, R18), like the step's escape check, and rejects more."""
+    sc = S.C1()
+    pos = sc.pos.copy()
+    for frac, ok in ((0.5, True), (2.0, False)):
+        pos[0, 0] = sc.params.box_lo[0] - frac * sc.radius[0]
+        d = Dem(sc.params)
+        if ok:
+            d.set_particles(pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+        else:
+            with pytest.raises(DemError) as e:
+                d.set_particles(pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+            assert "outside" in str(e.value)
+
+
 def test_checkpoint_roundtrip_bitwise():
     sc = S.C1()
     d1 = make(sc, flags=0)

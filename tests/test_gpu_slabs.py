@@ -195,3 +195,51 @@ def test_reset_particles_between_runs():
     b = union_state(fresh)
     for k in ("pos", "vel", "omega", "id"):
         assert np.array_equal(a[k], b[k])
+
+
+def test_slab_checkpoint_roundtrip():
+    """Restart from a checkpoint: every rank is given the gathered state and
+    the gathered contact list (dem_set_contacts keeps each rank's own) and
+    the run continues as the uninterrupted one: same contact pairs, state
+    equal to fp32 summation-order rounding (in-cell ties follow the new input
+    order)."""
+    sc = fast_gas(seed=6, n=5000)
+    ds = make_slabs(sc, 2, flags=0)
+    step_all(ds, 4)
+    u = union_state(ds)
+    c = union_contacts(ds)
+    step_all(ds, 6)
+    ref = union_state(ds)
+    keys = sorted(c)
+    ii = np.array([a for a, _ in keys], np.uint32)
+    jj = np.array([b for _, b in keys], np.uint32)
+    vv = np.array([c[k] for k in keys], np.float32)
+    fresh = [Dem(sc.params, flags=0, rank=r, world=2) for r in range(2)]
+    for d in fresh:
+        d.set_particles(u["pos"], u["vel"], u["omega"], u["radius"], u["mass"], u["id"])
+        d.set_contacts(ii, jj, vv)
+    for r, d in enumerate(fresh):
+        d.connect_local(fresh[r - 1] if r > 0 else None, fresh[r + 1] if r < 1 else None)
+    step_all(fresh, 6)
+    got = union_state(fresh)
+    assert np.array_equal(got["id"], ref["id"])
+    assert np.abs(got["pos"] - ref["pos"]).max() <= 1e-6 * np.abs(ref["pos"]).max()
+    assert np.abs(got["vel"] - ref["vel"]).max() <= 1e-4 * np.abs(ref["vel"]).max()
+    assert union_contacts(fresh).keys() == union_contacts(ds).keys()
+
+
+def test_slab_set_contacts_global_list():
+    """Every rank given the same global contact list keeps exactly its own."""
+    sc = fast_gas(seed=8, n=4000)
+    ds = make_slabs(sc, 3, flags=0)
+    step_all(ds, 3)
+    before = union_contacts(ds)
+    keys = sorted(before)
+    ii = np.array([a for a, _ in keys], np.uint32)
+    jj = np.array([b for _, b in keys], np.uint32)
+    vv = np.array([before[k] for k in keys], np.float32)
+    for d in ds:
+        d.set_contacts(ii, jj, vv)
+    after = union_contacts(ds)
+    assert after.keys() == before.keys()
+    assert all(np.array_equal(after[k], before[k].astype(np.float32)) for k in keys)
