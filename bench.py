@@ -398,7 +398,9 @@ def run_ours(args):
     elif not args.no_e2e:
         line["e2e"] = {"value": None, "unit": UNIT, "h2d_bytes_per_step": None,
                        "d2h_bytes_per_step": None,
-                       "unavailable": "slab ranks have no dem_set_contacts yet (round 1)"}
+                       "unavailable": ("a per-step host round trip at N > 1 needs every rank's "
+                                       "results gathered on the host each step (dem_get_state "
+                                       "returns a rank's own particles only); not built")}
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         line["cpu_baseline"] = cpu_baseline_on_state(d, sc)
     elif rank == 0:
