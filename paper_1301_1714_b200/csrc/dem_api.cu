@@ -77,6 +77,7 @@ struct dem_handle {
   int rank = 0, world = 1;
   uint8_t* xregion = nullptr;  // this rank's exchange region (cudaMalloc: IPC-shareable)
   XLayout xl{};
+  uint64_t xregion_bytes = 0;
   const uint8_t* xleft = nullptr;   // neighbours' regions (peer pointers)
   const uint8_t* xright = nullptr;
   bool xleft_ipc = false, xright_ipc = false;
@@ -262,7 +263,8 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   };
   if (h->slab) {  // this step's migrants and ghosts from the neighbours (peer memory)
     rec(K_OTHER, true);
-    launch_xunpack(h->stream, h->cap, s, h->g, h->K, h->xleft, h->xright, h->xl, h->xs,
+    launch_xunpack(h->stream, h->cap, s, h->g, h->K, h->xleft ? h->xleft + kXRegionHdr : nullptr,
+                   h->xright ? h->xright + kXRegionHdr : nullptr, h->xl, h->xs,
                    h->nslots);
     rec(K_OTHER, false);
     h->launches += 2;
@@ -308,7 +310,8 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   h->launches += 5;  // scan is two kernels
   if (h->slab) {  // pack and publish the next step's migrants and ghosts
     rec(K_OTHER, true);
-    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion, h->xl, h->xtiles, h->xs, 0);
+    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xtiles,
+                 h->xs, 0);
     rec(K_OTHER, false);
     h->launches += 3;
   }
@@ -361,11 +364,17 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
     return DEM_OK;
   }
   if (h->slab) {  // no roll-back across ranks: the handle must be set again
-    char buf[200];
-    snprintf(buf, sizeof buf, "%s (slab rank %d): particle id %u in step %u; set the particles again",
-             e.code == 11u ? "slab exchange failed (peer timeout or a migrant skipped a plane)"
-                           : err_name(e.code),
-             h->rank, e.id, e.step);
+    char buf[240];
+    if (e.code == 11u && (e.slot & 0xFFFFFF00u) == 0xFFFFFF00u)
+      snprintf(buf, sizeof buf,
+               "slab exchange failed (slab rank %d): neighbour publication of tag %u never "
+               "arrived (seen: left %u, right %u, low bits) in step %u; set the particles again",
+               h->rank, e.slot & 0xFFu, e.id >> 16, e.id & 0xFFFFu, e.step);
+    else
+      snprintf(buf, sizeof buf, "%s (slab rank %d): particle id %u in step %u; set the particles again",
+               e.code == 11u ? "slab exchange failed (a migrant skipped a plane)"
+                             : err_name(e.code),
+               h->rank, e.id, e.step);
     h->n = -1;
     return fail(h, e.code == 11u ? DEM_EPEER : -(int)e.code, buf);
   }
@@ -654,7 +663,21 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     dev_free(h, st_tiles);
     dev_free(h, ctr);
     n_own = kept;
-    const int64_t per_plane = n_own / std::max(1, z1 - z0) + 1;
+    // exchange capacities from the most populated z-plane of the whole input
+    // set, so that every rank given the same set builds the same layout (a
+    // neighbour reads this rank's blocks at its own offsets; checked at connect)
+    uint32_t* ph = nullptr;
+    if (!dalloc(h, &ph, (size_t)g.nz_global)) {
+      unstage();
+      return fail(h, DEM_ENOMEM, "allocation failed");
+    }
+    CUDA_TRY(h, cudaMemsetAsync(ph, 0, sizeof(uint32_t) * g.nz_global, st));
+    launch_plane_hist(st, n, in.pos, g, ph);
+    std::vector<uint32_t> hh((size_t)g.nz_global);
+    CUDA_TRY(h, cudaMemcpyAsync(hh.data(), ph, sizeof(uint32_t) * g.nz_global, cudaMemcpyDeviceToHost, st));
+    CUDA_TRY(h, cudaStreamSynchronize(st));
+    dev_free(h, ph);
+    const int64_t per_plane = (int64_t)*std::max_element(hh.begin(), hh.end()) + 1;
     const uint32_t gcap = (uint32_t)std::max<int64_t>(4096, 2 * per_plane + 1024);
     const uint32_t mcap = std::max<uint32_t>(1024, gcap / 4);
     cap = n_own + n_own / 4 + 2 * (int64_t)gcap + 2 * (int64_t)mcap;
@@ -694,11 +717,6 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
-      if (h->xregion) cudaFree(h->xregion);
-      h->xregion = nullptr;
-      h->connected = false;  // the neighbours must reconnect to the new region
-      if (cudaMalloc((void**)&h->xregion, 4 * h->xl.bytes) != cudaSuccess) ok = false;
-      else cudaMemset(h->xregion, 0, 4 * h->xl.bytes);
     }
     if (!ok) {
       unstage();
@@ -709,6 +727,23 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     h->ntiles = ntiles;
     h->cap_n = cap;
     h->cap_cells = ncl;
+  }
+  if (h->slab) {  // exchange region: (re)allocated when the layout needs more room
+    const uint64_t need = kXRegionHdr + 4 * h->xl.bytes;
+    if (!h->xregion || h->xregion_bytes < need) {
+      if (h->xregion) cudaFree(h->xregion);
+      h->xregion = nullptr;
+      h->xregion_bytes = 0;
+      h->connected = false;  // the neighbours must reconnect to the new region
+      if (cudaMalloc((void**)&h->xregion, need) != cudaSuccess) {
+        unstage();
+        h->n = -1;
+        return fail(h, DEM_ENOMEM, "exchange region allocation failed");
+      }
+      CUDA_TRY(h, cudaMemset(h->xregion, 0, need));
+      h->xregion_bytes = need;
+    }
+    CUDA_TRY(h, cudaMemcpy(h->xregion, &h->xl, sizeof(XLayout), cudaMemcpyHostToDevice));
   }
   h->g = g;
   h->h = hc;
@@ -760,9 +795,20 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     sb.flags = h->flags;
     sb.off = h->off;
     sb.err = h->err;
-    launch_xpack(st, cap, sb, g, h->K, h->xregion, h->xl, h->xtiles, h->xs, 1);
+    launch_xpack(st, cap, sb, g, h->K, h->xregion + kXRegionHdr, h->xl, h->xtiles, h->xs, 1);
+    DevErr e{};
+    CUDA_TRY(h, cudaMemcpyAsync(&e, h->err, sizeof e, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
     unstage();
+    if (e.code != 0u) {
+      h->n = -1;
+      char buf[200];
+      snprintf(buf, sizeof buf,
+               "dem_set_particles: publishing the boundary planes for the neighbours failed "
+               "(%s at output slot %u, particle id %u; ghost capacity %u, migrant capacity %u)",
+               err_name(e.code), e.slot, e.id, h->xl.ghost_cap, h->xl.mig_cap);
+      return fail(h, e.code == 6u ? DEM_EOVERFLOW : -(int)e.code, buf);
+    }
     h->ids_dense = false;  // ids are global: ORDER_ID is single-GPU only
     // dem_set_contacts maps global ids through a table of id_max + 1 entries
     h->id_bound = hp.id_max < (uint64_t)(4 * n + (1 << 20)) ? (int64_t)hp.id_max + 1 : 0;
@@ -1208,6 +1254,25 @@ int dem_exchange_ptr(dem_handle* h, void** out) {
   return DEM_OK;
 }
 
+// Both neighbours must have published the same exchange layout as this rank
+// (their blocks are read at this rank's offsets): the same particle set was
+// given to every rank.
+static int check_peer_layouts(dem_handle* h) {
+  const uint8_t* peers[2] = {h->xleft, h->xright};
+  for (const uint8_t* p : peers) {
+    if (!p) continue;
+    XLayout pl{};
+    CUDA_TRY(h, cudaMemcpy(&pl, p, sizeof pl, cudaMemcpyDeviceToHost));
+    if (pl.bytes != h->xl.bytes || pl.mig_cap != h->xl.mig_cap ||
+        pl.ghost_cap != h->xl.ghost_cap || pl.K != h->xl.K)
+      return fail(h, DEM_EINVAL,
+                  "neighbour exchange layout differs (ghost capacity " + std::to_string(pl.ghost_cap) +
+                      " vs " + std::to_string(h->xl.ghost_cap) +
+                      "): give every rank the same particle set in dem_set_particles");
+  }
+  return DEM_OK;
+}
+
 int dem_connect(dem_handle* h, const void* left64, const void* right64) {
   if (!h) return DEM_EINVAL;
   if (!h->slab) return fail(h, DEM_ESTATE, "not a slab rank");
@@ -1229,6 +1294,8 @@ int dem_connect(dem_handle* h, const void* left64, const void* right64) {
   }
   if ((h->rank > 0) != (h->xleft != nullptr) || (h->rank < h->world - 1) != (h->xright != nullptr))
     return fail(h, DEM_EINVAL, "a rank needs exactly its existing neighbours");
+  int rc = check_peer_layouts(h);
+  if (rc) return rc;
   h->connected = true;
   destroy_graphs(h);
   return DEM_OK;
@@ -1242,6 +1309,8 @@ int dem_connect_ptrs(dem_handle* h, void* left, void* right) {
   h->xleft_ipc = h->xright_ipc = false;
   if ((h->rank > 0) != (h->xleft != nullptr) || (h->rank < h->world - 1) != (h->xright != nullptr))
     return fail(h, DEM_EINVAL, "a rank needs exactly its existing neighbours");
+  int rc = check_peer_layouts(h);
+  if (rc) return rc;
   h->connected = true;
   destroy_graphs(h);
   return DEM_OK;

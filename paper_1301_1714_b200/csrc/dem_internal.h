@@ -110,6 +110,9 @@ struct XHeader {
   uint32_t n_ghost; // ghosts packed
   uint32_t pad;
 };
+// An exchange region = a header holding the writer's XLayout (read by the
+// neighbours at connect time) + 4 blocks (direction x parity).
+constexpr uint64_t kXRegionHdr = 256;
 struct XLayout {  // byte offsets inside one (direction, parity) block
   uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, bytes;
   uint32_t mig_cap, ghost_cap, K;
@@ -208,6 +211,7 @@ int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const Dev
                    uint32_t* nslots_out);
 // set_particles in slab mode: keep[i] = particle i's z-cell is owned by this rank.
 int launch_keep(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* keep);
+int launch_plane_hist(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* hist);
 
 // Introspection / state movement.
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,

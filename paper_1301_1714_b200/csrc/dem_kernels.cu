@@ -1390,6 +1390,14 @@ __global__ void k_keep(int64_t n, const float* pos, DevGrid g, uint32_t* keep) {
   keep[i] = (cz >= g.z0 && cz < g.z1) ? 1u : 0u;
 }
 
+// particles per global z-plane of the whole input set (identical on every
+// rank given the same set: the exchange capacities derive from its maximum)
+__global__ void k_plane_hist(int64_t n, const float* pos, DevGrid g, uint32_t* hist) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  atomicAdd(&hist[global_cz(g, pos[3 * i + 2])], 1u);
+}
+
 __global__ void k_flags(int64_t n, const float4* pos, DevGrid g, uint32_t* flags) {
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
@@ -1535,6 +1543,7 @@ __global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XS
   if (ld_volatile(&err->code) != 0u) return;
   const uint32_t tag = ld_volatile(&err->step_ctr) + 1u + xbase;
   const uint32_t par = tag & 1u;
+  __shared__ uint32_t s_seen[2];
   if (threadIdx.x == 0) s_ok = 1u;
   __syncthreads();
   if (threadIdx.x < 2) {
@@ -1546,9 +1555,11 @@ __global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XS
       const XHeader* h =
           reinterpret_cast<const XHeader*>(peer + (size_t)(dir * 2 + par) * L.bytes + L.header);
       unsigned long long spins = 0;
-      while (ld_acquire_sys(&h->tag) != tag) {
+      uint32_t seen;
+      while ((seen = ld_acquire_sys(&h->tag)) != tag) {
         if (++spins > (1ull << 27)) {  // peer never published (~30 s): fail, do not hang
           s_ok = 0u;
+          s_seen[threadIdx.x] = seen;
           break;
         }
         __nanosleep(200);
@@ -1561,8 +1572,9 @@ __global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XS
   }
   __syncthreads();
   if (threadIdx.x == 0) {
-    if (!s_ok) {
-      raise_error(err, 11u, 0u, 0u);
+    if (!s_ok) {  // slot: 0xFFFFFF00 | expected tag's low byte; id: tags seen (left, right)
+      raise_error(err, 11u, 0xFFFFFF00u | (tag & 0xFFu),
+                  ((s_seen[0] & 0xFFFFu) << 16) | (s_seen[1] & 0xFFFFu));
       return;
     }
     const uint32_t base = xs->n_out;
@@ -1934,6 +1946,12 @@ int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
       sweep_dispatch<1, false>(st, n, K, b, g, ph, variant);
   }
   return K_SWEEP;
+}
+
+int launch_plane_hist(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* hist) {
+  if (n <= 0) return K_OTHER;
+  k_plane_hist<<<blocks_for(n, 256), 256, 0, st>>>(n, pos, g, hist);
+  return K_OTHER;
 }
 
 int launch_keep(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* keep) {

@@ -10,7 +10,7 @@ import pytest
 
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
-from paper_1301_1714_b200.dem import DEM_F_DIAG, Dem
+from paper_1301_1714_b200.dem import DEM_F_DIAG, Dem, DemError
 
 from .parity import assert_T2_forces, assert_T2_history
 
@@ -243,3 +243,36 @@ def test_slab_set_contacts_global_list():
     after = union_contacts(ds)
     assert after.keys() == before.keys()
     assert all(np.array_equal(after[k], before[k].astype(np.float32)) for k in keys)
+
+
+@pytest.mark.parametrize("P", [2, 3])
+def test_slabs_settling_bed_match_single_gpu(P):
+    """The bench's workload (a settling bed, dense boundary planes, slabs of
+    unequal plane counts): slab ranks agree with the single-GPU run."""
+    sc = S.C4(scale=8)
+    one = Dem(sc.params, flags=DEM_F_DIAG)
+    one.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    ds = make_slabs(sc, P)
+    one.step(4)
+    step_all(ds, 4)
+    a = one.get_state(forces=True)
+    o = np.argsort(a["id"])
+    a = {k: v[o] for k, v in a.items()}
+    b = union_state(ds, forces=True)
+    assert np.array_equal(a["id"], b["id"])
+    assert np.abs(a["pos"] - b["pos"]).max() <= 1e-6 * np.abs(a["pos"]).max()
+    ca = {(int(x), int(y)) for x, y, _ in zip(*one.get_contacts())}
+    assert ca == set(union_contacts(ds))
+
+
+def test_slab_ranks_with_different_sets_refuse_to_connect():
+    """Every rank must be given the same particle set (the exchange layout is
+    derived from it); otherwise connecting fails instead of mis-reading."""
+    sc = S.C4(scale=8)
+    ds = [Dem(sc.params, flags=0, rank=r, world=2) for r in range(2)]
+    ds[0].set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    m = np.arange(sc.n) % 2 == 0  # half the particles on rank 1: sparser planes
+    ds[1].set_particles(sc.pos[m], sc.vel[m], sc.omega[m], sc.radius[m], sc.mass[m], sc.id[m])
+    with pytest.raises(DemError) as e:
+        ds[0].connect_local(None, ds[1])
+    assert "layout" in str(e.value)
