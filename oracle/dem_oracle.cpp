@@ -79,6 +79,14 @@ typedef struct {
   double mu;      /* μ                 Eq. 5   */
   double wCn, wCt, walpha, wmu; /* the same four for particle-wall pairs */
   double ksp, kda, ksh;         /* simple model, Eq. 1 */
+  /* Eqs. 8-10 and 5 write C_k, α (and μ) as functions of the pair (i, j)
+   * (PAPER.md:85-93): with nmat > 1 the four coefficients of a particle pair
+   * are mat[(m_i * nmat + m_j) * 4 + {0: C_n, 1: C_t, 2: α, 3: μ}] for the
+   * materials m_i, m_j of the two particles, and those of a particle-wall
+   * pair wmat[m_i * 4 + ...] (NULL: the wall scalars above). */
+  int32_t nmat;
+  const double* mat;
+  const double* wmat;
 } orc_params;
 
 /* ---------------------------------------------------------------- grid ---- */
@@ -356,6 +364,7 @@ typedef struct {
   double* r;     /* [n]  radius    */
   double* m;     /* [n]  mass      */
   uint32_t* id;  /* [n]  persistent id */
+  uint32_t* mat; /* [n]  material (orc_params.nmat > 1), NULL -> 0 */
 } orc_state;
 
 typedef struct {
@@ -418,7 +427,7 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
 
   /* step 4: reorder all the properties along SCM */
   std::vector<double> x(3 * N), v(3 * N), w(3 * N), r(N), m(N);
-  std::vector<uint32_t> id(N), hcnt(N), hpid(N * K);
+  std::vector<uint32_t> id(N), mt(N, 0u), hcnt(N), hpid(N * K);
   std::vector<double> hdt(N * K * 3);
   for (size_t j = 0; j < N; ++j) {
     size_t s = SCCM[j];
@@ -430,6 +439,7 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
     r[j] = st->r[s];
     m[j] = st->m[s];
     id[j] = st->id[s];
+    if (st->mat) mt[j] = st->mat[s];
     hcnt[j] = hist->cnt[s];
     for (int k = 0; k < K; ++k) {
       hpid[j * K + k] = hist->pid[s * K + k];
@@ -488,8 +498,14 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
           rw[a] = r[j] * w[3 * j + a] + r[t] * w[3 * t + a];
         }
         lookup(j, id[t], dold);
-        orc_pair_practical(nrm, delta, Rstar, mstar, vrel, rw, dold, p->Cn, p->Ct, p->alpha,
-                           p->mu, p->dt, p->flags, Fc, Tc, dnew, mag);
+        /* the pair's coefficients C_k(i, j), α(i, j), μ(i, j) (Eqs. 5, 8-10) */
+        double Cn = p->Cn, Ct = p->Ct, alpha = p->alpha, mu = p->mu;
+        if (p->nmat > 1) {
+          const double* c = &p->mat[((size_t)mt[j] * (size_t)p->nmat + mt[t]) * 4];
+          Cn = c[0], Ct = c[1], alpha = c[2], mu = c[3];
+        }
+        orc_pair_practical(nrm, delta, Rstar, mstar, vrel, rw, dold, Cn, Ct, alpha, mu, p->dt,
+                           p->flags, Fc, Tc, dnew, mag);
         for (int a = 0; a < 3; ++a) Ti[a] += r[j] * Tc[a];
         Tabs[j] += r[j] * mag[1];
         if (!push_hist(id[t], dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
@@ -530,8 +546,13 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
         uint32_t pid = ORC_WALL_PID0 + (uint32_t)wdx;
         lookup(j, pid, dold);
         /* R* = r_i, m* = m_i, v_j = ω_j = 0: the limits r_j, m_j -> ∞ */
-        orc_pair_practical(nrm, delta, r[j], m[j], &v[3 * j], rw, dold, p->wCn, p->wCt,
-                           p->walpha, p->wmu, p->dt, p->flags, Fc, Tc, dnew, mag);
+        double Cn = p->wCn, Ct = p->wCt, alpha = p->walpha, mu = p->wmu;
+        if (p->nmat > 1 && p->wmat) {
+          const double* c = &p->wmat[(size_t)mt[j] * 4];
+          Cn = c[0], Ct = c[1], alpha = c[2], mu = c[3];
+        }
+        orc_pair_practical(nrm, delta, r[j], m[j], &v[3 * j], rw, dold, Cn, Ct, alpha, mu, p->dt,
+                           p->flags, Fc, Tc, dnew, mag);
         for (int b = 0; b < 3; ++b) Ti[b] += r[j] * Tc[b];
         Tabs[j] += r[j] * mag[1];
         if (!push_hist(pid, dnew)) set_err(out, ORC_EOVERFLOW, (int64_t)j, id[j]);
@@ -572,6 +593,7 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
   std::memcpy(st->r, r.data(), N * 8);
   std::memcpy(st->m, m.data(), N * 8);
   std::memcpy(st->id, id.data(), N * 4);
+  if (st->mat) std::memcpy(st->mat, mt.data(), N * 4);
   std::memcpy(hist->cnt, ncnt.data(), N * 4);
   std::memcpy(hist->pid, npid.data(), N * K * 4);
   std::memcpy(hist->dt, ndt.data(), N * K * 3 * 8);

@@ -29,11 +29,12 @@ class OrcParams(C.Structure):
     _fields_ = [("model", C.c_int32), ("flags", C.c_uint32), ("dt", _D), ("g", _D * 3),
                 ("lo", _D * 3), ("hi", _D * 3), ("h", _D), ("Cn", _D), ("Ct", _D),
                 ("alpha", _D), ("mu", _D), ("wCn", _D), ("wCt", _D), ("walpha", _D),
-                ("wmu", _D), ("ksp", _D), ("kda", _D), ("ksh", _D)]
+                ("wmu", _D), ("ksp", _D), ("kda", _D), ("ksh", _D), ("nmat", C.c_int32),
+                ("mat", _P), ("wmat", _P)]
 
 
 class OrcState(C.Structure):
-    _fields_ = [("x", _P), ("v", _P), ("w", _P), ("r", _P), ("m", _P), ("id", _P)]
+    _fields_ = [("x", _P), ("v", _P), ("w", _P), ("r", _P), ("m", _P), ("id", _P), ("mat", _P)]
 
 
 class OrcHist(C.Structure):
@@ -124,6 +125,23 @@ def make_params(sp, radius: np.ndarray | None = None, brute: bool = False) -> Or
     p.walpha = wall(sp.wall_damping, p.alpha)
     p.wmu = wall(sp.wall_friction, p.mu)
     p.ksp, p.kda, p.ksh = _f32(sp.k_sp), _f32(sp.k_da), _f32(sp.k_sh)
+    # material pairs (Eqs. 5, 8-10 as functions of (i, j)): fp32-rounded like
+    # every parameter; the arrays are kept alive on the struct
+    mats = getattr(sp, "materials", None)
+    p.nmat = 1
+    if mats is not None and len(mats) > 1:
+        t = np.ascontiguousarray(np.asarray(mats, np.float32).astype(np.float64))
+        M = t.shape[0]
+        assert t.shape == (M, M, 4), "materials: (M, M, 4) of (C_n, C_t, alpha, mu)"
+        p.nmat = M
+        p._mat = t
+        p.mat = _ptr(t)
+        wm = getattr(sp, "wall_materials", None)
+        if wm is not None:
+            w = np.ascontiguousarray(np.asarray(wm, np.float32).astype(np.float64))
+            assert w.shape == (M, 4)
+            p._wmat = w
+            p.wmat = _ptr(w)
     return p
 
 
@@ -252,31 +270,34 @@ class State:
     radius: np.ndarray
     mass: np.ndarray
     id: np.ndarray
+    mat: np.ndarray | None = None  # material ids (materials tables), None -> 0
 
     @property
     def n(self):
         return int(self.pos.shape[0])
 
     @staticmethod
-    def from_arrays(pos, vel, omega, radius, mass, ids) -> "State":
+    def from_arrays(pos, vel, omega, radius, mass, ids, mat=None) -> "State":
         f = lambda a, s: np.array(a, dtype=np.float64, copy=True).reshape(s)  # noqa: E731
         n = np.asarray(pos).reshape(-1, 3).shape[0]
         return State(f(pos, (n, 3)), f(vel, (n, 3)), f(omega, (n, 3)), f(radius, (n,)),
-                     f(mass, (n,)), np.array(ids, dtype=np.uint32, copy=True))
+                     f(mass, (n,)), np.array(ids, dtype=np.uint32, copy=True),
+                     None if mat is None else np.array(mat, dtype=np.uint32, copy=True))
 
     @staticmethod
     def from_scene(sc) -> "State":
-        return State.from_arrays(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+        return State.from_arrays(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id,
+                                 getattr(sc, "material", None))
 
     def copy(self) -> "State":
         return State(*(a.copy() for a in (self.pos, self.vel, self.omega, self.radius, self.mass,
-                                          self.id)))
+                                          self.id)), None if self.mat is None else self.mat.copy())
 
     def rounded_fp32(self) -> "State":
         """The state rounded to fp32 and back (the 'x~' shadow of SURVEY T3)."""
         r = lambda a: a.astype(np.float32).astype(np.float64)  # noqa: E731
         return State(r(self.pos), r(self.vel), r(self.omega), r(self.radius), r(self.mass),
-                     self.id.copy())
+                     self.id.copy(), None if self.mat is None else self.mat.copy())
 
 
 @dataclass
@@ -352,7 +373,7 @@ class StepResult:
 
 def _structs(st: State, h: History):
     s = OrcState(_ptr(st.pos), _ptr(st.vel), _ptr(st.omega), _ptr(st.radius), _ptr(st.mass),
-                 _ptr(st.id))
+                 _ptr(st.id), None if st.mat is None else _ptr(st.mat))
     hh = OrcHist(h.K, _ptr(h.cnt), _ptr(h.pid), _ptr(h.dt))
     return s, hh
 

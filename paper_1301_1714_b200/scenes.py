@@ -58,6 +58,11 @@ class SimParams:
     max_contacts: int = 16  # K
     truncate_dt: bool = False  # reading R4 flag
     clamp_fn: bool = False  # reading R3 flag
+    # Eqs. 5, 8-10 as functions of the pair: None, or an
+    # (M, M, 4) symmetric table of (C_n, C_t, alpha, mu) per material pair and
+    # optionally an (M, 4) table for particle-wall pairs (None: wall_* above)
+    materials: tuple | None = None
+    wall_materials: tuple | None = None
 
     def replace(self, **kw) -> "SimParams":
         return dataclasses.replace(self, **kw)
@@ -74,6 +79,7 @@ class Scene:
     mass: np.ndarray  # (n,) float32
     id: np.ndarray  # (n,) uint32
     meta: dict = field(default_factory=dict)
+    material: np.ndarray | None = None  # (n,) uint32 material ids (params.materials)
 
     @property
     def n(self) -> int:
@@ -236,3 +242,36 @@ def stack(n: int, params: SimParams, gap: float = 0.0) -> Scene:
     pos = np.stack([np.full(n, 0.5 * L), ys, np.full(n, 0.5 * L)], axis=1)
     p = params.replace(box_lo=(0.0, 0.0, 0.0), box_hi=(L, H, L))
     return make_scene(f"stack{n}", p, pos)
+
+
+# ---------------------------------------------------------------- materials --
+
+def material_table(M: int, seed: int = 0, walls: bool = True):
+    """A symmetric (M, M, 4) table of (C_n, C_t, alpha, mu) around the R19
+    defaults (C x [0.5, 2], alpha in [0.1, 0.5], mu in [0.2, 0.8]) and an
+    (M, 4) particle-wall table, as nested tuples (SimParams fields)."""
+    rng = np.random.default_rng(seed)
+    t = np.empty((M, M, 4))
+    for i in range(M):
+        for j in range(i, M):
+            c = (7.326e6 * rng.uniform(0.5, 2.0), 7.326e6 * rng.uniform(0.5, 2.0),
+                 rng.uniform(0.1, 0.5), rng.uniform(0.2, 0.8))
+            t[i, j] = t[j, i] = c
+    w = np.stack([(7.326e6 * rng.uniform(0.5, 2.0), 7.326e6 * rng.uniform(0.5, 2.0),
+                   rng.uniform(0.1, 0.5), rng.uniform(0.2, 0.8)) for _ in range(M)])
+    def tup(a):
+        return tuple(tup(b) for b in a) if a.ndim > 1 else tuple(float(x) for x in a)
+
+    return tup(t), (tup(w) if walls else None)
+
+
+def mixed_gas(n: int, box_d: float, seed: int, M: int = 3, **kw) -> Scene:
+    """random_gas with M materials: random per-particle material ids and a
+    random symmetric pair table (material_table)."""
+    mats, walls = material_table(M, seed)
+    params = kw.pop("params", None) or SimParams()
+    sc = random_gas(n, box_d, seed, params=params.replace(materials=mats, wall_materials=walls),
+                    **kw)
+    sc.material = np.random.default_rng(seed + 1000).integers(0, M, n).astype(np.uint32)
+    sc.name = f"mixed{n}x{M}"
+    return sc

@@ -284,3 +284,95 @@ def test_sampled_step_equals_full_step(orc):
     for a, b in ((full.F, part.F), (full.T, part.T), (st.pos, st2.pos), (st.vel, st2.vel),
                  (st.omega, st2.omega), (h.cnt, h2.cnt), (h.dt, h2.dt)):
         assert np.array_equal(a[mask], b[mask])
+
+
+# ------------------------------------ material pairs (Eqs. 5, 8-10 of (i, j)) --
+
+def mat_table():
+    """Three materials; every pair has its own C_n (and so its own contact
+    duration) and its own α (and so its own restitution)."""
+    Cn = {(0, 0): 4e6, (0, 1): 6e6, (0, 2): 8e6, (1, 1): 1.0e7, (1, 2): 1.2e7, (2, 2): 1.4e7}
+    al = {(0, 0): 0.05, (0, 1): 0.1, (0, 2): 0.2, (1, 1): 0.3, (1, 2): 0.5, (2, 2): 0.75}
+    t = [[None] * 3 for _ in range(3)]
+    for (i, j), c in Cn.items():
+        t[i][j] = t[j][i] = (c, c, al[(i, j)], 0.5)
+    return tuple(tuple(r) for r in t), Cn, al
+
+
+@pytest.mark.parametrize("a,b", [(0, 1), (1, 2), (2, 2), (2, 0)])
+def test_material_pair_restitution_and_duration(orc, a, b):
+    """A head-on pair of materials (a, b) rebounds with e(α(a, b)) of the ODE
+    and stays in contact τ_c (m*/K)^{2/5} v0^{-1/5} with K = C_n(a, b) sqrt(R*):
+    the pair's own table entry is used, whichever side is i."""
+    table, Cn, al = mat_table()
+    key = (min(a, b), max(a, b))
+    v0 = 0.1
+    m = float(S.sphere_mass([S.R])[0])
+    mstar = m / 2
+    K = float(np.float32(Cn[key])) * math.sqrt(float(np.float32(S.R)) / 2)
+    tc_scale = (mstar / K) ** 0.4 * v0**-0.2
+    dt = float(np.float32(3.218 * tc_scale / 1000))
+    sc = S.two_body(v0, S.SimParams(dt=dt, materials=table), gap=0.0)
+    sc.material = np.array([a, b], np.uint32)
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(2, 8)
+    steps = 0
+    for _ in range(4000):
+        orc.step(p, st, h)
+        if 2 * st.radius[0] - np.linalg.norm(st.pos[1] - st.pos[0]) > 0:
+            steps += 1
+        elif steps:
+            break
+    lo = int(np.argmin(st.pos[:, 0]))
+    e = (st.vel[1 - lo, 0] - st.vel[lo, 0]) / v0
+    e_ode, tau = ode_restitution(float(np.float32(al[key])))
+    assert e == pytest.approx(e_ode, rel=2e-3)
+    assert steps * p.dt == pytest.approx(tau * tc_scale, abs=2 * p.dt)
+    assert sorted(st.mat.tolist()) == sorted([a, b])  # materials travel with the particles
+
+
+def test_material_wall_restitution(orc):
+    """A sphere of material b dropped on the floor rebounds with the wall
+    table's α(b) (R* = r, m* = m: the wall limits of R11)."""
+    table, _, _ = mat_table()
+    walls = ((4e6, 4e6, 0.05, 0.5), (1e7, 1e7, 0.5, 0.5), (1.4e7, 1.4e7, 0.75, 0.5))
+    for b in range(3):
+        v0 = 0.1
+        m = float(S.sphere_mass([S.R])[0])
+        K = float(np.float32(walls[b][0])) * math.sqrt(float(np.float32(S.R)))
+        tc_scale = (m / K) ** 0.4 * v0**-0.2
+        dt = float(np.float32(3.218 * tc_scale / 1000))
+        L = 8 * S.D
+        sp = S.SimParams(dt=dt, gravity=(0.0, 0.0, 0.0), materials=table, wall_materials=walls,
+                         box_hi=(L, L, L))
+        sc = S.make_scene("drop", sp, [[0.5 * L, float(S.R), 0.5 * L]], vel=[[0.0, -v0, 0.0]])
+        sc.material = np.array([b], np.uint32)
+        p = orc.make_params(sc.params, sc.radius)
+        st, h = orc.State.from_scene(sc), orc.History.empty(1, 8)
+        for _ in range(4000):
+            orc.step(p, st, h)
+            if st.vel[0, 1] > 0 and st.pos[0, 1] > st.radius[0]:
+                break
+        e_ode, _ = ode_restitution(float(np.float32(walls[b][2])))
+        assert st.vel[0, 1] / v0 == pytest.approx(e_ode, rel=2e-3)
+
+
+def test_uniform_material_table_equals_scalars(orc):
+    """A table whose every entry is the scalar parameters gives the scalar
+    run bitwise (the table only selects coefficients)."""
+    sc = S.random_gas(400, 8.0, 3, r_range=(0.3e-3, 0.5e-3), v_sigma=0.3)
+    sp = sc.params
+    c = (sp.stiffness_n, sp.stiffness_t, sp.damping, sp.friction)
+    w = (sp.stiffness_n, sp.stiffness_t, sp.damping, sp.friction)
+    spm = sp.replace(materials=tuple(tuple(c for _ in range(2)) for _ in range(2)),
+                     wall_materials=(w, w))
+    out = []
+    for params, mat in ((sp, None), (spm, np.arange(sc.n, dtype=np.uint32) % 2)):
+        p = orc.make_params(params, sc.radius)
+        st = orc.State.from_arrays(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id, mat)
+        h = orc.History.empty(sc.n, 16)
+        for _ in range(5):
+            assert orc.step(p, st, h).rc == 0
+        out.append((st.pos.copy(), st.vel.copy(), st.omega.copy()))
+    for a, b in zip(*out):
+        assert np.array_equal(a, b)
