@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define DEM_ABI_VERSION 1u
+#define DEM_ABI_VERSION 2u
 
 /* Error codes. */
 enum dem_error {
@@ -133,6 +133,17 @@ typedef struct {
   const dem_allocator* allocator; /* NULL -> cudaMallocAsync on the stream */
   int32_t rank, world_size;  /* world_size <= 1: single GPU; > 1: z-slab rank */
   const void* nccl_id;       /* unused (slab exchange is over CUDA IPC peer memory) */
+  /* Eqs. 5, 8-10 write C_k, α (and μ) as functions of the pair (i, j)
+   * (PAPER.md:85-93). n_materials <= 1: the scalars above for every pair.
+   * 2 <= n_materials <= 16: material_pairs (host, [M][M][4] = C_n, C_t, α, μ,
+   * symmetric, finite, >= 0) gives each particle pair its coefficients from
+   * the two particles' materials (dem_particles.material); material_walls
+   * (host, [M][4], or NULL for the wall scalars above) those of a
+   * particle-wall pair. Ids must then be < 2^27 (the material travels in the
+   * id word's bits 27-30). Copied at dem_create. */
+  uint32_t n_materials;
+  const float* material_pairs;
+  const float* material_walls;
 } dem_params;
 
 /* Particle arrays, all host or all device (mem_kind). Layout: pos/vel/omega
@@ -151,6 +162,7 @@ typedef struct {
   uint32_t* id;
   float* force;
   float* torque;
+  uint32_t* material;        /* [n] material ids < n_materials; NULL -> 0 (in) / not written (out) */
 } dem_particles;
 
 typedef struct {

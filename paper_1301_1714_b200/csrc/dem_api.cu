@@ -90,6 +90,7 @@ struct dem_handle {
   int cur = 0;
   int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
   int fcfg = -1;      // k_force configuration (0 dense, 1 light); -1: chosen at the first step
+  float4* mat_tables = nullptr;  // material pair + wall coefficients (cudaMalloc, dem_create)
 
   // graphs: g2[b] = two steps starting at parity b; g1[b] = one step
   cudaGraphExec_t g2[2] = {nullptr, nullptr};
@@ -416,6 +417,22 @@ int validate_params(const dem_params* p) {
     if (!(v >= 0.0f) || !std::isfinite(v)) return DEM_EINVAL;
   if (p->cell_edge < 0.0f || !std::isfinite(p->cell_edge)) return DEM_EINVAL;
   if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
+  if (p->n_materials > 1) {  // symmetric, finite, non-negative (SPEC MaterialTable)
+    const uint32_t M = p->n_materials;
+    if (M > 16 || !p->material_pairs) return DEM_EINVAL;
+    for (uint32_t i = 0; i < M; ++i)
+      for (uint32_t j = 0; j < M; ++j)
+        for (int c = 0; c < 4; ++c) {
+          const float v = p->material_pairs[((size_t)i * M + j) * 4 + c];
+          if (!(v >= 0.0f) || !std::isfinite(v) ||
+              v != p->material_pairs[((size_t)j * M + i) * 4 + c])
+            return DEM_EINVAL;
+        }
+    if (p->material_walls)
+      for (uint32_t k = 0; k < 4 * M; ++k)
+        if (!(p->material_walls[k] >= 0.0f) || !std::isfinite(p->material_walls[k]))
+          return DEM_EINVAL;
+  }
   return DEM_OK;
 }
 
@@ -499,6 +516,40 @@ int dem_create(const dem_params* p, dem_handle** out) {
   ph.kda = p->k_da;
   ph.ksh = p->k_sh;
   ph.flags = p->flags & (DEM_F_TRUNCATE_DT | DEM_F_CLAMP_FN);
+  // material pairs (Eqs. 5, 8-10 as functions of (i, j)): device tables
+  ph.nmat = 1;
+  ph.idmask = 0xFFFFFFFFu;
+  if (p->n_materials > 1) {
+    const uint32_t M = p->n_materials;
+    std::vector<float4> t((size_t)M * M), w(M);
+    for (uint32_t i = 0; i < M; ++i) {
+      for (uint32_t j = 0; j < M; ++j) {
+        const float* c = p->material_pairs + ((size_t)i * M + j) * 4;
+        t[(size_t)i * M + j] = make_float4(c[0], c[1], c[2], c[3]);
+      }
+      if (p->material_walls) {
+        const float* c = p->material_walls + (size_t)i * 4;
+        w[i] = make_float4(c[0], c[1], c[2], c[3]);
+      } else {
+        w[i] = make_float4(ph.wCn, ph.wCt, ph.walpha, ph.wmu);
+      }
+    }
+    if (cudaMalloc((void**)&h->mat_tables, sizeof(float4) * (t.size() + w.size())) != cudaSuccess ||
+        cudaMemcpy(h->mat_tables, t.data(), sizeof(float4) * t.size(), cudaMemcpyHostToDevice) !=
+            cudaSuccess ||
+        cudaMemcpy(h->mat_tables + t.size(), w.data(), sizeof(float4) * w.size(),
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (h->mat_tables) cudaFree(h->mat_tables);
+      cudaFreeHost(h->err_host);
+      if (h->own_stream) cudaStreamDestroy(h->stream);
+      delete h;
+      return fail(nullptr, DEM_ENOMEM, "material table allocation failed");
+    }
+    ph.nmat = M;
+    ph.mat = h->mat_tables;
+    ph.wmat = h->mat_tables + t.size();
+    ph.idmask = (1u << kMatShift) - 1u;
+  }
   *out = h;
   return DEM_OK;
 }
@@ -509,6 +560,7 @@ int dem_destroy(dem_handle* h) {
   if (h->xleft_ipc && h->xleft) cudaIpcCloseMemHandle((void*)h->xleft);
   if (h->xright_ipc && h->xright) cudaIpcCloseMemHandle((void*)h->xright);
   if (h->xregion) cudaFree(h->xregion);
+  if (h->mat_tables) cudaFree(h->mat_tables);
   free_buffers(h);
   for (auto& pr : h->prof) {
     cudaEventDestroy(pr.b);
@@ -547,6 +599,8 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   in.radius = n ? (const float*)stage(src->radius, n1) : nullptr;
   in.mass = n ? (const float*)stage(src->mass, n1) : nullptr;
   in.id = n ? (const uint32_t*)stage(src->id, (size_t)n * 4) : nullptr;
+  in.material = n && h->ph.nmat > 1 ? (const uint32_t*)stage(src->material, (size_t)n * 4) : nullptr;
+  in.nmat = h->ph.nmat;
   in.def_radius = h->p.radius;
   in.def_mass_coef = (float)(h->p.density * (4.0 / 3.0) * M_PI);
   auto unstage = [&]() {
@@ -573,13 +627,15 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   CUDA_TRY(h, cudaMemcpyAsync(&hp, probe, sizeof(Probe), cudaMemcpyDeviceToHost, st));
   CUDA_TRY(h, cudaStreamSynchronize(st));
   dev_free(h, probe);
-  if (hp.bad_radius || hp.bad_mass || hp.nonfinite || hp.outside || hp.bad_id) {
+  if (hp.bad_radius || hp.bad_mass || hp.nonfinite || hp.outside || hp.bad_id ||
+      hp.bad_material) {
     unstage();
-    char buf[200];
+    char buf[240];
     snprintf(buf, sizeof buf,
              "dem_set_particles: %u bad radii, %u bad masses, %u non-finite, %u outside the "
-             "box, %u ids >= 0xFFFFFFF0",
-             hp.bad_radius, hp.bad_mass, hp.nonfinite, hp.outside, hp.bad_id);
+             "box, %u ids >= %s, %u materials >= n_materials",
+             hp.bad_radius, hp.bad_mass, hp.nonfinite, hp.outside, hp.bad_id,
+             h->ph.nmat > 1 ? "2^27 (materials in use)" : "0xFFFFFFF0", hp.bad_material);
     return fail(h, DEM_EINVAL, buf);
   }
   // 3. the CDG (R15): h = cell_edge or 2 r_max (1 + 2^-10); n_a = floor(L_a / h) >= 3
@@ -826,7 +882,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     }
     CUDA_TRY(h, cudaMemsetAsync(seen, 0, sizeof(uint32_t) * n, st));
     CUDA_TRY(h, cudaMemsetAsync(dup, 0, sizeof(uint32_t), st));
-    launch_idcheck(st, n, h->omg[0], seen, dup);
+    launch_idcheck(st, n, h->ph.idmask, h->omg[0], seen, dup);
     uint32_t hdup = 0;
     CUDA_TRY(h, cudaMemcpyAsync(&hdup, dup, 4, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
@@ -980,12 +1036,12 @@ int dem_get_state(dem_handle* h, int32_t order, int64_t cap, const dem_particles
   cudaStream_t st = h->stream;
   const int64_t n = h->n;
   const bool dev = dst->mem_kind == DEM_MEM_DEVICE;
-  float *o[8] = {dst->pos, dst->vel, dst->omega, dst->radius, dst->mass, (float*)dst->id,
-                 dst->force, dst->torque};
-  const size_t sz[8] = {3, 3, 3, 1, 1, 1, 3, 3};
-  float* d[8] = {};
+  float *o[9] = {dst->pos, dst->vel, dst->omega, dst->radius, dst->mass, (float*)dst->id,
+                 dst->force, dst->torque, (float*)dst->material};
+  const size_t sz[9] = {3, 3, 3, 1, 1, 1, 3, 3, 1};
+  float* d[9] = {};
   std::vector<void*> tmp;
-  for (int k = 0; k < 8; ++k) {
+  for (int k = 0; k < 9; ++k) {
     if (!o[k]) continue;
     if (dev) {
       d[k] = o[k];
@@ -999,10 +1055,11 @@ int dem_get_state(dem_handle* h, int32_t order, int64_t cap, const dem_particles
     }
   }
   launch_unpack(st, n, order == DEM_ORDER_ID, h->pos[h->cur], h->vel[h->cur], h->omg[h->cur],
-                h->F, h->T, d[0], d[1], d[2], d[3], d[4], (uint32_t*)d[5], d[6], d[7]);
+                h->F, h->T, d[0], d[1], d[2], d[3], d[4], (uint32_t*)d[5], d[6], d[7],
+                h->ph.idmask, (uint32_t*)d[8]);
   h->launches++;
   if (!dev)
-    for (int k = 0; k < 8; ++k)
+    for (int k = 0; k < 9; ++k)
       if (o[k])
         CUDA_TRY(h, cudaMemcpyAsync(o[k], d[k], sizeof(float) * sz[k] * n,
                                     cudaMemcpyDeviceToHost, st));
@@ -1053,7 +1110,7 @@ int dem_get_contacts(dem_handle* h, int32_t mem_kind, int64_t cap, uint32_t* id_
       dd = dt3 ? (float*)dev_alloc(h, 12ull * m) : nullptr;
     }
     launch_emit_contacts(st, n, h->cap, h->K, h->hist[h->cur], h->cnt[h->cur], base,
-                         h->omg[h->cur], di, dj, dd);
+                         h->omg[h->cur], di, dj, dd, h->ph.idmask);
     h->launches++;
     if (!dev) {
       if (id_i) CUDA_TRY(h, cudaMemcpyAsync(id_i, di, 4ull * m, cudaMemcpyDeviceToHost, st));
@@ -1120,7 +1177,7 @@ int dem_set_contacts(dem_handle* h, int32_t mem_kind, int64_t m, const uint32_t*
   }
   CUDA_TRY(h, cudaMemsetAsync(flags, 0, 4, st));
   CUDA_TRY(h, cudaMemsetAsync(slot, 0xFF, sizeof(uint32_t) * nb, st));
-  launch_slot_of_id(st, n, h->omg[h->cur], slot);
+  launch_slot_of_id(st, n, h->ph.idmask, h->omg[h->cur], slot);
   launch_insert_contacts(st, m, nb, h->cap, h->K, di, dj, dd, slot, h->hist[h->cur], h->cnt[h->cur],
                          flags, h->slab ? 1 : 0);
   h->launches += 2;

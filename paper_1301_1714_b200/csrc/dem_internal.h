@@ -42,7 +42,15 @@ struct DevPhys {
   float wCn, wCt, walpha, wmu;
   float ksp, kda, ksh;
   uint32_t flags;
+  // material pairs (dem_params.n_materials > 1): coefficients (C_n, C_t, α, μ)
+  // of a particle pair mat[m_i * nmat + m_j], of a particle-wall pair wmat[m_i];
+  // the material is bits 27-30 of the id word (omg.w), idmask strips it
+  const float4* mat;
+  const float4* wmat;
+  uint32_t nmat;
+  uint32_t idmask;  // 0x07FFFFFF with materials, else 0xFFFFFFFF
 };
+constexpr uint32_t kMatShift = 27;
 
 // Device error record. code is the positive value of the dem_error.
 struct DevErr {
@@ -164,11 +172,13 @@ struct PackIn {
   const float* radius;
   const float* mass;
   const uint32_t* id;
+  const uint32_t* material;  // NULL -> 0
   float def_radius, def_mass_coef;  // mass = coef * r^3 when mass == NULL
+  uint32_t nmat;                    // > 1: material stored in the id word's bits 27-30
 };
 struct Probe {  // validation results of k_probe
   uint32_t bad_radius, bad_mass, nonfinite, outside, bad_id;
-  uint32_t rmax_bits, id_max, pad;
+  uint32_t rmax_bits, id_max, bad_material;
 };
 int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out);
 int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
@@ -178,7 +188,7 @@ int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, f
 int launch_flags(cudaStream_t st, int64_t n, const float4* pos, DevGrid g, uint32_t* flags);
 int launch_count(cudaStream_t st, int64_t n, const uint32_t* key, uint32_t* count,
                  uint32_t* prank);
-int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen,
+int launch_idcheck(cudaStream_t st, int64_t n, uint32_t idmask, const float4* omg, uint32_t* seen,
                    uint32_t* dup_flag);
 
 // One step = scan, scatter, rank, sweep.
@@ -217,11 +227,13 @@ int launch_plane_hist(cudaStream_t st, int64_t n, const float* pos, DevGrid g, u
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
                   const float4* omg, const float4* F, const float4* T, float* o_pos,
                   float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
-                  float* o_F, float* o_T);
+                  float* o_F, float* o_T, uint32_t idmask, uint32_t* o_mat);
 int launch_emit_contacts(cudaStream_t st, int64_t n, int64_t stride, uint32_t K,
                          const float4* hist, const uint32_t* cnt, const uint32_t* base,
-                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3);
-int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* slot_of_id);
+                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3,
+                         uint32_t idmask);
+int launch_slot_of_id(cudaStream_t st, int64_t n, uint32_t idmask, const float4* omg,
+                      uint32_t* slot_of_id);
 int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride, uint32_t K,
                            const uint32_t* id_i, const uint32_t* id_j, const float* dt3,
                            const uint32_t* slot_of_id, float4* hist, uint32_t* cnt,

@@ -144,7 +144,8 @@ __global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
   if (!fin) atomicAdd(&out->nonfinite, 1u);
   if (r > 0.0f && isfinite(r)) atomicMax(&out->rmax_bits, __float_as_uint(r));
   uint32_t id = in.id ? in.id[i] : (uint32_t)i;
-  if (id >= kWallPid0) atomicAdd(&out->bad_id, 1u);
+  if (id >= kWallPid0 || (in.nmat > 1 && id >= (1u << kMatShift))) atomicAdd(&out->bad_id, 1u);
+  if (in.nmat > 1 && in.material && in.material[i] >= in.nmat) atomicAdd(&out->bad_material, 1u);
   atomicMax(&out->id_max, id);
 }
 
@@ -166,6 +167,7 @@ __global__ void k_pack(int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel
   vel[i] = in.vel ? make_float4(in.vel[3 * q], in.vel[3 * q + 1], in.vel[3 * q + 2], m)
                   : make_float4(0.f, 0.f, 0.f, m);
   uint32_t id = in.id ? in.id[q] : (uint32_t)q;
+  if (in.nmat > 1 && in.material) id |= in.material[q] << kMatShift;  // the id word
   omg[i] = in.omega
                ? make_float4(in.omega[3 * q], in.omega[3 * q + 1], in.omega[3 * q + 2],
                              __uint_as_float(id))
@@ -182,10 +184,11 @@ __global__ void k_count(int64_t n, const uint32_t* key, uint32_t* count, uint32_
 }
 
 // Duplicate-id check for dense ids (max id < n): seen[] is zeroed by the host.
-__global__ void k_idcheck(int64_t n, const float4* omg, uint32_t* seen, uint32_t* dup) {
+__global__ void k_idcheck(int64_t n, uint32_t idmask, const float4* omg, uint32_t* seen,
+                          uint32_t* dup) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  uint32_t id = __float_as_uint(omg[i].w);
+  uint32_t id = __float_as_uint(omg[i].w) & idmask;
   if (id < (uint64_t)n && atomicExch(&seen[id], 1u) != 0u) atomicAdd(dup, 1u);
 }
 
@@ -500,6 +503,7 @@ struct Own {  // the particle of a sorted slot, as one contact evaluation needs 
 
 // Steps 7 for one particle pair (i owner, j partner): practical model with
 // history. `dold` is δ_t,old of the pair (0 if new). Returns F on i, Tc.
+template <bool MAT = true>
 __device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, float4 VQ, float4 WQ,
                                                     f3 n, float delta, f3 dold, const DevPhys& ph,
                                                     f3& Fc, f3& Tc, f3& dnew) {
@@ -510,22 +514,27 @@ __device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, floa
   const f3 rw = mk(__fadd_rn(__fmul_rn(o.P.w, o.W.x), __fmul_rn(Q.w, WQ.x)),
                    __fadd_rn(__fmul_rn(o.P.w, o.W.y), __fmul_rn(Q.w, WQ.y)),
                    __fadd_rn(__fmul_rn(o.P.w, o.W.z), __fmul_rn(Q.w, WQ.z)));
-  pair_practical(n, delta, Rs, ms, v, rw, dold, ph.Cn, ph.Ct, ph.alpha, ph.mu, ph.dt, ph.flags,
-                 Fc, Tc, dnew);
+  float Cn = ph.Cn, Ct = ph.Ct, alpha = ph.alpha, mu = ph.mu;
+  if (MAT && ph.nmat > 1) {  // C_k(i, j), α(i, j), μ(i, j) of the two materials (Eqs. 5, 8-10)
+    const uint32_t mi = __float_as_uint(o.W.w) >> kMatShift, mj = __float_as_uint(WQ.w) >> kMatShift;
+    const float4 c = __ldg(&ph.mat[mi * ph.nmat + mj]);
+    Cn = c.x, Ct = c.y, alpha = c.z, mu = c.w;
+  }
+  pair_practical(n, delta, Rs, ms, v, rw, dold, Cn, Ct, alpha, mu, ph.dt, ph.flags, Fc, Tc, dnew);
 }
 
 // Step 8 + step 1 + next step 2 for one particle (shared by both sweeps):
 // walls, integration, state write at slot j, next CM and its counting rank.
 // The outputs go to slot oj = j - (first owned sorted slot): the owned
 // particles of the next step are dense from 0.
-template <int MODEL, bool DIAG, class LookupFn>
+template <int MODEL, bool DIAG, bool MAT = true, class LookupFn>
 __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevGrid& g,
                                                 const DevPhys& ph, uint32_t N, uint32_t K,
                                                 uint32_t oj, const Own& o, f3 F, f3 T,
                                                 uint32_t ncnt, bool overflow, LookupFn lookup) {
   const uint32_t j = oj;  // output slot
   const float ri = o.P.w, mi = o.V.w;
-  const uint32_t my_id = __float_as_uint(o.W.w);
+  const uint32_t my_id = __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
   const float xs[3] = {o.P.x, o.P.y, o.P.z};
   // conservative fp32 prefilter: only particles within r (+ rounding margin)
@@ -552,8 +561,10 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       const uint32_t pid = kWallPid0 + (uint32_t)w;
       const f3 rwi = mk(__fmul_rn(ri, o.W.x), __fmul_rn(ri, o.W.y), __fmul_rn(ri, o.W.z));
       f3 Fc, Tc, dnew;
-      pair_practical(n, delta, ri, mi, mk(o.V.x, o.V.y, o.V.z), rwi, lookup(pid), ph.wCn, ph.wCt,
-                     ph.walpha, ph.wmu, ph.dt, ph.flags, Fc, Tc, dnew);
+      float4 c = make_float4(ph.wCn, ph.wCt, ph.walpha, ph.wmu);
+      if (MAT && ph.nmat > 1) c = __ldg(&ph.wmat[__float_as_uint(o.W.w) >> kMatShift]);
+      pair_practical(n, delta, ri, mi, mk(o.V.x, o.V.y, o.V.z), rwi, lookup(pid), c.x, c.y, c.z,
+                     c.w, ph.dt, ph.flags, Fc, Tc, dnew);
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
       T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
       if (ncnt < K) {
@@ -669,14 +680,14 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
         f3 n;
         float delta;
         if (!contact_geometry(o.P, Q, n, delta)) {
-          raise_error(b.err, 9u, j, __float_as_uint(o.W.w));
+          raise_error(b.err, 9u, j, __float_as_uint(o.W.w) & ph.idmask);
           continue;
         }
         const uint32_t q = __ldg(&b.perm[t]);
         const float4 VQ = __ldg(&b.vel_in[q]);
         if (MODEL == 0) {
           const float4 WQ = __ldg(&b.omg_in[q]);
-          const uint32_t pid = __float_as_uint(WQ.w);
+          const uint32_t pid = __float_as_uint(WQ.w) & ph.idmask;
           f3 Fc, Tc, dnew;
           eval_pair_practical(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
           F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
@@ -901,7 +912,7 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N_PENDING) : "memory");
 }
 
-template <int MODEL, bool DIAG, int CFG>
+template <int MODEL, bool DIAG, int CFG, bool MAT>
 __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
   using C = ForceCfg<CFG>;
@@ -1045,9 +1056,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       f3 n;
       float delta;
       if (!contact_geometry(po.P, Q, n, delta)) {
-        raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w));
+        raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu));
       } else if (MODEL == 0) {
-        const uint32_t pid = __float_as_uint(WQ.w);
+        const uint32_t pid = __float_as_uint(WQ.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
         const uint32_t no = s_nold[ow];
         f3 dold;
         if (k < no && __float_as_uint(Hr.w) == pid)
@@ -1055,7 +1066,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
         else
           dold = old_history(b.hist_in, N, s_slot[ow], no, 0xFFFFFFFFu, pid);
         f3 dnew;
-        eval_pair_practical(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+        eval_pair_practical<MAT>(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
         __stcs(&b.hist_out[(size_t)k * N + (j0 - jlo) + ow],
                make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
       } else {
@@ -1090,7 +1101,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
+  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
 // ---- half-list path (default): Newton's third law -------------------------
@@ -1232,9 +1243,9 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
     float delta;
     f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
     if (!contact_geometry(o.P, Q, n, delta)) {
-      raise_error(b.err, 9u, i - jlo, __float_as_uint(o.W.w));
+      raise_error(b.err, 9u, i - jlo, __float_as_uint(o.W.w) & ph.idmask);
     } else if (MODEL == 0) {
-      const uint32_t pid = __float_as_uint(WQ.w);
+      const uint32_t pid = __float_as_uint(WQ.w) & ph.idmask;
       const f3 dold = (k < n_old && __float_as_uint(Hk.w) == pid)
                           ? mk(Hk.x, Hk.y, Hk.z)
                           : old_history(b.hist_in, N, si, n_old, 0xFFFFFFFFu, pid);
@@ -1245,7 +1256,8 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
       if (cp < 0xFEu && nup_t + cp < K)
         __stcs(&b.hist_out[(size_t)(nup_t + cp) * N + (t - jlo)],
-               make_float4(-dnew.x, -dnew.y, -dnew.z, o.W.w));
+               make_float4(-dnew.x, -dnew.y, -dnew.z,
+                           __uint_as_float(__float_as_uint(o.W.w) & ph.idmask)));
     } else {
       const f3 u = mk(VQ.x - o.V.x, VQ.y - o.V.y, VQ.z - o.V.z);
       Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
@@ -1349,14 +1361,16 @@ void sweep_prepare(uint32_t K) {
   const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
   const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
   const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
-  cudaFuncSetAttribute(k_force<0, false, kForceDense>, A, sd);
-  cudaFuncSetAttribute(k_force<0, true, kForceDense>, A, sd);
-  cudaFuncSetAttribute(k_force<1, false, kForceDense>, A, sd);
-  cudaFuncSetAttribute(k_force<1, true, kForceDense>, A, sd);
-  cudaFuncSetAttribute(k_force<0, false, kForceLight>, A, sl);
-  cudaFuncSetAttribute(k_force<0, true, kForceLight>, A, sl);
-  cudaFuncSetAttribute(k_force<1, false, kForceLight>, A, sl);
-  cudaFuncSetAttribute(k_force<1, true, kForceLight>, A, sl);
+#define DEM_SET_SMEM(MODEL, DIAG)                                     \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false>, A, sd); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, true>, A, sd);  \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false>, A, sl); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true>, A, sl);
+  DEM_SET_SMEM(0, false)
+  DEM_SET_SMEM(0, true)
+  DEM_SET_SMEM(1, false)
+  DEM_SET_SMEM(1, true)
+#undef DEM_SET_SMEM
 }
 
 // --------------------------------------------------------- slab exchange --
@@ -1644,11 +1658,12 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
 __global__ void k_unpack(int64_t n, bool by_id, const float4* pos, const float4* vel,
                          const float4* omg, const float4* F, const float4* T, float* o_pos,
                          float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
-                         float* o_F, float* o_T) {
+                         float* o_F, float* o_T, uint32_t idmask, uint32_t* o_mat) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const float4 P = pos[i], V = vel[i], W = omg[i];
-  const uint32_t id = __float_as_uint(W.w);
+  const uint32_t word = __float_as_uint(W.w);
+  const uint32_t id = word & idmask;
   const int64_t d = by_id ? (int64_t)id : i;
   if (o_pos) { o_pos[3 * d] = P.x; o_pos[3 * d + 1] = P.y; o_pos[3 * d + 2] = P.z; }
   if (o_vel) { o_vel[3 * d] = V.x; o_vel[3 * d + 1] = V.y; o_vel[3 * d + 2] = V.z; }
@@ -1656,17 +1671,18 @@ __global__ void k_unpack(int64_t n, bool by_id, const float4* pos, const float4*
   if (o_r) o_r[d] = P.w;
   if (o_m) o_m[d] = V.w;
   if (o_id) o_id[d] = id;
+  if (o_mat) o_mat[d] = idmask == 0xFFFFFFFFu ? 0u : (word >> kMatShift);
   if (o_F && F) { float4 f = F[i]; o_F[3 * d] = f.x; o_F[3 * d + 1] = f.y; o_F[3 * d + 2] = f.z; }
   if (o_T && T) { float4 t = T[i]; o_T[3 * d] = t.x; o_T[3 * d + 1] = t.y; o_T[3 * d + 2] = t.z; }
 }
 
 __global__ void k_emit_contacts(int64_t n, int64_t stride, uint32_t K, const float4* hist,
                                 const uint32_t* cnt, const uint32_t* base, const float4* omg,
-                                uint32_t* id_i, uint32_t* id_j, float* dt3) {
+                                uint32_t* id_i, uint32_t* id_j, float* dt3, uint32_t idmask) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const uint32_t c = cnt[i], o = base[i];
-  const uint32_t me = __float_as_uint(omg[i].w);
+  const uint32_t me = __float_as_uint(omg[i].w) & idmask;
   for (uint32_t k = 0; k < c && k < K; ++k) {
     const float4 h = hist[(size_t)k * stride + i];
     if (id_i) id_i[o + k] = me;
@@ -1675,10 +1691,10 @@ __global__ void k_emit_contacts(int64_t n, int64_t stride, uint32_t K, const flo
   }
 }
 
-__global__ void k_slot_of_id(int64_t n, const float4* omg, uint32_t* slot_of_id) {
+__global__ void k_slot_of_id(int64_t n, uint32_t idmask, const float4* omg, uint32_t* slot_of_id) {
   int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
-  slot_of_id[__float_as_uint(omg[i].w)] = (uint32_t)i;
+  slot_of_id[__float_as_uint(omg[i].w) & idmask] = (uint32_t)i;
 }
 
 // flags[0] |= 1: id out of range, |= 2: capacity overflow. slot_of_id has
@@ -1814,10 +1830,10 @@ int launch_count(cudaStream_t st, int64_t n, const uint32_t* key, uint32_t* coun
   return K_HASH;
 }
 
-int launch_idcheck(cudaStream_t st, int64_t n, const float4* omg, uint32_t* seen,
+int launch_idcheck(cudaStream_t st, int64_t n, uint32_t idmask, const float4* omg, uint32_t* seen,
                    uint32_t* dup_flag) {
   if (n <= 0) return K_OTHER;
-  k_idcheck<<<blocks_for(n, 256), 256, 0, st>>>(n, omg, seen, dup_flag);
+  k_idcheck<<<blocks_for(n, 256), 256, 0, st>>>(n, idmask, omg, seen, dup_flag);
   return K_OTHER;
 }
 
@@ -1878,12 +1894,15 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
-    if (cfg == kForceLight)
-      launch_pdl(k_force<MODEL, DIAG, kForceLight>, blocks_for(n, 32 * kSweepWarps),
-                 32 * kSweepWarps, smem, st, b, g, ph, N, K);
-    else
-      launch_pdl(k_force<MODEL, DIAG, kForceDense>, blocks_for(n, 32 * kSweepWarps),
-                 32 * kSweepWarps, smem, st, b, g, ph, N, K);
+    const unsigned grid = blocks_for(n, 32 * kSweepWarps), block = 32 * kSweepWarps;
+    const bool mat = ph.nmat > 1;  // material pairs: their own instantiation
+    if (cfg == kForceLight) {
+      if (mat) launch_pdl(k_force<MODEL, DIAG, kForceLight, true>, grid, block, smem, st, b, g, ph, N, K);
+      else launch_pdl(k_force<MODEL, DIAG, kForceLight, false>, grid, block, smem, st, b, g, ph, N, K);
+    } else {
+      if (mat) launch_pdl(k_force<MODEL, DIAG, kForceDense, true>, grid, block, smem, st, b, g, ph, N, K);
+      else launch_pdl(k_force<MODEL, DIAG, kForceDense, false>, grid, block, smem, st, b, g, ph, N, K);
+    }
   }
 }
 
@@ -1988,25 +2007,27 @@ int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const Dev
 int launch_unpack(cudaStream_t st, int64_t n, bool by_id, const float4* pos, const float4* vel,
                   const float4* omg, const float4* F, const float4* T, float* o_pos,
                   float* o_vel, float* o_omg, float* o_r, float* o_m, uint32_t* o_id,
-                  float* o_F, float* o_T) {
+                  float* o_F, float* o_T, uint32_t idmask, uint32_t* o_mat) {
   if (n <= 0) return K_OTHER;
   k_unpack<<<blocks_for(n, 256), 256, 0, st>>>(n, by_id, pos, vel, omg, F, T, o_pos, o_vel,
-                                               o_omg, o_r, o_m, o_id, o_F, o_T);
+                                               o_omg, o_r, o_m, o_id, o_F, o_T, idmask, o_mat);
   return K_OTHER;
 }
 
 int launch_emit_contacts(cudaStream_t st, int64_t n, int64_t stride, uint32_t K,
                          const float4* hist, const uint32_t* cnt, const uint32_t* base,
-                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3) {
+                         const float4* omg, uint32_t* id_i, uint32_t* id_j, float* dt3,
+                         uint32_t idmask) {
   if (n <= 0) return K_OTHER;
   k_emit_contacts<<<blocks_for(n, 256), 256, 0, st>>>(n, stride, K, hist, cnt, base, omg, id_i,
-                                                      id_j, dt3);
+                                                      id_j, dt3, idmask);
   return K_OTHER;
 }
 
-int launch_slot_of_id(cudaStream_t st, int64_t n, const float4* omg, uint32_t* slot_of_id) {
+int launch_slot_of_id(cudaStream_t st, int64_t n, uint32_t idmask, const float4* omg,
+                      uint32_t* slot_of_id) {
   if (n <= 0) return K_OTHER;
-  k_slot_of_id<<<blocks_for(n, 256), 256, 0, st>>>(n, omg, slot_of_id);
+  k_slot_of_id<<<blocks_for(n, 256), 256, 0, st>>>(n, idmask, omg, slot_of_id);
   return K_OTHER;
 }
 

@@ -20,7 +20,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
 
-DEM_ABI_VERSION = 1
+DEM_ABI_VERSION = 2
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
 DEM_EOVERFLOW, DEM_ENONFINITE, DEM_EESCAPED, DEM_ECOINCIDENT, DEM_ESTATE = -6, -7, -8, -9, -10
 DEM_EPEER = -11
@@ -54,13 +54,16 @@ class DemParams(C.Structure):
                 ("cell_edge", _f), ("max_contacts", C.c_uint32), ("flags", C.c_uint32),
                 ("device", C.c_int32), ("stream", C.c_void_p),
                 ("allocator", C.POINTER(DemAllocator)), ("rank", C.c_int32),
-                ("world_size", C.c_int32), ("nccl_id", C.c_void_p)]
+                ("world_size", C.c_int32), ("nccl_id", C.c_void_p),
+                ("n_materials", C.c_uint32), ("material_pairs", C.c_void_p),
+                ("material_walls", C.c_void_p)]
 
 
 class DemParticles(C.Structure):
     _fields_ = [("mem_kind", C.c_int32), ("pos", C.c_void_p), ("vel", C.c_void_p),
                 ("omega", C.c_void_p), ("radius", C.c_void_p), ("mass", C.c_void_p),
-                ("id", C.c_void_p), ("force", C.c_void_p), ("torque", C.c_void_p)]
+                ("id", C.c_void_p), ("force", C.c_void_p), ("torque", C.c_void_p),
+                ("material", C.c_void_p)]
 
 
 class DemStats(C.Structure):
@@ -154,6 +157,17 @@ def params_from(sp, *, flags: int = 0, device: int = -1, stream=None, allocator=
     p.stream = stream
     p.allocator = allocator
     p.rank, p.world_size = rank, world
+    mats = getattr(sp, "materials", None)
+    if mats is not None and len(mats) > 1:  # (M, M, 4) C_n, C_t, alpha, mu per pair
+        t = np.ascontiguousarray(np.asarray(mats, np.float32))
+        p.n_materials = t.shape[0]
+        p._mat = t  # kept alive with the struct
+        p.material_pairs = t.ctypes.data
+        wm = getattr(sp, "wall_materials", None)
+        if wm is not None:
+            w = np.ascontiguousarray(np.asarray(wm, np.float32))
+            p._wmat = w
+            p.material_walls = w.ctypes.data
     return p
 
 
@@ -230,6 +244,7 @@ class Dem:
                                   world=world)
         self.rank, self.world = rank, world
         self.flags = self.params.flags
+        self.nmat = max(1, int(self.params.n_materials))
         h = C.c_void_p()
         rc = L.dem_create(C.byref(self.params), C.byref(h))
         if rc != DEM_OK:
@@ -260,16 +275,19 @@ class Dem:
         self.close()
 
     # ---------------------------------------------------------- set ----
-    def set_particles(self, pos, vel=None, omega=None, radius=None, mass=None, id=None):
+    def set_particles(self, pos, vel=None, omega=None, radius=None, mass=None, id=None,
+                      material=None):
         """dem_set_particles: numpy arrays (host) or CUDA tensors (device). A slab
-        rank keeps its own particles of the given set."""
+        rank keeps its own particles of the given set. `material`: per-particle
+        material ids (with SimParams.materials)."""
         device = _is_torch(pos) and pos.is_cuda
         n = int(pos.shape[0]) if pos is not None else 0
         args = [_Arg(pos, np.float32, device=device), _Arg(vel, np.float32, device=device),
                 _Arg(omega, np.float32, device=device), _Arg(radius, np.float32, device=device),
                 _Arg(mass, np.float32, device=device), _Arg(id, np.uint32, device=device)]
+        mat = _Arg(material, np.uint32, device=device)
         P = DemParticles(DEM_MEM_DEVICE if device else DEM_MEM_HOST, *(a.ptr for a in args),
-                         None, None)
+                         None, None, mat.ptr)
         self._check(lib().dem_set_particles(self.h, n, C.byref(P)), "dem_set_particles")
         self.n = n if self.world == 1 else int(self.stats()["n"])
 
@@ -337,6 +355,8 @@ class Dem:
             if forces:
                 out["force"] = np.empty((n, 3), np.float32)
                 out["torque"] = np.empty((n, 3), np.float32)
+            if self.nmat > 1:
+                out["material"] = np.empty(n, np.uint32)
             device = False
         else:
             device = any(_is_torch(v) for v in out.values() if v is not None)
@@ -349,7 +369,7 @@ class Dem:
 
         P = DemParticles(DEM_MEM_DEVICE if device else DEM_MEM_HOST, ptr("pos"), ptr("vel"),
                          ptr("omega"), ptr("radius"), ptr("mass"), ptr("id"), ptr("force"),
-                         ptr("torque"))
+                         ptr("torque"), ptr("material"))
         nout = C.c_int64()
         self._check(lib().dem_get_state(self.h, order, n, C.byref(P), C.byref(nout)),
                     "dem_get_state")

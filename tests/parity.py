@@ -11,7 +11,8 @@ from oracle import oracle as orc
 def oracle_inputs(d, K: int):
     """(State, History) of a Dem's current state in its internal order."""
     s = d.get_state()
-    st = orc.State.from_arrays(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"], s["id"])
+    st = orc.State.from_arrays(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"], s["id"],
+                               s.get("material"))
     if d.params.model == 0:
         id_i, id_j, dt3 = d.get_contacts()
         h = orc.History.from_pairs(st.id, K, id_i, id_j, dt3.astype(np.float64))

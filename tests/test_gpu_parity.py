@@ -403,6 +403,76 @@ def test_set_particles_accepts_what_a_step_produces():
             assert "outside" in str(e.value)
 
 
+# ------------------------------------------- material pairs (Eqs. 5, 8-10) --
+
+def mixed(M=3, n=3000, seed=7):
+    return S.mixed_gas(n, 14.0, seed, M=M, r_range=(0.25e-3, 0.5e-3), v_sigma=0.05,
+                       params=S.SimParams(max_contacts=32))
+
+
+@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
+                                     DEM_F_THREAD_PER_PARTICLE])
+def test_materials_one_step_T2(variant):
+    """Each particle pair takes C_n, C_t, α, μ from its two materials and each
+    wall contact from the particle's material: T2 against the oracle."""
+    sc = mixed()
+    p = orc.make_params(sc.params, sc.radius)
+    d = Dem(sc.params, flags=DEM_F_DIAG | variant)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id, material=sc.material)
+    for k in range(3):
+        st, h = oracle_inputs(d, 32)
+        assert st.mat is not None and st.mat.max() > 0
+        d.step(1)
+        g = d.get_state(forces=True)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        assert np.array_equal(g["id"], st.id) and np.array_equal(g["material"], st.mat)
+        assert_T2_forces(g["force"], g["torque"], res, what=f"mixed step {k + 1}")
+        assert_T2_history(contacts_dict(d), h.as_dict(st.id))
+
+
+def test_materials_uniform_table_bitwise():
+    """A table whose every entry is the scalar parameters reproduces the
+    scalar run bitwise on the GPU."""
+    sc = scenes_small()[1]
+    sp = sc.params
+    c = (sp.stiffness_n, sp.stiffness_t, sp.damping, sp.friction)
+    spm = sp.replace(materials=((c, c), (c, c)), wall_materials=(c, c))
+    runs = []
+    for params, mat in ((sp, None), (spm, (np.arange(sc.n) % 2).astype(np.uint32))):
+        d = Dem(params, flags=DEM_F_DIAG)
+        d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id, material=mat)
+        d.step(10)
+        runs.append(d.get_state(forces=True))
+    for k in ("pos", "vel", "omega", "id", "force", "torque"):
+        assert np.array_equal(runs[0][k], runs[1][k]), k
+
+
+def test_materials_checkpoint_and_validation():
+    sc = mixed(n=1500, seed=3)
+    d = Dem(sc.params, flags=0)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id, material=sc.material)
+    d.step(8)
+    s = d.get_state()
+    ci, cj, cd = d.get_contacts()
+    assert set(np.unique(s["material"])) == {0, 1, 2}
+    assert s["id"].max() < sc.n  # the material bits are not part of the id
+    e = Dem(sc.params, flags=0)
+    e.set_particles(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"], s["id"],
+                    material=s["material"])
+    e.set_contacts(ci, cj, cd)
+    d.step(7)
+    e.step(7)
+    a, b = d.get_state(), e.get_state()
+    for k in a:
+        assert np.array_equal(a[k], b[k]), k
+    bad = sc.material.copy()
+    bad[0] = 3  # only 3 materials
+    with pytest.raises(DemError):
+        Dem(sc.params).set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id,
+                                     material=bad)
+
+
 def test_checkpoint_roundtrip_bitwise():
     sc = S.C1()
     d1 = make(sc, flags=0)
