@@ -87,6 +87,12 @@ typedef struct {
   int32_t nmat;
   const double* mat;
   const double* wmat;
+  /* plates (reading R23): nplates <= 10 finite two-sided rectangles, 12
+   * doubles each: centre xyz, unit normal xyz, unit in-plane axis u xyz,
+   * half-length along u, half-length along v = n x u, unused. History
+   * partner id 0xFFFFFFF6 + k. */
+  int32_t nplates;
+  const double* plates;
 } orc_params;
 
 /* ---------------------------------------------------------------- grid ---- */
@@ -528,29 +534,21 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
           if (t != j) visit(t);
     }
 
-    /* step 8: walls = particles of infinite radius (reading R11),
-     * order -x, +x, -y, +y, -z, +z; n points from the particle to the wall. */
-    for (int wdx = 0; wdx < 6; ++wdx) {
-      int a = wdx / 2;
-      bool hi_side = (wdx & 1) != 0;
-      double dist = hi_side ? (p->hi[a] - x[3 * j + a]) : (x[3 * j + a] - p->lo[a]);
-      if (!(r[j] > dist)) continue;
+    /* step 8: walls = particles of infinite radius (reading R11);
+     * n points from the particle to the wall. */
+    auto wall_contact = [&](const double* nrm, double delta, uint32_t pid) {
       out->n_wall_contacts++;
-      double nrm[3] = {0.0, 0.0, 0.0};
-      nrm[a] = hi_side ? 1.0 : -1.0;
-      double delta = r[j] - dist;
       double Fc[3], mag[2] = {0.0, 0.0};
       if (practical) {
         double rw[3], dold[3], dnew[3], Tc[3];
         for (int b = 0; b < 3; ++b) rw[b] = r[j] * w[3 * j + b]; /* r_w ω_w := 0 */
-        uint32_t pid = ORC_WALL_PID0 + (uint32_t)wdx;
         lookup(j, pid, dold);
-        /* R* = r_i, m* = m_i, v_j = ω_j = 0: the limits r_j, m_j -> ∞ */
         double Cn = p->wCn, Ct = p->wCt, alpha = p->walpha, mu = p->wmu;
         if (p->nmat > 1 && p->wmat) {
           const double* c = &p->wmat[(size_t)mt[j] * 4];
           Cn = c[0], Ct = c[1], alpha = c[2], mu = c[3];
         }
+        /* R* = r_i, m* = m_i, v_j = ω_j = 0: the limits r_j, m_j -> ∞ */
         orc_pair_practical(nrm, delta, r[j], m[j], &v[3 * j], rw, dold, Cn, Ct, alpha, mu, p->dt,
                            p->flags, Fc, Tc, dnew, mag);
         for (int b = 0; b < 3; ++b) Ti[b] += r[j] * Tc[b];
@@ -563,6 +561,47 @@ static int step_impl(const orc_params* p, int64_t n, orc_state* st, orc_hist* hi
       }
       for (int b = 0; b < 3; ++b) Fi[b] += Fc[b];
       Fabs[j] += mag[0];
+    };
+    /* the 6 faces of the box, order -x, +x, -y, +y, -z, +z */
+    for (int wdx = 0; wdx < 6; ++wdx) {
+      int a = wdx / 2;
+      bool hi_side = (wdx & 1) != 0;
+      double dist = hi_side ? (p->hi[a] - x[3 * j + a]) : (x[3 * j + a] - p->lo[a]);
+      if (!(r[j] > dist)) continue;
+      double nrm[3] = {0.0, 0.0, 0.0};
+      nrm[a] = hi_side ? 1.0 : -1.0;
+      wall_contact(nrm, r[j] - dist, ORC_WALL_PID0 + (uint32_t)wdx);
+    }
+    /* plates (reading R23): finite two-sided rectangles, in the order given.
+     * The contact point is the point of the rectangle closest to the centre;
+     * contact iff its distance is below r_i. */
+    for (int k = 0; k < p->nplates; ++k) {
+      const double* P = &p->plates[12 * k]; /* centre, normal, u axis, half_u, half_v */
+      double c[3] = {P[0], P[1], P[2]}, nn[3] = {P[3], P[4], P[5]}, uu[3] = {P[6], P[7], P[8]};
+      double vv[3] = {nn[1] * uu[2] - nn[2] * uu[1], nn[2] * uu[0] - nn[0] * uu[2],
+                      nn[0] * uu[1] - nn[1] * uu[0]}; /* v = n x u */
+      double cp[3];  /* closest point of the rectangle */
+      double du = 0.0, dv = 0.0;
+      for (int b = 0; b < 3; ++b) {
+        du += (x[3 * j + b] - c[b]) * uu[b];
+        dv += (x[3 * j + b] - c[b]) * vv[b];
+      }
+      double qu = std::min(std::max(du, -P[9]), P[9]);
+      double qv = std::min(std::max(dv, -P[10]), P[10]);
+      double e[3], dist2 = 0.0;
+      for (int b = 0; b < 3; ++b) {
+        cp[b] = c[b] + qu * uu[b] + qv * vv[b];
+        e[b] = cp[b] - x[3 * j + b];
+        dist2 += e[b] * e[b];
+      }
+      double dist = std::sqrt(dist2);
+      if (!(r[j] > dist)) continue;
+      if (dist == 0.0) { /* centre on the plate: no direction (R18) */
+        set_err(out, ORC_ECOINCIDENT, (int64_t)j, id[j]);
+        continue;
+      }
+      double nrm[3] = {e[0] / dist, e[1] / dist, e[2] / dist};
+      wall_contact(nrm, r[j] - dist, ORC_WALL_PID0 + 6u + (uint32_t)k);
     }
   }
 

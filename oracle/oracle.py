@@ -30,7 +30,7 @@ class OrcParams(C.Structure):
                 ("lo", _D * 3), ("hi", _D * 3), ("h", _D), ("Cn", _D), ("Ct", _D),
                 ("alpha", _D), ("mu", _D), ("wCn", _D), ("wCt", _D), ("walpha", _D),
                 ("wmu", _D), ("ksp", _D), ("kda", _D), ("ksh", _D), ("nmat", C.c_int32),
-                ("mat", _P), ("wmat", _P)]
+                ("mat", _P), ("wmat", _P), ("nplates", C.c_int32), ("plates", _P)]
 
 
 class OrcState(C.Structure):
@@ -142,6 +142,15 @@ def make_params(sp, radius: np.ndarray | None = None, brute: bool = False) -> Or
             assert w.shape == (M, 4)
             p._wmat = w
             p.wmat = _ptr(w)
+    # plates (reading R23): 12 fp32-rounded numbers each
+    plates = getattr(sp, "plates", None)
+    p.nplates = 0
+    if plates:
+        a = np.ascontiguousarray(np.asarray(plates, np.float32).astype(np.float64))
+        assert a.ndim == 2 and a.shape[1] == 12 and a.shape[0] <= 10
+        p.nplates = a.shape[0]
+        p._plates = a
+        p.plates = _ptr(a)
     return p
 
 

@@ -63,6 +63,9 @@ class SimParams:
     # optionally an (M, 4) table for particle-wall pairs (None: wall_* above)
     materials: tuple | None = None
     wall_materials: tuple | None = None
+    # extra walls (reading R23): up to 10 finite two-sided rectangles, each
+    # plate(centre, normal, u, half_u, half_v)
+    plates: tuple | None = None
 
     def replace(self, **kw) -> "SimParams":
         return dataclasses.replace(self, **kw)
@@ -275,3 +278,15 @@ def mixed_gas(n: int, box_d: float, seed: int, M: int = 3, **kw) -> Scene:
     sc.material = np.random.default_rng(seed + 1000).integers(0, M, n).astype(np.uint32)
     sc.name = f"mixed{n}x{M}"
     return sc
+
+
+# ------------------------------------------------------------------ plates --
+
+def plate(centre, normal, u, half_u: float, half_v: float) -> tuple:
+    """A finite two-sided rectangular wall (reading R23): centre, unit normal,
+    unit in-plane axis u, half-lengths along u and v = normal x u."""
+    n = np.asarray(normal, np.float64)
+    uu = np.asarray(u, np.float64)
+    assert abs(np.linalg.norm(n) - 1) < 1e-6 and abs(np.linalg.norm(uu) - 1) < 1e-6
+    assert abs(n @ uu) < 1e-6 and half_u > 0 and half_v > 0
+    return tuple(float(x) for x in (*centre, *normal, *u, half_u, half_v, 0.0))

@@ -376,3 +376,85 @@ def test_uniform_material_table_equals_scalars(orc):
         out.append((st.pos.copy(), st.vel.copy(), st.omega.copy()))
     for a, b in zip(*out):
         assert np.array_equal(a, b)
+
+
+# ------------------------------------------ plates (finite walls, R23) --
+
+def plate_drop(orc, start, vel, plates, steps=4000, stop=None):
+    """One sphere in a large gravity-free box with the given plates."""
+    L = 40 * S.D
+    sp = S.SimParams(gravity=(0.0, 0.0, 0.0), box_hi=(L, L, L), plates=plates)
+    sc = S.make_scene("plate", sp, [start], vel=[vel])
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(1, 8)
+    touched = 0
+    for _ in range(steps):
+        r = orc.step(p, st, h)
+        assert r.rc == 0
+        touched += r.n_wall_contacts
+        if stop and stop(st):
+            break
+    return st, touched, p
+
+
+def test_plate_face_restitution_both_sides(orc):
+    """A sphere hitting a horizontal plate's face, from above or from below,
+    rebounds with the wall e(α) of the ODE (R* = r, m* = m; two-sided)."""
+    L = 40 * S.D
+    c = (0.5 * L, 0.5 * L, 0.5 * L)
+    pl = (S.plate(c, (0, 1, 0), (1, 0, 0), 5 * S.D, 5 * S.D),)
+    e_ode, _ = ode_restitution(float(np.float32(0.2522)))
+    for side in (+1, -1):
+        y0 = c[1] + side * (float(S.R) + 1e-6)
+        st, touched, _ = plate_drop(orc, (c[0] + 1.3 * S.D, y0, c[2] - 2.1 * S.D),
+                                    (0.0, -side * 0.1, 0.0), pl,
+                                    stop=lambda s: side * s.vel[0, 1] > 0
+                                    and abs(s.pos[0, 1] - c[1]) > s.radius[0] + 1e-5)
+        assert touched > 0
+        assert side * st.vel[0, 1] / 0.1 == pytest.approx(e_ode, rel=3e-3)
+
+
+def test_plate_edge_head_on(orc):
+    """A sphere moving along -x at the plate's height onto its edge line
+    (x = c_x + half_u) meets it head-on: horizontal normal, e(α) rebound, no
+    vertical velocity picked up."""
+    L = 40 * S.D
+    c = (0.5 * L, 0.5 * L, 0.5 * L)
+    a = 3 * S.D
+    pl = (S.plate(c, (0, 1, 0), (1, 0, 0), a, 5 * S.D),)
+    e_ode, _ = ode_restitution(float(np.float32(0.2522)))
+    st, touched, _ = plate_drop(orc, (c[0] + a + float(S.R) + 1e-6, c[1], c[2]), (-0.1, 0.0, 0.0),
+                                pl, stop=lambda s: s.vel[0, 0] > 0
+                                and s.pos[0, 0] - c[0] - a > s.radius[0] + 1e-5)
+    assert touched > 0
+    assert st.vel[0, 0] / 0.1 == pytest.approx(e_ode, rel=3e-3)
+    assert abs(st.vel[0, 1]) < 1e-12 and abs(st.vel[0, 2]) < 1e-12
+
+
+def test_plate_corner_force_direction_and_miss(orc):
+    """At rest overlapping a plate corner, the force points from the corner
+    to the centre with the Hertz magnitude C_n sqrt(r δ) δ; a sphere passing
+    beside the plate (beyond half_v + r) never touches it."""
+    L = 40 * S.D
+    c = np.array([0.5 * L] * 3)
+    a, b = 3 * S.D, 2 * S.D
+    pl = (S.plate(tuple(c), (0, 1, 0), (1, 0, 0), a, b),)
+    corner = c + np.array([a, 0.0, b])
+    dirn = np.array([1.0, 0.7, 0.4]) / np.linalg.norm([1.0, 0.7, 0.4])
+    x0 = corner + dirn * (float(S.R) - 2e-6)
+    sp = S.SimParams(gravity=(0.0, 0.0, 0.0), box_hi=(L, L, L), plates=pl)
+    sc = S.make_scene("corner", sp, [tuple(x0)])
+    p = orc.make_params(sc.params, sc.radius)
+    st = orc.State.from_scene(sc)
+    xs = st.pos[0].copy()
+    res = orc.step(p, st, orc.History.empty(1, 8))
+    corner32 = (c.astype(np.float32).astype(np.float64)
+                + np.array([np.float32(a), 0.0, np.float32(b)], np.float64))
+    d = xs - corner32
+    dist = np.linalg.norm(d)
+    delta = st.radius[0] - dist
+    want = p.wCn * math.sqrt(st.radius[0] * delta) * delta * d / dist
+    assert res.F[0] == pytest.approx(want, rel=1e-9)
+    st, touched, _ = plate_drop(orc, (c[0], c[1] + 2 * S.D, c[2] + b + float(S.R) + 1e-5),
+                                (0.0, -1.0, 0.0), pl, steps=1500)
+    assert touched == 0 and st.pos[0, 1] < c[1] - 0.01 * S.D
