@@ -144,6 +144,15 @@ typedef struct {
   uint32_t n_materials;
   const float* material_pairs;
   const float* material_walls;
+  /* Walls besides the box faces (reading R23, e.g. the §5 box with a slit,
+   * PAPER.md:139): n_plates <= 10 finite two-sided rectangles, plates = host
+   * [n_plates][12]: centre xyz, unit normal xyz, unit in-plane axis u xyz,
+   * half-length along u, half-length along v = normal x u, unused. A plate
+   * is a particle of infinite radius (R11) touching at the rectangle's point
+   * closest to the centre; wall coefficients; history partner id
+   * 0xFFFFFFF6 + k. Copied at dem_create. */
+  uint32_t n_plates;
+  const float* plates;
 } dem_params;
 
 /* Particle arrays, all host or all device (mem_kind). Layout: pos/vel/omega
@@ -180,6 +189,8 @@ typedef struct {
   int64_t kernel_count[8];
   int32_t force_cfg;     /* k_force configuration in use: 0 dense, 1 light, -1 not chosen yet */
   int32_t reserved;
+  double max_speed;      /* max |v| of the current state [m/s]: the last step moved no
+                            particle farther than max_speed * dt (the §5 termination test) */
 } dem_stats;
 
 /* Kernel indices of dem_stats.kernel_ms. */

@@ -91,6 +91,7 @@ struct dem_handle {
   int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
   int fcfg = -1;      // k_force configuration (0 dense, 1 light); -1: chosen at the first step
   float4* mat_tables = nullptr;  // material pair + wall coefficients (cudaMalloc, dem_create)
+  float* plate_buf = nullptr;    // plates (R23), 12 floats each (cudaMalloc, dem_create)
 
   // graphs: g2[b] = two steps starting at parity b; g1[b] = one step
   cudaGraphExec_t g2[2] = {nullptr, nullptr};
@@ -417,6 +418,18 @@ int validate_params(const dem_params* p) {
     if (!(v >= 0.0f) || !std::isfinite(v)) return DEM_EINVAL;
   if (p->cell_edge < 0.0f || !std::isfinite(p->cell_edge)) return DEM_EINVAL;
   if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
+  if (p->n_plates > 10 || (p->n_plates && !p->plates)) return DEM_EINVAL;
+  for (uint32_t k = 0; k < p->n_plates; ++k) {  // unit normal, unit axis in the plane, extents
+    const float* q = p->plates + 12 * k;
+    for (int c = 0; c < 11; ++c)
+      if (!std::isfinite(q[c])) return DEM_EINVAL;
+    const double nn = (double)q[3] * q[3] + (double)q[4] * q[4] + (double)q[5] * q[5];
+    const double uu = (double)q[6] * q[6] + (double)q[7] * q[7] + (double)q[8] * q[8];
+    const double nu = (double)q[3] * q[6] + (double)q[4] * q[7] + (double)q[5] * q[8];
+    if (std::fabs(nn - 1) > 1e-5 || std::fabs(uu - 1) > 1e-5 || std::fabs(nu) > 1e-5 ||
+        !(q[9] > 0.f) || !(q[10] > 0.f))
+      return DEM_EINVAL;
+  }
   if (p->n_materials > 1) {  // symmetric, finite, non-negative (SPEC MaterialTable)
     const uint32_t M = p->n_materials;
     if (M > 16 || !p->material_pairs) return DEM_EINVAL;
@@ -550,6 +563,22 @@ int dem_create(const dem_params* p, dem_handle** out) {
     ph.wmat = h->mat_tables + t.size();
     ph.idmask = (1u << kMatShift) - 1u;
   }
+  ph.nplates = 0;
+  ph.plates = nullptr;
+  if (p->n_plates) {
+    if (cudaMalloc((void**)&h->plate_buf, sizeof(float) * 12 * p->n_plates) != cudaSuccess ||
+        cudaMemcpy(h->plate_buf, p->plates, sizeof(float) * 12 * p->n_plates,
+                   cudaMemcpyHostToDevice) != cudaSuccess) {
+      if (h->plate_buf) cudaFree(h->plate_buf);
+      if (h->mat_tables) cudaFree(h->mat_tables);
+      cudaFreeHost(h->err_host);
+      if (h->own_stream) cudaStreamDestroy(h->stream);
+      delete h;
+      return fail(nullptr, DEM_ENOMEM, "plate allocation failed");
+    }
+    ph.plates = h->plate_buf;
+    ph.nplates = p->n_plates;
+  }
   *out = h;
   return DEM_OK;
 }
@@ -561,6 +590,7 @@ int dem_destroy(dem_handle* h) {
   if (h->xright_ipc && h->xright) cudaIpcCloseMemHandle((void*)h->xright);
   if (h->xregion) cudaFree(h->xregion);
   if (h->mat_tables) cudaFree(h->mat_tables);
+  if (h->plate_buf) cudaFree(h->plate_buf);
   free_buffers(h);
   for (auto& pr : h->prof) {
     cudaEventDestroy(pr.b);
@@ -1238,6 +1268,19 @@ int dem_get_stats(dem_handle* h, dem_stats* out) {
   for (int k = 0; k < 8; ++k) {
     out->kernel_ms[k] = h->kernel_ms[k];
     out->kernel_count[k] = h->kernel_count[k];
+  }
+  if (h->n > 0) {
+    uint32_t* ms = nullptr;
+    if (!dalloc(h, &ms, 1)) return fail(h, DEM_ENOMEM, "allocation failed");
+    CUDA_TRY(h, cudaMemsetAsync(ms, 0, 4, h->stream));
+    launch_max_speed(h->stream, h->n, h->vel[h->cur], ms);
+    uint32_t hb = 0;
+    CUDA_TRY(h, cudaMemcpyAsync(&hb, ms, 4, cudaMemcpyDeviceToHost, h->stream));
+    CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+    dev_free(h, ms);
+    float f;
+    memcpy(&f, &hb, 4);
+    out->max_speed = f;
   }
   if (h->n > 0 && h->p.model == DEM_MODEL_PRACTICAL) {
     unsigned long long* sm = nullptr;

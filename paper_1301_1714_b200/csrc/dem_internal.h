@@ -49,6 +49,9 @@ struct DevPhys {
   const float4* wmat;
   uint32_t nmat;
   uint32_t idmask;  // 0x07FFFFFF with materials, else 0xFFFFFFFF
+  // plates (R23): nplates finite two-sided rectangles, 12 floats each
+  const float* plates;
+  uint32_t nplates;
 };
 constexpr uint32_t kMatShift = 27;
 
@@ -240,6 +243,7 @@ int launch_insert_contacts(cudaStream_t st, int64_t m, int64_t n, int64_t stride
                            uint32_t* flags, int skip_unknown);
 int launch_analyze(cudaStream_t st, int64_t n, const StepBuffers& b, const DevGrid& g,
                    unsigned long long* acc);
+int launch_max_speed(cudaStream_t st, int64_t n, const float4* vel, uint32_t* out);
 int launch_cnt_stats(cudaStream_t st, int64_t n, const uint32_t* cnt,
                      unsigned long long* sum_max);
 

@@ -523,10 +523,52 @@ __device__ __forceinline__ void eval_pair_practical(const Own& o, float4 Q, floa
   pair_practical(n, delta, Rs, ms, v, rw, dold, Cn, Ct, alpha, mu, ph.dt, ph.flags, Fc, Tc, dnew);
 }
 
+// Plate k (R23) against particle P = (x, r): the rectangle's point closest
+// to the centre, in fp64 on the fp32 plate numbers (centre c, unit normal n,
+// unit axis u, half-lengths a, b along u and v = n x u). Returns (unit vector
+// from the centre to that point, δ = r - distance) when in contact, w <= 0
+// when not, w = NaN for a centre on the plate. Out of line: plates are few
+// and rarely touched, so the common path keeps its registers.
+__device__ __noinline__ float4 plate_contact(const float* __restrict__ pl, float4 P) {
+  if (fabsf((P.x - pl[0]) * pl[3] + (P.y - pl[1]) * pl[4] + (P.z - pl[2]) * pl[5]) >
+      P.w * 1.0001f + 1e-6f * (fabsf(P.x) + fabsf(P.y) + fabsf(P.z)) + 1e-30f)
+    return make_float4(0.f, 0.f, 0.f, -1.f);  // conservative fp32 reject: far from the plane
+  // the exact fp64 expression of R23, evaluated in a fixed order without
+  // contraction (the oracle's order), so contact decisions are bit-identical
+  const double c[3] = {pl[0], pl[1], pl[2]}, n[3] = {pl[3], pl[4], pl[5]};
+  const double u[3] = {pl[6], pl[7], pl[8]};
+  const double v[3] = {__dsub_rn(__dmul_rn(n[1], u[2]), __dmul_rn(n[2], u[1])),
+                       __dsub_rn(__dmul_rn(n[2], u[0]), __dmul_rn(n[0], u[2])),
+                       __dsub_rn(__dmul_rn(n[0], u[1]), __dmul_rn(n[1], u[0]))};
+  const double x[3] = {(double)P.x, (double)P.y, (double)P.z};
+  double du = 0.0, dv = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    du = __dadd_rn(du, __dmul_rn(__dsub_rn(x[a], c[a]), u[a]));
+    dv = __dadd_rn(dv, __dmul_rn(__dsub_rn(x[a], c[a]), v[a]));
+  }
+  const double qu = fmin(fmax(du, -(double)pl[9]), (double)pl[9]);
+  const double qv = fmin(fmax(dv, -(double)pl[10]), (double)pl[10]);
+  double e[3], d2 = 0.0;
+#pragma unroll
+  for (int a = 0; a < 3; ++a) {
+    e[a] = __dsub_rn(__dadd_rn(__dadd_rn(c[a], __dmul_rn(qu, u[a])), __dmul_rn(qv, v[a])), x[a]);
+    d2 = __dadd_rn(d2, __dmul_rn(e[a], e[a]));
+  }
+  const double dist = __dsqrt_rn(d2), r = (double)P.w;
+  if (!(r > dist)) return make_float4(0.f, 0.f, 0.f, -1.f);
+  if (dist == 0.0) return make_float4(0.f, 0.f, 0.f, __int_as_float(0x7fc00000));
+  return make_float4((float)__ddiv_rn(e[0], dist), (float)__ddiv_rn(e[1], dist),
+                     (float)__ddiv_rn(e[2], dist), (float)__dsub_rn(r, dist));
+}
+
+
 // Step 8 + step 1 + next step 2 for one particle (shared by both sweeps):
 // walls, integration, state write at slot j, next CM and its counting rank.
 // The outputs go to slot oj = j - (first owned sorted slot): the owned
 // particles of the next step are dense from 0.
+// MAT: the handle has material tables or plates (k_force is instantiated both
+// ways so that the common case carries neither).
 template <int MODEL, bool DIAG, bool MAT = true, class LookupFn>
 __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevGrid& g,
                                                 const DevPhys& ph, uint32_t N, uint32_t K,
@@ -545,20 +587,10 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
     const float m = ri + 1e-6f * (fabsf(xs[a]) + ri) + 1e-30f;
     near_wall |= (xs[a] - (float)g.lo[a] < m) | ((float)g.hi[a] - xs[a] < m);
   }
-#pragma unroll
-  for (int w = 0; w < 6; ++w) {
-    if (!near_wall) break;
-    const int a = w >> 1;
-    const bool hi = (w & 1) != 0;
-    const double dist = hi ? (g.hi[a] - (double)xs[a]) : ((double)xs[a] - g.lo[a]);
-    if (!((double)ri > dist)) continue;
-    const float delta = (float)((double)ri - dist);
-    f3 n = mk(0.f, 0.f, 0.f);
-    if (a == 0) n.x = hi ? 1.f : -1.f;
-    if (a == 1) n.y = hi ? 1.f : -1.f;
-    if (a == 2) n.z = hi ? 1.f : -1.f;
+  // one wall contact (a face or a plate): Eqs. 2-10 with R* = r_i, m* = m_i,
+  // v_j = ω_j = 0 (R11), the wall coefficients (per material if tabulated)
+  auto wall_contact = [&](f3 n, float delta, uint32_t pid) {
     if (MODEL == 0) {
-      const uint32_t pid = kWallPid0 + (uint32_t)w;
       const f3 rwi = mk(__fmul_rn(ri, o.W.x), __fmul_rn(ri, o.W.y), __fmul_rn(ri, o.W.z));
       f3 Fc, Tc, dnew;
       float4 c = make_float4(ph.wCn, ph.wCt, ph.walpha, ph.wmu);
@@ -577,6 +609,29 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       const f3 Fc = pair_simple(n, delta, mk(-o.V.x, -o.V.y, -o.V.z), ph.ksp, ph.kda, ph.ksh);
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
     }
+  };
+#pragma unroll
+  for (int w = 0; w < 6; ++w) {
+    if (!near_wall) break;
+    const int a = w >> 1;
+    const bool hi = (w & 1) != 0;
+    const double dist = hi ? (g.hi[a] - (double)xs[a]) : ((double)xs[a] - g.lo[a]);
+    if (!((double)ri > dist)) continue;
+    f3 n = mk(0.f, 0.f, 0.f);
+    if (a == 0) n.x = hi ? 1.f : -1.f;
+    if (a == 1) n.y = hi ? 1.f : -1.f;
+    if (a == 2) n.z = hi ? 1.f : -1.f;
+    wall_contact(n, (float)((double)ri - dist), kWallPid0 + (uint32_t)w);
+  }
+  // plates (R23), in the order given; geometry out of line (rarely taken)
+  for (uint32_t k = 0; MAT && k < ph.nplates; ++k) {
+    const float4 c = plate_contact(ph.plates + 12 * k, o.P);
+    if (!(c.w > 0.f) && !isnan(c.w)) continue;  // no contact
+    if (isnan(c.w)) {  // centre on the plate: no direction (R18)
+      raise_error(b.err, 9u, j, my_id);
+      continue;
+    }
+    wall_contact(mk(c.x, c.y, c.z), c.w, kWallPid0 + 6u + k);
   }
   if (overflow) raise_error(b.err, 6u, j, my_id);
   if (MODEL == 0) b.cnt_out[j] = ncnt;
@@ -1720,6 +1775,18 @@ __global__ void k_insert_contacts(int64_t m, int64_t id_bound, int64_t stride, u
                                         __uint_as_float(id_j[e]));
 }
 
+// max |v| over n particles (bits of a non-negative float order like the value)
+__global__ void k_max_speed(int64_t n, const float4* vel, uint32_t* out) {
+  float m = 0.f;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = vel[i];
+    m = fmaxf(m, sqrtf(v.x * v.x + v.y * v.y + v.z * v.z));
+  }
+  for (int d = 16; d > 0; d >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, d));
+  if (lane_id() == 0) atomicMax(out, __float_as_uint(m));
+}
+
 __global__ void k_cnt_stats(int64_t n, const uint32_t* cnt, unsigned long long* sum_max) {
   unsigned long long s = 0;
   uint32_t mx = 0;
@@ -1895,7 +1962,7 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
     const unsigned grid = blocks_for(n, 32 * kSweepWarps), block = 32 * kSweepWarps;
-    const bool mat = ph.nmat > 1;  // material pairs: their own instantiation
+    const bool mat = ph.nmat > 1 || ph.nplates > 0;  // materials/plates: their own instantiation
     if (cfg == kForceLight) {
       if (mat) launch_pdl(k_force<MODEL, DIAG, kForceLight, true>, grid, block, smem, st, b, g, ph, N, K);
       else launch_pdl(k_force<MODEL, DIAG, kForceLight, false>, grid, block, smem, st, b, g, ph, N, K);
@@ -2046,6 +2113,12 @@ int launch_analyze(cudaStream_t st, int64_t n, const StepBuffers& b, const DevGr
                    unsigned long long* acc) {
   if (n <= 0) return K_OTHER;
   k_analyze<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, acc);
+  return K_OTHER;
+}
+
+int launch_max_speed(cudaStream_t st, int64_t n, const float4* vel, uint32_t* out) {
+  if (n <= 0) return K_OTHER;
+  k_max_speed<<<296, 256, 0, st>>>(n, vel, out);
   return K_OTHER;
 }
 

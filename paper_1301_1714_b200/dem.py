@@ -56,7 +56,8 @@ class DemParams(C.Structure):
                 ("allocator", C.POINTER(DemAllocator)), ("rank", C.c_int32),
                 ("world_size", C.c_int32), ("nccl_id", C.c_void_p),
                 ("n_materials", C.c_uint32), ("material_pairs", C.c_void_p),
-                ("material_walls", C.c_void_p)]
+                ("material_walls", C.c_void_p), ("n_plates", C.c_uint32),
+                ("plates", C.c_void_p)]
 
 
 class DemParticles(C.Structure):
@@ -72,7 +73,7 @@ class DemStats(C.Structure):
                 ("max_contacts_seen", C.c_int64), ("launches", C.c_int64),
                 ("graph_launches", C.c_int64), ("kernel_ms", C.c_double * 8),
                 ("kernel_count", C.c_int64 * 8), ("force_cfg", C.c_int32),
-                ("reserved", C.c_int32)]
+                ("reserved", C.c_int32), ("max_speed", C.c_double)]
 
 
 class DemAnalysis(C.Structure):
@@ -168,6 +169,12 @@ def params_from(sp, *, flags: int = 0, device: int = -1, stream=None, allocator=
             w = np.ascontiguousarray(np.asarray(wm, np.float32))
             p._wmat = w
             p.material_walls = w.ctypes.data
+    plates = getattr(sp, "plates", None)
+    if plates:  # (n, 12) finite two-sided rectangles (R23)
+        a = np.ascontiguousarray(np.asarray(plates, np.float32))
+        p.n_plates = a.shape[0]
+        p._plates = a
+        p.plates = a.ctypes.data
     return p
 
 
@@ -425,7 +432,8 @@ class Dem:
                     launches=s.launches, graph_launches=s.graph_launches,
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
                     kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
-                    force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg])
+                    force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg],
+                    max_speed=s.max_speed)
 
 
     def analyze(self) -> dict:

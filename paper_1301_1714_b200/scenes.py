@@ -290,3 +290,49 @@ def plate(centre, normal, u, half_u: float, half_v: float) -> tuple:
     assert abs(np.linalg.norm(n) - 1) < 1e-6 and abs(np.linalg.norm(uu) - 1) < 1e-6
     assert abs(n @ uu) < 1e-6 and half_u > 0 and half_v > 0
     return tuple(float(x) for x in (*centre, *normal, *u, half_u, half_v, 0.0))
+
+
+def slit_box(nxyz: tuple = (64, 32, 64), seed: int = 6, slit_d: float = 6.0,
+             params: SimParams | None = None) -> Scene:
+    """The paper's §5 experiment: equal spheres falling from a
+    box through a slit at its bottom onto the floor. The paper gives no
+    dimensions; this geometry is a stated choice: a simple-cubic
+    block of nx*ny*nz spheres (spacing 1.02 d, jitter ±0.01 d horizontally, the bottom
+    layer resting on the box bottom) in an
+    open-topped box whose bottom, 40 d above the floor, has a slit of slit_d
+    diameters along x through its middle; box and bottom are plates (R23), the
+    floor and the outer walls are the domain faces. nxyz = (64, 32, 64) gives
+    the paper's 2^17 = 131,072 particles."""
+    nx, ny, nz = nxyz
+    sp_ = 1.02 * D
+    rng = np.random.default_rng(seed)
+    W_x, W_z = nx * sp_ + 2 * D, nz * sp_ + 2 * D  # inner box widths
+    H_box = ny * sp_ + 8 * D                        # box wall height
+    y_b = 40 * D                                    # box bottom
+    Lx, Lz = W_x + 40 * D, W_z + 40 * D
+    Ly = y_b + H_box + 10 * D
+    x0, z0 = 0.5 * (Lx - W_x), 0.5 * (Lz - W_z)
+    zc = z0 + 0.5 * W_z
+    i, j, k = np.meshgrid(np.arange(nx), np.arange(ny), np.arange(nz), indexing="ij")
+    pos = np.stack([x0 + D + (i.ravel() + 0.5) * sp_,
+                    y_b + R - 0.002 * D + j.ravel() * sp_,
+                    z0 + D + (k.ravel() + 0.5) * sp_], axis=1)
+    pos = pos + rng.uniform(-0.01 * D, 0.01 * D, pos.shape) * np.array([1.0, 0.1, 1.0])
+    half_slit = 0.5 * slit_d * D
+    hb = 0.5 * (0.5 * W_z - half_slit)  # half-width of each bottom plate along z
+    plates = (
+        # bottom, either side of the slit (normal +y, u = x)
+        plate((x0 + 0.5 * W_x, y_b, z0 + hb), (0, 1, 0), (1, 0, 0), 0.5 * W_x, hb),
+        plate((x0 + 0.5 * W_x, y_b, zc + half_slit + hb), (0, 1, 0), (1, 0, 0), 0.5 * W_x, hb),
+        # sides (normal +-x and +-z), from the bottom up
+        plate((x0, y_b + 0.5 * H_box, zc), (1, 0, 0), (0, 1, 0), 0.5 * H_box, 0.5 * W_z),
+        plate((x0 + W_x, y_b + 0.5 * H_box, zc), (1, 0, 0), (0, 1, 0), 0.5 * H_box, 0.5 * W_z),
+        plate((x0 + 0.5 * W_x, y_b + 0.5 * H_box, z0), (0, 0, 1), (1, 0, 0), 0.5 * W_x, 0.5 * H_box),
+        plate((x0 + 0.5 * W_x, y_b + 0.5 * H_box, z0 + W_z), (0, 0, 1), (1, 0, 0), 0.5 * W_x,
+              0.5 * H_box),
+    )
+    p = (params or SimParams()).replace(box_lo=(0.0, 0.0, 0.0), box_hi=(Lx, Ly, Lz),
+                                        plates=plates)
+    n = pos.shape[0]
+    return make_scene(f"slit{n}", p, pos, meta=dict(kind="slit", nxyz=nxyz, slit_d=slit_d,
+                                                   y_bottom=y_b, seed=seed))

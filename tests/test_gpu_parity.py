@@ -473,6 +473,70 @@ def test_materials_checkpoint_and_validation():
                                      material=bad)
 
 
+# ------------------------------------------------- plates (R23, slit box) --
+
+def plate_gas(seed=5, n=2500, materials=False):
+    """A gas crossing three plates (a large horizontal one, a vertical one, a
+    small tilted one): face, edge and corner contacts, both sides."""
+    L = 14.0 * S.D
+    c = 0.5 * L
+    t = np.array([1.0, 0.0, 1.0]) / math.sqrt(2.0)
+    plates = (S.plate((c, c, c), (0, 1, 0), (1, 0, 0), 4 * S.D, 3 * S.D),
+              S.plate((c - 3 * S.D, c, c), (1, 0, 0), (0, 0, 1), 2 * S.D, 2.5 * S.D),
+              S.plate((c + 3 * S.D, c - 3 * S.D, c + 2 * S.D), tuple(t), (0, 1, 0), 1.5 * S.D,
+                      1.0 * S.D))
+    kw = dict(r_range=(0.3e-3, 0.5e-3), v_sigma=0.2,
+              params=S.SimParams(max_contacts=32, plates=plates))
+    if materials:
+        return S.mixed_gas(n, 14.0, seed, M=2, **kw)
+    return S.random_gas(n, 14.0, seed, **kw)
+
+
+@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
+                                     DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("kind", ["plates", "plates+materials", "slit"])
+def test_plates_one_step_T2(kind, variant):
+    """Plate contacts (faces, edges, corners, both sides) bit-exactly the
+    oracle's (their history entries are part of the contact set), forces and
+    torques within T2, for every force-kernel variant."""
+    sc = S.slit_box((16, 6, 16)) if kind == "slit" else plate_gas(materials="mat" in kind)
+    K = sc.params.max_contacts
+    p = orc.make_params(sc.params, sc.radius)
+    d = Dem(sc.params, flags=DEM_F_DIAG | variant)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id,
+                    material=getattr(sc, "material", None))
+    plate_contacts = 0
+    for k in range(3):
+        st, h = oracle_inputs(d, K)
+        d.step(1)
+        g = d.get_state(forces=True)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        assert np.array_equal(g["id"], st.id)
+        assert_T2_forces(g["force"], g["torque"], res, what=f"{kind} step {k + 1}")
+        got = contacts_dict(d)
+        assert_T2_history(got, h.as_dict(st.id))
+        plate_contacts += sum(1 for (_, b) in got if b >= 0xFFFFFFF6)
+    assert plate_contacts > 0
+
+
+def test_slit_box_flows_through_the_slit():
+    """The §5 experiment at small scale: particles above the slit fall
+    through it onto the floor, those beside it stay on the box bottom, none
+    leaves the domain, no error."""
+    sc = S.slit_box((16, 6, 16))
+    d = Dem(sc.params)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+    d.step(30000)  # 60 ms: the column above the slit has reached the floor
+    s = d.get_state()
+    y = s["pos"][:, 1]
+    below = y < sc.meta["y_bottom"]
+    assert 0 < below.sum() < sc.n
+    assert (y > 0).all() and (y < sc.params.box_hi[1]).all()
+    assert (s["pos"][below, 1] < sc.meta["y_bottom"] - 5 * S.D).mean() > 0.5
+    assert d.stats()["max_speed"] > 0
+
+
 def test_checkpoint_roundtrip_bitwise():
     sc = S.C1()
     d1 = make(sc, flags=0)
