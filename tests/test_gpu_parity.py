@@ -275,6 +275,32 @@ def test_momentum_conservation_gpu():
     assert np.abs(P1 - P0).max() <= 1e-4 * A
 
 
+def test_energy_conservation_gpu():
+    """α = 0, μ = 0, g = 0, elastic walls: the GPU run's total energy (kinetic,
+    rotational and Hertz elastic, evaluated in fp64 from the fp32 state) stays
+    within the oracle's bound of the same experiment, with no secular drift."""
+    from .test_oracle_dynamics import total_energy
+    c1 = S.C1()
+    sp = S.SimParams(gravity=(0.0, 0.0, 0.0), damping=0.0, friction=0.0)
+    sc = S.make_scene("c1", sp.replace(box_hi=c1.params.box_hi), c1.pos, c1.vel * np.float32(4),
+                      c1.omega)
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc, flags=0)
+
+    def energy():
+        s = d.get_state()
+        st = orc.State.from_arrays(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"],
+                                   s["id"])
+        return total_energy(orc, st, p)
+    E0 = energy()
+    dev = []
+    for _ in range(20):
+        d.step(100)
+        dev.append(energy() / E0 - 1)
+    assert np.mean(np.abs(dev)) < 3e-3
+    assert abs(np.mean(dev[-5:]) - np.mean(dev[:5])) < 2e-3  # no drift
+
+
 def test_determinism_and_graph_equivalence():
     sc = S.C2()
     outs = []
