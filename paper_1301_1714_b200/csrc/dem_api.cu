@@ -804,6 +804,15 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
     }
+    // defined contents everywhere (once per allocation): several kernels load
+    // ahead of their bounds checks (entries past a count, slots past nslots)
+    // and discard the values; this keeps compute-sanitizer's initcheck clean
+    if (ok) {
+      std::vector<Alloc> fresh = h->allocs;
+      for (auto& a : fresh)
+        if (std::find(keepalive.begin(), keepalive.end(), a.p) == keepalive.end())
+          ok &= cudaMemsetAsync(a.p, 0, a.bytes, st) == cudaSuccess;
+    }
     if (!ok) {
       unstage();
       free_buffers(h);
@@ -844,6 +853,9 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
   CUDA_TRY(h, cudaMemsetAsync(h->off, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
   CUDA_TRY(h, cudaMemsetAsync(h->perm, 0, sizeof(uint32_t) * N, st));
+  // k_force reads the first 4 list entries before the count arrives (unused
+  // beyond it); defined contents keep compute-sanitizer's initcheck clean
+  CUDA_TRY(h, cudaMemsetAsync(h->clist, 0, sizeof(uint32_t) * N * h->K, st));
   CUDA_TRY(h, cudaMemsetAsync(h->cnt[0], 0, sizeof(uint32_t) * N, st));
   CUDA_TRY(h, cudaMemsetAsync(h->cnt[1], 0, sizeof(uint32_t) * N, st));
   for (int b = 0; b < 2; ++b)

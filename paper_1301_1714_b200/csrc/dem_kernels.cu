@@ -690,7 +690,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
 // The paper's mapping ("Assign the i-th thread to the SCM[i]-th
 // particle"): each thread loops over its candidates and evaluates its own
 // contacts, so a warp idles on the lanes without a contact (§6's "quarter").
-template <int MODEL, bool DIAG>
+template <int MODEL, bool DIAG, bool MAT>
 __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, DevPhys ph,
                                                    uint32_t N, uint32_t K) {
   pdl_enter();
@@ -744,7 +744,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
           const float4 WQ = __ldg(&b.omg_in[q]);
           const uint32_t pid = __float_as_uint(WQ.w) & ph.idmask;
           f3 Fc, Tc, dnew;
-          eval_pair_practical(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
+          eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, lookup(pid), ph, Fc, Tc, dnew);
           F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
           T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
           if (ncnt < K) {
@@ -762,7 +762,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
       }
     }
   }
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, ncnt, overflow, lookup);
+  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, ncnt, overflow, lookup);
 }
 
 // ---- default path: k_detect (steps 5-6) then k_force (steps 7-8, 1) -------
@@ -1250,7 +1250,7 @@ __global__ void __launch_bounds__(256) k_detect_half(StepBuffers b, DevGrid g, u
 // Each pair writes its result R (force on the lower particle, n x F_t) and
 // both history entries; no accumulation here, so no owner bookkeeping beyond
 // a shared-memory owner map.
-template <int MODEL>
+template <int MODEL, bool MAT>
 __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
                                               uint32_t K) {
   __shared__ uint8_t s_own[4][32 * 32];
@@ -1305,7 +1305,7 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
                           ? mk(Hk.x, Hk.y, Hk.z)
                           : old_history(b.hist_in, N, si, n_old, 0xFFFFFFFFu, pid);
       f3 dnew;
-      eval_pair_practical(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+      eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
       // this side's entry (upper part of i's list) and the partner's (lower part)
       __stcs(&b.hist_out[(size_t)k * N + (i - jlo)],
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
@@ -1326,7 +1326,7 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
 // lower partners ascending, then upper partners ascending (= ascending
 // partner slot) — then walls and integration (finish_particle).
 constexpr uint32_t kLowBatch = 8;  // lower-list entries sorted in registers
-template <int MODEL, bool DIAG>
+template <int MODEL, bool DIAG, bool MAT>
 __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N,
                                                 uint32_t K) {
   if (ld_volatile(&b.err->code) != 0u) return;
@@ -1406,7 +1406,7 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, N, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG>(b, g, ph, N, K, j - jlo, o, F, T, min(nup + nlow, K), overflow,
+  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, min(nup + nlow, K), overflow,
                                lookup);
 }
 
@@ -1836,11 +1836,15 @@ __global__ void __launch_bounds__(256) k_analyze(StepBuffers b, DevGrid g, uint3
         const int y = cy + dy;
         if (y < 0 || y >= g.ny) continue;
         const uint32_t row = (uint32_t)z * nxy + (uint32_t)y * (uint32_t)g.nx;
-        cand += __ldg(&b.off[row + xb + 1]) - __ldg(&b.off[row + xa]);
+        const uint32_t t0 = __ldg(&b.off[row + xa]), t1 = __ldg(&b.off[row + xb + 1]);
+        cand += t1 - t0;
+        // contacts with the exact predicate (R14), independent of which force
+        // path ran (the ablations keep no full contact counts)
+        for (uint32_t t = t0; t < t1; ++t)
+          if (t != j && in_contact(P, __ldg(&b.pos_sorted[t]))) ++cont;
       }
     }
     cand -= 1u;  // itself
-    cont = __ldg(&b.ccount[j]);
     const uint32_t c = (uint32_t)cz * nxy + (uint32_t)cy * (uint32_t)g.nx + (uint32_t)cx;
     const uint32_t o0 = __ldg(&b.off[c]);
     pop = __ldg(&b.off[c + 1]) - o0;
@@ -1957,7 +1961,10 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
                            const DevGrid& g, const DevPhys& ph, int variant) {
   const uint32_t N = (uint32_t)n;
   if (variant == 1) {  // the paper's mapping, one fused kernel
-    launch_pdl(k_sweep_tpp<MODEL, DIAG>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
+    if (ph.nmat > 1 || ph.nplates > 0)
+      launch_pdl(k_sweep_tpp<MODEL, DIAG, true>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
+    else
+      launch_pdl(k_sweep_tpp<MODEL, DIAG, false>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
@@ -1984,10 +1991,15 @@ int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers
 int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuffers& b,
                 const DevGrid& g, const DevPhys& ph) {
   if (n <= 0) return K_SWEEP;
-  if (model == 0)
-    k_pair<0><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
-  else
-    k_pair<1><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  const bool mat = ph.nmat > 1 || ph.nplates > 0;
+  const unsigned grid = blocks_for(n, 128);
+  if (model == 0) {
+    if (mat) k_pair<0, true><<<grid, 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+    else k_pair<0, false><<<grid, 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  } else {
+    if (mat) k_pair<1, true><<<grid, 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+    else k_pair<1, false><<<grid, 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
+  }
   // (one warp per 32 owned slots, 4 warps per block)
   return K_SWEEP;
 }
@@ -1996,17 +2008,19 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
                   const StepBuffers& b, const DevGrid& g, const DevPhys& ph) {
   if (n <= 0) return K_FINISH;
   const uint32_t N = (uint32_t)n;
+  const bool mat = ph.nmat > 1 || ph.nplates > 0;
+  const unsigned grid = blocks_for(n, 128);
+#define DEM_FIN(M, D)                                                                \
+  (mat ? k_finish<M, D, true><<<grid, 128, 0, st>>>(b, g, ph, N, K)                  \
+       : k_finish<M, D, false><<<grid, 128, 0, st>>>(b, g, ph, N, K))
   if (model == 0) {
-    if (diag)
-      k_finish<0, true><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
-    else
-      k_finish<0, false><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    if (diag) DEM_FIN(0, true);
+    else DEM_FIN(0, false);
   } else {
-    if (diag)
-      k_finish<1, true><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
-    else
-      k_finish<1, false><<<blocks_for(n, 128), 128, 0, st>>>(b, g, ph, N, K);
+    if (diag) DEM_FIN(1, true);
+    else DEM_FIN(1, false);
   }
+#undef DEM_FIN
   return K_FINISH;
 }
 

@@ -1,0 +1,43 @@
+"""Small workloads for compute-sanitizer (tools/sanitize.sh): every step
+kernel of every force-kernel variant, slabs, materials, plates, on C1/C2-sized
+scenes, eager launches, the library's own allocator."""
+import sys
+
+sys.path.insert(0, ".")
+from paper_1301_1714_b200 import scenes as S  # noqa: E402
+from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT,  # noqa: E402
+                                      DEM_F_HALF_LISTS, DEM_F_NO_GRAPH,
+                                      DEM_F_THREAD_PER_PARTICLE, Dem)
+
+
+def run(sc, flags, steps=3, material=None):
+    d = Dem(sc.params, flags=flags | DEM_F_NO_GRAPH | DEM_F_DIAG, torch_allocator=False)
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id, material=material)
+    d.step(steps)
+    d.get_state(forces=True)
+    ci, cj, cd = d.get_contacts()
+    d.set_contacts(ci, cj, cd)
+    d.step(1)
+    d.analyze()
+    d.stats()
+    d.close()
+
+
+for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE):
+    run(S.C1(), f)
+run(S.C2(S.SimParams(model="simple")), 0)
+mg = S.mixed_gas(800, 10.0, 2, M=3, params=S.SimParams(max_contacts=32))
+run(mg, DEM_F_FORCE_LIGHT, material=mg.material)
+run(S.slit_box((8, 4, 8)), DEM_F_FORCE_DENSE)
+# two slab ranks in one process
+sc = S.random_gas(3000, 16.0, 3, r_range=(0.3e-3, 0.5e-3), v_sigma=2.0,
+                  params=S.SimParams(max_contacts=32))
+ds = [Dem(sc.params, flags=DEM_F_NO_GRAPH, rank=r, world=2, torch_allocator=False) for r in range(2)]
+for d in ds:
+    d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+ds[0].connect_local(None, ds[1])
+ds[1].connect_local(ds[0], None)
+for _ in range(3):
+    for d in ds:
+        d.step(1)
+print("sanitize workload done", flush=True)
