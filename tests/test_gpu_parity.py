@@ -394,14 +394,15 @@ def analysis_from_oracle(p, s, K):
                 contact_hist=list(np.bincount(np.minimum(cont, 32), minlength=33)))
 
 
+@pytest.mark.parametrize("variant", [0, DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
-def test_analysis_matches_oracle(idx):
+def test_analysis_matches_oracle(idx, variant):
     """dem_analyze (the paper's §6 counts: candidates, contacts, SIMT lane
     slots of the thread-per-particle mapping, cell populations) equals the
     same counts taken from the oracle's grid and contact set, exactly."""
     sc = [S.C2(), scenes_small()[1]][idx]
     p = orc.make_params(sc.params, sc.radius)
-    d = make(sc, flags=0)
+    d = make(sc, flags=variant)
     d.step(3)
     s = d.get_state()
     d.step(1)
