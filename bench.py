@@ -389,8 +389,9 @@ def run_ours(args):
         **{k: an[k] for k in ("candidates_mean", "max_candidates", "contacts_mean",
                               "max_contacts", "contact_fraction",
                               "tpp_candidate_lane_efficiency", "tpp_contact_lane_efficiency",
-                              "max_per_cell")},
+                              "max_per_cell", "movers")},
         "force_cfg": d.stats()["force_cfg"],
+        "full_sorts": d.stats()["full_sorts"],
     }
     # end to end through the public API with pinned host buffers
     if not args.no_e2e and world == 1:

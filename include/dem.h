@@ -87,6 +87,12 @@ enum dem_flags {
                                   history entries per particle (> 7: dense). Both give
                                   bitwise-identical results */
   DEM_F_FORCE_LIGHT = 1u << 8, /* force-kernel configuration for few contacts per particle */
+  DEM_F_GENERAL_DETECT = 1u << 9, /* ablation: the candidate test evaluates S = r_i + r_j per
+                                     pair even when every radius is equal; default (single
+                                     GPU, one radius): S² is one constant. Same contact lists */
+  DEM_F_FULL_SORT = 1u << 10, /* ablation: the counting sort every step; default (single GPU):
+                                 a merge of the particles that changed cell into the last
+                                 sorted order. Bit-identical SCCM and offsets */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
@@ -188,7 +194,9 @@ typedef struct {
   double kernel_ms[8];
   int64_t kernel_count[8];
   int32_t force_cfg;     /* k_force configuration in use: 0 dense, 1 light, -1 not chosen yet */
-  int32_t reserved;
+  int32_t full_sorts;    /* steps sorted by the counting sort since dem_set_particles: the
+                            first, and any in which more than 4,096 particles changed cell;
+                            the others merge the few movers into the last sorted order */
   double max_speed;      /* max |v| of the current state [m/s]: the last step moved no
                             particle farther than max_speed * dt (the §5 termination test) */
 } dem_stats;
@@ -276,6 +284,9 @@ typedef struct {
   int64_t max_per_cell;      /* most particles in one cell (Eq. 13: √2 (h/d)³ at close packing) */
   int64_t occupied_cells;
   int64_t contact_hist[33];  /* particles with k contacts, k = 0..31; [32]: 32 or more */
+  int64_t movers;            /* particles the last step moved to another cell (the next merge
+                                re-sort's input); -1 without the merge re-sort (slabs,
+                                DEM_F_FULL_SORT) */
 } dem_analysis;
 
 /* Fill *out from the last step (DEM_ESTATE before the first step).

@@ -56,6 +56,15 @@ struct dem_handle {
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
   float4* pos_sorted = nullptr;
   uint32_t *clist = nullptr, *ccount = nullptr;
+  // merge re-sort (single GPU): SCM per sorted slot, the integrator's movers,
+  // [mover counter, movers this step], movers sorted by (key, slot) and by slot
+  uint32_t *skey = nullptr, *mov = nullptr, *mov_n = nullptr, *mv_u32 = nullptr;
+  int* mv_i32 = nullptr;
+  int2* mv_tab = nullptr;
+  bool merge = false;     // merge re-sort in use for this set
+  bool merge_ok = false;  // state in the last step's sorted order, movers listed
+  bool full_run = false;  // the rest of this dem_step call sorts by counting (mover overflow)
+  int64_t full_sorts = 0; // steps sorted by the counting sort since dem_set_particles
   uint8_t* cpos = nullptr;
   uint32_t *lcount = nullptr, *llist = nullptr;
   float4* R0 = nullptr;
@@ -71,6 +80,7 @@ struct dem_handle {
   int64_t cap_n = -1, cap_cells = -1;
 
   int64_t cap = 0;  // slot capacity = stride of the K-major arrays (single GPU: n)
+  float mono_r = 0.f;  // > 0: every particle of the set has this radius (single GPU only)
 
   // slab decomposition (world_size > 1), DESIGN.md §7
   bool slab = false;
@@ -96,6 +106,9 @@ struct dem_handle {
   // graphs: g2[b] = two steps starting at parity b; g1[b] = one step
   cudaGraphExec_t g2[2] = {nullptr, nullptr};
   cudaGraphExec_t g1[2] = {nullptr, nullptr};
+  // the same with the counting sort (merge mode: the first step, mover overflow)
+  cudaGraphExec_t gf2[2] = {nullptr, nullptr};
+  cudaGraphExec_t gf1[2] = {nullptr, nullptr};
 
   // profiling
   bool profiling = false;
@@ -166,7 +179,9 @@ void destroy_graphs(dem_handle* h) {
   for (int b = 0; b < 2; ++b) {
     if (h->g2[b]) cudaGraphExecDestroy(h->g2[b]);
     if (h->g1[b]) cudaGraphExecDestroy(h->g1[b]);
-    h->g2[b] = h->g1[b] = nullptr;
+    if (h->gf2[b]) cudaGraphExecDestroy(h->gf2[b]);
+    if (h->gf1[b]) cudaGraphExecDestroy(h->gf1[b]);
+    h->g2[b] = h->g1[b] = h->gf2[b] = h->gf1[b] = nullptr;
   }
 }
 
@@ -182,6 +197,9 @@ void free_buffers(dem_handle* h) {
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
+  h->skey = h->mov = h->mov_n = h->mv_u32 = nullptr;
+  h->mv_i32 = nullptr;
+  h->mv_tab = nullptr;
   h->cpos = nullptr;
   h->lcount = h->llist = nullptr;
   h->R0 = nullptr;
@@ -229,17 +247,36 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.scan_status_next = h->scan_status[b ^ 1];
   s.scan_ctr_next = h->scan_ctr + (b ^ 1);
   s.err = h->err;
+  if (h->merge) {
+    s.skey = h->skey;
+    s.mv.mov = h->mov;
+    s.mv.mov_n = h->mov_n;
+    s.mv.mv_m = h->mov_n + 1;
+    s.mv.dst = h->mv_u32;
+    s.mv.slot = h->mv_u32 + kMoverCap;
+    s.mv.key = h->mv_u32 + 2 * kMoverCap;
+    s.mv.evS = h->mv_u32 + 3 * kMoverCap;
+    s.mv.evC = h->mv_u32 + 5 * kMoverCap;
+    s.mv.evSc = h->mv_i32;
+    s.mv.evCc = h->mv_i32 + 2 * kMoverCap;
+    s.mv.tS = h->mv_tab;
+    s.mv.tC = h->mv_tab + mv_table_entries(h->cap);
+  }
   return s;
 }
 
-int kernels_per_step(const dem_handle* h) {
-  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 5 : (h->p.flags & DEM_F_HALF_LISTS) ? 7 : 6) +
-         (h->slab ? 5 : 0);
+int kernels_per_step(const dem_handle* h, bool full = false) {
+  // counting sort: scan (2) + scatter + rank (+ k_count in merge mode); merge: 2
+  const int sort = h->merge ? (full ? 5 : 2) : 4;
+  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3 : 2) +
+         sort + (h->slab ? 5 : 0);
 }
 
-// Enqueue one step from parity b: scan, scatter, rank, (detect,) sweep.
-// `ev` (profiling) receives an event pair around each kernel.
-int enqueue_step(dem_handle* h, int b, bool profile) {
+// Enqueue one step from parity b: the sort (counting: scan, scatter, rank;
+// merge: k_mv_sort, k_mv_perm, k_mv_off), (detect,) sweep. `full`: counting
+// sort in merge mode (cell counts from k_count; the integrator lists movers).
+// `profile` records an event pair around each kernel.
+int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   const StepBuffers s = step_buffers(h, b);
   const bool diag = (h->p.flags & DEM_F_DIAG) != 0;
   cudaEvent_t evb = nullptr;
@@ -271,16 +308,34 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
     rec(K_OTHER, false);
     h->launches += 2;
   }
-  rec(K_SCAN, true);
-  launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, s.scan_ctr,
-              h->err, 1);
-  rec(K_SCAN, false);
-  rec(K_SCATTER, true);
-  launch_scatter(h->stream, h->cap, s, h->ntiles);
-  rec(K_SCATTER, false);
-  rec(K_RANK, true);
-  launch_rank(h->stream, h->cap, s);
-  rec(K_RANK, false);
+  if (h->merge && !full) {  // merge re-sort
+    rec(K_SCATTER, true);
+    launch_mv_sort(h->stream, h->n, h->g.ncells, s);
+    rec(K_SCATTER, false);
+    rec(K_RANK, true);
+    launch_mv_apply(h->stream, h->n, h->g.ncells, s);
+    rec(K_RANK, false);
+    h->launches += 2;
+  } else {
+    if (h->merge) {  // the integrator listed movers, not cell counts
+      rec(K_HASH, true);
+      launch_count(h->stream, h->n, s.key_in, h->count, h->prank);
+      rec(K_HASH, false);
+      cudaMemsetAsync(h->mov_n, 0, sizeof(uint32_t), h->stream);
+      h->launches += 1;
+    }
+    rec(K_SCAN, true);
+    launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, s.scan_ctr,
+                h->err, 1);
+    rec(K_SCAN, false);
+    rec(K_SCATTER, true);
+    launch_scatter(h->stream, h->cap, s, h->ntiles);
+    rec(K_SCATTER, false);
+    rec(K_RANK, true);
+    launch_rank(h->stream, h->cap, s);
+    rec(K_RANK, false);
+    h->launches += 4;  // scan is two kernels
+  }
   // default: full contact lists (k_detect + warp-flattened k_force); the half
   // lists (Newton's third law) and the paper's fused mapping are ablations
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
@@ -301,7 +356,7 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   } else {
     if (variant >= 2) {
       rec(K_DETECT, true);
-      launch_detect(h->stream, h->cap, h->K, s, h->g);
+      launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r);
       rec(K_DETECT, false);
       h->launches += 1;
     }
@@ -309,7 +364,7 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
     launch_sweep(h->stream, h->cap, h->K, h->p.model, diag, s, h->g, h->ph, variant);
     rec(K_SWEEP, false);
   }
-  h->launches += 5;  // scan is two kernels
+  h->launches += 1;
   if (h->slab) {  // pack and publish the next step's migrants and ghosts
     rec(K_OTHER, true);
     launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xtiles,
@@ -322,13 +377,13 @@ int enqueue_step(dem_handle* h, int b, bool profile) {
   return DEM_OK;
 }
 
-int build_graph(dem_handle* h, int b, int nsteps, cudaGraphExec_t* out) {
+int build_graph(dem_handle* h, int b, int nsteps, cudaGraphExec_t* out, bool full = false) {
   cudaGraph_t graph;
   CUDA_TRY(h, cudaStreamBeginCapture(h->stream, cudaStreamCaptureModeThreadLocal));
   int parity = b;
   int64_t l0 = h->launches;
   for (int k = 0; k < nsteps; ++k) {
-    enqueue_step(h, parity, false);
+    enqueue_step(h, parity, false, full);
     parity ^= 1;
   }
   h->launches = l0;
@@ -386,7 +441,15 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
   h->steps = ctr0 + done;
   // restore the per-step scratch for the good state and clear the record
   CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * h->g.ncells, h->stream));
-  launch_count(h->stream, h->n, h->key[h->cur], h->count, h->prank);
+  // counting sort: the cell counts of the good state; merge mode: the next
+  // step sorts by counting (its k_count counts) since the failed step may have
+  // updated the offsets, SCM and mover list in place
+  if (h->merge) {
+    h->merge_ok = false;
+    CUDA_TRY(h, cudaMemsetAsync(h->mov_n, 0, 2 * sizeof(uint32_t), h->stream));
+  } else {
+    launch_count(h->stream, h->n, h->key[h->cur], h->count, h->prank);
+  }
   CUDA_TRY(h, cudaMemsetAsync(h->scan_status[0], 0, sizeof(unsigned long long) * h->ntiles,
                               h->stream));
   CUDA_TRY(h, cudaMemsetAsync(h->scan_status[1], 0, sizeof(unsigned long long) * h->ntiles,
@@ -396,6 +459,14 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
   clean.step_ctr = (uint32_t)h->steps;
   CUDA_TRY(h, cudaMemcpyAsync(h->err, &clean, sizeof(DevErr), cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
+  if (e.code == 12u) {  // more movers than the merge re-sort takes: redo by counting
+    const int64_t left = nsteps - done;
+    h->full_run = true;
+    int rc = dem_step(h, left);
+    h->full_run = false;
+    if (rc) return rc;
+    return dem_sync(h);
+  }
   int code = -(int)e.code;
   char buf[256];
   snprintf(buf, sizeof buf, "%s: particle id %u (slot %u) in step %lld; state kept at step %lld",
@@ -669,8 +740,14 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     return fail(h, DEM_EINVAL, buf);
   }
   // 3. the CDG (R15): h = cell_edge or 2 r_max (1 + 2^-10); n_a = floor(L_a / h) >= 3
-  float rmax = 0.f;
+  float rmax = 0.f, rmin = 0.f;
   memcpy(&rmax, &hp.rmax_bits, 4);
+  const uint32_t rmin_bits = ~hp.rmin_cbits;
+  memcpy(&rmin, &rmin_bits, 4);
+  // one radius: the candidate test's S² is a constant (slab ranks may receive
+  // migrants of another set, so only a single GPU uses it)
+  h->mono_r = (n > 0 && !h->slab && rmin == rmax && !(h->p.flags & DEM_F_GENERAL_DETECT)) ? rmax
+                                                                                          : 0.f;
   const double hmin = 2.0 * (double)rmax * (1.0 + std::ldexp(1.0, -10));
   double hc = h->p.cell_edge > 0.0f ? (double)h->p.cell_edge : hmin;
   if (hc < hmin || !(hc > 0.0)) {
@@ -800,6 +877,10 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
       ok &= dalloc(h, &h->cpos, N * h->K) && dalloc(h, &h->lcount, N) &&
             dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
             dalloc(h, &h->R1, N * h->K);
+    if (!h->slab)  // merge re-sort buffers (single GPU)
+      ok &= dalloc(h, &h->skey, N) && dalloc(h, &h->mov, kMoverCap) && dalloc(h, &h->mov_n, 2) &&
+            dalloc(h, &h->mv_u32, 7 * kMoverCap) && dalloc(h, &h->mv_i32, 4 * kMoverCap) &&
+            dalloc(h, &h->mv_tab, mv_table_entries(cap) + mv_table_entries(ncells + 1));
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
@@ -878,6 +959,15 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   launch_pack(st, n, in, g, h->pos[0], h->vel[0], h->omg[0], h->key[0], h->count, h->prank, dst,
               keep);
   h->launches += (n > 0) ? 2 : 1;
+  // merge re-sort (single GPU unless DEM_F_FULL_SORT): the first step sorts by
+  // counting with its own k_count, so the cell counts start from zero
+  h->merge = !h->slab && !(h->p.flags & DEM_F_FULL_SORT);
+  h->merge_ok = h->full_run = false;
+  h->full_sorts = 0;
+  if (h->merge) {
+    CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
+    CUDA_TRY(h, cudaMemsetAsync(h->mov_n, 0, 2 * sizeof(uint32_t), st));
+  }
   sweep_prepare(h->K);
   if (h->slab) {
     // 5b. publish the ghosts of the set state for the neighbours' first step
@@ -999,9 +1089,17 @@ int dem_step(dem_handle* h, int64_t nsteps) {
   const int64_t ctr0 = h->pending ? h->pend_ctr0 + h->pend_steps : h->steps;
   const int cur0 = h->cur;
   const bool eager = h->profiling || (h->p.flags & DEM_F_NO_GRAPH);
+  // merge mode: the first step after dem_set_particles (or a roll-back), and
+  // the rest of a call that overflowed the mover capacity, sort by counting
+  int64_t nfull = 0;
+  if (h->merge && (!h->merge_ok || h->full_run)) nfull = h->full_run ? nsteps : 1;
+  if (h->merge) {
+    h->merge_ok = true;
+    h->full_sorts += nfull;
+  }
   if (eager) {
     for (int64_t k = 0; k < nsteps; ++k) {
-      int rc = enqueue_step(h, h->cur, h->profiling);
+      int rc = enqueue_step(h, h->cur, h->profiling, k < nfull);
       if (rc) return rc;
       h->cur ^= 1;
     }
@@ -1018,29 +1116,37 @@ int dem_step(dem_handle* h, int64_t nsteps) {
       h->prof.clear();
     }
   } else {
-    for (int b = 0; b < 2; ++b) {
-      if (!h->g2[b]) {
-        int rc = build_graph(h, b, 2, &h->g2[b]);
-        if (rc) return rc;
+    auto run = [&](int64_t cnt, bool full) -> int {
+      cudaGraphExec_t* G2 = full ? h->gf2 : h->g2;
+      cudaGraphExec_t* G1 = full ? h->gf1 : h->g1;
+      for (int b = 0; b < 2 && cnt > 0; ++b) {
+        if (cnt >= 2 && !G2[b]) {
+          int rc = build_graph(h, b, 2, &G2[b], full);
+          if (rc) return rc;
+        }
+        if ((cnt & 1) && !G1[b]) {
+          int rc = build_graph(h, b, 1, &G1[b], full);
+          if (rc) return rc;
+        }
       }
-      if (!h->g1[b]) {
-        int rc = build_graph(h, b, 1, &h->g1[b]);
-        if (rc) return rc;
+      while (cnt >= 2) {
+        CUDA_TRY(h, cudaGraphLaunch(G2[h->cur], h->stream));
+        h->graph_launches++;
+        h->launches += 2 * kernels_per_step(h, full);
+        cnt -= 2;
       }
-    }
-    int64_t left = nsteps;
-    while (left >= 2) {
-      CUDA_TRY(h, cudaGraphLaunch(h->g2[h->cur], h->stream));
-      h->graph_launches++;
-      h->launches += 2 * kernels_per_step(h);
-      left -= 2;
-    }
-    if (left) {
-      CUDA_TRY(h, cudaGraphLaunch(h->g1[h->cur], h->stream));
-      h->graph_launches++;
-      h->launches += kernels_per_step(h);
-      h->cur ^= 1;
-    }
+      if (cnt) {
+        CUDA_TRY(h, cudaGraphLaunch(G1[h->cur], h->stream));
+        h->graph_launches++;
+        h->launches += kernels_per_step(h, full);
+        h->cur ^= 1;
+      }
+      return DEM_OK;
+    };
+    int rc = run(nfull, true);
+    if (rc) return rc;
+    rc = run(nsteps - nfull, false);
+    if (rc) return rc;
   }
   if (!h->pending) {
     h->pending = true;
@@ -1277,6 +1383,7 @@ int dem_get_stats(dem_handle* h, dem_stats* out) {
   out->launches = h->launches;
   out->graph_launches = h->graph_launches;
   out->force_cfg = h->fcfg;
+  out->full_sorts = (int32_t)h->full_sorts;
   for (int k = 0; k < 8; ++k) {
     out->kernel_ms[k] = h->kernel_ms[k];
     out->kernel_count[k] = h->kernel_count[k];
@@ -1335,6 +1442,12 @@ int dem_analyze(dem_handle* h, dem_analysis* out) {
   out->max_per_cell = (int64_t)a[7];
   out->occupied_cells = (int64_t)a[8];
   for (int k = 0; k < 33; ++k) out->contact_hist[k] = (int64_t)a[9 + k];
+  out->movers = -1;
+  if (h->merge) {
+    uint32_t m = 0;
+    CUDA_TRY(h, cudaMemcpy(&m, h->mov_n, sizeof m, cudaMemcpyDeviceToHost));
+    out->movers = (int64_t)m;
+  }
   return DEM_OK;
 }
 

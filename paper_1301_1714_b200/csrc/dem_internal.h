@@ -70,6 +70,20 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
+// merge re-sort buffers (k_mv_sort, k_mv_perm, k_mv_off; kMoverCap movers)
+struct MergeBuffers {
+  uint32_t* mov;    // slots whose new key differs from skey (listed by the integrator)
+  uint32_t* mov_n;  // [0] movers listed (may exceed the capacity), [1] = mv_m
+  uint32_t* mv_m;   // movers of this step's merge
+  uint32_t *dst, *slot, *key;  // per mover in (key, slot) order: new slot, slot, key
+  uint32_t* evS;    // 2m slot events: 2 pos + (1: mover slot, -1; 0: insertion point, +1)
+  int* evSc;        // running sum of the slot event weights before each event
+  uint32_t* evC;    // 2m cell events (positions)
+  int* evCc;        // running sums
+  int2* tS;         // per k_mv_apply slot block: (first event, running sum there)
+  int2* tC;         // per k_mv_apply cell block
+};
+
 struct StepBuffers {
   const float4* pos_in;
   const float4* vel_in;
@@ -108,7 +122,12 @@ struct StepBuffers {
   unsigned long long* scan_status_next;  // the other parity's (reset during this step)
   uint32_t* scan_ctr_next;
   DevErr* err;
+  // merge re-sort (single GPU): SCM of this step's sorted slots
+  // and the mover buffers (mv.mov == nullptr: counting sort, cell counts)
+  uint32_t* skey;
+  MergeBuffers mv;
 };
+constexpr uint32_t kMoverCap = 4096;  // movers per step the merge re-sort takes (one block)
 
 // ---- slab exchange ------------------------------------------
 // Per rank an exchange region (cudaMalloc, shareable by CUDA IPC) holding, for
@@ -182,6 +201,7 @@ struct PackIn {
 struct Probe {  // validation results of k_probe
   uint32_t bad_radius, bad_mass, nonfinite, outside, bad_id;
   uint32_t rmax_bits, id_max, bad_material;
+  uint32_t rmin_cbits;  // max of ~bits(r): r_min = ~rmin_cbits (zero-initialised like the rest)
 };
 int launch_probe(cudaStream_t st, int64_t n, PackIn in, DevGrid g, Probe* out);
 int launch_pack(cudaStream_t st, int64_t n, PackIn in, DevGrid g, float4* pos, float4* vel,
@@ -199,12 +219,19 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
+// merge re-sort: k_mv_sort, k_mv_perm, k_mv_off in place of
+// the counting sort when the state is in the previous step's sorted order
+int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
+int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
+int64_t mv_table_entries(int64_t count);  // entries of MergeBuffers::tS (count = n), tC (ncells + 1)
 // Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the
 // whole step (the paper's mapping) in a single kernel.
 void sweep_prepare(uint32_t K);  // host: kernel attributes (call outside stream capture)
+// mono_r > 0: every particle has radius mono_r (single GPU), so S² of R14 is one
+// constant and the fp32 candidate test is 3 instructions shorter (same decisions).
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
-                  const DevGrid& g);
+                  const DevGrid& g, float mono_r = 0.f);
 // half-list path (default): k_detect_half, k_pair, k_finish
 int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                        const DevGrid& g);

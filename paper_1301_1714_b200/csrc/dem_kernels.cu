@@ -142,7 +142,10 @@ __global__ void k_probe(int64_t n, PackIn in, DevGrid g, Probe* out) {
       atomicAdd(&out->outside, 1u);
   }
   if (!fin) atomicAdd(&out->nonfinite, 1u);
-  if (r > 0.0f && isfinite(r)) atomicMax(&out->rmax_bits, __float_as_uint(r));
+  if (r > 0.0f && isfinite(r)) {
+    atomicMax(&out->rmax_bits, __float_as_uint(r));
+    atomicMax(&out->rmin_cbits, ~__float_as_uint(r));
+  }
   uint32_t id = in.id ? in.id[i] : (uint32_t)i;
   if (id >= kWallPid0 || (in.nmat > 1 && id >= (1u << kMatShift))) atomicAdd(&out->bad_id, 1u);
   if (in.nmat > 1 && in.material && in.material[i] >= in.nmat) atomicAdd(&out->bad_material, 1u);
@@ -372,7 +375,7 @@ __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const uint32_t* __restrict__ nslots, const DevErr* err) {
+           const uint32_t* __restrict__ nslots, const DevErr* err, uint32_t* __restrict__ skey) {
   pdl_enter();
   // error word, slot count and the first loads go out together (tmp below the
   // capacity n is always in bounds; entries past nslots are ignored)
@@ -406,6 +409,227 @@ __global__ void __launch_bounds__(256)
     for (uint32_t t = a[u]; t < e[u]; ++t) r += (__ldg(&tmp[t]) < s[u]) ? 1u : 0u;
     perm[a[u] + r] = s[u];
     pos_sorted[a[u] + r] = P[u];
+    if (skey) skey[a[u] + r] = c[u];  // SCM, for the next step's merge re-sort
+  }
+}
+
+// ------------------------------------------- merge re-sort -----
+// Between two steps a particle rarely changes cell (|Δx| per step << h), and
+// the state is stored in the previous step's sorted order. So the stable sort
+// of Eq. 11 (ties by current slot, R16) is a merge: the *stayers* (slots whose
+// new key equals the previous SCM there) are already in order; only the few
+// *movers* need sorting, by (new key, slot). With A = the mover slots and, for
+// the i-th mover of that order (key c_i, slot s_i), its insertion point
+// x_i = clamp(s_i, off[c_i], off[c_i+1]) among the stayers (previous offsets:
+// a stayer at slot s precedes mover i exactly when s < x_i, because the
+// previous SCM is non-decreasing in the slot),
+//   stayer s  -> s + #{x_i <= s} - #{a in A, a <= s},
+//   mover i   -> i + x_i - #{a in A, a < x_i},
+//   off'[c]    = off[c] + #{c_i + 1 <= c} - #{a in A, SCM(a) + 1 <= c}.
+// Both deltas are step functions with 2m events; k_mv_sort lists them sorted,
+// with their running sums, so k_mv_perm and k_mv_off look up one block's
+// events once and stream. Bit-identical to the counting sort (the same unique
+// stable permutation). The integrator lists the movers (finish_particle);
+// more than kMoverCap raises code 12 and the host redoes that step (and the
+// rest of the call) with the counting sort.
+
+// first index in a[lo, hi) with a[idx] >= x (a ascending)
+__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t lo, uint32_t hi,
+                                                    uint32_t x) {
+  while (lo < hi) {
+    const uint32_t mid = (lo + hi) >> 1;
+    if (a[mid] < x) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+// One block of 1024 threads, all in shared memory. Outputs: mv_m = m; per
+// mover of the (key, slot) order its destination slot, slot and key; the slot
+// events evS[k] = 2 pos + isA with running sums evSc (sum of the weights
+// before k: +1 insertion point, -1 mover slot) and the cell events evC[k] =
+// pos with running sums evCc; per block of kMvBlock slots / cells of
+// k_mv_apply, the index of its first event and the running sum there (tS,
+// tC). Counts the step (the counting sort's k_tile_sum does otherwise) and
+// resets the mover counter for this step's integrator.
+constexpr uint32_t kMvBlock = 1024;  // slots or cells per k_mv_apply block
+constexpr size_t kMvSortSmem = (size_t)kMoverCap * (8 + 4 * 4 + 2 * 4 * 2);
+
+__global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_t* __restrict__ key,
+                                                  const uint32_t* __restrict__ skey,
+                                                  const uint32_t* __restrict__ off, uint32_t nbS,
+                                                  uint32_t nbC, DevErr* err) {
+  pdl_enter();
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  unsigned long long* sB = reinterpret_cast<unsigned long long*>(smem_raw);  // (key, slot)
+  uint32_t* sA = reinterpret_cast<uint32_t*>(sB + kMoverCap);  // mover slots ascending
+  uint32_t* sAo = sA + kMoverCap;                              // their previous keys (SCM)
+  uint32_t* sP = sAo + kMoverCap;                              // insertion points x_i
+  uint32_t* sBk = sP + kMoverCap;                              // keys of the (key, slot) order
+  uint32_t* sES = sBk + kMoverCap;                             // slot events [2 kMoverCap]
+  uint32_t* sEC = sES + 2 * kMoverCap;                         // cell events [2 kMoverCap]
+  const uint32_t t = threadIdx.x, T = blockDim.x;
+  if (ld_volatile(&err->code) != 0u) return;
+  if (t == 0) atomicAdd(&err->step_ctr, 1u);
+  const uint32_t m = ld_volatile(mb.mov_n);
+  __syncthreads();  // every thread has read the count before it is reset
+  if (m > kMoverCap) {
+    if (t == 0) raise_error(err, 12u, m, 0u);
+    return;
+  }
+  if (t == 0) {
+    *mb.mov_n = 0u;
+    *mb.mv_m = m;
+  }
+  uint32_t P = 1;
+  while (P < m) P <<= 1;
+  for (uint32_t i = t; i < P; i += T) {
+    if (i < m) {
+      const uint32_t sl = mb.mov[i];
+      sA[i] = sl;
+      sB[i] = ((unsigned long long)__ldg(&key[sl]) << 32) | sl;
+    } else {
+      sA[i] = 0xFFFFFFFFu;
+      sB[i] = ~0ull;
+    }
+  }
+  __syncthreads();
+  for (uint32_t k = 2; k <= P; k <<= 1) {  // bitonic: B by (key, slot), A by slot
+    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
+      for (uint32_t i = t; i < P; i += T) {
+        const uint32_t l = i ^ jj;
+        if (l > i) {
+          const bool up = (i & k) == 0;
+          const unsigned long long x = sB[i], y = sB[l];
+          if ((x > y) == up) {
+            sB[i] = y;
+            sB[l] = x;
+          }
+          const uint32_t u = sA[i], v = sA[l];
+          if ((u > v) == up) {
+            sA[i] = v;
+            sA[l] = u;
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+  for (uint32_t i = t; i < m; i += T) {
+    const uint32_t c = (uint32_t)(sB[i] >> 32), si = (uint32_t)sB[i];
+    sBk[i] = c;
+    sAo[i] = __ldg(&skey[sA[i]]);
+    sP[i] = min(max(si, __ldg(&off[c])), __ldg(&off[c + 1]));  // insertion point x_i
+  }
+  __syncthreads();
+  for (uint32_t i = t; i < m; i += T) {  // movers: destinations and their events
+    const uint32_t c = sBk[i], si = (uint32_t)sB[i], x = sP[i];
+    const uint32_t la = lower_bound_u32(sA, 0, m, x);  // #A < x
+    mb.dst[i] = i + x - la;
+    mb.slot[i] = si;
+    mb.key[i] = c;
+    sES[i + la] = 2u * x;  // ties: insertion points before mover slots
+    mb.evSc[i + la] = (int)i - (int)la;
+    const uint32_t lo = lower_bound_u32(sAo, 0, m, c);  // #A with SCM < c
+    sEC[i + lo] = c + 1u;  // ties: key events before SCM events
+    mb.evCc[i + lo] = (int)i - (int)lo;
+  }
+  for (uint32_t k = t; k < m; k += T) {
+    const uint32_t a = sA[k], ao = sAo[k];
+    const uint32_t np = lower_bound_u32(sP, 0, m, a + 1u);   // #x <= a
+    sES[k + np] = 2u * a + 1u;
+    mb.evSc[k + np] = (int)np - (int)k;
+    const uint32_t nb = lower_bound_u32(sBk, 0, m, ao + 1u);  // #keys <= SCM(a)
+    sEC[k + nb] = ao + 1u;
+    mb.evCc[k + nb] = (int)nb - (int)k;
+  }
+  __syncthreads();  // (also makes this block's global writes visible to itself)
+  const uint32_t ne = 2u * m;
+  for (uint32_t k = t; k < ne; k += T) {
+    mb.evS[k] = sES[k];
+    mb.evC[k] = sEC[k];
+  }
+  // per k_mv_apply block: first event and the running sum before it
+  for (uint32_t b = t; b <= nbS; b += T) {
+    const uint32_t k = lower_bound_u32(sES, 0, ne, 2u * b * kMvBlock);
+    mb.tS[b] = make_int2((int)k, k < ne ? mb.evSc[k] : 0);
+  }
+  for (uint32_t b = t; b <= nbC; b += T) {
+    const uint32_t k = lower_bound_u32(sEC, 0, ne, b * kMvBlock + 1u);
+    mb.tC[b] = make_int2((int)k, k < ne ? mb.evCc[k] : 0);
+  }
+}
+
+// k_mv_apply, blocks [0, nbS): new slots of the stayers (4 per thread, a block
+// = kMvBlock consecutive slots) and of the movers (grid-stride): perm (SCCM),
+// positions gathered into sorted order (step 4), SCM for the next step.
+// Blocks [nbS, nbS + nbC): off'[c] = off[c] + (running sum of the cell events
+// at positions <= c), in place, touched only where that sum is not zero
+// (between a mover's old and new cell). The movers' insertion points were
+// taken from the previous offsets by k_mv_sort.
+constexpr int kMvItems = 4;
+__global__ void __launch_bounds__(256)
+    k_mv_apply(uint32_t n, uint32_t ncells, uint32_t nbS, MergeBuffers mb,
+               const uint32_t* __restrict__ key, const float4* __restrict__ pos_in,
+               uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
+               uint32_t* __restrict__ skey, uint32_t* __restrict__ off, const DevErr* err) {
+  pdl_enter();
+  const uint32_t e = ld_volatile(&err->code);
+  const uint32_t m = __ldg(mb.mv_m);
+  if (blockIdx.x >= nbS) {  // offsets
+    const uint32_t b = blockIdx.x - nbS;
+    const int2 t0 = __ldg(&mb.tC[b]);
+    const uint32_t k1 = (uint32_t)__ldg(&mb.tC[b + 1]).x;
+    if (e != 0u || m == 0u) return;
+    if ((uint32_t)t0.x == k1 && t0.y == 0) return;  // no shift anywhere in this block
+#pragma unroll
+    for (int u = 0; u < kMvItems; ++u) {
+      const uint32_t c = b * kMvBlock + u * blockDim.x + threadIdx.x;
+      if (c > ncells) continue;
+      int d = t0.y;
+      for (uint32_t k = (uint32_t)t0.x; k < k1; ++k) {  // this block's events (rare)
+        if (__ldg(&mb.evC[k]) > c) break;
+        d = k + 1 < 2u * m ? __ldg(&mb.evCc[k + 1]) : 0;
+      }
+      if (d != 0) off[c] = (uint32_t)((int)__ldcs(&off[c]) + d);
+    }
+    return;
+  }
+  const uint32_t B0 = blockIdx.x * kMvBlock;
+  uint32_t c[kMvItems];
+  float4 P[kMvItems];
+#pragma unroll
+  for (int u = 0; u < kMvItems; ++u) {
+    const uint32_t s = B0 + u * blockDim.x + threadIdx.x;
+    c[u] = s < n ? __ldg(&key[s]) : 0u;
+    P[u] = s < n ? __ldcs(&pos_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const int2 t0 = __ldg(&mb.tS[blockIdx.x]);
+  const uint32_t k1 = (uint32_t)__ldg(&mb.tS[blockIdx.x + 1]).x;
+  if (e != 0u) return;
+#pragma unroll
+  for (int u = 0; u < kMvItems; ++u) {
+    const uint32_t s = B0 + u * blockDim.x + threadIdx.x;
+    if (s >= n) continue;
+    int d = t0.y;
+    bool mover = false;
+    for (uint32_t k = (uint32_t)t0.x; k < k1; ++k) {  // this block's events (rare)
+      const uint32_t ev = __ldg(&mb.evS[k]);
+      if ((ev >> 1) > s) break;
+      d = k + 1 < 2u * m ? __ldg(&mb.evSc[k + 1]) : 0;
+      mover |= ev == 2u * s + 1u;
+    }
+    if (mover) continue;
+    const uint32_t j = (uint32_t)((int)s + d);
+    perm[j] = s;
+    pos_sorted[j] = P[u];
+    skey[j] = c[u];
+  }
+  for (uint32_t g = blockIdx.x * blockDim.x + threadIdx.x; g < m; g += nbS * blockDim.x) {
+    // mover g of the (key, slot) order
+    const uint32_t j = __ldg(&mb.dst[g]), sm = __ldg(&mb.slot[g]);
+    perm[j] = sm;
+    pos_sorted[j] = __ldg(&pos_in[sm]);
+    skey[j] = __ldg(&mb.key[g]);
   }
 }
 
@@ -575,6 +799,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
                                                 uint32_t oj, const Own& o, f3 F, f3 T,
                                                 uint32_t ncnt, bool overflow, LookupFn lookup) {
   const uint32_t j = oj;  // output slot
+  const uint32_t sk = b.mv.mov ? __ldg(&b.skey[j]) : 0u;  // this step's SCM at j (merge re-sort)
   const float ri = o.P.w, mi = o.V.w;
   const uint32_t my_id = __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
@@ -683,7 +908,20 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
     }
   }
   b.key_out[j] = k2;
-  b.prank[j] = count_into_cell(b.count, k2);  // counted into its cell for the next sort
+  if (b.mv.mov) {  // merge re-sort: list the particles that change cell (warp-aggregated)
+    const uint32_t act = __activemask();
+    const uint32_t mv = __ballot_sync(act, k2 != sk);
+    if (mv) {
+      const uint32_t leader = __ffs(mv) - 1;
+      uint32_t base = 0;
+      if (lane_id() == leader) base = atomicAdd(b.mv.mov_n, (uint32_t)__popc(mv));
+      base = __shfl_sync(act, base, leader);
+      const uint32_t idx = base + (uint32_t)__popc(mv & lanemask_lt());
+      if (k2 != sk && idx < kMoverCap) b.mv.mov[idx] = j;
+    }
+  } else {
+    b.prank[j] = count_into_cell(b.count, k2);  // counted into its cell for the next sort
+  }
 }
 
 // ---- variant 1: one thread per sorted particle for the whole step ---------
@@ -791,15 +1029,19 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // the caller then rescans with EXACT, which settles band candidates in fp64.
 // fl(d² - S²) keeps the sign of d² - S², and outside the band the fp32 and
 // exact decisions agree (in_contact's bound), so both scans give one list.
-template <bool EXACT>
+// MONO: all radii equal, S2c = fl((2r)²) (what the general expression gives
+// for every pair) and the band test |d² - S²| <= 16u S² (exact: 16u = 2^-20)
+// sets `amb` to 0 — the same decisions in three fewer instructions.
+template <bool EXACT, bool MONO = false>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
                                                 int cx, int cy, int cz, uint32_t j, uint32_t N,
-                                                uint32_t K, float& amb) {
+                                                uint32_t K, float& amb, float S2c = 0.f) {
   const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
   const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
   const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
   uint32_t npair = 0;
   uint32_t* out = b.clist + j;
+  float mr = __int_as_float(0x7f800000);  // MONO: min |d² - S²| over the candidates
 #pragma unroll 1
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
@@ -821,9 +1063,13 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
         const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
         const float d2 = dx * dx + dy * dy + dz2 * dz2;
         const float S = P.w + Q.w;
-        const float S2 = S * S;
+        const float S2 = MONO ? S2c : S * S;
         bool hit;
-        if (EXACT) {
+        if (!EXACT && MONO) {
+          const float rr = d2 - S2;
+          hit = rr < 0.f;
+          mr = fminf(mr, fabsf(rr));  // closest to the threshold (band test after the loop)
+        } else if (EXACT) {
           hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
           if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
             const double Sd = (double)P.w + (double)Q.w;
@@ -842,6 +1088,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
       }
     }
   }
+  if (MONO && !EXACT && mr <= S2c * 9.5367431640625e-7f) amb = 0.f;  // ±16u band (16u = 2^-20: exact)
   return npair;
 }
 
@@ -854,8 +1101,9 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
 #ifndef DEM_DETECT_MINB
 #define DEM_DETECT_MINB 6
 #endif
+template <bool MONO>
 __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
-                                                                 uint32_t N, uint32_t K) {
+                                                                 uint32_t N, uint32_t K, float S2c) {
   pdl_enter();
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
   uint32_t jlo, jhi;
@@ -869,7 +1117,7 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
   const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
   const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
   float amb = -1.f;
-  uint32_t npair = detect_scan<false>(b, g, P, cx, cy, cz, j, N, K, amb);
+  uint32_t npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
   if (amb >= 0.f) npair = detect_scan<true>(b, g, P, cx, cy, cz, j, N, K, amb);
   __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
 }
@@ -1413,6 +1661,7 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
 void sweep_prepare(uint32_t K) {
+  cudaFuncSetAttribute(k_mv_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMvSortSmem);
   const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
   const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
   const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -1952,9 +2201,27 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
   launch_pdl(k_rank, (unsigned)((n + per - 1) / per), 256, 0, st, n, b.key_in, b.off, b.tmp, b.perm,
-             b.pos_in, b.pos_sorted, b.nslots, b.err);
+             b.pos_in, b.pos_sorted, b.nslots, b.err, b.skey);
   return K_RANK;
 }
+
+static uint32_t mv_blocks(int64_t count) { return (uint32_t)((count + kMvBlock - 1) / kMvBlock); }
+
+int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
+  launch_pdl(k_mv_sort, 1, 1024, kMvSortSmem, st, b.mv, (const uint32_t*)b.key_in,
+             (const uint32_t*)b.skey, (const uint32_t*)b.off, mv_blocks(n),
+             mv_blocks((int64_t)ncells + 1), b.err);
+  return K_SCATTER;
+}
+
+int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
+  const uint32_t nbS = mv_blocks(n), nbC = mv_blocks((int64_t)ncells + 1);
+  launch_pdl(k_mv_apply, nbS + nbC, 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.key_in, b.pos_in,
+             b.perm, b.pos_sorted, b.skey, b.off, (const DevErr*)b.err);
+  return K_RANK;
+}
+
+int64_t mv_table_entries(int64_t n) { return (int64_t)mv_blocks(n) + 1; }
 
 template <int MODEL, bool DIAG>
 static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
@@ -2025,9 +2292,14 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 }
 
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
-                  const DevGrid& g) {
+                  const DevGrid& g, float mono_r) {
   if (n <= 0) return K_DETECT;
-  launch_pdl(k_detect, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K);
+  if (mono_r > 0.f) {
+    const float S = mono_r + mono_r;
+    launch_pdl(k_detect<true>, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K, S * S);
+  } else {
+    launch_pdl(k_detect<false>, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K, 0.f);
+  }
   return K_DETECT;
 }
 

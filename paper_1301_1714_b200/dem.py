@@ -30,6 +30,8 @@ DEM_F_THREAD_PER_PARTICLE = 32
 DEM_F_HALF_LISTS = 64
 DEM_F_FORCE_DENSE = 128
 DEM_F_FORCE_LIGHT = 256
+DEM_F_GENERAL_DETECT = 512
+DEM_F_FULL_SORT = 1024
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
@@ -73,7 +75,7 @@ class DemStats(C.Structure):
                 ("max_contacts_seen", C.c_int64), ("launches", C.c_int64),
                 ("graph_launches", C.c_int64), ("kernel_ms", C.c_double * 8),
                 ("kernel_count", C.c_int64 * 8), ("force_cfg", C.c_int32),
-                ("reserved", C.c_int32), ("max_speed", C.c_double)]
+                ("full_sorts", C.c_int32), ("max_speed", C.c_double)]
 
 
 class DemAnalysis(C.Structure):
@@ -81,7 +83,7 @@ class DemAnalysis(C.Structure):
                 ("contacts", C.c_int64), ("max_contacts", C.c_int64),
                 ("warp_candidate_slots", C.c_int64), ("warp_contact_slots", C.c_int64),
                 ("max_per_cell", C.c_int64), ("occupied_cells", C.c_int64),
-                ("contact_hist", C.c_int64 * 33)]
+                ("contact_hist", C.c_int64 * 33), ("movers", C.c_int64)]
 
 
 class DemError(RuntimeError):
@@ -433,7 +435,7 @@ class Dem:
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
                     kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
                     force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg],
-                    max_speed=s.max_speed)
+                    full_sorts=s.full_sorts, max_speed=s.max_speed)
 
 
     def analyze(self) -> dict:
@@ -448,6 +450,7 @@ class Dem:
             warp_candidate_slots=a.warp_candidate_slots,
             warp_contact_slots=a.warp_contact_slots, max_per_cell=a.max_per_cell,
             occupied_cells=a.occupied_cells, contact_hist=list(a.contact_hist),
+            movers=a.movers,
             candidates_mean=a.candidates / n, contacts_mean=a.contacts / n,
             # contacts among candidates: the paper's "about a quarter"
             contact_fraction=a.contacts / max(a.candidates, 1),

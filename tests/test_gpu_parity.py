@@ -10,7 +10,8 @@ import pytest
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
 from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
-                                      DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
+                                      DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
+                                      DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
                                       Dem, DemError)
 
@@ -59,9 +60,93 @@ def test_hash_sort_offsets_bit_exact(name):
     assert np.array_equal(key1, orc.hash_cells(p, s1["pos"].astype(np.float64)))
 
 
+# ------------------------------------------ merge re-sort -----
+
+def _check_sorts(d, nsteps, per_call=1):
+    """Eq. 11 (stable, R16) and the lower-bound offsets of every step, taken
+    from the key array before it, against the oracle's definitions."""
+    for _ in range(nsteps // per_call):
+        key0, _, _ = d.get_grid()
+        d.step(per_call)
+        if per_call == 1:
+            _, perm, off = d.get_grid()
+            SCM, SCCM = orc.sort_map(key0)
+            assert np.array_equal(perm, SCCM)
+            assert np.array_equal(off, orc.cell_offsets(SCM, off.shape[0] - 1))
+
+
+@pytest.mark.parametrize("name", ["C1", "C3", "gas"])
+@pytest.mark.parametrize("graph", [True, False])
+def test_merge_resort_bit_exact(name, graph):
+    """After the first step the state is in the last sorted order and only the
+    particles that changed cell are sorted and merged in (k_mv_sort, k_mv_perm,
+    k_mv_off): SCCM and the offsets stay bit-exact every step."""
+    sc = scenes_small()[1] if name == "gas" else S.CONFIGS[name]()
+    d = make(sc, flags=0 if graph else DEM_F_NO_GRAPH)
+    _check_sorts(d, 25)
+    assert d.stats()["full_sorts"] == 1
+
+
+def cell_crossers_scene(n_side=24, gap=3e-8):
+    """n_side³ separated spheres (no contacts, g = 0), each 3e-8 m below a
+    cell face in x and moving +x at 0.01 m/s (2e-8 m per step): none changes
+    cell in step 1, all of them (> 4,096) in step 2, so step 3 has more movers
+    than the merge re-sort takes and must be redone by counting."""
+    p = S.SimParams(gravity=(0.0, 0.0, 0.0))
+    h = 2.0 * S.R * (1.0 + 2.0 ** -10)
+    L = (3 * n_side + 4) * h
+    p = p.replace(box_lo=(0.0, 0.0, 0.0), box_hi=(L, L, L))
+    g = np.stack(np.meshgrid(*[np.arange(n_side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    c = (3 * g + 2).astype(np.float64)
+    pos = (c + 0.5) * h
+    pos[:, 0] = (c[:, 0] + 1.0) * h - gap  # just below the face x = (c + 1) h
+    vel = np.zeros_like(pos)
+    vel[:, 0] = 0.01
+    return S.make_scene("crossers", p, pos.astype(np.float32), vel.astype(np.float32))
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_merge_resort_overflow_fallback(graph):
+    """More movers than kMoverCap: the step is rolled back and redone (with
+    the rest of the call) by the counting sort; the run equals the
+    counting-sort-only run bitwise and the grid stays bit-exact."""
+    sc = cell_crossers_scene()
+    assert sc.n > 4096
+    base = 0 if graph else DEM_F_NO_GRAPH
+    a = make(sc, flags=DEM_F_DIAG | base)
+    b = make(sc, flags=DEM_F_DIAG | base | DEM_F_FULL_SORT)
+    a.step(6)
+    b.step(6)
+    assert a.stats()["full_sorts"] == 5  # step 1, then steps 3-6 of the overflowing call
+    sa, sb = a.get_state(forces=True), b.get_state(forces=True)
+    for k in ("pos", "vel", "omega", "id", "force"):
+        assert np.array_equal(sa[k], sb[k]), k
+    c = make(sc, flags=base)
+    _check_sorts(c, 6)  # one step per call: step 3 overflows, later calls merge again
+    assert c.stats()["full_sorts"] == 2
+
+
+def test_merge_resort_equals_counting_sort_bitwise():
+    """Whole runs with the merge re-sort and with the counting sort every
+    step (DEM_F_FULL_SORT) agree bitwise (C3: settled contacts, migrations
+    between cells every step)."""
+    sc = S.C3()
+    runs = []
+    for f in (0, DEM_F_FULL_SORT):
+        d = make(sc, flags=DEM_F_DIAG | f)
+        d.step(30)
+        runs.append((d.get_state(forces=True), contacts_dict(d), d.get_grid()))
+    for k in ("pos", "vel", "omega", "id", "force", "torque"):
+        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
+    assert runs[0][1].keys() == runs[1][1].keys()
+    for x, y in zip(runs[0][2], runs[1][2]):
+        assert np.array_equal(x, y)
+
+
 # ------------------------------------------------------ T2 one step -------
 
-@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
+@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_GENERAL_DETECT,
+                                     DEM_F_HALF_LISTS,
                                      DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
@@ -117,16 +202,17 @@ def test_one_step_T2_C3_full():
     assert_T2_history(contacts_dict(d), h.as_dict(st.id))
 
 
-def band_pairs_scene(seed=11, m=8):
+def band_pairs_scene(seed=11, m=8, mono=False):
     """m³ isolated pairs at separations S(1 + k 2⁻²³), |k| <= 40 (before the
     fp32 rounding of the positions): ~60 pairs fall inside the ±16u fp32 band
-    of R14, where k_detect must rescan with the exact fp64 predicate."""
+    of R14, where k_detect must rescan with the exact fp64 predicate. mono:
+    every radius r (k_detect's constant-S² test)."""
     rng = np.random.default_rng(seed)
     g = np.stack(np.meshgrid(*[np.arange(m)] * 3, indexing="ij"), -1).reshape(-1, 3)
     a = (g * 4.0 + 2.0) * S.D
     u = rng.normal(size=a.shape)
     u /= np.linalg.norm(u, axis=1, keepdims=True)
-    r = rng.choice([0.5 * S.R, 0.75 * S.R, S.R], size=(a.shape[0], 2))
+    r = rng.choice([S.R] if mono else [0.5 * S.R, 0.75 * S.R, S.R], size=(a.shape[0], 2))
     sep = (r[:, 0] + r[:, 1]) * (1.0 + rng.integers(-40, 41, a.shape[0]) * 2.0 ** -23)
     b = a + u * sep[:, None]
     pos = np.concatenate([a, b]).astype(np.float32)
@@ -136,8 +222,9 @@ def band_pairs_scene(seed=11, m=8):
     return S.make_scene("band_pairs", p, pos, radius=rad)
 
 
-def test_touching_pairs_in_fp32_band():
-    sc = band_pairs_scene()
+@pytest.mark.parametrize("mono", [False, True])
+def test_touching_pairs_in_fp32_band(mono):
+    sc = band_pairs_scene(mono=mono)
     p = orc.make_params(sc.params, sc.radius)
     # the decisions the band has to settle: fp32 d², S² vs the exact fp64 predicate
     n = sc.n // 2
@@ -148,6 +235,7 @@ def test_touching_pairs_in_fp32_band():
     in_band = np.abs(d2f.astype(np.float64) - S2) <= 16 * 2.0 ** -24 * S2
     assert in_band.sum() >= 40 and exact[in_band].any() and not exact[in_band].all()
     for flags in (DEM_F_DIAG | DEM_F_FORCE_DENSE, DEM_F_DIAG | DEM_F_FORCE_LIGHT,
+                  DEM_F_DIAG | DEM_F_GENERAL_DETECT,
                   DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
         d = make(sc, flags=flags)
         st, h = oracle_inputs(d, 16)
@@ -352,6 +440,23 @@ def test_force_configs_bitwise(name):
         assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
     assert runs[0][1].keys() == runs[1][1].keys()
     assert all(np.array_equal(runs[0][1][x], runs[1][1][x]) for x in runs[0][1])
+
+
+@pytest.mark.parametrize("name", ["C1", "C3"])
+def test_mono_detect_bitwise(name):
+    """One radius: k_detect's constant-S² candidate test makes the decisions of
+    the per-pair S = r_i + r_j test (DEM_F_GENERAL_DETECT), so whole runs agree
+    bitwise."""
+    sc = S.CONFIGS[name]()
+    assert np.all(sc.radius == sc.radius[0])
+    runs = []
+    for f in (0, DEM_F_GENERAL_DETECT):
+        d = make(sc, flags=DEM_F_DIAG | f)
+        d.step(8)
+        runs.append((d.get_state(forces=True), contacts_dict(d)))
+    for k in ("pos", "vel", "omega", "id", "force", "torque"):
+        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
+    assert runs[0][1].keys() == runs[1][1].keys()
 
 
 def test_force_config_choice():
