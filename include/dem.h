@@ -201,7 +201,10 @@ typedef struct {
                             particle farther than max_speed * dt (the §5 termination test) */
 } dem_stats;
 
-/* Kernel indices of dem_stats.kernel_ms. */
+/* Kernel indices of dem_stats.kernel_ms. Counting sort: DEM_K_HASH cell
+ * counts (k_count, merge mode's counting steps only), DEM_K_SCAN offsets,
+ * DEM_K_SCATTER, DEM_K_RANK; merge re-sort: DEM_K_SCATTER the movers' sort
+ * (k_mv_sort), DEM_K_RANK the merge and offset shifts (k_mv_apply). */
 enum dem_kernel { DEM_K_HASH = 0, DEM_K_SCAN = 1, DEM_K_SCATTER = 2, DEM_K_RANK = 3,
                   DEM_K_SWEEP = 4 /* contact forces (k_pair, or the fused sweep) */,
                   DEM_K_OTHER = 5 /* slab exchange, introspection */,

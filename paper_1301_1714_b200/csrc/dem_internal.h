@@ -6,7 +6,7 @@
 //   vel_m[b][j]  = (vx, vy, vz, m)                   float4
 //   omg_id[b][j] = (wx, wy, wz, bits(id))            float4
 //   key[b][j]    = CM (cell of this slot's position) u32
-//   hist[b][k*N + j] = (δt_x, δt_y, δt_z, bits(pid)) float4, k < cnt[b][j] <= K
+//   hist[b][j*K + k] = (δt_x, δt_y, δt_z, bits(pid)) float4, k < cnt[b][j] <= K (slot-major)
 // and, per step: prank[N] (rank of a slot inside its cell from the counting
 // atomics), count[ncells] (particles per cell, zero between steps),
 // off[ncells+1] (= exclusive scan of count = lower_bound offsets of SCM),

@@ -106,6 +106,13 @@ __device__ __forceinline__ f3 cross(f3 a, f3 b) {
   return {a.y * b.z - a.z * b.y, a.z * b.x - a.x * b.z, a.x * b.y - a.y * b.x};
 }
 
+// Tangential history (Eq. 7 δ_t) layout: slot-major, entry k of slot j at
+// j K + k, so the contacts of one particle — consecutive lanes of a k_force
+// round — read and write one contiguous run.
+__device__ __forceinline__ size_t hix(uint32_t slot, uint32_t k, uint32_t K) {
+  return (size_t)slot * K + k;
+}
+
 // Approximate MUFU reciprocal / square root (|rel. error| ~ 2^-22): the
 // force arithmetic is fp32 with a 1e-4 parity tolerance, and IEEE div/sqrt
 // expand into slow-path subroutines. Deterministic, so the pair evaluation
@@ -825,7 +832,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
       T = mk(T.x + ri * Tc.x, T.y + ri * Tc.y, T.z + ri * Tc.z);
       if (ncnt < K) {
-        b.hist_out[(size_t)ncnt * N + j] = make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
+        b.hist_out[hix(j, ncnt, K)] = make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
         ++ncnt;
       } else {
         overflow = true;
@@ -944,7 +951,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   const uint32_t n_old = MODEL == 0 ? __ldg(&b.cnt_in[s]) : 0u;
   auto lookup = [&](uint32_t pid) -> f3 {
     for (uint32_t k = 0; k < n_old; ++k) {
-      const float4 h = __ldg(&b.hist_in[(size_t)k * N + s]);
+      const float4 h = __ldg(&b.hist_in[hix(s, k, K)]);
       if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
     }
     return mk(0.f, 0.f, 0.f);
@@ -986,7 +993,7 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
           F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
           T = mk(T.x + o.P.w * Tc.x, T.y + o.P.w * Tc.y, T.z + o.P.w * Tc.z);
           if (ncnt < K) {
-            b.hist_out[(size_t)ncnt * N + (j - jlo)] =
+            b.hist_out[hix(j - jlo, ncnt, K)] =
                 make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid));
             ++ncnt;
           } else {
@@ -1182,15 +1189,15 @@ constexpr int kSweepWarps = 4;
 
 // δ_t,old of partner `pid` in the old list of old slot s (n entries): try
 // index k first, then scan (R10: absent -> 0).
-__device__ __forceinline__ f3 old_history(const float4* __restrict__ hist_in, uint32_t N,
+__device__ __forceinline__ f3 old_history(const float4* __restrict__ hist_in, uint32_t K,
                                           uint32_t s, uint32_t n, uint32_t k, uint32_t pid) {
   if (k < n) {
-    const float4 h = __ldcs(&hist_in[(size_t)k * N + s]);
+    const float4 h = __ldcs(&hist_in[hix(s, k, K)]);
     if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
   }
   for (uint32_t x = 0; x < n; ++x) {
     if (x == k) continue;
-    const float4 h = __ldcs(&hist_in[(size_t)x * N + s]);
+    const float4 h = __ldcs(&hist_in[hix(s, x, K)]);
     if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
   }
   return mk(0.f, 0.f, 0.f);
@@ -1311,7 +1318,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       cp_async16(&pf[32 + lane], &b.vel_in[q]);
       if (MODEL == 0) {
         cp_async16(&pf[64 + lane], &b.omg_in[q]);
-        if (k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[(size_t)k * N + s_slot[ow]]);
+        if (k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[hix(s_slot[ow], k, K)]);
       }
     }
     cp_async_commit();
@@ -1367,10 +1374,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
         if (k < no && __float_as_uint(Hr.w) == pid)
           dold = mk(Hr.x, Hr.y, Hr.z);
         else
-          dold = old_history(b.hist_in, N, s_slot[ow], no, 0xFFFFFFFFu, pid);
+          dold = old_history(b.hist_in, K, s_slot[ow], no, 0xFFFFFFFFu, pid);
         f3 dnew;
         eval_pair_practical<MAT>(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
-        __stcs(&b.hist_out[(size_t)k * N + (j0 - jlo) + ow],
+        __stcs(&b.hist_out[hix((j0 - jlo) + ow, k, K)],
                make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
       } else {
         const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
@@ -1402,7 +1409,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   }
   if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
-    return old_history(b.hist_in, N, s, n_old, n_old, pid);
+    return old_history(b.hist_in, K, s, n_old, n_old, pid);
   };
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
@@ -1538,7 +1545,7 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
     o.V = __ldg(&b.vel_in[si]);
     o.W = MODEL == 0 ? __ldg(&b.omg_in[si]) : z4;
     const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[si]), K) : 0u;
-    const float4 Hk = (MODEL == 0 && k < K) ? __ldcs(&b.hist_in[(size_t)k * N + si]) : z4;
+    const float4 Hk = (MODEL == 0 && k < K) ? __ldcs(&b.hist_in[hix(si, k, K)]) : z4;
     const uint32_t nup_t = (MODEL == 0 && cp < 0xFEu) ? min(__ldcs(&b.ccount[t]), K) : 0u;
     const float4 VQ = __ldg(&b.vel_in[q]);
     const float4 WQ = MODEL == 0 ? __ldg(&b.omg_in[q]) : z4;
@@ -1551,14 +1558,14 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
       const uint32_t pid = __float_as_uint(WQ.w) & ph.idmask;
       const f3 dold = (k < n_old && __float_as_uint(Hk.w) == pid)
                           ? mk(Hk.x, Hk.y, Hk.z)
-                          : old_history(b.hist_in, N, si, n_old, 0xFFFFFFFFu, pid);
+                          : old_history(b.hist_in, K, si, n_old, 0xFFFFFFFFu, pid);
       f3 dnew;
       eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
       // this side's entry (upper part of i's list) and the partner's (lower part)
-      __stcs(&b.hist_out[(size_t)k * N + (i - jlo)],
+      __stcs(&b.hist_out[hix(i - jlo, k, K)],
              make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
       if (cp < 0xFEu && nup_t + cp < K)
-        __stcs(&b.hist_out[(size_t)(nup_t + cp) * N + (t - jlo)],
+        __stcs(&b.hist_out[hix(t - jlo, nup_t + cp, K)],
                make_float4(-dnew.x, -dnew.y, -dnew.z,
                            __uint_as_float(__float_as_uint(o.W.w) & ph.idmask)));
     } else {
@@ -1652,7 +1659,7 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
       if (k0 + u < nup) add(r0[u], r1[u], 1.f);
   }
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
-    return old_history(b.hist_in, N, s, n_old, n_old, pid);
+    return old_history(b.hist_in, K, s, n_old, n_old, pid);
   };
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, min(nup + nlow, K), overflow,
                                lookup);
@@ -1811,7 +1818,7 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
           const uint32_t nc = b.cnt_out[o];
           reinterpret_cast<uint32_t*>(blk + L.mig_cnt)[e] = nc;
           float4* h = reinterpret_cast<float4*>(blk + L.mig_hist) + (size_t)e * K;
-          for (uint32_t k = 0; k < nc; ++k) h[k] = b.hist_out[(size_t)k * N + o];
+          for (uint32_t k = 0; k < nc; ++k) h[k] = b.hist_out[hix(o, k, K)];
         } else {  // ghost: state only
           if (e >= L.ghost_cap) {
             raise_error(b.err, 6u, o, __float_as_uint(W.w));
@@ -1937,7 +1944,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
     const uint32_t nc = min(__ldcv(reinterpret_cast<const uint32_t*>(blk + L.mig_cnt) + e), K);
     const float4* h = reinterpret_cast<const float4*>(blk + L.mig_hist) + (size_t)e * K;
     float4* hist = const_cast<float4*>(b.hist_in);
-    for (uint32_t k = 0; k < nc; ++k) hist[(size_t)k * N + slot] = __ldcv(h + k);
+    for (uint32_t k = 0; k < nc; ++k) hist[hix(slot, k, K)] = __ldcv(h + k);
     const_cast<uint32_t*>(b.cnt_in)[slot] = nc;
   } else {
     P = __ldcv(reinterpret_cast<const float4*>(blk + L.gh_pos) + e);
@@ -1988,7 +1995,7 @@ __global__ void k_emit_contacts(int64_t n, int64_t stride, uint32_t K, const flo
   const uint32_t c = cnt[i], o = base[i];
   const uint32_t me = __float_as_uint(omg[i].w) & idmask;
   for (uint32_t k = 0; k < c && k < K; ++k) {
-    const float4 h = hist[(size_t)k * stride + i];
+    const float4 h = hist[hix(i, k, K)];
     if (id_i) id_i[o + k] = me;
     if (id_j) id_j[o + k] = __float_as_uint(h.w);
     if (dt3) { dt3[3 * (o + k)] = h.x; dt3[3 * (o + k) + 1] = h.y; dt3[3 * (o + k) + 2] = h.z; }
@@ -2020,7 +2027,7 @@ __global__ void k_insert_contacts(int64_t m, int64_t id_bound, int64_t stride, u
   if (s == 0xFFFFFFFFu) return;
   const uint32_t k = atomicAdd(&cnt[s], 1u);
   if (k >= K) { atomicOr(flags, 2u); return; }
-  hist[(size_t)k * stride + s] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
+  hist[hix(s, k, K)] = make_float4(dt3[3 * e], dt3[3 * e + 1], dt3[3 * e + 2],
                                         __uint_as_float(id_j[e]));
 }
 

@@ -746,7 +746,15 @@ def test_profile_mode_times_every_kernel():
     d.profile(True)
     d.step(10)
     st = d.stats()
-    for k in ("scan", "scatter", "rank", "sweep"):
+    for k in ("scatter", "rank", "sweep", "detect"):
         assert st["kernel_count"][k] == 10
         assert st["kernel_ms"][k] > 0
+    # the counting sort (cell counts, scan) runs only in the first step; the
+    # merge re-sort's two kernels are timed as scatter and rank afterwards
+    assert st["kernel_count"]["hash"] == 1 and st["kernel_count"]["scan"] == 1
+    assert st["full_sorts"] == 1
     assert st["steps"] == 10
+    f = make(sc, flags=DEM_F_FULL_SORT)
+    f.profile(True)
+    f.step(10)
+    assert all(f.stats()["kernel_count"][k] == 10 for k in ("scan", "scatter", "rank", "sweep"))
