@@ -227,6 +227,10 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.tmp = h->tmp;
   s.perm = h->perm;
   s.pos_sorted = h->pos_sorted;
+  // one radius on the default path (k_detect<MONO> + k_force): the sorted
+  // positions carry their old slot in .w, so contact lists hold old slots
+  s.sw_r = (h->mono_r > 0.f && !(h->p.flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS)))
+               ? h->mono_r : 0.f;
   s.clist = h->clist;
   s.ccount = h->ccount;
   s.nslots = h->nslots;

@@ -99,6 +99,8 @@ struct StepBuffers {
   uint32_t* tmp;
   uint32_t* perm;
   float4* pos_sorted;  // (x,y,z,r) gathered into SCM order by k_rank (step 4, positions)
+  float sw_r;          // > 0: one radius sw_r and the default path: pos_sorted[j].w holds
+                       // bits(SCCM[j]) instead of r (the contact lists then carry old slots)
   uint32_t* clist;     // contacts found by k_detect: clist[k*N + j] = partner's sorted slot
   uint32_t* ccount;    // number of pair contacts of sorted slot j (K+1: overflow)
   const uint32_t* nslots;  // device: input slots of this step (owned + appended)

@@ -382,7 +382,8 @@ __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const uint32_t* __restrict__ nslots, const DevErr* err, uint32_t* __restrict__ skey) {
+           const uint32_t* __restrict__ nslots, const DevErr* err, uint32_t* __restrict__ skey,
+           bool sw) {
   pdl_enter();
   // error word, slot count and the first loads go out together (tmp below the
   // capacity n is always in bounds; entries past nslots are ignored)
@@ -415,6 +416,7 @@ __global__ void __launch_bounds__(256)
     uint32_t r = 0;
     for (uint32_t t = a[u]; t < e[u]; ++t) r += (__ldg(&tmp[t]) < s[u]) ? 1u : 0u;
     perm[a[u] + r] = s[u];
+    if (sw) P[u].w = __uint_as_float(s[u]);  // one radius: .w carries the old slot
     pos_sorted[a[u] + r] = P[u];
     if (skey) skey[a[u] + r] = c[u];  // SCM, for the next step's merge re-sort
   }
@@ -459,7 +461,8 @@ __device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t 
 // tC). Counts the step (the counting sort's k_tile_sum does otherwise) and
 // resets the mover counter for this step's integrator.
 constexpr uint32_t kMvBlock = 1024;  // slots or cells per k_mv_apply block
-constexpr size_t kMvSortSmem = (size_t)kMoverCap * (8 + 4 * 4 + 2 * 4 * 2);
+constexpr size_t kMvSortSmem = (size_t)kMoverCap * (8 + 4 * 4 + 2 * 4 * 4);
+constexpr uint32_t kMvRankSortMax = 512;  // up to this many movers: rank sort, else bitonic
 
 __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_t* __restrict__ key,
                                                   const uint32_t* __restrict__ skey,
@@ -474,6 +477,8 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
   uint32_t* sBk = sP + kMoverCap;                              // keys of the (key, slot) order
   uint32_t* sES = sBk + kMoverCap;                             // slot events [2 kMoverCap]
   uint32_t* sEC = sES + 2 * kMoverCap;                         // cell events [2 kMoverCap]
+  int* sESc = reinterpret_cast<int*>(sEC + 2 * kMoverCap);      // running sums of the slot
+  int* sECc = sESc + 2 * kMoverCap;                             // and the cell events
   const uint32_t t = threadIdx.x, T = blockDim.x;
   if (ld_volatile(&err->code) != 0u) return;
   if (t == 0) atomicAdd(&err->step_ctr, 1u);
@@ -487,6 +492,31 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     *mb.mov_n = 0u;
     *mb.mv_m = m;
   }
+  if (m <= kMvRankSortMax) {
+    // few movers (the common case): each thread places one element at its
+    // rank among the unsorted ones (keys unique: slots are), in the event
+    // arrays' space, which is free until the events are written
+    unsigned long long* uB = reinterpret_cast<unsigned long long*>(sEC);
+    uint32_t* uA = sES;
+    if (t < m) {
+      const uint32_t sl = mb.mov[t];
+      uA[t] = sl;
+      uB[t] = ((unsigned long long)__ldg(&key[sl]) << 32) | sl;
+    }
+    __syncthreads();
+    if (t < m) {
+      const unsigned long long x = uB[t];
+      const uint32_t a = uA[t];
+      uint32_t rb = 0, ra = 0;
+      for (uint32_t i = 0; i < m; ++i) {  // broadcast shared-memory reads
+        rb += uB[i] < x ? 1u : 0u;
+        ra += uA[i] < a ? 1u : 0u;
+      }
+      sB[rb] = x;
+      sA[ra] = a;
+    }
+    __syncthreads();
+  } else {
   uint32_t P = 1;
   while (P < m) P <<= 1;
   for (uint32_t i = t; i < P; i += T) {
@@ -521,6 +551,7 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
       __syncthreads();
     }
   }
+  }
   for (uint32_t i = t; i < m; i += T) {
     const uint32_t c = (uint32_t)(sB[i] >> 32), si = (uint32_t)sB[i];
     sBk[i] = c;
@@ -535,34 +566,46 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     mb.slot[i] = si;
     mb.key[i] = c;
     sES[i + la] = 2u * x;  // ties: insertion points before mover slots
-    mb.evSc[i + la] = (int)i - (int)la;
+    sESc[i + la] = (int)i - (int)la;
     const uint32_t lo = lower_bound_u32(sAo, 0, m, c);  // #A with SCM < c
     sEC[i + lo] = c + 1u;  // ties: key events before SCM events
-    mb.evCc[i + lo] = (int)i - (int)lo;
+    sECc[i + lo] = (int)i - (int)lo;
   }
   for (uint32_t k = t; k < m; k += T) {
     const uint32_t a = sA[k], ao = sAo[k];
     const uint32_t np = lower_bound_u32(sP, 0, m, a + 1u);   // #x <= a
     sES[k + np] = 2u * a + 1u;
-    mb.evSc[k + np] = (int)np - (int)k;
+    sESc[k + np] = (int)np - (int)k;
     const uint32_t nb = lower_bound_u32(sBk, 0, m, ao + 1u);  // #keys <= SCM(a)
     sEC[k + nb] = ao + 1u;
-    mb.evCc[k + nb] = (int)nb - (int)k;
+    sECc[k + nb] = (int)nb - (int)k;
   }
   __syncthreads();  // (also makes this block's global writes visible to itself)
   const uint32_t ne = 2u * m;
   for (uint32_t k = t; k < ne; k += T) {
     mb.evS[k] = sES[k];
     mb.evC[k] = sEC[k];
+    mb.evSc[k] = sESc[k];
+    mb.evCc[k] = sECc[k];
   }
-  // per k_mv_apply block: first event and the running sum before it
-  for (uint32_t b = t; b <= nbS; b += T) {
-    const uint32_t k = lower_bound_u32(sES, 0, ne, 2u * b * kMvBlock);
-    mb.tS[b] = make_int2((int)k, k < ne ? mb.evSc[k] : 0);
+  // per k_mv_apply block: first event and the running sum before it. Each
+  // thread takes a run of consecutive blocks: one binary search, then a merge.
+  const uint32_t GS = (nbS + T) / T, GC = (nbC + T) / T;
+  {
+    const uint32_t b0 = t * GS, b1 = min(b0 + GS, nbS + 1u);
+    uint32_t k = b0 < b1 ? lower_bound_u32(sES, 0, ne, 2u * b0 * kMvBlock) : 0u;
+    for (uint32_t b = b0; b < b1; ++b) {
+      while (k < ne && sES[k] < 2u * b * kMvBlock) ++k;
+      mb.tS[b] = make_int2((int)k, k < ne ? sESc[k] : 0);
+    }
   }
-  for (uint32_t b = t; b <= nbC; b += T) {
-    const uint32_t k = lower_bound_u32(sEC, 0, ne, b * kMvBlock + 1u);
-    mb.tC[b] = make_int2((int)k, k < ne ? mb.evCc[k] : 0);
+  {
+    const uint32_t b0 = t * GC, b1 = min(b0 + GC, nbC + 1u);
+    uint32_t k = b0 < b1 ? lower_bound_u32(sEC, 0, ne, b0 * kMvBlock + 1u) : 0u;
+    for (uint32_t b = b0; b < b1; ++b) {
+      while (k < ne && sEC[k] < b * kMvBlock + 1u) ++k;
+      mb.tC[b] = make_int2((int)k, k < ne ? sECc[k] : 0);
+    }
   }
 }
 
@@ -578,7 +621,8 @@ __global__ void __launch_bounds__(256)
     k_mv_apply(uint32_t n, uint32_t ncells, uint32_t nbS, MergeBuffers mb,
                const uint32_t* __restrict__ key, const float4* __restrict__ pos_in,
                uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
-               uint32_t* __restrict__ skey, uint32_t* __restrict__ off, const DevErr* err) {
+               uint32_t* __restrict__ skey, uint32_t* __restrict__ off, const DevErr* err,
+               bool sw) {
   pdl_enter();
   const uint32_t e = ld_volatile(&err->code);
   const uint32_t m = __ldg(mb.mv_m);
@@ -628,6 +672,7 @@ __global__ void __launch_bounds__(256)
     if (mover) continue;
     const uint32_t j = (uint32_t)((int)s + d);
     perm[j] = s;
+    if (sw) P[u].w = __uint_as_float(s);  // one radius: .w carries the old slot
     pos_sorted[j] = P[u];
     skey[j] = c[u];
   }
@@ -635,7 +680,9 @@ __global__ void __launch_bounds__(256)
     // mover g of the (key, slot) order
     const uint32_t j = __ldg(&mb.dst[g]), sm = __ldg(&mb.slot[g]);
     perm[j] = sm;
-    pos_sorted[j] = __ldg(&pos_in[sm]);
+    float4 Pm = __ldg(&pos_in[sm]);
+    if (sw) Pm.w = __uint_as_float(sm);
+    pos_sorted[j] = Pm;
     skey[j] = __ldg(&mb.key[g]);
   }
 }
@@ -1039,6 +1086,9 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // MONO: all radii equal, S2c = fl((2r)²) (what the general expression gives
 // for every pair) and the band test |d² - S²| <= 16u S² (exact: 16u = 2^-20)
 // sets `amb` to 0 — the same decisions in three fewer instructions.
+// MONO also means pos_sorted[t].w holds the old slot SCCM[t] (b.sw_r): the
+// list stores that (what k_force reads partner state by) and the radius is
+// b.sw_r.
 template <bool EXACT, bool MONO = false>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
                                                 int cx, int cy, int cz, uint32_t j, uint32_t N,
@@ -1066,7 +1116,9 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
     for (int r = 0; r < 3; ++r) {
 #pragma unroll 1
       for (uint32_t t = t0[r]; t < t1[r]; ++t) {
-        const float4 Q = __ldg(&b.pos_sorted[t]);
+        float4 Q = __ldg(&b.pos_sorted[t]);
+        const uint32_t qs = MONO ? __float_as_uint(Q.w) : t;  // what the list stores
+        if (MONO) Q.w = b.sw_r;
         const float dx = Q.x - P.x, dy = Q.y - P.y, dz2 = Q.z - P.z;
         const float d2 = dx * dx + dy * dy + dz2 * dz2;
         const float S = P.w + Q.w;
@@ -1088,7 +1140,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
           amb = fmaxf(amb, fmaf(S2, 9.5367431640625e-7f, -fabsf(rr)));  // 16u S² - |r|
         }
         if (hit && t != j) {
-          if (npair < K) __stcg(out, t);
+          if (npair < K) __stcg(out, qs);
           out += N;
           ++npair;
         }
@@ -1117,7 +1169,8 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
   owned_range(b, g, N, jlo, jhi);
   const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
   if (j >= jhi) return;
-  const float4 P = __ldg(&b.pos_sorted[j]);
+  float4 P = __ldg(&b.pos_sorted[j]);
+  if (MONO) P.w = b.sw_r;
   if (err != 0u) return;
   // own cell: the step-2 hash of the own position (identical to CM by construction)
   const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
@@ -1125,7 +1178,7 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
   const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
   float amb = -1.f;
   uint32_t npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
-  if (amb >= 0.f) npair = detect_scan<true>(b, g, P, cx, cy, cz, j, N, K, amb);
+  if (amb >= 0.f) npair = detect_scan<true, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
   __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
 }
 
@@ -1186,6 +1239,7 @@ struct WarpSmemLayout {
   }
 };
 constexpr int kSweepWarps = 4;
+constexpr uint32_t kForceKC = 16;  // K with its own k_force instantiation
 
 // δ_t,old of partner `pid` in the old list of old slot s (n entries): try
 // index k first, then scan (R10: absent -> 0).
@@ -1222,10 +1276,13 @@ __device__ __forceinline__ void cp_async_wait() {
   asm volatile("cp.async.wait_group %0;" ::"n"(N_PENDING) : "memory");
 }
 
-template <int MODEL, bool DIAG, int CFG, bool MAT>
+// KC: the list capacity K as a compile-time constant (0: the runtime Kr), so
+// the shared-memory layout and the history addressing fold to constants.
+template <int MODEL, bool DIAG, int CFG, bool MAT, uint32_t KC = 0>
 __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
-    k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t K) {
+    k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t Kr) {
   using C = ForceCfg<CFG>;
+  const uint32_t K = KC ? KC : Kr;
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
@@ -1252,16 +1309,20 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   // ---- own particle (step 4 gather through SCCM) and its contact list. The
   // first four list entries are read before the count is known (entries past
   // the count are never used), so they do not wait for it.
-  const uint32_t s = valid ? __ldcs(&b.perm[j]) : 0u;
+  // one radius (b.sw_r > 0): the sorted position carries the old slot SCCM[j]
+  // in .w and the lists hold partner old slots, so no SCCM gathers at all
+  const bool sw = b.sw_r > 0.f;
+  Own o;
+  o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
   const uint32_t nc = valid ? __ldcs(&b.ccount[j]) : 0u;
   uint32_t t_first[4];
 #pragma unroll
   for (int u = 0; u < 4; ++u) t_first[u] = valid && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
+  const uint32_t s = !valid ? 0u : sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
+  if (sw) o.P.w = valid ? b.sw_r : 1.f;
   if (err != 0u) return;  // warp-uniform (one load per warp instruction)
   const bool overflow = nc > K;
   const uint32_t npair = min(nc, K);
-  Own o;
-  o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
@@ -1297,7 +1358,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
         t4[u] = k0 == 0 ? t_first[u]
                         : (k0 + u < khi ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
 #pragma unroll
-      for (int u = 0; u < 4; ++u) q4[u] = k0 + u < khi ? __ldg(&b.perm[t4[u]]) : 0u;
+      for (int u = 0; u < 4; ++u) q4[u] = k0 + u < khi ? (sw ? t4[u] : __ldg(&b.perm[t4[u]])) : 0u;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
         if (k0 + u < khi) s_cq[C::kChunk ? mybase + k0 + u - c0 : (k0 + u) * 32 + lane] = q4[u];
@@ -1676,7 +1737,9 @@ void sweep_prepare(uint32_t K) {
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false>, A, sd); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, true>, A, sd);  \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false>, A, sl); \
-  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true>, A, sl);
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true>, A, sl); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, kForceKC>, A, sd); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, A, sl);
   DEM_SET_SMEM(0, false)
   DEM_SET_SMEM(0, true)
   DEM_SET_SMEM(1, false)
@@ -2078,7 +2141,8 @@ __global__ void __launch_bounds__(256) k_analyze(StepBuffers b, DevGrid g, uint3
   const bool valid = j < jhi;
   uint32_t cand = 0, cont = 0, pop = 0, first = 0;
   if (valid) {
-    const float4 P = __ldg(&b.pos_sorted[j]);
+    float4 P = __ldg(&b.pos_sorted[j]);
+    if (b.sw_r > 0.f) P.w = b.sw_r;  // (.w holds the old slot then)
     const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
     const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
     const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
@@ -2097,7 +2161,11 @@ __global__ void __launch_bounds__(256) k_analyze(StepBuffers b, DevGrid g, uint3
         // contacts with the exact predicate (R14), independent of which force
         // path ran (the ablations keep no full contact counts)
         for (uint32_t t = t0; t < t1; ++t)
-          if (t != j && in_contact(P, __ldg(&b.pos_sorted[t]))) ++cont;
+          if (t != j) {
+            float4 Q = __ldg(&b.pos_sorted[t]);
+            if (b.sw_r > 0.f) Q.w = b.sw_r;
+            if (in_contact(P, Q)) ++cont;
+          }
       }
     }
     cand -= 1u;  // itself
@@ -2208,7 +2276,7 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
   launch_pdl(k_rank, (unsigned)((n + per - 1) / per), 256, 0, st, n, b.key_in, b.off, b.tmp, b.perm,
-             b.pos_in, b.pos_sorted, b.nslots, b.err, b.skey);
+             b.pos_in, b.pos_sorted, b.nslots, b.err, b.skey, b.sw_r > 0.f);
   return K_RANK;
 }
 
@@ -2224,7 +2292,7 @@ int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffer
 int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
   const uint32_t nbS = mv_blocks(n), nbC = mv_blocks((int64_t)ncells + 1);
   launch_pdl(k_mv_apply, nbS + nbC, 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.key_in, b.pos_in,
-             b.perm, b.pos_sorted, b.skey, b.off, (const DevErr*)b.err);
+             b.perm, b.pos_sorted, b.skey, b.off, (const DevErr*)b.err, b.sw_r > 0.f);
   return K_RANK;
 }
 
@@ -2244,11 +2312,14 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
     const unsigned grid = blocks_for(n, 32 * kSweepWarps), block = 32 * kSweepWarps;
     const bool mat = ph.nmat > 1 || ph.nplates > 0;  // materials/plates: their own instantiation
+    const bool k16 = K == kForceKC;  // the default capacity: compile-time K
     if (cfg == kForceLight) {
       if (mat) launch_pdl(k_force<MODEL, DIAG, kForceLight, true>, grid, block, smem, st, b, g, ph, N, K);
+      else if (k16) launch_pdl(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, grid, block, smem, st, b, g, ph, N, K);
       else launch_pdl(k_force<MODEL, DIAG, kForceLight, false>, grid, block, smem, st, b, g, ph, N, K);
     } else {
       if (mat) launch_pdl(k_force<MODEL, DIAG, kForceDense, true>, grid, block, smem, st, b, g, ph, N, K);
+      else if (k16) launch_pdl(k_force<MODEL, DIAG, kForceDense, false, kForceKC>, grid, block, smem, st, b, g, ph, N, K);
       else launch_pdl(k_force<MODEL, DIAG, kForceDense, false>, grid, block, smem, st, b, g, ph, N, K);
     }
   }

@@ -19,7 +19,7 @@ ncu --set full --clock-control none --import-source on -k regex:"k_force|k_detec
     -o gpurun_out/full_C4_${TAG} -f \
     python bench.py --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 echo "ncu full rc=$?"
-ncu --set full --clock-control none -k regex:"k_scan|k_scatter|k_rank" -s 12 -c 3 \
+ncu --set full --clock-control none -k regex:"k_scan|k_tile|k_scatter|k_rank|k_mv" -s 12 -c 4 \
     -o gpurun_out/sort_C4_${TAG} -f \
     python bench.py --steps 2 --warmup 5 --no-e2e --no-cpu-baseline > /dev/null 2>&1
 echo "ncu sort rc=$?"
