@@ -360,7 +360,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   } else {
     if (variant >= 2) {
       rec(K_DETECT, true);
-      launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r);
+      launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r, variant == 3);
       rec(K_DETECT, false);
       h->launches += 1;
     }

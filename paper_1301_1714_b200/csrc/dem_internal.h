@@ -233,7 +233,7 @@ void sweep_prepare(uint32_t K);  // host: kernel attributes (call outside stream
 // mono_r > 0: every particle has radius mono_r (single GPU), so S² of R14 is one
 // constant and the fp32 candidate test is 3 instructions shorter (same decisions).
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
-                  const DevGrid& g, float mono_r = 0.f);
+                  const DevGrid& g, float mono_r = 0.f, bool light = false);
 // half-list path (default): k_detect_half, k_pair, k_finish
 int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                        const DevGrid& g);

@@ -1157,11 +1157,18 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
 // ascending sorted slot). Few registers, so the SM keeps many warps in flight
 // to hide the neighbour-row latency; the rare particle with a candidate in the
 // fp32 uncertainty band rescans exactly.
+// Two occupancy targets: 6 blocks of 256 (40 registers) and 8 (32 registers,
+// a few spilled). The sparse lists of a light handle (c̄ <= 7: ~26 candidates,
+// ~5 contacts) gain from the extra warps (C4: 160 -> 153 us); the dense C2/C3
+// sets lose 3-8%, so the choice follows the k_force configuration.
 #ifndef DEM_DETECT_MINB
 #define DEM_DETECT_MINB 6
 #endif
-template <bool MONO>
-__global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
+#ifndef DEM_DETECT_MINB_LIGHT
+#define DEM_DETECT_MINB_LIGHT 8
+#endif
+template <bool MONO, bool LIGHT = false>
+__global__ void __launch_bounds__(256, LIGHT ? DEM_DETECT_MINB_LIGHT : DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
                                                                  uint32_t N, uint32_t K, float S2c) {
   pdl_enter();
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
@@ -1204,11 +1211,17 @@ __global__ void __launch_bounds__(256, DEM_DETECT_MINB) k_detect(StepBuffers b, 
 // Both keep each window of two rounds' results in shared memory and let the
 // owners accumulate once per window.
 constexpr int kForceDense = 0, kForceLight = 1;
+#ifndef DEM_LIGHT_MINB
+#define DEM_LIGHT_MINB 8
+#endif
+#ifndef DEM_LIGHT_CHUNK
+#define DEM_LIGHT_CHUNK 256u
+#endif
 template <int CFG>
 struct ForceCfg {
   static constexpr bool kOwnSmem = CFG == kForceLight;
-  static constexpr uint32_t kChunk = CFG == kForceLight ? 256u : 0u;  // 0: per (k, lane)
-  static constexpr int kMinBlocks = CFG == kForceLight ? 8 : 7;
+  static constexpr uint32_t kChunk = CFG == kForceLight ? DEM_LIGHT_CHUNK : 0u;  // 0: per (k, lane)
+  static constexpr int kMinBlocks = CFG == kForceLight ? DEM_LIGHT_MINB : 7;
 };
 constexpr uint32_t kResW = 64;  // contacts per accumulation window (two rounds)
 struct WarpSmemLayout {
@@ -1240,6 +1253,14 @@ struct WarpSmemLayout {
 };
 constexpr int kSweepWarps = 4;
 constexpr uint32_t kForceKC = 16;  // K with its own k_force instantiation
+#ifndef DEM_FORCE_FIRST
+#define DEM_FORCE_FIRST 4
+#endif
+#ifndef DEM_HIST_UNCOND
+#define DEM_HIST_UNCOND 1
+#endif
+constexpr int kForceFirst = DEM_FORCE_FIRST;  // list entries read before the count arrives
+constexpr bool kHistUncond = DEM_HIST_UNCOND != 0;
 
 // δ_t,old of partner `pid` in the old list of old slot s (n entries): try
 // index k first, then scan (R10: absent -> 0).
@@ -1315,9 +1336,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   Own o;
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
   const uint32_t nc = valid ? __ldcs(&b.ccount[j]) : 0u;
-  uint32_t t_first[4];
+  uint32_t t_first[kForceFirst];
 #pragma unroll
-  for (int u = 0; u < 4; ++u) t_first[u] = valid && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
+  for (int u = 0; u < kForceFirst; ++u)
+    t_first[u] = valid && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
   const uint32_t s = !valid ? 0u : sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
   if (sw) o.P.w = valid ? b.sw_r : 1.f;
   if (err != 0u) return;  // warp-uniform (one load per warp instruction)
@@ -1355,7 +1377,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       uint32_t t4[4], q4[4];
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        t4[u] = k0 == 0 ? t_first[u]
+        t4[u] = k0 == 0                       ? t_first[u]
+                : kForceFirst > 4 && k0 == 4 ? t_first[(kForceFirst > 4 ? 4 : 0) + u]
                         : (k0 + u < khi ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
 #pragma unroll
       for (int u = 0; u < 4; ++u) q4[u] = k0 + u < khi ? (sw ? t4[u] : __ldg(&b.perm[t4[u]])) : 0u;
@@ -1379,7 +1402,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       cp_async16(&pf[32 + lane], &b.vel_in[q]);
       if (MODEL == 0) {
         cp_async16(&pf[64 + lane], &b.omg_in[q]);
-        if (k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[hix(s_slot[ow], k, K)]);
+        // (unconditional: k < K is in bounds and the use checks k < n_old, so
+        // the copy does not wait for the owner's history count)
+        if (kHistUncond || k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[hix(s_slot[ow], k, K)]);
       }
     }
     cp_async_commit();
@@ -2370,13 +2395,16 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 }
 
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
-                  const DevGrid& g, float mono_r) {
+                  const DevGrid& g, float mono_r, bool light) {
   if (n <= 0) return K_DETECT;
+  const unsigned grid = blocks_for(n, 256);
   if (mono_r > 0.f) {
     const float S = mono_r + mono_r;
-    launch_pdl(k_detect<true>, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K, S * S);
+    if (light) launch_pdl(k_detect<true, true>, grid, 256, 0, st, b, g, (uint32_t)n, K, S * S);
+    else launch_pdl(k_detect<true>, grid, 256, 0, st, b, g, (uint32_t)n, K, S * S);
   } else {
-    launch_pdl(k_detect<false>, blocks_for(n, 256), 256, 0, st, b, g, (uint32_t)n, K, 0.f);
+    if (light) launch_pdl(k_detect<false, true>, grid, 256, 0, st, b, g, (uint32_t)n, K, 0.f);
+    else launch_pdl(k_detect<false>, grid, 256, 0, st, b, g, (uint32_t)n, K, 0.f);
   }
   return K_DETECT;
 }
