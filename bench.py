@@ -273,10 +273,11 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        from paper_1301_1714_b200.dem import DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE
+        from paper_1301_1714_b200.dem import (DEM_F_FORCE_LANES, DEM_F_HALF_LISTS,
+                                              DEM_F_THREAD_PER_PARTICLE)
         d = Dem(sc.params, device=local, stream=stream, rank=rank, world=world,
                 flags={"full": 0, "half": DEM_F_HALF_LISTS,
-                       "tpp": DEM_F_THREAD_PER_PARTICLE}[args.sweep])
+                       "tpp": DEM_F_THREAD_PER_PARTICLE, "lanes": DEM_F_FORCE_LANES}[args.sweep])
         # every rank passes the whole set; a slab rank keeps its own planes
         d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
         if world > 1:
@@ -362,7 +363,8 @@ def run_ours(args):
             "bound": "hbm",
             "kernel": {"half": "sweep = k_detect_half + k_pair + k_finish",
                        "full": "sweep = k_detect + k_force",
-                       "tpp": "sweep = k_sweep_tpp"}[args.sweep],
+                       "tpp": "sweep = k_sweep_tpp",
+                       "lanes": "sweep = k_detect + k_force_lane"}[args.sweep],
             "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
             "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
@@ -479,7 +481,7 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp"],
+    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes"],
                     help="full contact lists + warp-flattened force rounds (default); half "
                          "lists, each pair once (Newton's third law); or the paper's fused "
                          "thread per particle")

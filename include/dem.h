@@ -93,6 +93,8 @@ enum dem_flags {
   DEM_F_FULL_SORT = 1u << 10, /* ablation: the counting sort every step; default (single GPU):
                                  a merge of the particles that changed cell into the last
                                  sorted order. Bit-identical SCCM and offsets */
+  DEM_F_FORCE_LANES = 1u << 11, /* force-kernel configuration: one thread per particle over its
+                                   contact list (bitwise-identical results) */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
@@ -193,7 +195,7 @@ typedef struct {
   /* per-kernel device time accumulated while profiling (dem_profile) */
   double kernel_ms[8];
   int64_t kernel_count[8];
-  int32_t force_cfg;     /* k_force configuration in use: 0 dense, 1 light, -1 not chosen yet */
+  int32_t force_cfg;     /* force configuration in use: 0 dense, 1 light, 2 lanes, -1 not chosen yet */
   int32_t full_sorts;    /* steps sorted by the counting sort since dem_set_particles: the
                             first, and any in which more than 4,096 particles changed cell;
                             the others merge the few movers into the last sorted order */

@@ -344,6 +344,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   // lists (Newton's third law) and the paper's fused mapping are ablations
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
                       : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
+                      : (h->fcfg == 2)                         ? 4
                       : (h->fcfg == 1)                         ? 3
                                                                : 2;
   if (variant == 0) {  // half lists: detect, pair, finish
@@ -360,7 +361,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   } else {
     if (variant >= 2) {
       rec(K_DETECT, true);
-      launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r, variant == 3);
+      launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r, variant >= 3);
       rec(K_DETECT, false);
       h->launches += 1;
     }
@@ -1069,8 +1070,9 @@ int dem_step(dem_handle* h, int64_t nsteps) {
   }
   if (h->fcfg < 0) {  // choose the k_force configuration
     const uint32_t fl = h->p.flags;
-    if (fl & (DEM_F_FORCE_DENSE | DEM_F_FORCE_LIGHT) || h->p.model != DEM_MODEL_PRACTICAL) {
-      h->fcfg = (fl & DEM_F_FORCE_LIGHT) ? 1 : 0;
+    if (fl & (DEM_F_FORCE_DENSE | DEM_F_FORCE_LIGHT | DEM_F_FORCE_LANES) ||
+        h->p.model != DEM_MODEL_PRACTICAL) {
+      h->fcfg = (fl & DEM_F_FORCE_LANES) ? 2 : (fl & DEM_F_FORCE_LIGHT) ? 1 : 0;
     } else {
       // one eager step in the dense configuration, then the history entries
       // per particle it produced (c̄, walls included) decide the rest

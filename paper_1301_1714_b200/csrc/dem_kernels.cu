@@ -1500,6 +1500,105 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
+// k_force_lane (configuration "lanes"): one thread per sorted particle walks
+// its own compacted contact list (k_detect's, so §6's divergence of contacts
+// among candidates stays out of it; what remains is the spread of list
+// lengths inside a warp: 0.93 of the lanes busy on C4, 0.95 on C3, bench
+// `analysis`). The owner's state stays in its registers — no shuffles, no
+// owner map, no results window — and contact k+1's partner state and
+// predicted δ_t,old entry are in flight (cp.async, double-buffered per
+// thread) while contact k is evaluated; the list entry two ahead is loaded
+// one contact earlier still. Same arithmetic and the same per-owner order
+// as k_force, so the results are bitwise equal to the other configurations.
+#ifndef DEM_LANES_MINB
+#define DEM_LANES_MINB 8
+#endif
+constexpr int kLanesThreads = 128;
+template <int MODEL, bool DIAG, bool MAT, uint32_t KC = 0>
+__global__ void __launch_bounds__(kLanesThreads, DEM_LANES_MINB)
+    k_force_lane(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t Kr) {
+  const uint32_t K = KC ? KC : Kr;
+  pdl_enter();
+  __shared__ float4 pf[2][4][kLanesThreads];  // [buffer][pos, vel, omg, hist][thread]
+  const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
+  uint32_t jlo, jhi;
+  owned_range(b, g, N, jlo, jhi);
+  const uint32_t tid = threadIdx.x;
+  const uint32_t j = jlo + blockIdx.x * kLanesThreads + tid;
+  if (j >= jhi) return;  // (no block-level synchronisation below)
+  const bool sw = b.sw_r > 0.f;
+  Own o;
+  o.P = __ldg(&b.pos_sorted[j]);
+  const uint32_t nc = __ldcs(&b.ccount[j]);
+  // the first two list entries, before the count arrives (entries past the
+  // count are never used)
+  const uint32_t e0 = K > 0 ? __ldcs(&b.clist[j]) : 0u;
+  const uint32_t e1 = K > 1 ? __ldcs(&b.clist[(size_t)N + j]) : 0u;
+  const uint32_t s = sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
+  if (sw) o.P.w = b.sw_r;
+  if (err != 0u) return;
+  const bool overflow = nc > K;
+  const uint32_t npair = min(nc, K);
+  o.V = __ldg(&b.vel_in[s]);
+  o.W = __ldg(&b.omg_in[s]);
+  const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+  // contact k's partner (list entry e) and history entry (s, k) -> buffer k & 1
+  auto issue = [&](uint32_t k, uint32_t e) {
+    const uint32_t q = sw ? e : __ldg(&b.perm[e]);
+    float4(*buf)[kLanesThreads] = pf[k & 1u];
+    cp_async16(&buf[0][tid], &b.pos_in[q]);
+    cp_async16(&buf[1][tid], &b.vel_in[q]);
+    if (MODEL == 0) {
+      cp_async16(&buf[2][tid], &b.omg_in[q]);
+      cp_async16(&buf[3][tid], &b.hist_in[hix(s, k, K)]);  // (k < K: in bounds; checked at use)
+    }
+    cp_async_commit();
+  };
+  // one contact in flight ahead of the one being evaluated (two ahead
+  // measured no faster)
+  if (npair > 0) issue(0, e0);
+  uint32_t en = e1;                                                      // entry of contact k + 1
+  uint32_t enn = npair > 2 ? __ldcs(&b.clist[(size_t)2 * N + j]) : 0u;  // of contact k + 2
+  f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+  for (uint32_t k = 0; k < npair; ++k) {
+    if (k + 1 < npair) {
+      issue(k + 1, en);
+      en = enn;
+      if (k + 3 < npair) enn = __ldcs(&b.clist[(size_t)(k + 3) * N + j]);
+      cp_async_wait<1>();  // contact k's group is complete
+    } else {
+      cp_async_wait<0>();
+    }
+    const float4(*buf)[kLanesThreads] = pf[k & 1u];
+    const float4 Q = buf[0][tid], VQ = buf[1][tid];
+    f3 n;
+    float delta;
+    if (!contact_geometry(o.P, Q, n, delta)) {
+      raise_error(b.err, 9u, j - jlo, __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu));
+    } else if (MODEL == 0) {
+      const float4 WQ = buf[2][tid], Hr = buf[3][tid];
+      const uint32_t pid = __float_as_uint(WQ.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
+      const f3 dold = (k < n_old && __float_as_uint(Hr.w) == pid)
+                          ? mk(Hr.x, Hr.y, Hr.z)
+                          : old_history(b.hist_in, K, s, n_old, 0xFFFFFFFFu, pid);
+      f3 Fc, Tc, dnew;
+      eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+      __stcs(&b.hist_out[hix(j - jlo, k, K)], make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+      T = mk(T.x + Tc.x, T.y + Tc.y, T.z + Tc.z);
+    } else {
+      const f3 u = mk(VQ.x - o.V.x, VQ.y - o.V.y, VQ.z - o.V.z);
+      const f3 Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+      F = mk(F.x + Fc.x, F.y + Fc.y, F.z + Fc.z);
+    }
+  }
+  if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
+  auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
+    return old_history(b.hist_in, K, s, n_old, n_old, pid);
+  };
+  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
+}
+
 // ---- half-list path (default): Newton's third law -------------------------
 // Eq. 3/Eq. 4 with the R1 orientation make the pair force antisymmetric and
 // the unscaled torque n x F_t symmetric, bitwise (P11): F_ji = -F_ij,
@@ -2332,6 +2431,12 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
       launch_pdl(k_sweep_tpp<MODEL, DIAG, true>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
     else
       launch_pdl(k_sweep_tpp<MODEL, DIAG, false>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
+  } else if (variant == 4) {  // full contact lists, one lane per particle
+    const unsigned grid = blocks_for(n, kLanesThreads);
+    const bool mat = ph.nmat > 1 || ph.nplates > 0;
+    if (mat) launch_pdl(k_force_lane<MODEL, DIAG, true>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
+    else if (K == kForceKC) launch_pdl(k_force_lane<MODEL, DIAG, false, kForceKC>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
+    else launch_pdl(k_force_lane<MODEL, DIAG, false>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;

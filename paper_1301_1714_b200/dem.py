@@ -32,6 +32,7 @@ DEM_F_FORCE_DENSE = 128
 DEM_F_FORCE_LIGHT = 256
 DEM_F_GENERAL_DETECT = 512
 DEM_F_FULL_SORT = 1024
+DEM_F_FORCE_LANES = 2048
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
@@ -434,7 +435,7 @@ class Dem:
                     launches=s.launches, graph_launches=s.graph_launches,
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
                     kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
-                    force_cfg={-1: None, 0: "dense", 1: "light"}[s.force_cfg],
+                    force_cfg={-1: None, 0: "dense", 1: "light", 2: "lanes"}[s.force_cfg],
                     full_sorts=s.full_sorts, max_speed=s.max_speed)
 
 

@@ -10,7 +10,7 @@ import pytest
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
 from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
-                                      DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
+                                      DEM_F_FORCE_LANES, DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
                                       DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
                                       Dem, DemError)
@@ -145,8 +145,8 @@ def test_merge_resort_equals_counting_sort_bitwise():
 
 # ------------------------------------------------------ T2 one step -------
 
-@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_GENERAL_DETECT,
-                                     DEM_F_HALF_LISTS,
+@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
+                                     DEM_F_GENERAL_DETECT, DEM_F_HALF_LISTS,
                                      DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
@@ -235,7 +235,7 @@ def test_touching_pairs_in_fp32_band(mono):
     in_band = np.abs(d2f.astype(np.float64) - S2) <= 16 * 2.0 ** -24 * S2
     assert in_band.sum() >= 40 and exact[in_band].any() and not exact[in_band].all()
     for flags in (DEM_F_DIAG | DEM_F_FORCE_DENSE, DEM_F_DIAG | DEM_F_FORCE_LIGHT,
-                  DEM_F_DIAG | DEM_F_GENERAL_DETECT,
+                  DEM_F_DIAG | DEM_F_FORCE_LANES, DEM_F_DIAG | DEM_F_GENERAL_DETECT,
                   DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
         d = make(sc, flags=flags)
         st, h = oracle_inputs(d, 16)
@@ -426,20 +426,22 @@ def test_sweep_variants_agree(other):
 
 @pytest.mark.parametrize("name", ["C2", "gas"])
 def test_force_configs_bitwise(name):
-    """The dense and light k_force configurations differ only in where the
-    owner state and partner slots are staged: same contacts, same arithmetic,
-    same summation order, so whole runs agree bitwise."""
+    """The dense, light and lanes force configurations differ only in how a
+    warp's contacts are dealt to lanes and where owner state and partner slots
+    are staged: same contacts, same arithmetic, same per-owner summation
+    order, so whole runs agree bitwise."""
     sc = S.C2() if name == "C2" else scenes_small()[1]
     runs = []
-    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT):
+    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES):
         d = make(sc, flags=DEM_F_DIAG | f)
         d.step(12)
         runs.append((d.get_state(forces=True), contacts_dict(d), d.stats()["force_cfg"]))
-    assert [r[2] for r in runs] == ["dense", "light"]
-    for k in ("pos", "vel", "omega", "id", "force", "torque"):
-        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
-    assert runs[0][1].keys() == runs[1][1].keys()
-    assert all(np.array_equal(runs[0][1][x], runs[1][1][x]) for x in runs[0][1])
+    assert [r[2] for r in runs] == ["dense", "light", "lanes"]
+    for r in runs[1:]:
+        for k in ("pos", "vel", "omega", "id", "force", "torque"):
+            assert np.array_equal(runs[0][0][k], r[0][k]), k
+        assert runs[0][1].keys() == r[1].keys()
+        assert all(np.array_equal(runs[0][1][x], r[1][x]) for x in runs[0][1])
 
 
 @pytest.mark.parametrize("name", ["C1", "C3"])
@@ -542,8 +544,8 @@ def mixed(M=3, n=3000, seed=7):
                        params=S.SimParams(max_contacts=32))
 
 
-@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
-                                     DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
+                                     DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
 def test_materials_one_step_T2(variant):
     """Each particle pair takes C_n, C_t, α, μ from its two materials and each
     wall contact from the particle's material: T2 against the oracle."""
@@ -624,8 +626,8 @@ def plate_gas(seed=5, n=2500, materials=False):
     return S.random_gas(n, 14.0, seed, **kw)
 
 
-@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS,
-                                     DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
+                                     DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("kind", ["plates", "plates+materials", "slit"])
 def test_plates_one_step_T2(kind, variant):
     """Plate contacts (faces, edges, corners, both sides) bit-exactly the
