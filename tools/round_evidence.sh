@@ -11,6 +11,8 @@ python bench.py --config C2 --model simple --steps 100 --warmup 10 --no-cpu-base
 python bench.py --config C2 --steps 100 --warmup 10 --no-cpu-baseline --no-e2e > gpurun_out/bench_C2practical_${TAG}.json 2>&1
 python bench.py --sweep tpp --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_tpp_${TAG}.json 2>&1
 python bench.py --sweep half --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_half_${TAG}.json 2>&1
+python bench.py --sweep lanes --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_lanes_${TAG}.json 2>&1
+python bench.py --config C5 --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > gpurun_out/bench_C5_${TAG}.json 2>&1
 ncu --metrics gpu__time_duration.sum --clock-control none -s 30 -c 40 --csv \
     --log-file gpurun_out/launches_C4_${TAG}.csv \
     python bench.py --steps 10 --warmup 5 --no-e2e --no-cpu-baseline > /dev/null 2>&1
