@@ -883,7 +883,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
             dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
             dalloc(h, &h->R1, N * h->K);
     if (!h->slab)  // merge re-sort buffers (single GPU)
-      ok &= dalloc(h, &h->skey, N) && dalloc(h, &h->mov, kMoverCap) && dalloc(h, &h->mov_n, 2) &&
+      ok &= dalloc(h, &h->skey, N) && dalloc(h, &h->mov, 3 * kMoverCap) && dalloc(h, &h->mov_n, 2) &&
             dalloc(h, &h->mv_u32, 7 * kMoverCap) && dalloc(h, &h->mv_i32, 4 * kMoverCap) &&
             dalloc(h, &h->mv_tab, mv_table_entries(cap) + mv_table_entries(ncells + 1));
     if (h->slab) {

@@ -72,7 +72,8 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 // merge re-sort buffers (k_mv_sort, k_mv_perm, k_mv_off; kMoverCap movers)
 struct MergeBuffers {
-  uint32_t* mov;    // slots whose new key differs from skey (listed by the integrator)
+  uint32_t* mov;    // [3 kMoverCap]: slots whose new key differs from skey (listed by the
+                    // integrator), then their new keys, then their previous keys
   uint32_t* mov_n;  // [0] movers listed (may exceed the capacity), [1] = mv_m
   uint32_t* mv_m;   // movers of this step's merge
   uint32_t *dst, *slot, *key;  // per mover in (key, slot) order: new slot, slot, key

@@ -480,9 +480,19 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
   int* sESc = reinterpret_cast<int*>(sEC + 2 * kMoverCap);      // running sums of the slot
   int* sECc = sESc + 2 * kMoverCap;                             // and the cell events
   const uint32_t t = threadIdx.x, T = blockDim.x;
-  if (ld_volatile(&err->code) != 0u) return;
-  if (t == 0) atomicAdd(&err->step_ctr, 1u);
+  // the error word, the mover count and (rank-sort path) this thread's mover
+  // entry — slot, new key, previous key, as the integrator listed them — go
+  // out together (entries past the count are in bounds and never used)
+  const uint32_t ecode = ld_volatile(&err->code);
   const uint32_t m = ld_volatile(mb.mov_n);
+  uint32_t msl = 0u, mkn = 0u, mko = 0u;
+  if (t < kMvRankSortMax) {
+    msl = __ldcg(&mb.mov[t]);
+    mkn = __ldcg(&mb.mov[kMoverCap + t]);
+    mko = __ldcg(&mb.mov[2 * kMoverCap + t]);
+  }
+  if (ecode != 0u) return;
+  if (t == 0) atomicAdd(&err->step_ctr, 1u);
   __syncthreads();  // every thread has read the count before it is reset
   if (m > kMoverCap) {
     if (t == 0) raise_error(err, 12u, m, 0u);
@@ -496,24 +506,29 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     // few movers (the common case): each thread places one element at its
     // rank among the unsorted ones (keys unique: slots are), in the event
     // arrays' space, which is free until the events are written
+    // (the insertion point x = clamp(slot, off[c], off[c+1]) depends on the
+    // mover alone, so its loads go out before the sort)
     unsigned long long* uB = reinterpret_cast<unsigned long long*>(sEC);
     uint32_t* uA = sES;
+    uint32_t xi = 0u;
     if (t < m) {
-      const uint32_t sl = mb.mov[t];
-      uA[t] = sl;
-      uB[t] = ((unsigned long long)__ldg(&key[sl]) << 32) | sl;
+      uA[t] = msl;
+      uB[t] = ((unsigned long long)mkn << 32) | msl;
+      xi = min(max(msl, __ldg(&off[mkn])), __ldg(&off[mkn + 1]));
     }
     __syncthreads();
     if (t < m) {
       const unsigned long long x = uB[t];
-      const uint32_t a = uA[t];
       uint32_t rb = 0, ra = 0;
       for (uint32_t i = 0; i < m; ++i) {  // broadcast shared-memory reads
         rb += uB[i] < x ? 1u : 0u;
-        ra += uA[i] < a ? 1u : 0u;
+        ra += uA[i] < msl ? 1u : 0u;
       }
       sB[rb] = x;
-      sA[ra] = a;
+      sBk[rb] = mkn;
+      sP[rb] = xi;
+      sA[ra] = msl;
+      sAo[ra] = mko;
     }
     __syncthreads();
   } else {
@@ -551,7 +566,6 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
       __syncthreads();
     }
   }
-  }
   for (uint32_t i = t; i < m; i += T) {
     const uint32_t c = (uint32_t)(sB[i] >> 32), si = (uint32_t)sB[i];
     sBk[i] = c;
@@ -559,6 +573,7 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     sP[i] = min(max(si, __ldg(&off[c])), __ldg(&off[c + 1]));  // insertion point x_i
   }
   __syncthreads();
+  }
   for (uint32_t i = t; i < m; i += T) {  // movers: destinations and their events
     const uint32_t c = sBk[i], si = (uint32_t)sB[i], x = sP[i];
     const uint32_t la = lower_bound_u32(sA, 0, m, x);  // #A < x
@@ -971,7 +986,11 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       if (lane_id() == leader) base = atomicAdd(b.mv.mov_n, (uint32_t)__popc(mv));
       base = __shfl_sync(act, base, leader);
       const uint32_t idx = base + (uint32_t)__popc(mv & lanemask_lt());
-      if (k2 != sk && idx < kMoverCap) b.mv.mov[idx] = j;
+      if (k2 != sk && idx < kMoverCap) {  // slot, new key, previous key (k_mv_sort)
+        b.mv.mov[idx] = j;
+        b.mv.mov[kMoverCap + idx] = k2;
+        b.mv.mov[2 * kMoverCap + idx] = sk;
+      }
     }
   } else {
     b.prank[j] = count_into_cell(b.count, k2);  // counted into its cell for the next sort
