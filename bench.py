@@ -375,6 +375,13 @@ def run_ours(args):
             "step_frac_of_8TBps": b_step * n_local / (ms_step * 1e-3) / 8e12,
         },
         "kernel_ms_avg": kernel_avg,
+        "kernel_classes": {"hash": "k_count (counting-sort steps after a merge run)",
+                           "scan": "k_tile_sum + k_scan_apply (counting sort)",
+                           "scatter": "k_mv_sort (merge re-sort) or k_scatter (counting sort)",
+                           "rank": "k_mv_apply (merge re-sort) or k_rank (counting sort)",
+                           "detect": "k_detect / k_detect_half",
+                           "sweep": "k_force / k_force_lane / k_pair / k_sweep_tpp",
+                           "finish": "k_finish (half lists)", "other": "slab exchange"},
         "ms_per_step_profiled": ms_step_profiled,
         "timing": ("value/ms_per_step: K-step CUDA-graph replay region (CUDA events on the "
                    "handle's stream); roofline kernel durations: CUDA events around every "
