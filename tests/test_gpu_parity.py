@@ -126,6 +126,27 @@ def test_merge_resort_overflow_fallback(graph):
     assert c.stats()["full_sorts"] == 2
 
 
+@pytest.mark.parametrize("n_side", [7, 10, 15])
+def test_merge_resort_mover_counts(n_side):
+    """All n_side³ spheres change cell in step 2, so step 3 merges 343 movers
+    (k_mv_sort's rank sort, <= 512), 1,000 or 3,375 (its bitonic sort): the
+    grid is bit-exact every step, with no fallback to counting, and the run
+    equals the counting-sort run bitwise."""
+    sc = cell_crossers_scene(n_side=n_side)
+    d = make(sc, flags=0)
+    _check_sorts(d, 2)
+    assert d.analyze()["movers"] == n_side ** 3  # step 2 moved every sphere: step 3 merges them
+    _check_sorts(d, 3)
+    assert d.stats()["full_sorts"] == 1
+    a = make(sc, flags=DEM_F_DIAG)
+    b = make(sc, flags=DEM_F_DIAG | DEM_F_FULL_SORT)
+    a.step(5)
+    b.step(5)
+    sa, sb = a.get_state(forces=True), b.get_state(forces=True)
+    for k in ("pos", "vel", "omega", "id", "force"):
+        assert np.array_equal(sa[k], sb[k]), k
+
+
 def test_merge_resort_equals_counting_sort_bitwise():
     """Whole runs with the merge re-sort and with the counting sort every
     step (DEM_F_FULL_SORT) agree bitwise (C3: settled contacts, migrations
