@@ -1320,6 +1320,11 @@ __device__ __forceinline__ void cp_async16(void* smem_dst, const void* gmem_src)
                "l"(gmem_src)
                : "memory");
 }
+// the same with the shared-memory destination as a 32-bit shared address
+__device__ __forceinline__ void cp_async16_s(uint32_t smem_dst, const void* gmem_src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_dst), "l"(gmem_src)
+               : "memory");
+}
 __device__ __forceinline__ void cp_async_commit() {
   asm volatile("cp.async.commit_group;" ::: "memory");
 }
@@ -1423,19 +1428,20 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
 
   // prefetch of round r0's partner state + predicted δ_t,old entry (the
   // contact's own index in the owner's old list) into the buffer
+  const uint32_t pf_s = smem_u32(pf) + lane * 16u;  // this lane's prefetch slots (shared addr)
   auto prefetch = [&](uint32_t r0) {
     const uint32_t m = r0 + lane;
     if (m < M) {
       const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
       const uint32_t q = C::kChunk ? s_cq[m % C::kChunk] : s_cq[k * 32 + ow];
-      cp_async16(&pf[lane], &b.pos_in[q]);
-      cp_async16(&pf[32 + lane], &b.vel_in[q]);
+      cp_async16_s(pf_s, &b.pos_in[q]);
+      cp_async16_s(pf_s + 32u * 16u, &b.vel_in[q]);
       if (MODEL == 0) {
-        cp_async16(&pf[64 + lane], &b.omg_in[q]);
+        cp_async16_s(pf_s + 64u * 16u, &b.omg_in[q]);
         // (unconditional: k < K is in bounds and the use checks k < n_old, so
         // the copy does not wait for the owner's history count)
-        if (kHistUncond || k < s_nold[ow]) cp_async16(&pf[96 + lane], &b.hist_in[hix(s_slot[ow], k, K)]);
+        if (kHistUncond || k < s_nold[ow]) cp_async16_s(pf_s + 96u * 16u, &b.hist_in[hix(s_slot[ow], k, K)]);
       }
     }
     cp_async_commit();
