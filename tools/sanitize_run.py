@@ -5,8 +5,9 @@ import sys
 
 sys.path.insert(0, ".")
 from paper_1301_1714_b200 import scenes as S  # noqa: E402
-from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT,  # noqa: E402
-                                      DEM_F_HALF_LISTS, DEM_F_NO_GRAPH,
+import numpy as np  # noqa: E402
+from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LANES,  # noqa: E402
+                                      DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS, DEM_F_NO_GRAPH,
                                       DEM_F_THREAD_PER_PARTICLE, Dem)
 
 
@@ -23,8 +24,30 @@ def run(sc, flags, steps=3, material=None):
     d.close()
 
 
-for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE):
+for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_HALF_LISTS,
+          DEM_F_THREAD_PER_PARTICLE):
     run(S.C1(), f)
+
+
+def crossers(n_side, gap=3e-8):
+    """n_side³ separated spheres just below a cell face, moving +x: all change
+    cell in step 2, so step 3's merge re-sort takes n_side³ movers (512: the
+    rank sort of k_mv_sort, 729: its bitonic sort)."""
+    p = S.SimParams(gravity=(0.0, 0.0, 0.0))
+    h = 2.0 * S.R * (1.0 + 2.0 ** -10)
+    L = (3 * n_side + 4) * h
+    p = p.replace(box_lo=(0.0, 0.0, 0.0), box_hi=(L, L, L))
+    g = np.stack(np.meshgrid(*[np.arange(n_side)] * 3, indexing="ij"), -1).reshape(-1, 3)
+    c = (3 * g + 2).astype(np.float64)
+    pos = (c + 0.5) * h
+    pos[:, 0] = (c[:, 0] + 1.0) * h - gap
+    vel = np.zeros_like(pos)
+    vel[:, 0] = 0.01
+    return S.make_scene("crossers", p, pos.astype(np.float32), vel.astype(np.float32))
+
+
+for ns in (8, 9):
+    run(crossers(ns), 0, steps=4)
 run(S.C2(S.SimParams(model="simple")), 0)
 mg = S.mixed_gas(800, 10.0, 2, M=3, params=S.SimParams(max_contacts=32))
 run(mg, DEM_F_FORCE_LIGHT, material=mg.material)
