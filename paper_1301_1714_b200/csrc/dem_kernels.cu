@@ -1242,8 +1242,13 @@ __global__ void __launch_bounds__(256, LIGHT ? DEM_DETECT_MINB_LIGHT : DEM_DETEC
 // Both keep each window of two rounds' results in shared memory and let the
 // owners accumulate once per window.
 constexpr int kForceDense = 0, kForceLight = 1;
+// k_force blocks: DEM_SWEEP_WARPS warps each; resident warps per SM the
+// register budget targets: light 32 (64 registers), dense 28 (72)
+#ifndef DEM_SWEEP_WARPS
+#define DEM_SWEEP_WARPS 1
+#endif
 #ifndef DEM_LIGHT_MINB
-#define DEM_LIGHT_MINB 8
+#define DEM_LIGHT_MINB (32 / DEM_SWEEP_WARPS)
 #endif
 #ifndef DEM_LIGHT_CHUNK
 #define DEM_LIGHT_CHUNK 256u
@@ -1252,7 +1257,7 @@ template <int CFG>
 struct ForceCfg {
   static constexpr bool kOwnSmem = CFG == kForceLight;
   static constexpr uint32_t kChunk = CFG == kForceLight ? DEM_LIGHT_CHUNK : 0u;  // 0: per (k, lane)
-  static constexpr int kMinBlocks = CFG == kForceLight ? DEM_LIGHT_MINB : 7;
+  static constexpr int kMinBlocks = CFG == kForceLight ? DEM_LIGHT_MINB : 28 / DEM_SWEEP_WARPS;
 };
 constexpr uint32_t kResW = 64;  // contacts per accumulation window (two rounds)
 struct WarpSmemLayout {
@@ -1282,7 +1287,7 @@ struct WarpSmemLayout {
     return L;
   }
 };
-constexpr int kSweepWarps = 4;
+constexpr int kSweepWarps = DEM_SWEEP_WARPS;  // warps per k_force block
 constexpr uint32_t kForceKC = 16;  // K with its own k_force instantiation
 #ifndef DEM_FORCE_FIRST
 #define DEM_FORCE_FIRST 4
