@@ -1198,8 +1198,13 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
 #ifndef DEM_DETECT_MINB_LIGHT
 #define DEM_DETECT_MINB_LIGHT 8
 #endif
+// threads per k_detect block; the MINB targets above are in blocks of 256
+#ifndef DEM_DETECT_TPB
+#define DEM_DETECT_TPB 256
+#endif
 template <bool MONO, bool LIGHT = false>
-__global__ void __launch_bounds__(256, LIGHT ? DEM_DETECT_MINB_LIGHT : DEM_DETECT_MINB) k_detect(StepBuffers b, DevGrid g,
+__global__ void __launch_bounds__(DEM_DETECT_TPB, (LIGHT ? DEM_DETECT_MINB_LIGHT : DEM_DETECT_MINB) *
+                                                      256 / DEM_DETECT_TPB) k_detect(StepBuffers b, DevGrid g,
                                                                  uint32_t N, uint32_t K, float S2c) {
   pdl_enter();
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
@@ -2547,14 +2552,15 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                   const DevGrid& g, float mono_r, bool light) {
   if (n <= 0) return K_DETECT;
-  const unsigned grid = blocks_for(n, 256);
+  constexpr unsigned T = DEM_DETECT_TPB;
+  const unsigned grid = blocks_for(n, T);
   if (mono_r > 0.f) {
     const float S = mono_r + mono_r;
-    if (light) launch_pdl(k_detect<true, true>, grid, 256, 0, st, b, g, (uint32_t)n, K, S * S);
-    else launch_pdl(k_detect<true>, grid, 256, 0, st, b, g, (uint32_t)n, K, S * S);
+    if (light) launch_pdl(k_detect<true, true>, grid, T, 0, st, b, g, (uint32_t)n, K, S * S);
+    else launch_pdl(k_detect<true>, grid, T, 0, st, b, g, (uint32_t)n, K, S * S);
   } else {
-    if (light) launch_pdl(k_detect<false, true>, grid, 256, 0, st, b, g, (uint32_t)n, K, 0.f);
-    else launch_pdl(k_detect<false>, grid, 256, 0, st, b, g, (uint32_t)n, K, 0.f);
+    if (light) launch_pdl(k_detect<false, true>, grid, T, 0, st, b, g, (uint32_t)n, K, 0.f);
+    else launch_pdl(k_detect<false>, grid, T, 0, st, b, g, (uint32_t)n, K, 0.f);
   }
   return K_DETECT;
 }
