@@ -56,9 +56,9 @@ struct dem_handle {
   uint32_t *prank = nullptr, *count = nullptr, *off = nullptr, *tmp = nullptr, *perm = nullptr;
   float4* pos_sorted = nullptr;
   uint32_t *clist = nullptr, *ccount = nullptr;
-  // merge re-sort (single GPU): SCM per sorted slot, the integrator's movers,
+  // merge re-sort (single GPU): the integrator's movers,
   // [mover counter, movers this step], movers sorted by (key, slot) and by slot
-  uint32_t *skey = nullptr, *mov = nullptr, *mov_n = nullptr, *mv_u32 = nullptr;
+  uint32_t *mov = nullptr, *mov_n = nullptr, *mv_u32 = nullptr;
   int* mv_i32 = nullptr;
   int2* mv_tab = nullptr;
   bool merge = false;     // merge re-sort in use for this set
@@ -197,7 +197,7 @@ void free_buffers(dem_handle* h) {
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
-  h->skey = h->mov = h->mov_n = h->mv_u32 = nullptr;
+  h->mov = h->mov_n = h->mv_u32 = nullptr;
   h->mv_i32 = nullptr;
   h->mv_tab = nullptr;
   h->cpos = nullptr;
@@ -252,13 +252,11 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.scan_ctr_next = h->scan_ctr + (b ^ 1);
   s.err = h->err;
   if (h->merge) {
-    s.skey = h->skey;
     s.mv.mov = h->mov;
     s.mv.mov_n = h->mov_n;
     s.mv.mv_m = h->mov_n + 1;
     s.mv.dst = h->mv_u32;
     s.mv.slot = h->mv_u32 + kMoverCap;
-    s.mv.key = h->mv_u32 + 2 * kMoverCap;
     s.mv.evS = h->mv_u32 + 3 * kMoverCap;
     s.mv.evC = h->mv_u32 + 5 * kMoverCap;
     s.mv.evSc = h->mv_i32;
@@ -883,7 +881,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
             dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
             dalloc(h, &h->R1, N * h->K);
     if (!h->slab)  // merge re-sort buffers (single GPU)
-      ok &= dalloc(h, &h->skey, N) && dalloc(h, &h->mov, 3 * kMoverCap) && dalloc(h, &h->mov_n, 2) &&
+      ok &= dalloc(h, &h->mov, 3 * kMoverCap) && dalloc(h, &h->mov_n, 2) &&
             dalloc(h, &h->mv_u32, 7 * kMoverCap) && dalloc(h, &h->mv_i32, 4 * kMoverCap) &&
             dalloc(h, &h->mv_tab, mv_table_entries(cap) + mv_table_entries(ncells + 1));
     if (h->slab) {

@@ -72,11 +72,12 @@ constexpr int kScanTile = kScanThreads * kScanItems;
 
 // merge re-sort buffers (k_mv_sort, k_mv_perm, k_mv_off; kMoverCap movers)
 struct MergeBuffers {
-  uint32_t* mov;    // [3 kMoverCap]: slots whose new key differs from skey (listed by the
-                    // integrator), then their new keys, then their previous keys
+  uint32_t* mov;    // [3 kMoverCap]: slots whose new key differs from the key of their
+                    // sorted position (listed by the integrator), then their new keys,
+                    // then their previous keys
   uint32_t* mov_n;  // [0] movers listed (may exceed the capacity), [1] = mv_m
   uint32_t* mv_m;   // movers of this step's merge
-  uint32_t *dst, *slot, *key;  // per mover in (key, slot) order: new slot, slot, key
+  uint32_t *dst, *slot;  // per mover in (key, slot) order: new slot, slot
   uint32_t* evS;    // 2m slot events: 2 pos + (1: mover slot, -1; 0: insertion point, +1)
   int* evSc;        // running sum of the slot event weights before each event
   uint32_t* evC;    // 2m cell events (positions)
@@ -125,9 +126,8 @@ struct StepBuffers {
   unsigned long long* scan_status_next;  // the other parity's (reset during this step)
   uint32_t* scan_ctr_next;
   DevErr* err;
-  // merge re-sort (single GPU): SCM of this step's sorted slots
-  // and the mover buffers (mv.mov == nullptr: counting sort, cell counts)
-  uint32_t* skey;
+  // merge re-sort (single GPU): the mover buffers
+  // (mv.mov == nullptr: counting sort, cell counts)
   MergeBuffers mv;
 };
 constexpr uint32_t kMoverCap = 4096;  // movers per step the merge re-sort takes (one block)

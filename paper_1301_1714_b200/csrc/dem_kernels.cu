@@ -382,8 +382,7 @@ __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const uint32_t* __restrict__ nslots, const DevErr* err, uint32_t* __restrict__ skey,
-           bool sw) {
+           const uint32_t* __restrict__ nslots, const DevErr* err, bool sw) {
   pdl_enter();
   // error word, slot count and the first loads go out together (tmp below the
   // capacity n is always in bounds; entries past nslots are ignored)
@@ -418,7 +417,6 @@ __global__ void __launch_bounds__(256)
     perm[a[u] + r] = s[u];
     if (sw) P[u].w = __uint_as_float(s[u]);  // one radius: .w carries the old slot
     pos_sorted[a[u] + r] = P[u];
-    if (skey) skey[a[u] + r] = c[u];  // SCM, for the next step's merge re-sort
   }
 }
 
@@ -465,7 +463,6 @@ constexpr size_t kMvSortSmem = (size_t)kMoverCap * (8 + 4 * 4 + 2 * 4 * 4);
 constexpr uint32_t kMvRankSortMax = 512;  // up to this many movers: rank sort, else bitonic
 
 __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_t* __restrict__ key,
-                                                  const uint32_t* __restrict__ skey,
                                                   const uint32_t* __restrict__ off, uint32_t nbS,
                                                   uint32_t nbC, DevErr* err) {
   pdl_enter();
@@ -532,15 +529,18 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     }
     __syncthreads();
   } else {
+  // A sorted as (slot, previous key) pairs in the slot events' space (free
+  // until the events are written), so each mover keeps its SCM beside it
+  unsigned long long* uA = reinterpret_cast<unsigned long long*>(sES);
   uint32_t P = 1;
   while (P < m) P <<= 1;
   for (uint32_t i = t; i < P; i += T) {
     if (i < m) {
       const uint32_t sl = mb.mov[i];
-      sA[i] = sl;
+      uA[i] = ((unsigned long long)sl << 32) | mb.mov[2 * kMoverCap + i];
       sB[i] = ((unsigned long long)__ldg(&key[sl]) << 32) | sl;
     } else {
-      sA[i] = 0xFFFFFFFFu;
+      uA[i] = ~0ull;
       sB[i] = ~0ull;
     }
   }
@@ -556,10 +556,10 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
             sB[i] = y;
             sB[l] = x;
           }
-          const uint32_t u = sA[i], v = sA[l];
+          const unsigned long long u = uA[i], v = uA[l];
           if ((u > v) == up) {
-            sA[i] = v;
-            sA[l] = u;
+            uA[i] = v;
+            uA[l] = u;
           }
         }
       }
@@ -569,7 +569,8 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
   for (uint32_t i = t; i < m; i += T) {
     const uint32_t c = (uint32_t)(sB[i] >> 32), si = (uint32_t)sB[i];
     sBk[i] = c;
-    sAo[i] = __ldg(&skey[sA[i]]);
+    sA[i] = (uint32_t)(uA[i] >> 32);
+    sAo[i] = (uint32_t)uA[i];
     sP[i] = min(max(si, __ldg(&off[c])), __ldg(&off[c + 1]));  // insertion point x_i
   }
   __syncthreads();
@@ -579,7 +580,6 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
     const uint32_t la = lower_bound_u32(sA, 0, m, x);  // #A < x
     mb.dst[i] = i + x - la;
     mb.slot[i] = si;
-    mb.key[i] = c;
     sES[i + la] = 2u * x;  // ties: insertion points before mover slots
     sESc[i + la] = (int)i - (int)la;
     const uint32_t lo = lower_bound_u32(sAo, 0, m, c);  // #A with SCM < c
@@ -634,9 +634,9 @@ __global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_
 constexpr int kMvItems = 4;
 __global__ void __launch_bounds__(256)
     k_mv_apply(uint32_t n, uint32_t ncells, uint32_t nbS, MergeBuffers mb,
-               const uint32_t* __restrict__ key, const float4* __restrict__ pos_in,
+               const float4* __restrict__ pos_in,
                uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
-               uint32_t* __restrict__ skey, uint32_t* __restrict__ off, const DevErr* err,
+               uint32_t* __restrict__ off, const DevErr* err,
                bool sw, bool split) {
   pdl_enter();
   // block b: slots [b kMvBlock, (b+1) kMvBlock) if b < nbS and cells
@@ -650,7 +650,6 @@ __global__ void __launch_bounds__(256)
   const uint32_t e = ld_volatile(&err->code);
   const uint32_t m = __ldg(mb.mv_m);
   const uint32_t B0 = b * kMvBlock;
-  uint32_t c[kMvItems];
   float4 P[kMvItems];
   int2 tS0 = make_int2(0, 0), tC0 = make_int2(0, 0);
   uint32_t kS1 = 0u, kC1 = 0u;
@@ -658,7 +657,6 @@ __global__ void __launch_bounds__(256)
 #pragma unroll
     for (int u = 0; u < kMvItems; ++u) {
       const uint32_t s = B0 + u * blockDim.x + threadIdx.x;
-      c[u] = s < n ? __ldg(&key[s]) : 0u;
       P[u] = s < n ? __ldcs(&pos_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
     }
     tS0 = __ldg(&mb.tS[b]);
@@ -687,7 +685,6 @@ __global__ void __launch_bounds__(256)
       perm[j] = s;
       if (sw) P[u].w = __uint_as_float(s);  // one radius: .w carries the old slot
       pos_sorted[j] = P[u];
-      skey[j] = c[u];
     }
   }
   for (uint32_t g = b * blockDim.x + threadIdx.x; g < m; g += gridDim.x * blockDim.x) {
@@ -697,7 +694,6 @@ __global__ void __launch_bounds__(256)
     float4 Pm = __ldg(&pos_in[sm]);
     if (sw) Pm.w = __uint_as_float(sm);
     pos_sorted[j] = Pm;
-    skey[j] = __ldg(&mb.key[g]);
   }
   // offsets, in place, only where a shift is non-zero
   if (!cells || m == 0u || ((uint32_t)tC0.x == kC1 && tC0.y == 0)) return;
@@ -880,7 +876,9 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
                                                 uint32_t oj, const Own& o, f3 F, f3 T,
                                                 uint32_t ncnt, bool overflow, LookupFn lookup) {
   const uint32_t j = oj;  // output slot
-  const uint32_t sk = b.mv.mov ? __ldg(&b.skey[j]) : 0u;  // this step's SCM at j (merge re-sort)
+  // this step's SCM at j (merge re-sort): the key of the sorted position itself
+  // (the sort ordered these very coordinates by it), so no SCM array is kept
+  const uint32_t sk = b.mv.mov ? cell_key(g, o.P.x, o.P.y, o.P.z) : 0u;
   const float ri = o.P.w, mi = o.V.w;
   const uint32_t my_id = __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
@@ -2447,7 +2445,7 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
   launch_pdl(k_rank, (unsigned)((n + per - 1) / per), 256, 0, st, n, b.key_in, b.off, b.tmp, b.perm,
-             b.pos_in, b.pos_sorted, b.nslots, b.err, b.skey, b.sw_r > 0.f);
+             b.pos_in, b.pos_sorted, b.nslots, b.err, b.sw_r > 0.f);
   return K_RANK;
 }
 
@@ -2455,7 +2453,7 @@ static uint32_t mv_blocks(int64_t count) { return (uint32_t)((count + kMvBlock -
 
 int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
   launch_pdl(k_mv_sort, 1, 1024, kMvSortSmem, st, b.mv, (const uint32_t*)b.key_in,
-             (const uint32_t*)b.skey, (const uint32_t*)b.off, mv_blocks(n),
+             (const uint32_t*)b.off, mv_blocks(n),
              mv_blocks((int64_t)ncells + 1), b.err);
   return K_SCATTER;
 }
@@ -2465,8 +2463,8 @@ int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffe
   // both parts in one block when the grid spans several waves (no tail of
   // near-empty offset blocks: C4 36 -> 29 us); separate blocks under a wave
   const bool split = nbS + nbC <= 148u * 6u;
-  launch_pdl(k_mv_apply, split ? nbS + nbC : (nbS > nbC ? nbS : nbC), 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.key_in, b.pos_in,
-             b.perm, b.pos_sorted, b.skey, b.off, (const DevErr*)b.err, b.sw_r > 0.f, split);
+  launch_pdl(k_mv_apply, split ? nbS + nbC : (nbS > nbC ? nbS : nbC), 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.pos_in,
+             b.perm, b.pos_sorted, b.off, (const DevErr*)b.err, b.sw_r > 0.f, split);
   return K_RANK;
 }
 
