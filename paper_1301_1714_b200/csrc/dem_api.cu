@@ -1362,6 +1362,12 @@ int dem_get_grid(dem_handle* h, int64_t cap, uint32_t* key, uint32_t* perm, uint
   if (off && cap < (int64_t)h->g.ncells + 1) return fail(h, DEM_EINVAL, "capacity too small");
   cudaStream_t st = h->stream;
   if (key && n) CUDA_TRY(h, cudaMemcpyAsync(key, h->key[h->cur], 4 * n, cudaMemcpyDeviceToHost, st));
+  // merge re-sort with one radius: SCCM lives in the sorted positions' .w
+  // (k_mv_apply does not write perm on that path)
+  if (perm && n && h->merge && step_buffers(h, h->cur).sw_r > 0.f) {
+    launch_perm_from_w(st, n, h->pos_sorted, h->perm);
+    CUDA_TRY(h, cudaGetLastError());
+  }
   if (perm && n) CUDA_TRY(h, cudaMemcpyAsync(perm, h->perm, 4 * n, cudaMemcpyDeviceToHost, st));
   if (off)
     CUDA_TRY(h, cudaMemcpyAsync(off, h->off, 4 * ((size_t)h->g.ncells + 1),

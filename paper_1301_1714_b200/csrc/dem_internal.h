@@ -226,6 +226,7 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
 // the counting sort when the state is in the previous step's sorted order
 int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
 int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
+int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uint32_t* perm);
 int64_t mv_table_entries(int64_t count);  // entries of MergeBuffers::tS (count = n), tC (ncells + 1)
 // Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the

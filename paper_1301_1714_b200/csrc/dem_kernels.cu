@@ -682,17 +682,19 @@ __global__ void __launch_bounds__(256)
       }
       if (mover) continue;
       const uint32_t j = (uint32_t)((int)s + d);
-      perm[j] = s;
-      if (sw) P[u].w = __uint_as_float(s);  // one radius: .w carries the old slot
+      // one radius: .w carries the old slot, and nothing on that path reads
+      // perm (dem_get_grid extracts it from .w), so it is not written
+      if (sw) P[u].w = __uint_as_float(s);
+      else perm[j] = s;
       pos_sorted[j] = P[u];
     }
   }
   for (uint32_t g = b * blockDim.x + threadIdx.x; g < m; g += gridDim.x * blockDim.x) {
     // mover g of the (key, slot) order
     const uint32_t j = __ldg(&mb.dst[g]), sm = __ldg(&mb.slot[g]);
-    perm[j] = sm;
     float4 Pm = __ldg(&pos_in[sm]);
     if (sw) Pm.w = __uint_as_float(sm);
+    else perm[j] = sm;
     pos_sorted[j] = Pm;
   }
   // offsets, in place, only where a shift is non-zero
@@ -1168,7 +1170,9 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
           hit = rr < 0.f;
           amb = fmaxf(amb, fmaf(S2, 9.5367431640625e-7f, -fabsf(rr)));  // 16u S² - |r|
         }
-        if (hit && t != j) {
+        // only the middle row (y = cy) can hold slot j itself: the other two
+        // rows skip the self test (r is unrolled, so it folds away there)
+        if (hit && (r != 1 || t != j)) {
           if (npair < K) __stcg(out, qs);
           out += N;
           ++npair;
@@ -2466,6 +2470,19 @@ int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffe
   launch_pdl(k_mv_apply, split ? nbS + nbC : (nbS > nbC ? nbS : nbC), 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.pos_in,
              b.perm, b.pos_sorted, b.off, (const DevErr*)b.err, b.sw_r > 0.f, split);
   return K_RANK;
+}
+
+// SCCM from the sorted positions' .w (one-radius path, where k_mv_apply
+// keeps the old slot there instead of writing perm): dem_get_grid only
+__global__ void k_perm_from_w(int64_t n, const float4* __restrict__ pos_sorted,
+                              uint32_t* __restrict__ perm) {
+  const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (j < n) perm[j] = __float_as_uint(pos_sorted[j].w);
+}
+
+int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uint32_t* perm) {
+  if (n > 0) k_perm_from_w<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(n, pos_sorted, perm);
+  return 0;
 }
 
 int64_t mv_table_entries(int64_t n) { return (int64_t)mv_blocks(n) + 1; }
