@@ -1115,8 +1115,10 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // fl(d² - S²) keeps the sign of d² - S², and outside the band the fp32 and
 // exact decisions agree (in_contact's bound), so both scans give one list.
 // MONO: all radii equal, S2c = fl((2r)²) (what the general expression gives
-// for every pair) and the band test |d² - S²| <= 16u S² (exact: 16u = 2^-20)
-// sets `amb` to 0 — the same decisions in three fewer instructions.
+// for every pair); a candidate is decided with the EXACT scan's own fp32
+// thresholds — touching below S²(1 - 16u), apart from S²(1 + 16u) on — and one
+// in between sets `amb` to 0, so outside the band both scans decide alike and
+// a non-touching candidate costs a single compare.
 // MONO also means pos_sorted[t].w holds the old slot SCCM[t] (b.sw_r): the
 // list stores that (what k_force reads partner state by) and the radius is
 // b.sw_r.
@@ -1129,7 +1131,10 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
   const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
   uint32_t npair = 0;
   uint32_t* out = b.clist + j;
-  float mr = __int_as_float(0x7f800000);  // MONO: min |d² - S²| over the candidates
+  // MONO fast scan: candidates with d² < S²(1 + 16u) take the hit branch, and
+  // those of them above S²(1 - 16u) are in the band (the EXACT scan's own
+  // thresholds), so a non-touching candidate costs one compare
+  const float S2lo = S2c * 0.99999904632568359375f, S2hi = S2c * 1.00000095367431640625f;
 #pragma unroll 1
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
@@ -1156,9 +1161,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
         const float S2 = MONO ? S2c : S * S;
         bool hit;
         if (!EXACT && MONO) {
-          const float rr = d2 - S2;
-          hit = rr < 0.f;
-          mr = fminf(mr, fabsf(rr));  // closest to the threshold (band test after the loop)
+          hit = d2 < S2hi;  // (the band test is in the hit branch below)
         } else if (EXACT) {
           hit = d2 <= S2 * 0.99999904632568359375f;  // (1 - 16u) S²: clearly touching
           if (!hit && d2 < S2 * 1.00000095367431640625f) {  // inside the band: exact (R14)
@@ -1173,6 +1176,12 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
         // only the middle row (y = cy) can hold slot j itself: the other two
         // rows skip the self test (r is unrolled, so it folds away there)
         if (hit && (r != 1 || t != j)) {
+          if (!EXACT && MONO) {
+            // band: the caller rescans exactly. volatile keeps the test in this
+            // branch (if-converted, it would cost every candidate two instructions)
+            asm volatile("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f00000000, %3, p;}"
+                         : "=f"(amb) : "f"(d2), "f"(S2lo), "f"(amb));
+          }
           if (npair < K) __stcg(out, qs);
           out += N;
           ++npair;
@@ -1180,7 +1189,6 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
       }
     }
   }
-  if (MONO && !EXACT && mr <= S2c * 9.5367431640625e-7f) amb = 0.f;  // ±16u band (16u = 2^-20: exact)
   return npair;
 }
 
