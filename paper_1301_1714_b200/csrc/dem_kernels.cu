@@ -1534,6 +1534,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       __syncwarp();
       // each owner adds its contacts of this window, in candidate order
       const uint32_t lo = max(mybase, w0), hi = min(mybase + npair, r0 + 32);
+#pragma unroll 4
       for (uint32_t x = lo; x < hi; ++x) {
         const float4 r4 = s_r4[x - w0];
         F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
