@@ -67,10 +67,10 @@ __device__ void raise_error(DevErr* e, uint32_t code, uint32_t slot, uint32_t id
 // R15: c_a = clamp(floor((x_a - lo_a) * inv_h), 0, n_a - 1). __dsub_rn and
 // __dmul_rn keep it two correctly rounded operations.
 __device__ __forceinline__ int cell_coord(float x, double lo, double inv_h, int n) {
-  double t = floor(__dmul_rn(__dsub_rn((double)x, lo), inv_h));
-  t = fmax(t, 0.0);
-  t = fmin(t, (double)(n - 1));
-  return (int)t;
+  // floor and int conversion in one cvt.rmi (saturating; NaN -> 0), then the
+  // clamp in integers: the same cell as flooring and clamping in fp64
+  const int c = __double2int_rd(__dmul_rn(__dsub_rn((double)x, lo), inv_h));
+  return min(max(c, 0), n - 1);
 }
 
 // Local cell key of a position: global (cx, cy, cz) of R15, z shifted to the
