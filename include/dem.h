@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define DEM_ABI_VERSION 2u
+#define DEM_ABI_VERSION 3u
 
 /* Error codes. */
 enum dem_error {
@@ -50,7 +50,7 @@ enum dem_error {
   DEM_EABI = -2,        /* params->abi_version != DEM_ABI_VERSION */
   DEM_ENOMEM = -3,      /* device allocation failed */
   DEM_ECUDA = -4,       /* a CUDA runtime call failed (dem_last_error has the text) */
-  DEM_ENCCL = -5,       /* an NCCL call failed (multi-GPU) */
+  DEM_ENCCL = -5,       /* reserved (no NCCL on the data path: the slab exchange is CUDA IPC) */
   DEM_EOVERFLOW = -6,   /* a particle had more than max_contacts contacts (history
                            capacity K). The step is rejected: the state and history stay
                            at the last completed step. */
@@ -72,7 +72,7 @@ enum dem_model {
 
 enum dem_flags {
   DEM_F_TRUNCATE_DT = 1u << 0, /* R4: δ_t = -(F_t' + η v_t)/k_t when Eq. 5 caps F_t */
-  DEM_F_CLAMP_FN = 1u << 1,    /* R3: Eq. 5 uses max(0, repulsive part of F_n)      */
+  DEM_F_CLAMP_FN = 1u << 1,    /* R3 flag: no tensile F_n (Eq. 4), so |F_n| >= 0 in Eq. 5 */
   DEM_F_DIAG = 1u << 2,        /* keep per-particle F and T of the last step (dem_get_state) */
   DEM_F_ASYNC = 1u << 3,       /* dem_step does not synchronise; errors surface at the next
                                   synchronising call */
@@ -134,13 +134,13 @@ typedef struct {
   float wall_friction;
   float k_sp, k_da, k_sh;    /* simple model (Eq. 1) [N/m, N s/m, N s/m] */
   float cell_edge;           /* CDG cell edge h; 0 -> 2 r_max (1 + 2^-10) in fp64 (R15) */
-  uint32_t max_contacts;     /* history capacity K per particle; 0 -> 16 */
+  uint32_t max_contacts;     /* history capacity K per particle; 0 -> 16; <= 64 (else DEM_EINVAL;
+                                <= 32 with DEM_F_HALF_LISTS) */
   uint32_t flags;            /* enum dem_flags */
   int32_t device;            /* CUDA ordinal; -1 -> current device */
   void* stream;              /* cudaStream_t; NULL -> a stream owned by the handle */
   const dem_allocator* allocator; /* NULL -> cudaMallocAsync on the stream */
   int32_t rank, world_size;  /* world_size <= 1: single GPU; > 1: z-slab rank */
-  const void* nccl_id;       /* unused (slab exchange is over CUDA IPC peer memory) */
   /* Eqs. 5, 8-10 write C_k, α (and μ) as functions of the pair (i, j)
    * (PAPER.md:85-93). n_materials <= 1: the scalars above for every pair.
    * 2 <= n_materials <= 16: material_pairs (host, [M][M][4] = C_n, C_t, α, μ,
@@ -324,10 +324,6 @@ int dem_exchange_ptr(dem_handle* h, void** out);
 int dem_connect(dem_handle* h, const void* left64, const void* right64);
 /* Same-process neighbours: their dem_exchange_ptr values (NULL at the ends). */
 int dem_connect_ptrs(dem_handle* h, void* left, void* right);
-
-/* Fill out128 with a new ncclUniqueId (unused: the slab exchange uses CUDA IPC
- * peer memory; returns DEM_ENCCL). */
-int dem_nccl_unique_id(void* out128);
 
 const char* dem_strerror(int code);
 /* Text of the last error on this handle (includes particle id and step for

@@ -58,7 +58,7 @@ enum {
 
 enum {
   ORC_F_TRUNCATE_DT = 1u, /* reading R4: Cundall-Strack truncation when capped */
-  ORC_F_CLAMP_FN = 2u,    /* reading R3: |F_n| of Eq. 5 uses max(0, repulsive part) */
+  ORC_F_CLAMP_FN = 2u,    /* reading R3 flag: no tensile F_n (Eq. 4 normal part >= 0 along -n) */
   ORC_F_BRUTE = 1u << 16, /* oracle-only: all-pairs O(N^2) detection instead of the CDG */
 };
 
@@ -322,12 +322,13 @@ void orc_pair_practical(const double* n, double delta, double Rstar, double msta
     Fn[a] = -kn * delta * n[a] - eta * (vnm * n[a]);
     Ft[a] = -kt * dt_new[a] - eta * vt[a];
   }
-  double fn_mag = norm3(Fn);
-  if (flags & ORC_F_CLAMP_FN) {
-    /* reading R3: only the repulsive part of F_n bounds friction */
-    double rep = -dot3(Fn, n);
-    fn_mag = rep > 0.0 ? rep : 0.0;
+  if ((flags & ORC_F_CLAMP_FN) && kn * delta + eta * vnm < 0.0) {
+    /* reading R3 flag: the contact cannot pull, so a tensile
+     * F_n (damping outweighing the spring while separating) is set to 0; |F_n|
+     * of Eq. 5 is then 0 as well */
+    for (int a = 0; a < 3; ++a) Fn[a] = 0.0;
   }
+  double fn_mag = norm3(Fn);
   int capped = orc_friction_cap(Ft, fn_mag, mu); /* Eq. 5 */
   if (capped && (flags & ORC_F_TRUNCATE_DT) && kt > 0.0) {
     /* reading R4 (flag): Cundall-Strack, δ_t = -(F_t' + η v_t)/k_t */

@@ -491,6 +491,11 @@ int validate_params(const dem_params* p) {
   for (float v : nonneg)
     if (!(v >= 0.0f) || !std::isfinite(v)) return DEM_EINVAL;
   if (p->cell_edge < 0.0f || !std::isfinite(p->cell_edge)) return DEM_EINVAL;
+  // list capacity K: at most kMaxContacts (a warp's contacts are indexed in
+  // 16 bits, list indices in a byte); the half-list ablation packs its lower
+  // lists as (slot << 5 | index), so it needs K <= 32
+  if (p->max_contacts > kMaxContacts) return DEM_EINVAL;
+  if ((p->flags & DEM_F_HALF_LISTS) && p->max_contacts > 32) return DEM_EINVAL;
   if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
   if (p->n_plates > 10 || (p->n_plates && !p->plates)) return DEM_EINVAL;
   for (uint32_t k = 0; k < p->n_plates; ++k) {  // unit normal, unit axis in the plane, extents
@@ -1549,11 +1554,6 @@ int dem_connect_ptrs(dem_handle* h, void* left, void* right) {
   h->connected = true;
   destroy_graphs(h);
   return DEM_OK;
-}
-
-int dem_nccl_unique_id(void* out128) {
-  (void)out128;
-  return fail(nullptr, DEM_ENCCL, "multi-GPU slabs are not built into this library yet");
 }
 
 }  // extern "C"

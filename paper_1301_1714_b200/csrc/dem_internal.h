@@ -19,6 +19,7 @@
 namespace dem {
 
 constexpr uint32_t kWallPid0 = 0xFFFFFFF0u;
+constexpr uint32_t kMaxContacts = 64;  // largest list capacity K dem_create accepts
 
 struct DevGrid {
   int nx, ny, nz;    // local grid (nz = planes held by this rank, ghosts included)

@@ -734,15 +734,16 @@ __device__ __forceinline__ void pair_practical(f3 n, float delta, float Rs, floa
              -knd * n.z - eta * (vn * n.z));  // Eq. 4, normal
   f3 Ft = mk(-kt * dnew.x - eta * vt.x, -kt * dnew.y - eta * vt.y,
              -kt * dnew.z - eta * vt.z);  // Eq. 4, tangential
-  float fn = fsqrt(dot(Fn, Fn));
-  if (flags & 2u) {  // DEM_F_CLAMP_FN (R3)
-    float rep = -dot(Fn, n);
-    fn = rep > 0.f ? rep : 0.f;
-  }
+  // DEM_F_CLAMP_FN (R3 flag): no tensile normal force. knd and η (v·n) are
+  // the same numbers from either side of the pair, so the decision is too (P11)
+  if ((flags & 2u) && knd + eta * vn < 0.f) Fn = mk(0.f, 0.f, 0.f);
+  const float fn = fsqrt(dot(Fn, Fn));
   const float ft2 = dot(Ft, Ft);
   const float lim = mu * fn;
   if (ft2 > lim * lim) {  // Eq. 5: |F_t| > μ|F_n|
-    const float sc = lim * frcp(fsqrt(ft2));
+    // (ft2 held at >= FLT_MIN: the .ftz sqrt would flush a subnormal ft2 to 0
+    // and lim * rcp(0) be inf, or NaN for lim = 0 — μ = 0 or a clamped F_n)
+    const float sc = lim * frcp(fsqrt(fmaxf(ft2, 1.17549435e-38f)));
     Ft = mk(Ft.x * sc, Ft.y * sc, Ft.z * sc);
     if ((flags & 1u) && kt > 0.f) {  // DEM_F_TRUNCATE_DT (R4)
       const float ik = frcp(kt);
@@ -787,10 +788,12 @@ __device__ __forceinline__ bool in_contact(float4 P, float4 Q) {
 // overlap δ = S - D evaluated as (S² - d²)/(S + D) with the numerator in fp64
 // (S² is exact in fp64; d² has the fixed order of R14) — the cancellation of
 // S - D is in exact-ish fp64, the division in fp32. Symmetric in (i, j).
-// Returns false for coincident centres (d² = 0, R18).
+// Returns false for coincident centres (R18): d² = 0, or d² below FLT_MIN,
+// whose fp32 value the .ftz square root would flush (|Δ| < 1.1e-19 m, only
+// reachable for centres within ~1e-12 m of the coordinate origin; DESIGN R18).
 __device__ __forceinline__ bool contact_geometry(float4 P, float4 Q, f3& n, float& delta) {
   const double d2 = exact_d2(P, Q);
-  if (d2 == 0.0) return false;
+  if (!(d2 >= 1.17549435082228751e-38)) return false;
   const double S = (double)P.w + (double)Q.w;
   const float num = (float)__dsub_rn(__dmul_rn(S, S), d2);
   const float D = fsqrt((float)d2);

@@ -20,7 +20,7 @@ import numpy as np
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
 
-DEM_ABI_VERSION = 2
+DEM_ABI_VERSION = 3
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
 DEM_EOVERFLOW, DEM_ENONFINITE, DEM_EESCAPED, DEM_ECOINCIDENT, DEM_ESTATE = -6, -7, -8, -9, -10
 DEM_EPEER = -11
@@ -57,7 +57,7 @@ class DemParams(C.Structure):
                 ("cell_edge", _f), ("max_contacts", C.c_uint32), ("flags", C.c_uint32),
                 ("device", C.c_int32), ("stream", C.c_void_p),
                 ("allocator", C.POINTER(DemAllocator)), ("rank", C.c_int32),
-                ("world_size", C.c_int32), ("nccl_id", C.c_void_p),
+                ("world_size", C.c_int32),
                 ("n_materials", C.c_uint32), ("material_pairs", C.c_void_p),
                 ("material_walls", C.c_void_p), ("n_plates", C.c_uint32),
                 ("plates", C.c_void_p)]
@@ -117,7 +117,6 @@ def lib() -> C.CDLL:
         L.dem_get_stats.argtypes = [VP, C.POINTER(DemStats)]
         L.dem_profile.argtypes = [VP, I32]
         L.dem_analyze.argtypes = [VP, C.POINTER(DemAnalysis)]
-        L.dem_nccl_unique_id.argtypes = [VP]
         L.dem_exchange_handle.argtypes = [VP, P]
         L.dem_exchange_ptr.argtypes = [VP, C.POINTER(VP)]
         L.dem_connect.argtypes = [VP, P, P]

@@ -47,13 +47,29 @@ def ode_restitution(alpha):
     return -s.y_events[0][0][1], s.t_events[0][0]
 
 
-def run_head_on(orc, alpha, v0, steps_per_tc=1000):
+def ode_restitution_clamped(alpha):
+    """The same ODE with the contact unable to pull (reading R3 flag, SURVEY
+    §8(c) A3): x'' = -max(0, x^{3/2} + α x^{1/4} x'). Returns (e, τ_c)."""
+    def f(t, y):
+        x = max(y[0], 0.0)
+        return [y[1], -max(0.0, alpha * x**0.25 * y[1] + x**1.5)]
+
+    def hit(t, y):
+        return y[0]
+    hit.terminal, hit.direction = True, -1
+    s = solve_ivp(f, [0, 50], [0.0, 1.0], events=hit, rtol=1e-12, atol=1e-14, method="DOP853",
+                  first_step=1e-6)
+    return -s.y_events[0][0][1], s.t_events[0][0]
+
+
+def run_head_on(orc, alpha, v0, steps_per_tc=1000, clamp_fn=False):
     m = float(S.sphere_mass([S.R])[0])
     mstar = m / 2
     K = float(np.float32(7.326e6)) * math.sqrt(float(np.float32(S.R)) / 2)
     tc_scale = (mstar / K) ** 0.4 * v0**-0.2
     dt = float(np.float32(3.218 * tc_scale / steps_per_tc))
-    sc = S.two_body(v0, S.SimParams(damping=alpha, friction=0.5, dt=dt), gap=0.0)
+    sc = S.two_body(v0, S.SimParams(damping=alpha, friction=0.5, dt=dt, clamp_fn=clamp_fn),
+                    gap=0.0)
     p = orc.make_params(sc.params, sc.radius)
     st, h = orc.State.from_scene(sc), orc.History.empty(2, 8)
     steps, dmax = 0, 0.0
@@ -100,6 +116,28 @@ def test_restitution_anchor_values():
     assert e0 == pytest.approx(1.0, abs=1e-9)
     assert tau0 == pytest.approx(2 * 0.4 * beta(0.4, 0.5) * 1.25**0.4, rel=1e-9)
     assert ode_restitution(0.2522)[0] == pytest.approx(0.70, abs=1e-3)
+
+
+# e(α) with F_n clamped >= 0, computed independently of this
+# repository (DOP853 at rtol 1e-12)
+E_CLAMPED = {0.1: 0.872291, 0.3: 0.677805, 0.5: 0.539421, 1.0: 0.330500}
+
+
+@pytest.mark.parametrize("alpha", sorted(E_CLAMPED))
+def test_clamped_restitution(orc, alpha):
+    """Reading R3 flag (DEM_F_CLAMP_FN): no tensile normal force. The
+    restitution is the clamped ODE's (SURVEY Appendix values), higher than
+    the literal model's; the literal run at the same α keeps the ODE value
+    without the clamp, so a dropped or inverted clamp fails one of the two."""
+    e_ode, tau = ode_restitution_clamped(alpha)
+    assert e_ode == pytest.approx(E_CLAMPED[alpha], abs=2e-6)
+    assert e_ode > ode_restitution(alpha)[0] + 0.003
+    for v0 in (0.01, 1.0):
+        e, tc, _, scale, _, _, dt = run_head_on(orc, alpha, v0, clamp_fn=True)
+        assert e == pytest.approx(e_ode, rel=2e-3)
+        assert tc == pytest.approx(tau * scale, abs=2 * dt)
+    e_lit = run_head_on(orc, alpha, 0.1, clamp_fn=False)[0]
+    assert e_lit == pytest.approx(ode_restitution(alpha)[0], rel=2e-3)
 
 
 # ------------------------------------------------------- P8 static stack --
@@ -165,6 +203,115 @@ def test_wall_contact_impulse_invariant(orc):
         Fn = r.F[0, 1]
         Ft = math.hypot(r.F[0, 0], r.F[0, 2])
         assert Ft == pytest.approx(p.wmu * abs(Fn), rel=1e-9)
+
+
+# --------------------------- tangential stiffness C_{k,t} (Eqs. 3, 6-9) ---
+
+def hertz_rest(load, Cn, Rstar):
+    """Static overlap of a Hertz contact carrying `load`: k_n δ = C_n sqrt(R* δ) δ
+    = load (P8's closed form)."""
+    return (load / (Cn * math.sqrt(Rstar))) ** (2 / 3)
+
+
+def test_stuck_sphere_tangential_oscillation(orc):
+    """A sphere resting on the floor (α = 0, static overlap of P8) is given a
+    small horizontal velocity v0. Friction holds (|F_t| < μ|F_n|), so the
+    contact point's slip s obeys m s'' = -(1 + m r^2/I) k_t s with I = 0.4 m r^2
+    (Newton for v and ω, Eqs. 3, 6, 7), k_t = C_t sqrt(δ r) (Eq. 9, wall R* = r):
+    v(t) = v0 (5/7 + (2/7) cos Ωt), Ω^2 = 3.5 k_t / m. With C_t = 3 C_n a swap of
+    C_n and C_t changes Ω by 3^{2/3}."""
+    m = float(S.sphere_mass([S.R])[0])
+    sp = S.SimParams(damping=0.0, stiffness_t=3 * 7.326e6, dt=1e-7)
+    p0 = orc.make_params(sp, np.array([S.R], np.float32))
+    g, r = -p0.g[1], float(np.float32(S.R))
+    d0 = hertz_rest(m * g, p0.wCn, r)
+    L = 8 * S.D
+    v0 = 1e-4
+    sc = S.make_scene("stuck", sp.replace(box_hi=(L, L, L)),
+                      [[0.5 * L, r - d0, 0.5 * L]], vel=[[v0, 0, 0]])
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(1, 8)
+    assert p.wCt == pytest.approx(3 * p.wCn, rel=1e-7)
+    kt = p.wCt * math.sqrt(d0 * r)
+    Om = math.sqrt(3.5 * kt / st.mass[0])
+    n = int(3 * 2 * math.pi / Om / p.dt)
+    v = np.empty(n)
+    for k in range(n):
+        res = orc.step(p, st, h)
+        assert math.hypot(res.F[0, 0], res.F[0, 2]) < p.wmu * abs(res.F[0, 1])  # stuck
+        v[k] = st.vel[0, 0]
+    t = p.dt * np.arange(1, n + 1)
+    model = v0 * (5 / 7 + 2 / 7 * np.cos(Om * t))
+    assert np.abs(v - model).max() <= 2e-3 * v0
+    # spin: angular momentum about the contact point, I ω_z - m r v, is
+    # conserved (every force passes through that point or the centre above
+    # it), so ω_z = -(5/2)(v0 - v)/r
+    v0f = float(sc.vel[0, 0])  # the fp32 input
+    assert st.omega[0, 2] == pytest.approx(-2.5 * (v0f - st.vel[0, 0]) / r, rel=1e-6, abs=1e-12)
+    # the same run with C_t = C_n is measurably different (the pin has teeth)
+    sp2 = sp.replace(stiffness_t=7.326e6, box_hi=(L, L, L))
+    sc2 = S.make_scene("stuck", sp2, [[0.5 * L, r - d0, 0.5 * L]], vel=[[v0, 0, 0]])
+    p2 = orc.make_params(sc2.params, sc2.radius)
+    st2, h2 = orc.State.from_scene(sc2), orc.History.empty(1, 8)
+    for k in range(n // 6):
+        orc.step(p2, st2, h2)
+    assert abs(st2.vel[0, 0] - model[n // 6 - 1]) > 0.2 * v0
+
+
+def test_stuck_stack_tangential_modes(orc):
+    """Two spheres stacked on the floor (A below, B on top; α = 0, static
+    overlaps of P8), B given a horizontal velocity v0. Both contacts stick, so
+    the small-motion dynamics are linear: per sphere m v' = ΣF_x, I ω_z' = ΣT_z,
+    and each contact's slip rate (Eq. 6, n vertical) and tangential spring
+    (Eqs. 7, 9) give F = -k s. Particle pair: k_p = C_t sqrt(δ_p r/2) (Eq. 9,
+    R* = r/2), wall: k_w = C_t,w sqrt(δ_w r). The oracle's trajectory must
+    follow expm(A t) of that 6x6 linear system; C_t = 3 C_n for pairs and
+    C_t,w = 2 C_n for the wall, so swapping C_n and C_t in either the pair or
+    the wall composition moves a mode frequency by > 25%."""
+    from scipy.linalg import expm
+    m = float(S.sphere_mass([S.R])[0])
+    Cn = 7.326e6
+    sp = S.SimParams(damping=0.0, stiffness_t=3 * Cn, wall_stiffness_t=2 * Cn, dt=1e-7)
+    p0 = orc.make_params(sp, np.array([S.R], np.float32))
+    g, r = -p0.g[1], float(np.float32(S.R))
+    dw = hertz_rest(2 * m * g, p0.wCn, r)
+    dp = hertz_rest(m * g, p0.Cn, r / 2)
+    L = 8 * S.D
+    yA = r - dw
+    yB = yA + 2 * r - dp
+    v0 = 1e-4
+    sc = S.make_scene("stack2", sp.replace(box_hi=(L, L, L)),
+                      [[0.5 * L, yA, 0.5 * L], [0.5 * L, yB, 0.5 * L]], vel=[[0, 0, 0], [v0, 0, 0]])
+    p = orc.make_params(sc.params, sc.radius)
+    st, h = orc.State.from_scene(sc), orc.History.empty(2, 8)
+    mA = st.mass[0]
+    I = 0.4 * mA * r * r
+    kw = p.wCt * math.sqrt(dw * r)
+    kp = p.Ct * math.sqrt(dp * r / 2)
+    # y = (vA, wA, vB, wB, s_w, s_p); contact normals vertical (n = -y from the
+    # upper body), slip of the contact point: s_w' = vA + r wA,
+    # s_p' = (vB - vA) + r (wB + wA). Tangential force on the upper body -k s
+    # (and +k_p s_p on A); its torque about the upper centre r(n x F) = -r k s
+    # along z, and on A from the pair r(n_A x F_A) = -r k_p s_p.
+    A = np.zeros((6, 6))
+    A[0, 4], A[0, 5] = -kw / mA, kp / mA
+    A[1, 4], A[1, 5] = -r * kw / I, -r * kp / I
+    A[2, 5] = -kp / mA
+    A[3, 5] = -r * kp / I
+    A[4, 0], A[4, 1] = 1.0, r
+    A[5, 0], A[5, 1], A[5, 2], A[5, 3] = -1.0, r, 1.0, r
+    y0 = np.array([0, 0, v0, 0, 0, 0], np.float64)
+    wmax = np.abs(np.linalg.eigvals(A).imag).max()
+    n = int(4 * 2 * math.pi / wmax / p.dt)
+    every = max(1, n // 40)
+    for k in range(1, n + 1):
+        res = orc.step(p, st, h)
+        assert res.rc == 0 and res.n_pair_contacts == 2 and res.n_wall_contacts == 1
+        if k % every == 0:
+            want = expm(A * (k * p.dt)) @ y0
+            got = np.array([st.vel[0, 0], st.omega[0, 2], st.vel[1, 0], st.omega[1, 2]])
+            scale = np.array([v0, v0 / r, v0, v0 / r])  # velocities, spins
+            assert (np.abs(got - want[:4]) / scale).max() <= 2e-3, (k, got, want[:4])
 
 
 # ------------------------------------------------------ P12/P13/P15 -------
