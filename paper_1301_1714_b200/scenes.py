@@ -225,6 +225,17 @@ def random_gas(n: int, box_d: float, seed: int, r_range=(0.4 * D, 0.6 * D), v_si
     return make_scene(f"gas{n}", p, pos, vel, omg, radius=radius, meta=dict(seed=seed))
 
 
+def flag_gas(clamp_fn: bool = False, truncate_dt: bool = False, seed: int = 21) -> Scene:
+    """A fast, spinning, overlapping gas with strong damping, low friction and
+    C_t = 2.5 C_n: many contacts hit the Eq. 5 cap (so DEM_F_TRUNCATE_DT
+    rewrites δ_t) and many separate with a tensile F_n (so DEM_F_CLAMP_FN
+    zeroes it). For the flag parity tests."""
+    sp = SimParams(max_contacts=32, stiffness_t=2.5 * 7.326e6, damping=0.8, friction=0.2,
+                   clamp_fn=clamp_fn, truncate_dt=truncate_dt)
+    return random_gas(3000, 14.0, seed, r_range=(0.3 * D, 0.5 * D), v_sigma=0.4, w_sigma=200.0,
+                      params=sp)
+
+
 def two_body(v0: float, params: SimParams, gap: float = 1e-6, box_d: float = 8.0) -> Scene:
     """Head-on pair along x approaching at relative speed v0 (no gravity)."""
     L = box_d * D

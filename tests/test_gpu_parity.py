@@ -9,7 +9,7 @@ import pytest
 
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
-from paper_1301_1714_b200.dem import (DEM_EESCAPED, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
+from paper_1301_1714_b200.dem import (DEM_ECOINCIDENT, DEM_EESCAPED, DEM_ENONFINITE, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
                                       DEM_F_FORCE_LANES, DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
                                       DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
@@ -191,6 +191,46 @@ def test_one_step_T2(idx, variant):
         assert np.all(dv <= tolF / st.mass * dt + 3e-7 * np.linalg.norm(st.vel, axis=1) + 1e-12)
         dx = np.abs(g["pos"] - st.pos).max(axis=1)
         assert np.all(dx <= dv * dt + 2 * np.spacing(np.abs(st.pos).astype(np.float32)).max(axis=1))
+
+
+@pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
+                                     DEM_F_THREAD_PER_PARTICLE])
+@pytest.mark.parametrize("flags", ["clamp", "truncate", "clamp+truncate", "none"])
+def test_flags_one_step_T2(flags, variant):
+    """Readings R3 (DEM_F_CLAMP_FN) and R4 (DEM_F_TRUNCATE_DT) and a scalar
+    C_t != C_n, T2 against the oracle for four consecutive steps."""
+    sc = S.flag_gas(clamp_fn="clamp" in flags, truncate_dt="trunc" in flags)
+    K = sc.params.max_contacts
+    p = orc.make_params(sc.params, sc.radius)
+    assert p.Ct == pytest.approx(2.5 * p.Cn, rel=1e-7)
+    d = make(sc, flags=DEM_F_DIAG | variant)
+    for k in range(4):
+        st, h = oracle_inputs(d, K)
+        d.step(1)
+        g = d.get_state(forces=True)
+        res = orc.step(p, st, h)
+        assert res.rc == 0
+        assert np.array_equal(g["id"], st.id)
+        assert_T2_forces(g["force"], g["torque"], res, what=f"{flags} step {k + 1}")
+        assert_T2_history(contacts_dict(d), h.as_dict(st.id))
+
+
+@pytest.mark.parametrize("name", ["C3", "C4/4"])
+def test_bench_instantiation_bitwise(name):
+    """The bench runs k_force without DEM_F_DIAG (no F/T output) while every
+    T2 test sets it: the two instantiations must produce the same run bitwise
+    (state and δ_t), in the same force configuration."""
+    sc = S.C3() if name == "C3" else S.C4(scale=4)
+    runs = []
+    for flags in (DEM_F_DIAG, 0):
+        d = make(sc, flags=flags)
+        d.step(12)
+        runs.append((d.get_state(), contacts_dict(d), d.stats()["force_cfg"]))
+    assert runs[0][2] == runs[1][2] == ("dense" if name == "C3" else "light")
+    for k in ("pos", "vel", "omega", "id"):
+        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
+    assert runs[0][1].keys() == runs[1][1].keys()
+    assert all(np.array_equal(runs[0][1][x], runs[1][1][x]) for x in runs[0][1])
 
 
 def test_one_step_T2_C2_both_models():
@@ -741,6 +781,59 @@ def test_escape_is_reported():
         d.step(5)
     assert e.value.code == DEM_EESCAPED
     assert "particle id 0" in str(e.value)
+
+
+def test_coincident_centres_are_reported():
+    """R18: two centres at the same point while in contact leave n undefined:
+    DEM_ECOINCIDENT from the step (the oracle says the same for this input),
+    the state stays that of the last good step."""
+    sc = S.C1()
+    pos = sc.pos.copy()
+    pos[1] = pos[0]
+    sc2 = S.make_scene("coinc", sc.params, pos, sc.vel, sc.omega)
+    p = orc.make_params(sc2.params, sc2.radius)
+    d = make(sc2, flags=0)
+    s0 = d.get_state()
+    with pytest.raises(DemError) as e:
+        d.step(3)
+    assert e.value.code == DEM_ECOINCIDENT
+    assert "particle id 0" in str(e.value) or "particle id 1" in str(e.value)
+    assert d.stats()["steps"] == 0
+    assert np.array_equal(d.get_state()["pos"], s0["pos"])
+    st = orc.State.from_scene(sc2)
+    assert orc.step(p, st, orc.History.empty(sc2.n, 16)).rc == orc.ECOINCIDENT
+
+
+@pytest.mark.parametrize("graph", [True, False])
+def test_nonfinite_is_reported(graph):
+    """NaN injection through the public API: a checkpointed tangential history
+    (dem_set_contacts does not validate δ_t values) with one NaN entry makes
+    that particle's force, velocity and position NaN in the next step, which
+    the integrator reports as DEM_ENONFINITE with the particle's id; the state
+    stays the last good one."""
+    sc = S.C1()
+    base = 0 if graph else DEM_F_NO_GRAPH
+    d = make(sc, flags=base)
+    d.step(5)
+    s = d.get_state()
+    ci, cj, cd = d.get_contacts()
+    slot = {int(i): x for x, i in enumerate(s["id"])}
+    pair = np.nonzero(cj < S_WALL)[0]
+    a = np.array([slot[int(i)] for i in ci[pair]])
+    b = np.array([slot[int(j)] for j in cj[pair]])
+    ov = s["radius"][a] + s["radius"][b] - np.linalg.norm(s["pos"][a] - s["pos"][b], axis=1)
+    k = int(pair[np.argmax(ov)])  # the deepest contact: still touching next step
+    cd = cd.copy()
+    cd[k, 1] = np.nan
+    e = Dem(sc.params, flags=base)
+    e.set_particles(s["pos"], s["vel"], s["omega"], s["radius"], s["mass"], s["id"])
+    e.set_contacts(ci, cj, cd)
+    with pytest.raises(DemError) as err:
+        e.step(4)
+    assert err.value.code == DEM_ENONFINITE
+    assert f"particle id {int(ci[k])} " in str(err.value)
+    assert e.stats()["steps"] == 0
+    assert np.array_equal(e.get_state()["pos"], s["pos"])
 
 
 def test_device_tensors_and_order_id(cuda):
