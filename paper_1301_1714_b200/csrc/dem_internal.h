@@ -105,7 +105,9 @@ struct StepBuffers {
   float sw_r;          // > 0: one radius sw_r and the default path: pos_sorted[j].w holds
                        // bits(SCCM[j]) instead of r (the contact lists then carry old slots)
   uint32_t* clist;     // contacts found by k_detect: clist[k*N + j] = partner's sorted slot
-  uint32_t* ccount;    // number of pair contacts of sorted slot j (K+1: overflow)
+  uint32_t* ccount;    // per owned slot, from k_detect: base | n << 16 | overflow << 31 (its
+                       // first contact in its warp's flattened order, its contacts n <= K,
+                       // more than K found); the half-list ablation keeps a plain count
   const uint32_t* nslots;  // device: input slots of this step (owned + appended)
   uint32_t* flags;     // slab mode: per output slot, bit0/1 migrate to left/right neighbour,
                        // bit2/3 ghost for left/right neighbour

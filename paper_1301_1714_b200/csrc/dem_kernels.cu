@@ -1223,19 +1223,34 @@ __global__ void __launch_bounds__(DEM_DETECT_TPB, (LIGHT ? DEM_DETECT_MINB_LIGHT
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
   uint32_t jlo, jhi;
   owned_range(b, g, N, jlo, jhi);
+  const uint32_t lane = lane_id();
   const uint32_t j = jlo + blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= jhi) return;
-  float4 P = __ldg(&b.pos_sorted[j]);
+  if (j - lane >= jhi) return;  // whole warp past the end (warp-uniform)
+  const bool valid = j < jhi;
+  float4 P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 0.f);
   if (MONO) P.w = b.sw_r;
-  if (err != 0u) return;
-  // own cell: the step-2 hash of the own position (identical to CM by construction)
-  const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
-  const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
-  const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
-  float amb = -1.f;
-  uint32_t npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
-  if (amb >= 0.f) npair = detect_scan<true, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
-  __stcg(&b.ccount[j], npair);  // > K marks an overflow (raised by k_force)
+  if (err != 0u) return;  // warp-uniform
+  uint32_t npair = 0;
+  if (valid) {
+    // own cell: the step-2 hash of the own position (identical to CM by construction)
+    const int cx = cell_coord(P.x, g.lo[0], g.inv_h, g.nx);
+    const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
+    const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+    float amb = -1.f;
+    npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
+    if (amb >= 0.f) npair = detect_scan<true, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
+  }
+  // the warp — the 32 sorted slots of one k_force warp — scans its (capped)
+  // counts: each slot's first contact in the warp's flattened order, its
+  // count and an overflow bit, so k_force needs no scan
+  const uint32_t n = min(npair, K);
+  uint32_t incl = n;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= (uint32_t)d) incl += v;
+  }
+  if (valid) __stcg(&b.ccount[j], (incl - n) | (n << 16) | (npair > K ? 0x80000000u : 0u));
 }
 
 // k_force: warp per 32 consecutive sorted particles. The warp's contacts are
@@ -1316,18 +1331,23 @@ constexpr uint32_t kForceKC = 16;  // K with its own k_force instantiation
 constexpr int kForceFirst = DEM_FORCE_FIRST;  // list entries read before the count arrives
 constexpr bool kHistUncond = DEM_HIST_UNCOND != 0;
 
-// δ_t,old of partner `pid` in the old list of old slot s (n entries): try
-// index k first, then scan (R10: absent -> 0).
+// δ_t,old of partner `pid` in the old list of old slot s (n entries) when
+// the caller's guess, index k (the contact's own index in the new list;
+// n: none), missed (R10: absent -> 0). Lists are in candidate order, so a
+// contact that formed or broke earlier in the list shifts the rest by one:
+// entries k - 1 and k + 1 are tried first, then the others in order. (A scan
+// from 0 cost a dependent L2 round trip per entry before the shifted entry,
+// and ~1-3% of the C4 contacts miss their guess — a third to half of the
+// 32-contact rounds.) Serial on purpose: a wider probe raised the register
+// pressure of the common path (spills in k_force's round loop).
 __device__ __forceinline__ f3 old_history(const float4* __restrict__ hist_in, uint32_t K,
                                           uint32_t s, uint32_t n, uint32_t k, uint32_t pid) {
-  if (k < n) {
-    const float4 h = __ldcs(&hist_in[hix(s, k, K)]);
-    if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
-  }
-  for (uint32_t x = 0; x < n; ++x) {
-    if (x == k) continue;
-    const float4 h = __ldcs(&hist_in[hix(s, x, K)]);
-    if (__float_as_uint(h.w) == pid) return mk(h.x, h.y, h.z);
+  const float4* __restrict__ h = hist_in + (size_t)s * K;
+  for (uint32_t t = 0; t < n + 2u; ++t) {
+    const uint32_t x = t == 0u ? k - 1u : t == 1u ? k + 1u : t - 2u;
+    if (x >= n || (t >= 2u && x + 1u - k <= 2u)) continue;  // out of range / tried already
+    const float4 e = __ldcs(&h[x]);
+    if (__float_as_uint(e.w) == pid) return mk(e.x, e.y, e.z);
   }
   return mk(0.f, 0.f, 0.f);
 }
@@ -1394,7 +1414,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   const bool sw = b.sw_r > 0.f;
   Own o;
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  const uint32_t nc = valid ? __ldcs(&b.ccount[j]) : 0u;
+  const uint32_t meta = valid ? __ldcs(&b.ccount[j]) : 0u;  // k_detect's (base, n) word
   uint32_t t_first[kForceFirst];
 #pragma unroll
   for (int u = 0; u < kForceFirst; ++u)
@@ -1402,8 +1422,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   const uint32_t s = !valid ? 0u : sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
   if (sw) o.P.w = valid ? b.sw_r : 1.f;
   if (err != 0u) return;  // warp-uniform (one load per warp instruction)
-  const bool overflow = nc > K;
-  const uint32_t npair = min(nc, K);
+  const bool overflow = (meta >> 31) != 0u;
+  const uint32_t npair = (meta >> 16) & 0xFFu;
+  const uint32_t mybase = meta & 0xFFFFu;
+  const uint32_t M = __reduce_max_sync(0xffffffffu, mybase + npair);
   o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
@@ -1413,15 +1435,6 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     s_ost[lane] = o.V;
     s_ost[32 + lane] = o.W;
   }
-  // exclusive warp scan of the per-lane contact counts
-  uint32_t incl = npair;
-#pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= (uint32_t)d) incl += v;
-  }
-  const uint32_t mybase = incl - npair;
-  const uint32_t M = __shfl_sync(0xffffffffu, incl, 31);
   s_base[lane] = mybase;
   if (lane == 31) s_base[32] = M;
   for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
@@ -1520,7 +1533,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
         if (k < no && __float_as_uint(Hr.w) == pid)
           dold = mk(Hr.x, Hr.y, Hr.z);
         else
-          dold = old_history(b.hist_in, K, s_slot[ow], no, 0xFFFFFFFFu, pid);
+          dold = old_history(b.hist_in, K, s_slot[ow], no, k, pid);
         f3 dnew;
         eval_pair_practical<MAT>(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
         __stcs(&b.hist_out[hix((j0 - jlo) + ow, k, K)],
@@ -1590,7 +1603,7 @@ __global__ void __launch_bounds__(kLanesThreads, DEM_LANES_MINB)
   const bool sw = b.sw_r > 0.f;
   Own o;
   o.P = __ldg(&b.pos_sorted[j]);
-  const uint32_t nc = __ldcs(&b.ccount[j]);
+  const uint32_t meta = __ldcs(&b.ccount[j]);  // k_detect's (base, n) word
   // the first two list entries, before the count arrives (entries past the
   // count are never used)
   const uint32_t e0 = K > 0 ? __ldcs(&b.clist[j]) : 0u;
@@ -1598,8 +1611,8 @@ __global__ void __launch_bounds__(kLanesThreads, DEM_LANES_MINB)
   const uint32_t s = sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
   if (sw) o.P.w = b.sw_r;
   if (err != 0u) return;
-  const bool overflow = nc > K;
-  const uint32_t npair = min(nc, K);
+  const bool overflow = (meta >> 31) != 0u;
+  const uint32_t npair = (meta >> 16) & 0xFFu;
   o.V = __ldg(&b.vel_in[s]);
   o.W = __ldg(&b.omg_in[s]);
   const uint32_t n_old = MODEL == 0 ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
@@ -1641,7 +1654,7 @@ __global__ void __launch_bounds__(kLanesThreads, DEM_LANES_MINB)
       const uint32_t pid = __float_as_uint(WQ.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
       const f3 dold = (k < n_old && __float_as_uint(Hr.w) == pid)
                           ? mk(Hr.x, Hr.y, Hr.z)
-                          : old_history(b.hist_in, K, s, n_old, 0xFFFFFFFFu, pid);
+                          : old_history(b.hist_in, K, s, n_old, k, pid);
       f3 Fc, Tc, dnew;
       eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
       __stcs(&b.hist_out[hix(j - jlo, k, K)], make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
@@ -1804,7 +1817,7 @@ __global__ void __launch_bounds__(128) k_pair(StepBuffers b, DevGrid g, DevPhys 
       const uint32_t pid = __float_as_uint(WQ.w) & ph.idmask;
       const f3 dold = (k < n_old && __float_as_uint(Hk.w) == pid)
                           ? mk(Hk.x, Hk.y, Hk.z)
-                          : old_history(b.hist_in, K, si, n_old, 0xFFFFFFFFu, pid);
+                          : old_history(b.hist_in, K, si, n_old, k, pid);
       f3 dnew;
       eval_pair_practical<MAT>(o, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
       // this side's entry (upper part of i's list) and the partner's (lower part)
