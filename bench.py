@@ -377,8 +377,8 @@ def run_ours(args):
         "kernel_ms_avg": kernel_avg,
         "kernel_classes": {"hash": "k_count (counting-sort steps after a merge run)",
                            "scan": "k_tile_sum + k_scan_apply (counting sort)",
-                           "scatter": "k_mv_sort (merge re-sort) or k_scatter (counting sort)",
-                           "rank": "k_mv_apply (merge re-sort) or k_rank (counting sort)",
+                           "scatter": "k_scatter (counting sort)",
+                           "rank": "k_merge (merge re-sort) or k_rank (counting sort)",
                            "detect": "k_detect / k_detect_half",
                            "sweep": "k_force / k_force_lane / k_pair / k_sweep_tpp",
                            "finish": "k_finish (half lists)", "other": "slab exchange"},

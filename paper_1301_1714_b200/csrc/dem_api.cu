@@ -58,12 +58,13 @@ struct dem_handle {
   uint32_t *clist = nullptr, *ccount = nullptr;
   // merge re-sort (single GPU): the integrator's movers,
   // [mover counter, movers this step], movers sorted by (key, slot) and by slot
-  uint32_t *mov = nullptr, *mov_n = nullptr, *mv_u32 = nullptr;
-  int* mv_i32 = nullptr;
-  int2* mv_tab = nullptr;
+  uint4* mov = nullptr;      // merge re-sort: two mover lists (by state parity), mov_cap each
+  uint32_t* mov_n = nullptr; // their counts
+  uint32_t mov_cap = 0;
   bool merge = false;     // merge re-sort in use for this set
   bool merge_ok = false;  // state in the last step's sorted order, movers listed
   bool full_run = false;  // the rest of this dem_step call sorts by counting (mover overflow)
+  bool mv_redo = false;   // inside the redo of a mover overflow
   int64_t full_sorts = 0; // steps sorted by the counting sort since dem_set_particles
   uint8_t* cpos = nullptr;
   uint32_t *lcount = nullptr, *llist = nullptr;
@@ -197,9 +198,8 @@ void free_buffers(dem_handle* h) {
   h->prank = h->count = h->off = h->tmp = h->perm = h->scan_ctr = nullptr;
   h->pos_sorted = nullptr;
   h->clist = h->ccount = h->nslots = h->flags = nullptr;
-  h->mov = h->mov_n = h->mv_u32 = nullptr;
-  h->mv_i32 = nullptr;
-  h->mv_tab = nullptr;
+  h->mov = nullptr;
+  h->mov_n = nullptr;
   h->cpos = nullptr;
   h->lcount = h->llist = nullptr;
   h->R0 = nullptr;
@@ -252,24 +252,19 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.scan_ctr_next = h->scan_ctr + (b ^ 1);
   s.err = h->err;
   if (h->merge) {
-    s.mv.mov = h->mov;
-    s.mv.mov_n = h->mov_n;
-    s.mv.mv_m = h->mov_n + 1;
-    s.mv.dst = h->mv_u32;
-    s.mv.slot = h->mv_u32 + kMoverCap;
-    s.mv.evS = h->mv_u32 + 3 * kMoverCap;
-    s.mv.evC = h->mv_u32 + 5 * kMoverCap;
-    s.mv.evSc = h->mv_i32;
-    s.mv.evCc = h->mv_i32 + 2 * kMoverCap;
-    s.mv.tS = h->mv_tab;
-    s.mv.tC = h->mv_tab + mv_table_entries(h->cap);
+    // movers of input parity b (listed by the previous step), and this step's
+    s.mv.list_in = h->mov + (size_t)b * h->mov_cap;
+    s.mv.n_in = h->mov_n + b;
+    s.mv.list_out = h->mov + (size_t)(b ^ 1) * h->mov_cap;
+    s.mv.n_out = h->mov_n + (b ^ 1);
+    s.mv.cap = h->mov_cap;
   }
   return s;
 }
 
 int kernels_per_step(const dem_handle* h, bool full = false) {
   // counting sort: scan (2) + scatter + rank (+ k_count in merge mode); merge: 2
-  const int sort = h->merge ? (full ? 5 : 2) : 4;
+  const int sort = h->merge ? (full ? 5 : 1) : 4;
   return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3 : 2) +
          sort + (h->slab ? 5 : 0);
 }
@@ -311,19 +306,16 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     h->launches += 2;
   }
   if (h->merge && !full) {  // merge re-sort
-    rec(K_SCATTER, true);
-    launch_mv_sort(h->stream, h->n, h->g.ncells, s);
-    rec(K_SCATTER, false);
     rec(K_RANK, true);
-    launch_mv_apply(h->stream, h->n, h->g.ncells, s);
+    launch_merge(h->stream, h->n, h->g.ncells, s);
     rec(K_RANK, false);
-    h->launches += 2;
+    h->launches += 1;
   } else {
     if (h->merge) {  // the integrator listed movers, not cell counts
       rec(K_HASH, true);
       launch_count(h->stream, h->n, s.key_in, h->count, h->prank);
       rec(K_HASH, false);
-      cudaMemsetAsync(h->mov_n, 0, sizeof(uint32_t), h->stream);
+      cudaMemsetAsync(h->mov_n + (b ^ 1), 0, sizeof(uint32_t), h->stream);  // this step's list
       h->launches += 1;
     }
     rec(K_SCAN, true);
@@ -462,11 +454,17 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
   clean.step_ctr = (uint32_t)h->steps;
   CUDA_TRY(h, cudaMemcpyAsync(h->err, &clean, sizeof(DevErr), cudaMemcpyHostToDevice, h->stream));
   CUDA_TRY(h, cudaStreamSynchronize(h->stream));
-  if (e.code == 12u) {  // more movers than the merge re-sort takes: redo by counting
+  if (e.code == 12u) {
+    // more movers than the merge re-sort takes: that step is redone by
+    // counting (merge_ok is false) and the next ones merge again; a second
+    // overflow inside the redo sorts the rest of the call by counting
     const int64_t left = nsteps - done;
-    h->full_run = true;
+    const bool again = h->mv_redo;
+    h->mv_redo = true;
+    h->full_run = again;
     int rc = dem_step(h, left);
     h->full_run = false;
+    h->mv_redo = again;
     if (rc) return rc;
     return dem_sync(h);
   }
@@ -886,9 +884,8 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
             dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
             dalloc(h, &h->R1, N * h->K);
     if (!h->slab)  // merge re-sort buffers (single GPU)
-      ok &= dalloc(h, &h->mov, 3 * kMoverCap) && dalloc(h, &h->mov_n, 2) &&
-            dalloc(h, &h->mv_u32, 7 * kMoverCap) && dalloc(h, &h->mv_i32, 4 * kMoverCap) &&
-            dalloc(h, &h->mv_tab, mv_table_entries(cap) + mv_table_entries(ncells + 1));
+      ok &= dalloc(h, &h->mov, 2 * (size_t)mover_cap(cap)) && dalloc(h, &h->mov_n, 2);
+    h->mov_cap = h->slab ? 0u : mover_cap(cap);
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
@@ -1459,8 +1456,8 @@ int dem_analyze(dem_handle* h, dem_analysis* out) {
   for (int k = 0; k < 33; ++k) out->contact_hist[k] = (int64_t)a[9 + k];
   out->movers = -1;
   if (h->merge) {
-    uint32_t m = 0;
-    CUDA_TRY(h, cudaMemcpy(&m, h->mov_n, sizeof m, cudaMemcpyDeviceToHost));
+    uint32_t m = 0;  // the movers the next step will merge (listed by the last step)
+    CUDA_TRY(h, cudaMemcpy(&m, h->mov_n + h->cur, sizeof m, cudaMemcpyDeviceToHost));
     out->movers = (int64_t)m;
   }
   return DEM_OK;

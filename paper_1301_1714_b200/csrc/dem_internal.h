@@ -71,20 +71,15 @@ constexpr int kScanThreads = 256;
 constexpr int kScanItems = 16;
 constexpr int kScanTile = kScanThreads * kScanItems;
 
-// merge re-sort buffers (k_mv_sort, k_mv_perm, k_mv_off; kMoverCap movers)
+// merge re-sort (k_merge): mover lists double-buffered by the
+// parity of the state they index
 struct MergeBuffers {
-  uint32_t* mov;    // [3 kMoverCap]: slots whose new key differs from the key of their
-                    // sorted position (listed by the integrator), then their new keys,
-                    // then their previous keys
-  uint32_t* mov_n;  // [0] movers listed (may exceed the capacity), [1] = mv_m
-  uint32_t* mv_m;   // movers of this step's merge
-  uint32_t *dst, *slot;  // per mover in (key, slot) order: new slot, slot
-  uint32_t* evS;    // 2m slot events: 2 pos + (1: mover slot, -1; 0: insertion point, +1)
-  int* evSc;        // running sum of the slot event weights before each event
-  uint32_t* evC;    // 2m cell events (positions)
-  int* evCc;        // running sums
-  int2* tS;         // per k_mv_apply slot block: (first event, running sum there)
-  int2* tC;         // per k_mv_apply cell block
+  const uint4* list_in;   // movers of this step's input order, listed by the previous
+                          // step's integrator: (slot, new key, previous key, insertion point)
+  const uint32_t* n_in;   // their number (may exceed cap: the step is redone by counting)
+  uint4* list_out;        // this step's integrator lists the next step's movers here
+  uint32_t* n_out;        // (zeroed by this step's k_merge, or memset on a counting step)
+  uint32_t cap;           // list capacity
 };
 
 struct StepBuffers {
@@ -133,7 +128,12 @@ struct StepBuffers {
   // (mv.mov == nullptr: counting sort, cell counts)
   MergeBuffers mv;
 };
-constexpr uint32_t kMoverCap = 4096;  // movers per step the merge re-sort takes (one block)
+// movers per step the merge re-sort takes: a few per mille of the particles
+// move cell per step on the settling bed (C4: ~500 of 4.2 M)
+inline uint32_t mover_cap(int64_t n) {
+  const int64_t c = n / 512;
+  return (uint32_t)(c < 4096 ? 4096 : c > 65536 ? 65536 : c);
+}
 
 // ---- slab exchange ------------------------------------------
 // Per rank an exchange region (cudaMalloc, shareable by CUDA IPC) holding, for
@@ -225,12 +225,10 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
-// merge re-sort: k_mv_sort, k_mv_perm, k_mv_off in place of
-// the counting sort when the state is in the previous step's sorted order
-int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
-int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
+// merge re-sort: one k_merge in place of the counting sort
+// when the state is in the previous step's sorted order
+int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
 int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uint32_t* perm);
-int64_t mv_table_entries(int64_t count);  // entries of MergeBuffers::tS (count = n), tC (ncells + 1)
 // Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the
 // whole step (the paper's mapping) in a single kernel.

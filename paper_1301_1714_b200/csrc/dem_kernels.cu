@@ -425,290 +425,156 @@ __global__ void __launch_bounds__(256)
 // the state is stored in the previous step's sorted order. So the stable sort
 // of Eq. 11 (ties by current slot, R16) is a merge: the *stayers* (slots whose
 // new key equals the previous SCM there) are already in order; only the few
-// *movers* need sorting, by (new key, slot). With A = the mover slots and, for
-// the i-th mover of that order (key c_i, slot s_i), its insertion point
-// x_i = clamp(s_i, off[c_i], off[c_i+1]) among the stayers (previous offsets:
-// a stayer at slot s precedes mover i exactly when s < x_i, because the
-// previous SCM is non-decreasing in the slot),
-//   stayer s  -> s + #{x_i <= s} - #{a in A, a <= s},
-//   mover i   -> i + x_i - #{a in A, a < x_i},
-//   off'[c]    = off[c] + #{c_i + 1 <= c} - #{a in A, SCM(a) + 1 <= c}.
-// Both deltas are step functions with 2m events; k_mv_sort lists them sorted,
-// with their running sums, so k_mv_perm and k_mv_off look up one block's
-// events once and stream. Bit-identical to the counting sort (the same unique
-// stable permutation). The integrator lists the movers (finish_particle);
-// more than kMoverCap raises code 12 and the host redoes that step (and the
-// rest of the call) with the counting sort.
+// *movers* need placing. With A = the mover slots a_i, their new keys c_i,
+// previous keys c'_i and insertion points x_i = clamp(a_i, off[c_i],
+// off[c_i+1]) among the stayers (previous offsets: a stayer at slot s
+// precedes mover i exactly when s < x_i, because the previous SCM is
+// non-decreasing in the slot), the stable order is
+//   stayer s -> s + #{i: x_i <= s} - #{i: a_i <= s},
+//   mover i  -> r_i + x_i - #{j: a_j < x_i},  r_i = #{j: (c_j, a_j) < (c_i, a_i)},
+//   off'[c]   = off[c] + #{i: c_i < c} - #{i: c'_i < c}.
+// Every one of these is a count over the mover list, so one kernel places
+// everything with no sort at all: block b takes the slots and the cells
+// [1024 b, 1024 b + 1024), counts the movers below its range (a block
+// reduction over the list, which stays in L2), collects the few events
+// inside it in shared memory, and moves its stayers and shifts its offsets;
+// block b also places movers b, b + grid, ... (a block-wide count each).
+// Bit-identical to the counting sort (the same unique stable permutation).
+// The integrator of the previous step listed the movers as (a, c, c', x)
+// (finish_particle: it has the sorted slot, both keys and these offsets);
+// more than the capacity raises code 12 and the host redoes that step with
+// the counting sort. (Round 1 sorted the movers in one block first and built
+// per-block event tables: 20-30 us on one SM per step on C4.)
+constexpr uint32_t kMergeSpan = 1024;  // slots and cells per k_merge block
+constexpr int kMergeItems = kMergeSpan / 256;
+constexpr uint32_t kMergeEv = 512;     // in-block events held in shared memory
 
-// first index in a[lo, hi) with a[idx] >= x (a ascending)
-__device__ __forceinline__ uint32_t lower_bound_u32(const uint32_t* a, uint32_t lo, uint32_t hi,
-                                                    uint32_t x) {
-  while (lo < hi) {
-    const uint32_t mid = (lo + hi) >> 1;
-    if (a[mid] < x) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
-// One block of 1024 threads, all in shared memory. Outputs: mv_m = m; per
-// mover of the (key, slot) order its destination slot, slot and key; the slot
-// events evS[k] = 2 pos + isA with running sums evSc (sum of the weights
-// before k: +1 insertion point, -1 mover slot) and the cell events evC[k] =
-// pos with running sums evCc; per block of kMvBlock slots / cells of
-// k_mv_apply, the index of its first event and the running sum there (tS,
-// tC). Counts the step (the counting sort's k_tile_sum does otherwise) and
-// resets the mover counter for this step's integrator.
-constexpr uint32_t kMvBlock = 1024;  // slots or cells per k_mv_apply block
-constexpr size_t kMvSortSmem = (size_t)kMoverCap * (8 + 4 * 4 + 2 * 4 * 4);
-constexpr uint32_t kMvRankSortMax = 512;  // up to this many movers: rank sort, else bitonic
-
-__global__ void __launch_bounds__(1024) k_mv_sort(MergeBuffers mb, const uint32_t* __restrict__ key,
-                                                  const uint32_t* __restrict__ off, uint32_t nbS,
-                                                  uint32_t nbC, DevErr* err) {
-  pdl_enter();
-  extern __shared__ __align__(16) uint8_t smem_raw[];
-  unsigned long long* sB = reinterpret_cast<unsigned long long*>(smem_raw);  // (key, slot)
-  uint32_t* sA = reinterpret_cast<uint32_t*>(sB + kMoverCap);  // mover slots ascending
-  uint32_t* sAo = sA + kMoverCap;                              // their previous keys (SCM)
-  uint32_t* sP = sAo + kMoverCap;                              // insertion points x_i
-  uint32_t* sBk = sP + kMoverCap;                              // keys of the (key, slot) order
-  uint32_t* sES = sBk + kMoverCap;                             // slot events [2 kMoverCap]
-  uint32_t* sEC = sES + 2 * kMoverCap;                         // cell events [2 kMoverCap]
-  int* sESc = reinterpret_cast<int*>(sEC + 2 * kMoverCap);      // running sums of the slot
-  int* sECc = sESc + 2 * kMoverCap;                             // and the cell events
-  const uint32_t t = threadIdx.x, T = blockDim.x;
-  // the error word, the mover count and (rank-sort path) this thread's mover
-  // entry — slot, new key, previous key, as the integrator listed them — go
-  // out together (entries past the count are in bounds and never used)
-  const uint32_t ecode = ld_volatile(&err->code);
-  const uint32_t m = ld_volatile(mb.mov_n);
-  uint32_t msl = 0u, mkn = 0u, mko = 0u;
-  if (t < kMvRankSortMax) {
-    msl = __ldcg(&mb.mov[t]);
-    mkn = __ldcg(&mb.mov[kMoverCap + t]);
-    mko = __ldcg(&mb.mov[2 * kMoverCap + t]);
-  }
-  if (ecode != 0u) return;
-  if (t == 0) atomicAdd(&err->step_ctr, 1u);
-  __syncthreads();  // every thread has read the count before it is reset
-  if (m > kMoverCap) {
-    if (t == 0) raise_error(err, 12u, m, 0u);
-    return;
-  }
-  if (t == 0) {
-    *mb.mov_n = 0u;
-    *mb.mv_m = m;
-  }
-  if (m <= kMvRankSortMax) {
-    // few movers (the common case): each thread places one element at its
-    // rank among the unsorted ones (keys unique: slots are), in the event
-    // arrays' space, which is free until the events are written
-    // (the insertion point x = clamp(slot, off[c], off[c+1]) depends on the
-    // mover alone, so its loads go out before the sort)
-    unsigned long long* uB = reinterpret_cast<unsigned long long*>(sEC);
-    uint32_t* uA = sES;
-    uint32_t xi = 0u;
-    if (t < m) {
-      uA[t] = msl;
-      uB[t] = ((unsigned long long)mkn << 32) | msl;
-      xi = min(max(msl, __ldg(&off[mkn])), __ldg(&off[mkn + 1]));
-    }
-    __syncthreads();
-    if (t < m) {
-      const unsigned long long x = uB[t];
-      uint32_t rb = 0, ra = 0;
-      for (uint32_t i = 0; i < m; ++i) {  // broadcast shared-memory reads
-        rb += uB[i] < x ? 1u : 0u;
-        ra += uA[i] < msl ? 1u : 0u;
-      }
-      sB[rb] = x;
-      sBk[rb] = mkn;
-      sP[rb] = xi;
-      sA[ra] = msl;
-      sAo[ra] = mko;
-    }
-    __syncthreads();
-  } else {
-  // A sorted as (slot, previous key) pairs in the slot events' space (free
-  // until the events are written), so each mover keeps its SCM beside it
-  unsigned long long* uA = reinterpret_cast<unsigned long long*>(sES);
-  uint32_t P = 1;
-  while (P < m) P <<= 1;
-  for (uint32_t i = t; i < P; i += T) {
-    if (i < m) {
-      const uint32_t sl = mb.mov[i];
-      uA[i] = ((unsigned long long)sl << 32) | mb.mov[2 * kMoverCap + i];
-      sB[i] = ((unsigned long long)__ldg(&key[sl]) << 32) | sl;
-    } else {
-      uA[i] = ~0ull;
-      sB[i] = ~0ull;
-    }
-  }
-  __syncthreads();
-  for (uint32_t k = 2; k <= P; k <<= 1) {  // bitonic: B by (key, slot), A by slot
-    for (uint32_t jj = k >> 1; jj > 0; jj >>= 1) {
-      for (uint32_t i = t; i < P; i += T) {
-        const uint32_t l = i ^ jj;
-        if (l > i) {
-          const bool up = (i & k) == 0;
-          const unsigned long long x = sB[i], y = sB[l];
-          if ((x > y) == up) {
-            sB[i] = y;
-            sB[l] = x;
-          }
-          const unsigned long long u = uA[i], v = uA[l];
-          if ((u > v) == up) {
-            uA[i] = v;
-            uA[l] = u;
-          }
-        }
-      }
-      __syncthreads();
-    }
-  }
-  for (uint32_t i = t; i < m; i += T) {
-    const uint32_t c = (uint32_t)(sB[i] >> 32), si = (uint32_t)sB[i];
-    sBk[i] = c;
-    sA[i] = (uint32_t)(uA[i] >> 32);
-    sAo[i] = (uint32_t)uA[i];
-    sP[i] = min(max(si, __ldg(&off[c])), __ldg(&off[c + 1]));  // insertion point x_i
-  }
-  __syncthreads();
-  }
-  for (uint32_t i = t; i < m; i += T) {  // movers: destinations and their events
-    const uint32_t c = sBk[i], si = (uint32_t)sB[i], x = sP[i];
-    const uint32_t la = lower_bound_u32(sA, 0, m, x);  // #A < x
-    mb.dst[i] = i + x - la;
-    mb.slot[i] = si;
-    sES[i + la] = 2u * x;  // ties: insertion points before mover slots
-    sESc[i + la] = (int)i - (int)la;
-    const uint32_t lo = lower_bound_u32(sAo, 0, m, c);  // #A with SCM < c
-    sEC[i + lo] = c + 1u;  // ties: key events before SCM events
-    sECc[i + lo] = (int)i - (int)lo;
-  }
-  for (uint32_t k = t; k < m; k += T) {
-    const uint32_t a = sA[k], ao = sAo[k];
-    const uint32_t np = lower_bound_u32(sP, 0, m, a + 1u);   // #x <= a
-    sES[k + np] = 2u * a + 1u;
-    sESc[k + np] = (int)np - (int)k;
-    const uint32_t nb = lower_bound_u32(sBk, 0, m, ao + 1u);  // #keys <= SCM(a)
-    sEC[k + nb] = ao + 1u;
-    sECc[k + nb] = (int)nb - (int)k;
-  }
-  __syncthreads();  // (also makes this block's global writes visible to itself)
-  const uint32_t ne = 2u * m;
-  for (uint32_t k = t; k < ne; k += T) {
-    mb.evS[k] = sES[k];
-    mb.evC[k] = sEC[k];
-    mb.evSc[k] = sESc[k];
-    mb.evCc[k] = sECc[k];
-  }
-  // per k_mv_apply block: first event and the running sum before it. Each
-  // thread takes a run of consecutive blocks: one binary search, then a merge.
-  const uint32_t GS = (nbS + T) / T, GC = (nbC + T) / T;
-  {
-    const uint32_t b0 = t * GS, b1 = min(b0 + GS, nbS + 1u);
-    uint32_t k = b0 < b1 ? lower_bound_u32(sES, 0, ne, 2u * b0 * kMvBlock) : 0u;
-    for (uint32_t b = b0; b < b1; ++b) {
-      while (k < ne && sES[k] < 2u * b * kMvBlock) ++k;
-      mb.tS[b] = make_int2((int)k, k < ne ? sESc[k] : 0);
-    }
-  }
-  {
-    const uint32_t b0 = t * GC, b1 = min(b0 + GC, nbC + 1u);
-    uint32_t k = b0 < b1 ? lower_bound_u32(sEC, 0, ne, b0 * kMvBlock + 1u) : 0u;
-    for (uint32_t b = b0; b < b1; ++b) {
-      while (k < ne && sEC[k] < b * kMvBlock + 1u) ++k;
-      mb.tC[b] = make_int2((int)k, k < ne ? sECc[k] : 0);
-    }
-  }
-}
-
-// k_mv_apply, block b < nbS: new slots of the stayers (4 per thread, a block
-// = kMvBlock consecutive slots) and of the movers (grid-stride): perm (SCCM),
-// positions gathered into sorted order (step 4), SCM for the next step.
-// Block b < nbC: off'[c] = off[c] + (running sum of the cell events at
-// positions <= c) for its kMvBlock cells, in place, touched only where that
-// sum is not zero (between a mover's old and new cell). The movers' insertion
-// points were taken from the previous offsets by k_mv_sort.
-constexpr int kMvItems = 4;
-__global__ void __launch_bounds__(256)
-    k_mv_apply(uint32_t n, uint32_t ncells, uint32_t nbS, MergeBuffers mb,
-               const float4* __restrict__ pos_in,
-               uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
-               uint32_t* __restrict__ off, const DevErr* err,
-               bool sw, bool split) {
-  pdl_enter();
-  // block b: slots [b kMvBlock, (b+1) kMvBlock) if b < nbS and cells
-  // [b kMvBlock, (b+1) kMvBlock) if b < nbC (one grid for both parts, so no
-  // tail of near-empty offset blocks); every load of both parts goes out
-  // first. `split` (grids under one wave): cells in blocks nbS + b instead.
-  const uint32_t b = blockIdx.x;
-  const uint32_t nbC = (ncells + kMvBlock) / kMvBlock;  // ncells + 1 offsets
-  const uint32_t bc = split ? b - nbS : b;             // cell block (if in range)
-  const bool cells = split ? b >= nbS : b < nbC;
-  const uint32_t e = ld_volatile(&err->code);
-  const uint32_t m = __ldg(mb.mv_m);
-  const uint32_t B0 = b * kMvBlock;
-  float4 P[kMvItems];
-  int2 tS0 = make_int2(0, 0), tC0 = make_int2(0, 0);
-  uint32_t kS1 = 0u, kC1 = 0u;
-  if (b < nbS) {
+__device__ __forceinline__ int block_sum(int v, int* red) {  // 256 threads
 #pragma unroll
-    for (int u = 0; u < kMvItems; ++u) {
-      const uint32_t s = B0 + u * blockDim.x + threadIdx.x;
-      P[u] = s < n ? __ldcs(&pos_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
-    }
-    tS0 = __ldg(&mb.tS[b]);
-    kS1 = (uint32_t)__ldg(&mb.tS[b + 1]).x;
-  }
-  if (cells) {
-    tC0 = __ldg(&mb.tC[bc]);
-    kC1 = (uint32_t)__ldg(&mb.tC[bc + 1]).x;
+  for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
+  __syncthreads();  // (red reused)
+  if ((threadIdx.x & 31u) == 0u) red[threadIdx.x >> 5] = v;
+  __syncthreads();
+  int s = 0;
+#pragma unroll
+  for (int w = 0; w < 8; ++w) s += red[w];
+  return s;
+}
+
+__global__ void __launch_bounds__(256)
+    k_merge(uint32_t n, uint32_t ncells, MergeBuffers mb, const float4* __restrict__ pos_in,
+            uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
+            uint32_t* __restrict__ off, DevErr* err, bool sw) {
+  pdl_enter();
+  __shared__ int red[2][8];
+  __shared__ uint32_t s_ne[2];
+  __shared__ int2 s_ev[2][kMergeEv];  // (position, weight): slot events, cell events
+  const uint32_t b = blockIdx.x, t = threadIdx.x;
+  const uint32_t B0 = b * kMergeSpan, B1 = B0 + kMergeSpan;
+  // the error word, the mover count and this block's positions go out together
+  const uint32_t e = ld_volatile(&err->code);
+  const uint32_t m = ld_volatile(mb.n_in);
+  float4 P[kMergeItems];
+#pragma unroll
+  for (int u = 0; u < kMergeItems; ++u) {
+    const uint32_t s = B0 + u * 256u + t;
+    P[u] = s < n ? __ldcs(&pos_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   }
   if (e != 0u) return;
-  if (b < nbS) {
+  if (b == 0 && t == 0) {
+    atomicAdd(&err->step_ctr, 1u);  // (the counting sort's k_tile_sum does it otherwise)
+    if (m > mb.cap) raise_error(err, 12u, m, 0u);  // (recorded as this step)
+    else *mb.n_out = 0u;  // this step's integrator lists the next movers
+  }
+  if (m > mb.cap) return;  // more movers than listed: the host redoes the step by counting
+  if (t < 2) s_ne[t] = 0u;
+  __syncthreads();
+  // movers below this block's slots / cells, and the events inside them
+  int dS = 0, dC = 0;
+  for (uint32_t i = t; i < m; i += 256u) {
+    const uint4 v = __ldcg(&mb.list_in[i]);  // (a, c, c', x)
+    dS += (int)(v.w < B0) - (int)(v.x < B0);
+    dC += (int)(v.y < B0) - (int)(v.z < B0);
+    auto push = [&](int k, uint32_t p, int w) {
+      const uint32_t q = atomicAdd(&s_ne[k], 1u);
+      if (q < kMergeEv) s_ev[k][q] = make_int2((int)p, w);
+    };
+    if (v.w - B0 < kMergeSpan) push(0, v.w, 1);   // insertion point: stayers from x on
+    if (v.x - B0 < kMergeSpan) push(0, v.x, -1);  // mover slot: stayers from a on
+    if (v.y - B0 < kMergeSpan) push(1, v.y, 1);   // new key: cells above c
+    if (v.z - B0 < kMergeSpan) push(1, v.z, -1);  // previous key: cells above c'
+  }
+  dS = block_sum(dS, red[0]);
+  dC = block_sum(dC, red[1]);
+  const uint32_t neS = s_ne[0], neC = s_ne[1];
+  const bool spill = neS > kMergeEv || neC > kMergeEv;  // (clustered movers: exact slow path)
+  // stayers: new slot s + #{x <= s} - #{a <= s}; movers are skipped
 #pragma unroll
-    for (int u = 0; u < kMvItems; ++u) {
-      const uint32_t s = B0 + u * blockDim.x + threadIdx.x;
-      if (s >= n) continue;
-      int d = tS0.y;
-      bool mover = false;
-      for (uint32_t k = (uint32_t)tS0.x; k < kS1; ++k) {  // this block's events (rare)
-        const uint32_t ev = __ldg(&mb.evS[k]);
-        if ((ev >> 1) > s) break;
-        d = k + 1 < 2u * m ? __ldg(&mb.evSc[k + 1]) : 0;
-        mover |= ev == 2u * s + 1u;
+  for (int u = 0; u < kMergeItems; ++u) {
+    const uint32_t s = B0 + u * 256u + t;
+    if (s >= n) continue;
+    int d = dS;
+    bool mover = false;
+    if (!spill) {
+      for (uint32_t k = 0; k < neS; ++k) {
+        const int2 ev = s_ev[0][k];
+        if ((uint32_t)ev.x <= s) d += ev.y;
+        mover |= ev.y < 0 && (uint32_t)ev.x == s;
       }
-      if (mover) continue;
-      const uint32_t j = (uint32_t)((int)s + d);
-      // one radius: .w carries the old slot, and nothing on that path reads
-      // perm (dem_get_grid extracts it from .w), so it is not written
-      if (sw) P[u].w = __uint_as_float(s);
-      else perm[j] = s;
-      pos_sorted[j] = P[u];
+    } else {
+      d = 0;
+      for (uint32_t i = 0; i < m; ++i) {
+        const uint4 v = __ldcg(&mb.list_in[i]);
+        d += (int)(v.w <= s) - (int)(v.x <= s);
+        mover |= v.x == s;
+      }
     }
+    if (mover) continue;
+    const uint32_t j = (uint32_t)((int)s + d);
+    // one radius: .w carries the old slot, and nothing on that path reads
+    // perm (dem_get_grid extracts it from .w), so it is not written
+    if (sw) P[u].w = __uint_as_float(s);
+    else perm[j] = s;
+    pos_sorted[j] = P[u];
   }
-  for (uint32_t g = b * blockDim.x + threadIdx.x; g < m; g += gridDim.x * blockDim.x) {
-    // mover g of the (key, slot) order
-    const uint32_t j = __ldg(&mb.dst[g]), sm = __ldg(&mb.slot[g]);
-    float4 Pm = __ldg(&pos_in[sm]);
-    if (sw) Pm.w = __uint_as_float(sm);
-    else perm[j] = sm;
-    pos_sorted[j] = Pm;
-  }
-  // offsets, in place, only where a shift is non-zero
-  if (!cells || m == 0u || ((uint32_t)tC0.x == kC1 && tC0.y == 0)) return;
+  // offsets, in place, only where the shift is not zero
+  if (B0 <= ncells && !(dC == 0 && neC == 0)) {
 #pragma unroll
-  for (int u = 0; u < kMvItems; ++u) {
-    const uint32_t cc = bc * kMvBlock + u * blockDim.x + threadIdx.x;
-    if (cc > ncells) continue;
-    int d = tC0.y;
-    for (uint32_t k = (uint32_t)tC0.x; k < kC1; ++k) {  // this block's events (rare)
-      if (__ldg(&mb.evC[k]) > cc) break;
-      d = k + 1 < 2u * m ? __ldg(&mb.evCc[k + 1]) : 0;
+    for (int u = 0; u < kMergeItems; ++u) {
+      const uint32_t c = B0 + u * 256u + t;
+      if (c > ncells) continue;
+      int d = dC;
+      if (!spill) {
+        for (uint32_t k = 0; k < neC; ++k) {
+          const int2 ev = s_ev[1][k];
+          if ((uint32_t)ev.x < c) d += ev.y;
+        }
+      } else {
+        d = 0;
+        for (uint32_t i = 0; i < m; ++i) {
+          const uint4 v = __ldcg(&mb.list_in[i]);
+          d += (int)(v.y < c) - (int)(v.z < c);
+        }
+      }
+      if (d != 0) off[c] = (uint32_t)((int)__ldcs(&off[c]) + d);
     }
-    if (d != 0) off[cc] = (uint32_t)((int)__ldcs(&off[cc]) + d);
+  }
+  // movers b, b + grid, ...: r_i + x_i - #{a_j < x_i}, counted block-wide
+  for (uint32_t i = b; i < m; i += gridDim.x) {
+    const uint4 mi = __ldcg(&mb.list_in[i]);
+    int r = 0;
+    for (uint32_t jj = t; jj < m; jj += 256u) {
+      const uint4 v = __ldcg(&mb.list_in[jj]);
+      r += (int)(v.y < mi.y || (v.y == mi.y && v.x < mi.x)) - (int)(v.x < mi.w);
+    }
+    r = block_sum(r, red[0]);
+    if (t == 0) {
+      const uint32_t j = (uint32_t)(r + (int)mi.w);
+      float4 Pm = __ldg(&pos_in[mi.x]);
+      if (sw) Pm.w = __uint_as_float(mi.x);
+      else perm[j] = mi.x;
+      pos_sorted[j] = Pm;
+    }
   }
 }
 
@@ -883,7 +749,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
   const uint32_t j = oj;  // output slot
   // this step's SCM at j (merge re-sort): the key of the sorted position itself
   // (the sort ordered these very coordinates by it), so no SCM array is kept
-  const uint32_t sk = b.mv.mov ? cell_key(g, o.P.x, o.P.y, o.P.z) : 0u;
+  const uint32_t sk = b.mv.list_out ? cell_key(g, o.P.x, o.P.y, o.P.z) : 0u;
   const float ri = o.P.w, mi = o.V.w;
   const uint32_t my_id = __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
@@ -992,19 +858,20 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
     }
   }
   b.key_out[j] = k2;
-  if (b.mv.mov) {  // merge re-sort: list the particles that change cell (warp-aggregated)
+  if (b.mv.list_out) {  // merge re-sort: list the particles that change cell (warp-aggregated)
     const uint32_t act = __activemask();
     const uint32_t mv = __ballot_sync(act, k2 != sk);
     if (mv) {
       const uint32_t leader = __ffs(mv) - 1;
       uint32_t base = 0;
-      if (lane_id() == leader) base = atomicAdd(b.mv.mov_n, (uint32_t)__popc(mv));
+      if (lane_id() == leader) base = atomicAdd(b.mv.n_out, (uint32_t)__popc(mv));
       base = __shfl_sync(act, base, leader);
       const uint32_t idx = base + (uint32_t)__popc(mv & lanemask_lt());
-      if (k2 != sk && idx < kMoverCap) {  // slot, new key, previous key (k_mv_sort)
-        b.mv.mov[idx] = j;
-        b.mv.mov[kMoverCap + idx] = k2;
-        b.mv.mov[2 * kMoverCap + idx] = sk;
+      if (k2 != sk && idx < b.mv.cap) {
+        // slot, new key, previous key and the insertion point among this
+        // step's order (these offsets are the next step's previous ones)
+        const uint32_t x = min(max(j, __ldg(&b.off[k2])), __ldg(&b.off[k2 + 1]));
+        b.mv.list_out[idx] = make_uint4(j, k2, sk, x);
       }
     }
   } else {
@@ -1927,7 +1794,6 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
 void sweep_prepare(uint32_t K) {
-  cudaFuncSetAttribute(k_mv_sort, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMvSortSmem);
   const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
   const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
   const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
@@ -2478,22 +2344,11 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   return K_RANK;
 }
 
-static uint32_t mv_blocks(int64_t count) { return (uint32_t)((count + kMvBlock - 1) / kMvBlock); }
-
-int launch_mv_sort(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
-  launch_pdl(k_mv_sort, 1, 1024, kMvSortSmem, st, b.mv, (const uint32_t*)b.key_in,
-             (const uint32_t*)b.off, mv_blocks(n),
-             mv_blocks((int64_t)ncells + 1), b.err);
-  return K_SCATTER;
-}
-
-int launch_mv_apply(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
-  const uint32_t nbS = mv_blocks(n), nbC = mv_blocks((int64_t)ncells + 1);
-  // both parts in one block when the grid spans several waves (no tail of
-  // near-empty offset blocks: C4 36 -> 29 us); separate blocks under a wave
-  const bool split = nbS + nbC <= 148u * 6u;
-  launch_pdl(k_mv_apply, split ? nbS + nbC : (nbS > nbC ? nbS : nbC), 256, 0, st, (uint32_t)n, ncells, nbS, b.mv, b.pos_in,
-             b.perm, b.pos_sorted, b.off, (const DevErr*)b.err, b.sw_r > 0.f, split);
+int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
+  const int64_t span = n > (int64_t)ncells + 1 ? n : (int64_t)ncells + 1;
+  const unsigned grid = (unsigned)((span + kMergeSpan - 1) / kMergeSpan);
+  launch_pdl(k_merge, grid, 256, 0, st, (uint32_t)n, ncells, b.mv, b.pos_in, b.perm, b.pos_sorted,
+             b.off, b.err, b.sw_r > 0.f);
   return K_RANK;
 }
 
@@ -2510,7 +2365,6 @@ int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uin
   return 0;
 }
 
-int64_t mv_table_entries(int64_t n) { return (int64_t)mv_blocks(n) + 1; }
 
 template <int MODEL, bool DIAG>
 static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,

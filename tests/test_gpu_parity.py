@@ -79,8 +79,7 @@ def _check_sorts(d, nsteps, per_call=1):
 @pytest.mark.parametrize("graph", [True, False])
 def test_merge_resort_bit_exact(name, graph):
     """After the first step the state is in the last sorted order and only the
-    particles that changed cell are sorted and merged in (k_mv_sort, k_mv_perm,
-    k_mv_off): SCCM and the offsets stay bit-exact every step."""
+    particles that changed cell are merged in (k_merge): SCCM and the offsets stay bit-exact every step."""
     sc = scenes_small()[1] if name == "gas" else S.CONFIGS[name]()
     d = make(sc, flags=0 if graph else DEM_F_NO_GRAPH)
     _check_sorts(d, 25)
@@ -107,17 +106,18 @@ def cell_crossers_scene(n_side=24, gap=3e-8):
 
 @pytest.mark.parametrize("graph", [True, False])
 def test_merge_resort_overflow_fallback(graph):
-    """More movers than kMoverCap: the step is rolled back and redone (with
-    the rest of the call) by the counting sort; the run equals the
-    counting-sort-only run bitwise and the grid stays bit-exact."""
+    """More movers than the list holds (4,096 at this size): that step is
+    rolled back and redone by the counting sort, and the rest of the
+    20-step call merges again; the run equals the counting-sort-only run
+    bitwise and the grid stays bit-exact."""
     sc = cell_crossers_scene()
     assert sc.n > 4096
     base = 0 if graph else DEM_F_NO_GRAPH
     a = make(sc, flags=DEM_F_DIAG | base)
     b = make(sc, flags=DEM_F_DIAG | base | DEM_F_FULL_SORT)
-    a.step(6)
-    b.step(6)
-    assert a.stats()["full_sorts"] == 5  # step 1, then steps 3-6 of the overflowing call
+    a.step(20)
+    b.step(20)
+    assert a.stats()["full_sorts"] == 2  # step 1 and the redone step 3; steps 4-20 merged
     sa, sb = a.get_state(forces=True), b.get_state(forces=True)
     for k in ("pos", "vel", "omega", "id", "force"):
         assert np.array_equal(sa[k], sb[k]), k
@@ -128,10 +128,11 @@ def test_merge_resort_overflow_fallback(graph):
 
 @pytest.mark.parametrize("n_side", [7, 10, 15])
 def test_merge_resort_mover_counts(n_side):
-    """All n_side³ spheres change cell in step 2, so step 3 merges 343 movers
-    (k_mv_sort's rank sort, <= 512), 1,000 or 3,375 (its bitonic sort): the
-    grid is bit-exact every step, with no fallback to counting, and the run
-    equals the counting-sort run bitwise."""
+    """All n_side³ spheres change cell in step 2, so step 3 merges 343, 1,000
+    or 3,375 movers, more events per k_merge block than its shared-memory
+    list holds (the exact per-slot path): the grid is bit-exact every step,
+    with no fallback to counting, and the run equals the counting-sort run
+    bitwise."""
     sc = cell_crossers_scene(n_side=n_side)
     d = make(sc, flags=0)
     _check_sorts(d, 2)
@@ -862,12 +863,13 @@ def test_profile_mode_times_every_kernel():
     d.profile(True)
     d.step(10)
     st = d.stats()
-    for k in ("scatter", "rank", "sweep", "detect"):
+    for k in ("rank", "sweep", "detect"):
         assert st["kernel_count"][k] == 10
         assert st["kernel_ms"][k] > 0
-    # the counting sort (cell counts, scan) runs only in the first step; the
-    # merge re-sort's two kernels are timed as scatter and rank afterwards
+    # the counting sort (cell counts, scan, scatter) runs only in the first
+    # step; the merge re-sort's one kernel is timed as rank afterwards
     assert st["kernel_count"]["hash"] == 1 and st["kernel_count"]["scan"] == 1
+    assert st["kernel_count"]["scatter"] == 1
     assert st["full_sorts"] == 1
     assert st["steps"] == 10
     f = make(sc, flags=DEM_F_FULL_SORT)
