@@ -125,6 +125,10 @@ def describe(sc) -> str:
     if sc.name.startswith("C4"):
         return (f"{sc.name}: {sc.n:,}-sphere pre-compressed settling bed (SC {m['nxyz']}, "
                 f"spacing 0.998 d, r = 0.5 mm) under gravity, {sc.params.model} model")
+    if m.get("kind") == "poly_bed":
+        return (f"{sc.name}: {sc.n:,}-sphere polydisperse bed (r ~ U[0.25, 0.5] mm capped to "
+                f"touch, SC {m['nxyz']} sites at {m['spacing'] * 1e3:.2f} mm) compacted under "
+                f"gravity before timing, {sc.params.model} model, K = {sc.params.max_contacts}")
     if m.get("kind") == "fcc":
         return (f"{sc.name}: {sc.n:,}-sphere jittered FCC dense packing {m['ncells']} cells, "
                 f"{sc.params.model} model")
@@ -279,7 +283,19 @@ def run_ours(args):
                 flags={"full": 0, "half": DEM_F_HALF_LISTS,
                        "tpp": DEM_F_THREAD_PER_PARTICLE, "lanes": DEM_F_FORCE_LANES}[args.sweep])
         # every rank passes the whole set; a slab rank keeps its own planes
-        d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+        if args.config == "C5" and args.c5_prep > 0:
+            # C5: the loose polydisperse lattice is compacted under gravity
+            # first (untimed; strong damping so it comes to rest within the
+            # preparation), then handed over with its tangential history
+            prep = Dem(sc.params.replace(damping=1.0), device=local, stream=stream)
+            prep.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
+            prep.step(args.c5_prep)
+            s0, c0 = prep.get_state(), prep.get_contacts()
+            prep.close()
+            d.set_particles(s0["pos"], s0["vel"], s0["omega"], s0["radius"], s0["mass"], s0["id"])
+            d.set_contacts(*c0)
+        else:
+            d.set_particles(sc.pos, sc.vel, sc.omega, sc.radius, sc.mass, sc.id)
         if world > 1:
             d.connect_group()
         d.step(max(args.warmup, 3))
@@ -301,24 +317,30 @@ def run_ours(args):
         launches_timed = st["launches"] - launches0
         d.profile(False)
         c_bar = st["contacts"] / max(1, st["n"]) if sc.params.model == "practical" else 0.0
-        # graph-replay region (the library's default path), same K: the headline
-        torch.cuda.synchronize()
-        barrier()
-        g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        # graph-replay regions (the library's default path): --reps repetitions
+        # of exactly K steps, each bracketed by barrier + synchronize; the
+        # headline is their median
+        ms_reps = []
         with ClockSampler(torch.cuda.current_device()) as clk_graph:
-            g0.record(stream)
-            d.step(args.steps)
-            g1.record(stream)
-            torch.cuda.synchronize()
-        barrier()
-        ms_graph = g0.elapsed_time(g1)
+            for _ in range(args.reps):
+                torch.cuda.synchronize()
+                barrier()
+                g0, g1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+                g0.record(stream)
+                d.step(args.steps)
+                g1.record(stream)
+                torch.cuda.synchronize()
+                barrier()
+                ms_reps.append(g0.elapsed_time(g1))
+        st_graph = d.stats()
 
     ms_max = ms
-    ms_graph_max = ms_graph
+    ms_reps_max = list(ms_reps)
     if world > 1:
-        t = torch.tensor([ms, ms_graph], device="cpu" if share else "cuda")
+        t = torch.tensor([ms] + ms_reps, device="cpu" if share else "cuda")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms_max, ms_graph_max = float(t[0]), float(t[1])
+        ms_max, ms_reps_max = float(t[0]), [float(x) for x in t[1:]]
+    ms_graph_max = statistics.median(ms_reps_max)
 
     # headline: the graph-replay region; the profiled region (events around every
     # kernel) gives the per-kernel durations of the roofline
@@ -337,11 +359,17 @@ def run_ours(args):
     sweep_ms = kernel_avg["detect"] + kernel_avg["sweep"] + kernel_avg["finish"]
     achieved = b_sweep * n_local / (sweep_ms * 1e-3) / 1e9
     step_kernel_ms = sum(kernel_avg.values())
-    traffic = None
+    # DRAM bytes of one k_detect + k_force launch from a committed ncu --set
+    # full capture of this bench command (tools/ncu_traffic.sh), with the c̄ and
+    # step of that capture beside it (ncu cannot run inside the timed region)
+    traffic, traffic_src = None, None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.model}.json")
-    if os.path.exists(tr_path):
+    if os.path.exists(tr_path) and args.sweep == "full":
         try:
-            traffic = json.load(open(tr_path)).get("sweep_dram_bytes_per_step")
+            tj = json.load(open(tr_path))
+            traffic = tj.get("sweep_dram_bytes_per_step")
+            traffic_src = {k: tj.get(k) for k in ("file", "step", "c_bar", "commit",
+                                                  "bytes_per_particle", "alg_bytes_per_particle")}
         except Exception:
             traffic = None
     line = {
@@ -358,6 +386,9 @@ def run_ours(args):
             "n_particles_rank0": n_local,
             "l2": l2_note(b_step * n_local),
             "dt": sc.params.dt, "sweep": args.sweep,
+            "c_bar_after_graph_reps": (st_graph["contacts"] / max(1, st_graph["n"])
+                                       if sc.params.model == "practical" else 0.0),
+            **({"prep_steps": args.c5_prep} if args.config == "C5" else {}),
         },
         "roofline": {
             "bound": "hbm",
@@ -367,6 +398,7 @@ def run_ours(args):
                        "lanes": "sweep = k_detect + k_force_lane"}[args.sweep],
             "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
+            "traffic_source": traffic_src,
             "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
             "kernel_ms_avg": sweep_ms, "kernel_share_of_step": sweep_ms / step_kernel_ms
             if step_kernel_ms else None,
@@ -383,10 +415,11 @@ def run_ours(args):
                            "sweep": "k_force / k_force_lane / k_pair / k_sweep_tpp",
                            "finish": "k_finish (half lists)", "other": "slab exchange"},
         "ms_per_step_profiled": ms_step_profiled,
-        "timing": ("value/ms_per_step: K-step CUDA-graph replay region (CUDA events on the "
-                   "handle's stream); roofline kernel durations: CUDA events around every "
-                   "kernel over a separate K-step region of eager launches timed just before "
-                   "it (ms_per_step_profiled)"),
+        "ms_per_step_reps": [x / args.steps for x in ms_reps_max],
+        "timing": (f"value/ms_per_step: median of {args.reps} K-step CUDA-graph replay regions "
+                   "(CUDA events on the handle's stream, max over ranks); roofline kernel "
+                   "durations: CUDA events around every kernel over a separate K-step region of "
+                   "eager launches timed just before them (ms_per_step_profiled)"),
         "gpu_launches": int(launches_timed),
         "clocks": clk_graph.summary(),
         "clocks_profiled": clk.summary(),
@@ -493,6 +526,9 @@ def main():
                          "lists, each pair once (Newton's third law); or the paper's fused "
                          "thread per particle")
     ap.add_argument("--e2e-steps", type=int, default=5)
+    ap.add_argument("--reps", type=int, default=5, help="timed K-step graph regions (median)")
+    ap.add_argument("--c5-prep", type=int, default=40000,
+                    help="C5: untimed compaction steps under gravity before the warm-up")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

@@ -17,6 +17,10 @@ ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
 INCLUDE = os.path.join(ROOT, "include")
 LIB = os.path.join(HERE, "libdem.so")
+# the same sources with the ablation kernels (the paper's thread-per-particle
+# mapping, half lists, one lane per particle) compiled in: tests and
+# `bench.py --sweep` load it for those flags; the product library has none
+LIB_ABLATIONS = os.path.join(HERE, "libdem_ablations.so")
 SOURCES = [os.path.join(CSRC, f) for f in ("dem_kernels.cu", "dem_api.cu")]
 HEADERS = [os.path.join(CSRC, "dem_internal.h"), os.path.join(INCLUDE, "dem.h")]
 
@@ -36,10 +40,10 @@ def nvcc() -> str:
     return "nvcc"
 
 
-def stale() -> bool:
-    if not os.path.exists(LIB):
+def stale(lib: str = LIB) -> bool:
+    if not os.path.exists(lib):
         return True
-    t = os.path.getmtime(LIB)
+    t = os.path.getmtime(lib)
     return any(os.path.getmtime(f) > t for f in SOURCES + HEADERS)
 
 
@@ -49,6 +53,8 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     target = out or LIB
     if not force and out is None and not stale():
         return LIB
+    if out is None and target == LIB and "DEM_ABLATIONS=1" not in defines:
+        build_ablations(force)
     tmp = target + f".tmp{os.getpid()}"
     cmd = [nvcc(), *NVCC_FLAGS, *(f"-D{d}" for d in defines), "-I", INCLUDE, "-I", CSRC,
            *SOURCES, "-o", tmp]
@@ -57,6 +63,12 @@ def build(force: bool = False, verbose: bool = False, out: str | None = None,
     subprocess.check_call(cmd)
     os.replace(tmp, target)
     return target
+
+
+def build_ablations(force: bool = False, verbose: bool = False) -> str:
+    if force or stale(LIB_ABLATIONS):
+        build(force=True, verbose=verbose, out=LIB_ABLATIONS, defines=("DEM_ABLATIONS=1",))
+    return LIB_ABLATIONS
 
 
 if __name__ == "__main__":

@@ -247,9 +247,6 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.F_out = h->F;
   s.T_out = h->T;
   s.scan_status = h->scan_status[b];
-  s.scan_ctr = h->scan_ctr + b;
-  s.scan_status_next = h->scan_status[b ^ 1];
-  s.scan_ctr_next = h->scan_ctr + (b ^ 1);
   s.err = h->err;
   if (h->merge) {
     // movers of input parity b (listed by the previous step), and this step's
@@ -319,11 +316,11 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
       h->launches += 1;
     }
     rec(K_SCAN, true);
-    launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, s.scan_ctr,
+    launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, nullptr,
                 h->err, 1);
     rec(K_SCAN, false);
     rec(K_SCATTER, true);
-    launch_scatter(h->stream, h->cap, s, h->ntiles);
+    launch_scatter(h->stream, h->cap, s);
     rec(K_SCATTER, false);
     rec(K_RANK, true);
     launch_rank(h->stream, h->cap, s);
@@ -494,6 +491,10 @@ int validate_params(const dem_params* p) {
   // lists as (slot << 5 | index), so it needs K <= 32
   if (p->max_contacts > kMaxContacts) return DEM_EINVAL;
   if ((p->flags & DEM_F_HALF_LISTS) && p->max_contacts > 32) return DEM_EINVAL;
+  // the ablations live in libdem_ablations.so
+  if ((p->flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES)) &&
+      !ablations_built())
+    return DEM_EINVAL;
   if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
   if (p->n_plates > 10 || (p->n_plates && !p->plates)) return DEM_EINVAL;
   for (uint32_t k = 0; k < p->n_plates; ++k) {  // unit normal, unit axis in the plane, extents

@@ -119,10 +119,7 @@ struct StepBuffers {
   uint32_t* cnt_out;
   float4* F_out;  // DEM_F_DIAG only
   float4* T_out;
-  unsigned long long* scan_status;       // this parity's look-back words
-  uint32_t* scan_ctr;                    // this parity's dynamic tile counter
-  unsigned long long* scan_status_next;  // the other parity's (reset during this step)
-  uint32_t* scan_ctr_next;
+  unsigned long long* scan_status;       // the counting sort's tile sums (this parity's)
   DevErr* err;
   // merge re-sort (single GPU): the mover buffers
   // (mv.mov == nullptr: counting sort, cell counts)
@@ -223,7 +220,7 @@ int launch_idcheck(cudaStream_t st, int64_t n, uint32_t idmask, const float4* om
 // One step = scan, scatter, rank, sweep.
 int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
                 unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
-int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next);
+int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
 // merge re-sort: one k_merge in place of the counting sort
 // when the state is in the previous step's sorted order
@@ -233,6 +230,9 @@ int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uin
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the
 // whole step (the paper's mapping) in a single kernel.
 void sweep_prepare(uint32_t K);  // host: kernel attributes (call outside stream capture)
+// whether this library carries the ablation kernels (DEM_F_THREAD_PER_PARTICLE,
+// DEM_F_HALF_LISTS, DEM_F_FORCE_LANES): libdem_ablations.so yes, libdem.so no
+bool ablations_built();
 // mono_r > 0: every particle has radius mono_r (single GPU), so S² of R14 is one
 // constant and the fp32 candidate test is 3 instructions shorter (same decisions).
 int launch_detect(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,

@@ -1,28 +1,36 @@
 // dem_kernels.cu — the sm_100a kernels of one DEM timestep (arXiv 1301.1714).
 //
-// Per step (§4.2), four kernels:
-//   k_scan    step 3, first half: exclusive scan of the per-cell counts that the
-//             previous step's integrator accumulated -> off[] (= lower_bound
-//             offsets of SCM, SPEC cell ranges). Single pass, decoupled look-back.
-//   k_scatter step 3: tmp[off[CM[i]] + prank[i]] = i (a counting sort; prank came
-//             from warp-aggregated atomics, so the order inside a cell is not yet
-//             fixed).
-//   k_rank    step 3: perm[off[c] + #{t in cell c: tmp[t] < s}] = s — the stable
-//             order inside each cell, giving SCCM with SCM[j] = CM[SCCM[j]]
-//             (Eq. 11) and ties in ascending current slot (R16).
-//   k_sweep   steps 4-8 + 1: one thread per sorted slot j reads its particle
-//             through SCCM (the reorder of step 4 is this gather), visits the 27
-//             cells of Eq. 12 in ascending cell / slot order, decides contact with
-//             the fp64-defined predicate (R14), evaluates Eq. 1 or Eqs. 2-10
-//             with history, then the 6 walls (step 8), integrates (step 1, R9),
-//             writes the new state at slot j, hashes the new position (step 2 of
-//             the next step) and counts it into its cell for the next sort.
+// One step on the default single-GPU path (§4.2),
+// three kernels:
+//   k_merge   steps 3-4: the stable sort of Eq. 11 as a merge of the few
+//             particles that changed cell into the last sorted order (every
+//             quantity is a count over the mover list the integrator made);
+//             SCCM travels in the sorted positions, the cell offsets (SPEC
+//             cell ranges) are shifted in place.
+//   k_detect  steps 5-6: one thread per sorted slot scans the 27 cells of
+//             Eq. 12 with the fp64-defined contact predicate (R14) and writes
+//             its contact list and its warp-flattened (base, count) word.
+//   k_force   steps 7-8, 1 and the next step's 2: a warp per 32 sorted slots
+//             deals its contacts 32 per round to all lanes (Eqs. 2-10 with the
+//             tangential history remapped through the old slots, Eq. 7), then
+//             each particle adds its contacts in candidate order, applies the
+//             walls, integrates, writes its state at the sorted slot (step 4's
+//             reorder), hashes the new position and lists itself if it changed
+//             cell.
+// The first step after dem_set_particles (and a step whose movers overflow
+// the list) sorts by counting instead: k_count/k_tile_sum/k_scan_apply (the
+// scan is the offset array), k_scatter, k_rank. Slab ranks add the exchange
+// kernels (k_xwait, k_xappend, k_xpack_*, k_xpublish).
 // All arithmetic of the step runs here; the host only enqueues.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
 
 #include "dem_internal.h"
+
+#ifndef DEM_ABLATIONS  // 1: also build the ablation kernels (libdem_ablations.so)
+#define DEM_ABLATIONS 0
+#endif
 
 namespace dem {
 
@@ -344,14 +352,12 @@ constexpr int kItems = 4;
 __global__ void __launch_bounds__(256)
     k_scatter(int64_t n, const uint32_t* __restrict__ nslots, const uint32_t* __restrict__ key,
               const uint32_t* __restrict__ prank, const uint32_t* __restrict__ off,
-              uint32_t* __restrict__ tmp, unsigned long long* status_next, uint32_t* ctr_next,
-              uint32_t ntiles_next, const DevErr* err) {
+              uint32_t* __restrict__ tmp, const DevErr* err) {
   pdl_enter();
   // error word, slot count and the first loads go out together (loads below
   // the capacity n are always in bounds; entries past nslots are ignored)
   const uint32_t e = ld_volatile(&err->code);
   const int64_t ns = (int64_t)__ldg(nslots);  // this step's input slots
-  const int64_t tid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t k[kItems], r[kItems], o[kItems];
 #pragma unroll
@@ -361,9 +367,6 @@ __global__ void __launch_bounds__(256)
     r[u] = i < n ? __ldg(&prank[i]) : 0u;
   }
   if (e != 0u) return;
-  // reset the other parity's scan state for the next step
-  for (int64_t t = tid; t < ntiles_next; t += (int64_t)gridDim.x * blockDim.x) status_next[t] = 0ull;
-  if (tid == 0) *ctr_next = 0u;
   n = min(n, ns);
 #pragma unroll
   for (int u = 0; u < kItems; ++u) o[u] = base + (int64_t)u * blockDim.x < n ? __ldg(&off[k[u]]) : 0u;
@@ -879,7 +882,8 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
   }
 }
 
-// ---- variant 1: one thread per sorted particle for the whole step ---------
+#if DEM_ABLATIONS  // (built into libdem_ablations.so only)
+// ---- ablation: one thread per sorted particle for the whole step ----------
 // The paper's mapping ("Assign the i-th thread to the SCM[i]-th
 // particle"): each thread loops over its candidates and evaluates its own
 // contacts, so a warp idles on the lanes without a contact (§6's "quarter").
@@ -957,6 +961,8 @@ __global__ void __launch_bounds__(128) k_sweep_tpp(StepBuffers b, DevGrid g, Dev
   }
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, ncnt, overflow, lookup);
 }
+
+#endif  // DEM_ABLATIONS
 
 // ---- default path: k_detect (steps 5-6) then k_force (steps 7-8, 1) -------
 // k_detect: one light thread per sorted particle scans its 27-cell candidates
@@ -1441,6 +1447,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
+#if DEM_ABLATIONS  // (libdem_ablations.so only)
 // k_force_lane (configuration "lanes"): one thread per sorted particle walks
 // its own compacted contact list (k_detect's, so §6's divergence of contacts
 // among candidates stays out of it; what remains is the spread of list
@@ -1540,7 +1547,7 @@ __global__ void __launch_bounds__(kLanesThreads, DEM_LANES_MINB)
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
 }
 
-// ---- half-list path (default): Newton's third law -------------------------
+// ---- half-list ablation (DEM_F_HALF_LISTS): Newton's third law ----------
 // Eq. 3/Eq. 4 with the R1 orientation make the pair force antisymmetric and
 // the unscaled torque n x F_t symmetric, bitwise (P11): F_ji = -F_ij,
 // δ_t,ji = -δ_t,ij, T_j = r_j Tc, T_i = r_i Tc. So each contact pair is
@@ -1790,6 +1797,8 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
   finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, min(nup + nlow, K), overflow,
                                lookup);
 }
+
+#endif  // DEM_ABLATIONS
 
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
@@ -2263,6 +2272,8 @@ __global__ void __launch_bounds__(256) k_analyze(StepBuffers b, DevGrid g, uint3
 
 // ------------------------------------------------------------ launchers ----
 
+bool ablations_built() { return DEM_ABLATIONS != 0; }
+
 static inline unsigned blocks_for(int64_t n, int threads) {
   return (unsigned)((n + threads - 1) / threads);
 }
@@ -2325,14 +2336,12 @@ int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, 
   return K_SCAN;
 }
 
-int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b, uint32_t ntiles_next) {
+int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b) {
   const int64_t per = 256 * kItems;
   int64_t blocks = (n + per - 1) / per;
-  const int64_t need = ((int64_t)ntiles_next + 255) / 256;
-  if (blocks < need) blocks = need;
   if (blocks < 1) blocks = 1;
   launch_pdl(k_scatter, (unsigned)blocks, 256, 0, st, n, b.nslots, b.key_in, b.prank, b.off, b.tmp,
-             b.scan_status_next, b.scan_ctr_next, ntiles_next, b.err);
+             b.err);
   return K_SCATTER;
 }
 
@@ -2370,6 +2379,8 @@ template <int MODEL, bool DIAG>
 static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                            const DevGrid& g, const DevPhys& ph, int variant) {
   const uint32_t N = (uint32_t)n;
+  if (variant == 1 || variant == 4) {
+#if DEM_ABLATIONS
   if (variant == 1) {  // the paper's mapping, one fused kernel
     if (ph.nmat > 1 || ph.nplates > 0)
       launch_pdl(k_sweep_tpp<MODEL, DIAG, true>, blocks_for(n, 128), 128, 0, st, b, g, ph, N, K);
@@ -2381,6 +2392,8 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     if (mat) launch_pdl(k_force_lane<MODEL, DIAG, true>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
     else if (K == kForceKC) launch_pdl(k_force_lane<MODEL, DIAG, false, kForceKC>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
     else launch_pdl(k_force_lane<MODEL, DIAG, false>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
+  }
+#endif
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;
@@ -2401,14 +2414,17 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
 
 int launch_detect_half(cudaStream_t st, int64_t n, uint32_t K, const StepBuffers& b,
                        const DevGrid& g) {
+#if DEM_ABLATIONS
   if (n <= 0) return K_DETECT;
   cudaMemsetAsync(b.lcount, 0, sizeof(uint32_t) * n, st);
   k_detect_half<<<blocks_for(n, 256), 256, 0, st>>>(b, g, (uint32_t)n, K);
+#endif
   return K_DETECT;
 }
 
 int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuffers& b,
                 const DevGrid& g, const DevPhys& ph) {
+#if DEM_ABLATIONS
   if (n <= 0) return K_SWEEP;
   const bool mat = ph.nmat > 1 || ph.nplates > 0;
   const unsigned grid = blocks_for(n, 128);
@@ -2420,11 +2436,13 @@ int launch_pair(cudaStream_t st, int64_t n, uint32_t K, int model, const StepBuf
     else k_pair<1, false><<<grid, 128, 0, st>>>(b, g, ph, (uint32_t)n, K);
   }
   // (one warp per 32 owned slots, 4 warps per block)
+#endif
   return K_SWEEP;
 }
 
 int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
                   const StepBuffers& b, const DevGrid& g, const DevPhys& ph) {
+#if DEM_ABLATIONS
   if (n <= 0) return K_FINISH;
   const uint32_t N = (uint32_t)n;
   const bool mat = ph.nmat > 1 || ph.nplates > 0;
@@ -2440,6 +2458,7 @@ int launch_finish(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
     else DEM_FIN(1, false);
   }
 #undef DEM_FIN
+#endif
   return K_FINISH;
 }
 

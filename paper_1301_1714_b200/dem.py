@@ -19,6 +19,9 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
+# the ablation kernels (the paper's fused thread-per-particle mapping, half
+# lists, one lane per particle) live in a second build of the same sources
+ABLATIONS_PATH = os.environ.get("DEM_LIB_ABLATIONS") or os.path.join(HERE, "libdem_ablations.so")
 
 DEM_ABI_VERSION = 3
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
@@ -93,17 +96,16 @@ class DemError(RuntimeError):
         self.code = code
 
 
-_lib = None
+_libs = {}
 
 
-def lib() -> C.CDLL:
-    """Load libdem.so; raise loudly if it has not been built."""
-    global _lib
-    if _lib is None:
-        if not os.path.exists(LIB_PATH):
-            raise ImportError(f"{LIB_PATH} is missing: build it with "
+def lib(path: str = LIB_PATH) -> C.CDLL:
+    """Load libdem.so (or the ablation build); raise loudly if it has not been built."""
+    if path not in _libs:
+        if not os.path.exists(path):
+            raise ImportError(f"{path} is missing: build it with "
                               "`python -m paper_1301_1714_b200.build` (nvcc, sm_100a)")
-        L = C.CDLL(LIB_PATH)
+        L = C.CDLL(path)
         P, I64, I32, VP = C.c_void_p, C.c_int64, C.c_int32, C.c_void_p
         L.dem_create.argtypes = [C.POINTER(DemParams), C.POINTER(VP)]
         L.dem_destroy.argtypes = [VP]
@@ -125,8 +127,8 @@ def lib() -> C.CDLL:
         L.dem_strerror.restype = C.c_char_p
         L.dem_last_error.argtypes = [VP]
         L.dem_last_error.restype = C.c_char_p
-        _lib = L
-    return _lib
+        _libs[path] = L
+    return _libs[path]
 
 
 def _f32(x) -> float:
@@ -221,7 +223,8 @@ class Dem:
     def __init__(self, sp, *, flags: int = 0, device: int = 0, stream=None,
                  torch_allocator: bool = True, radius: Optional[float] = None,
                  density: float = 2500.0, rank: int = 0, world: int = 1):
-        L = lib()
+        ablation = flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES)
+        L = self.L = lib(ABLATIONS_PATH if ablation else LIB_PATH)
         self._keep = []
         alloc_p = None
         stream_ptr = None
@@ -264,11 +267,11 @@ class Dem:
     # ------------------------------------------------------------------
     def _check(self, rc: int, where: str):
         if rc != DEM_OK:
-            raise DemError(rc, where, lib().dem_last_error(self.h).decode())
+            raise DemError(rc, where, self.L.dem_last_error(self.h).decode())
 
     def close(self):
         if getattr(self, "h", None):
-            lib().dem_destroy(self.h)
+            self.L.dem_destroy(self.h)
             self.h = None
 
     def __del__(self):
@@ -297,7 +300,7 @@ class Dem:
         mat = _Arg(material, np.uint32, device=device)
         P = DemParticles(DEM_MEM_DEVICE if device else DEM_MEM_HOST, *(a.ptr for a in args),
                          None, None, mat.ptr)
-        self._check(lib().dem_set_particles(self.h, n, C.byref(P)), "dem_set_particles")
+        self._check(self.L.dem_set_particles(self.h, n, C.byref(P)), "dem_set_particles")
         self.n = n if self.world == 1 else int(self.stats()["n"])
 
     def set_contacts(self, id_i, id_j, dt3):
@@ -307,43 +310,43 @@ class Dem:
         a = _Arg(id_i, np.uint32, device=device)
         b = _Arg(id_j, np.uint32, device=device)
         d = _Arg(dt3, np.float32, device=device)
-        self._check(lib().dem_set_contacts(self.h, DEM_MEM_DEVICE if device else DEM_MEM_HOST,
+        self._check(self.L.dem_set_contacts(self.h, DEM_MEM_DEVICE if device else DEM_MEM_HOST,
                                            m, a.ptr, b.ptr, d.ptr), "dem_set_contacts")
 
     # --------------------------------------------------------- step ----
     def step(self, nsteps: int = 1):
         """dem_step: advance nsteps timesteps."""
-        self._check(lib().dem_step(self.h, int(nsteps)), "dem_step")
+        self._check(self.L.dem_step(self.h, int(nsteps)), "dem_step")
         if self.world > 1:
             self.n = int(self.stats()["n"])
 
     def sync(self):
-        self._check(lib().dem_sync(self.h), "dem_sync")
+        self._check(self.L.dem_sync(self.h), "dem_sync")
 
     def profile(self, enable: bool = True):
-        self._check(lib().dem_profile(self.h, 1 if enable else 0), "dem_profile")
+        self._check(self.L.dem_profile(self.h, 1 if enable else 0), "dem_profile")
 
     # -------------------------------------------------------- slabs ----
     def exchange_handle(self) -> bytes:
         """dem_exchange_handle: 64-byte CUDA IPC handle of this rank's exchange region."""
         buf = C.create_string_buffer(64)
-        self._check(lib().dem_exchange_handle(self.h, buf), "dem_exchange_handle")
+        self._check(self.L.dem_exchange_handle(self.h, buf), "dem_exchange_handle")
         return buf.raw
 
     def exchange_ptr(self) -> int:
         p = C.c_void_p()
-        self._check(lib().dem_exchange_ptr(self.h, C.byref(p)), "dem_exchange_ptr")
+        self._check(self.L.dem_exchange_ptr(self.h, C.byref(p)), "dem_exchange_ptr")
         return p.value
 
     def connect(self, left: Optional[bytes], right: Optional[bytes]):
         """dem_connect: the neighbours' IPC handles (None at the domain ends)."""
         lb = C.create_string_buffer(left, 64) if left else None
         rb = C.create_string_buffer(right, 64) if right else None
-        self._check(lib().dem_connect(self.h, lb, rb), "dem_connect")
+        self._check(self.L.dem_connect(self.h, lb, rb), "dem_connect")
 
     def connect_local(self, left: Optional["Dem"], right: Optional["Dem"]):
         """dem_connect_ptrs: same-process neighbours."""
-        self._check(lib().dem_connect_ptrs(self.h, left.exchange_ptr() if left else None,
+        self._check(self.L.dem_connect_ptrs(self.h, left.exchange_ptr() if left else None,
                                            right.exchange_ptr() if right else None),
                     "dem_connect_ptrs")
 
@@ -380,7 +383,7 @@ class Dem:
                          ptr("omega"), ptr("radius"), ptr("mass"), ptr("id"), ptr("force"),
                          ptr("torque"), ptr("material"))
         nout = C.c_int64()
-        self._check(lib().dem_get_state(self.h, order, n, C.byref(P), C.byref(nout)),
+        self._check(self.L.dem_get_state(self.h, order, n, C.byref(P), C.byref(nout)),
                     "dem_get_state")
         return out
 
@@ -392,21 +395,21 @@ class Dem:
         if out is not None:
             oi, oj, od = out
             cap = min(len(oi), len(oj), len(od))
-            rc = lib().dem_get_contacts(self.h, DEM_MEM_HOST, cap, oi.ctypes.data, oj.ctypes.data,
+            rc = self.L.dem_get_contacts(self.h, DEM_MEM_HOST, cap, oi.ctypes.data, oj.ctypes.data,
                                         od.ctypes.data, C.byref(m))
             if rc == DEM_OK:
                 k = int(m.value)
                 return oi[:k], oj[:k], od[:k]
             if rc != DEM_EINVAL:
                 self._check(rc, "dem_get_contacts")
-        rc = lib().dem_get_contacts(self.h, DEM_MEM_HOST, 0, None, None, None, C.byref(m))
+        rc = self.L.dem_get_contacts(self.h, DEM_MEM_HOST, 0, None, None, None, C.byref(m))
         if rc not in (DEM_OK, DEM_EINVAL):
             self._check(rc, "dem_get_contacts")
         cap = int(m.value)
         id_i = np.empty(cap, np.uint32)
         id_j = np.empty(cap, np.uint32)
         dt3 = np.empty((cap, 3), np.float32)
-        self._check(lib().dem_get_contacts(self.h, DEM_MEM_HOST, cap, id_i.ctypes.data,
+        self._check(self.L.dem_get_contacts(self.h, DEM_MEM_HOST, cap, id_i.ctypes.data,
                                            id_j.ctypes.data, dt3.ctypes.data, C.byref(m)),
                     "dem_get_contacts")
         k = int(m.value)
@@ -416,19 +419,19 @@ class Dem:
         """dem_get_grid -> (key = CM of the current state, perm = SCCM of the
         last sort, off = cell offsets of the last sort)."""
         nc = C.c_int64()
-        self._check(lib().dem_get_grid(self.h, 0, None, None, None, C.byref(nc)), "dem_get_grid")
+        self._check(self.L.dem_get_grid(self.h, 0, None, None, None, C.byref(nc)), "dem_get_grid")
         ncells = int(nc.value)
         key = np.empty(self.n, np.uint32)
         perm = np.empty(self.n, np.uint32)
         off = np.empty(ncells + 1, np.uint32)
-        self._check(lib().dem_get_grid(self.h, max(self.n, ncells + 1), key.ctypes.data,
+        self._check(self.L.dem_get_grid(self.h, max(self.n, ncells + 1), key.ctypes.data,
                                        perm.ctypes.data, off.ctypes.data, C.byref(nc)),
                     "dem_get_grid")
         return key, perm, off
 
     def stats(self) -> dict:
         s = DemStats()
-        self._check(lib().dem_get_stats(self.h, C.byref(s)), "dem_get_stats")
+        self._check(self.L.dem_get_stats(self.h, C.byref(s)), "dem_get_stats")
         return dict(n=s.n, ncells=s.ncells, dims=tuple(s.dims), cell_edge=s.cell_edge,
                     steps=s.steps, contacts=s.contacts, max_contacts_seen=s.max_contacts_seen,
                     launches=s.launches, graph_launches=s.graph_launches,
@@ -442,7 +445,7 @@ class Dem:
         """The paper's §6 quantities for the last step (dem_analyze), raw
         counts plus the ratios the paper argues with."""
         a = DemAnalysis()
-        self._check(lib().dem_analyze(self.h, C.byref(a)), "dem_analyze")
+        self._check(self.L.dem_analyze(self.h, C.byref(a)), "dem_analyze")
         n = max(a.n, 1)
         return dict(
             n=a.n, candidates=a.candidates, max_candidates=a.max_candidates,

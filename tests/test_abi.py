@@ -64,3 +64,22 @@ def test_no_cpu_fallback_without_device(libdem):
     with pytest.raises(dem.DemError) as e:
         dem.Dem(scenes.SimParams(), torch_allocator=False)
     assert e.value.code == dem.DEM_ECUDA
+
+
+def test_ablations_only_in_their_build(libdem):
+    """The product library carries only the default path: the ablation flags
+    (the paper's fused mapping, half lists, one lane per particle) are
+    rejected there and accepted by libdem_ablations.so, which exports the
+    same symbols."""
+    from paper_1301_1714_b200 import scenes
+    abl = dem.lib(dem.ABLATIONS_PATH)
+    for s in dem.exported_symbols():
+        assert hasattr(abl, s)
+    for f in (dem.DEM_F_THREAD_PER_PARTICLE, dem.DEM_F_HALF_LISTS, dem.DEM_F_FORCE_LANES):
+        p = dem.params_from(scenes.SimParams(), flags=f)
+        h = C.c_void_p()
+        assert libdem.dem_create(C.byref(p), C.byref(h)) == dem.DEM_EINVAL
+        rc = abl.dem_create(C.byref(p), C.byref(h))
+        assert rc != dem.DEM_EINVAL  # (DEM_ECUDA without a device)
+        if rc == dem.DEM_OK:
+            abl.dem_destroy(h)

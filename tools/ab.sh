@@ -4,7 +4,7 @@
 cd "$(dirname "$0")/.."
 mkdir -p gpurun_out
 TAG=${TAG:-ab}
-python -c "import __graft_entry__ as g; g.build()" > gpurun_out/build_${TAG}.log 2>&1
+python -c "from paper_1301_1714_b200 import build as B; B.build()" > gpurun_out/build_${TAG}.log 2>&1
 if [ -n "$TESTS" ]; then
   timeout ${TEST_TIMEOUT:-1200} python -m pytest tests -m gpu -x -q ${PYTEST_K:+-k "$PYTEST_K"} > gpurun_out/pytest_${TAG}.log 2>&1
   echo "pytest rc=$?" >> gpurun_out/pytest_${TAG}.log
