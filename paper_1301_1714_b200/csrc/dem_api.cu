@@ -751,10 +751,11 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   memcpy(&rmax, &hp.rmax_bits, 4);
   const uint32_t rmin_bits = ~hp.rmin_cbits;
   memcpy(&rmin, &rmin_bits, 4);
-  // one radius: the candidate test's S² is a constant (slab ranks may receive
-  // migrants of another set, so only a single GPU uses it)
-  h->mono_r = (n > 0 && !h->slab && rmin == rmax && !(h->p.flags & DEM_F_GENERAL_DETECT)) ? rmax
-                                                                                          : 0.f;
+  // one radius: the candidate test's S² is a constant and the sorted
+  // positions carry old slots. Slab ranks are each given the whole set, so
+  // they all see the same radii; dem_connect refuses a neighbour whose set
+  // said otherwise (XLayout::mono_bits)
+  h->mono_r = (n > 0 && rmin == rmax && !(h->p.flags & DEM_F_GENERAL_DETECT)) ? rmax : 0.f;
   const double hmin = 2.0 * (double)rmax * (1.0 + std::ldexp(1.0, -10));
   double hc = h->p.cell_edge > 0.0f ? (double)h->p.cell_edge : hmin;
   if (hc < hmin || !(hc > 0.0)) {
@@ -852,6 +853,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     const uint32_t mcap = std::max<uint32_t>(1024, gcap / 4);
     cap = n_own + n_own / 4 + 2 * (int64_t)gcap + 2 * (int64_t)mcap;
     h->xl = XLayout::make(mcap, gcap, h->K);
+    memcpy(&h->xl.mono_bits, &h->mono_r, 4);
   }
   const int64_t ncl = g.ncells;  // cells the scan covers (local + trash in slab mode)
   // 4. buffers (reallocated when the capacity or the grid changes)
@@ -1502,7 +1504,7 @@ static int check_peer_layouts(dem_handle* h) {
     XLayout pl{};
     CUDA_TRY(h, cudaMemcpy(&pl, p, sizeof pl, cudaMemcpyDeviceToHost));
     if (pl.bytes != h->xl.bytes || pl.mig_cap != h->xl.mig_cap ||
-        pl.ghost_cap != h->xl.ghost_cap || pl.K != h->xl.K)
+        pl.ghost_cap != h->xl.ghost_cap || pl.K != h->xl.K || pl.mono_bits != h->xl.mono_bits)
       return fail(h, DEM_EINVAL,
                   "neighbour exchange layout differs (ghost capacity " + std::to_string(pl.ghost_cap) +
                       " vs " + std::to_string(h->xl.ghost_cap) +

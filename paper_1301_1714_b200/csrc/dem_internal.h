@@ -149,11 +149,13 @@ constexpr uint64_t kXRegionHdr = 256;
 struct XLayout {  // byte offsets inside one (direction, parity) block
   uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, bytes;
   uint32_t mig_cap, ghost_cap, K;
+  uint32_t mono_bits;  // the set's one radius (bits; 0: several): neighbours must agree
   __host__ __device__ static XLayout make(uint32_t mig_cap, uint32_t ghost_cap, uint32_t K) {
     XLayout L;
     L.mig_cap = mig_cap;
     L.ghost_cap = ghost_cap;
     L.K = K;
+    L.mono_bits = 0;
     uint64_t o = 0;
     L.header = o;
     o += 256;
