@@ -31,8 +31,9 @@ for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_HALF_LI
 
 def crossers(n_side, gap=3e-8):
     """n_side³ separated spheres just below a cell face, moving +x: all change
-    cell in step 2, so step 3's merge re-sort takes n_side³ movers (512: the
-    rank sort of k_mv_sort, 729: its bitonic sort)."""
+    cell in step 2, so step 3's merge re-sort takes n_side³ movers (512, 729:
+    more events per k_merge block than its shared list; 13,824: more movers
+    than the list holds, so that step is rolled back and redone by counting)."""
     p = S.SimParams(gravity=(0.0, 0.0, 0.0))
     h = 2.0 * S.R * (1.0 + 2.0 ** -10)
     L = (3 * n_side + 4) * h
@@ -46,7 +47,7 @@ def crossers(n_side, gap=3e-8):
     return S.make_scene("crossers", p, pos.astype(np.float32), vel.astype(np.float32))
 
 
-for ns in (8, 9):
+for ns in (8, 9, 24):
     run(crossers(ns), 0, steps=4)
 run(S.C2(S.SimParams(model="simple")), 0)
 mg = S.mixed_gas(800, 10.0, 2, M=3, params=S.SimParams(max_contacts=32))
