@@ -448,10 +448,31 @@ __global__ void __launch_bounds__(256)
 // more than the capacity raises code 12 and the host redoes that step with
 // the counting sort. (Round 1 sorted the movers in one block first and built
 // per-block event tables: 20-30 us on one SM per step on C4.)
-constexpr uint32_t kMergeSpan = 1024;  // slots and cells per k_merge block
+#ifndef DEM_MERGE_SPAN
+#define DEM_MERGE_SPAN 1024
+#endif
+constexpr uint32_t kMergeSpan = DEM_MERGE_SPAN;  // slots and cells per k_merge block
 constexpr int kMergeItems = kMergeSpan / 256;
 constexpr uint32_t kMergeEv = 512;     // in-block events held in shared memory
 
+// two block sums (256 threads) with one pair of barriers
+__device__ __forceinline__ int2 block_sum2(int a, int c, int2* red) {
+#pragma unroll
+  for (int d = 16; d > 0; d >>= 1) {
+    a += __shfl_xor_sync(0xffffffffu, a, d);
+    c += __shfl_xor_sync(0xffffffffu, c, d);
+  }
+  __syncthreads();  // (red reused)
+  if ((threadIdx.x & 31u) == 0u) red[threadIdx.x >> 5] = make_int2(a, c);
+  __syncthreads();
+  int2 s = make_int2(0, 0);
+#pragma unroll
+  for (int w = 0; w < 8; ++w) {
+    s.x += red[w].x;
+    s.y += red[w].y;
+  }
+  return s;
+}
 __device__ __forceinline__ int block_sum(int v, int* red) {  // 256 threads
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) v += __shfl_xor_sync(0xffffffffu, v, d);
@@ -470,6 +491,7 @@ __global__ void __launch_bounds__(256)
             uint32_t* __restrict__ off, DevErr* err, bool sw) {
   pdl_enter();
   __shared__ int red[2][8];
+  __shared__ int2 red2[8];
   __shared__ uint32_t s_ne[2];
   __shared__ int2 s_ev[2][kMergeEv];  // (position, weight): slot events, cell events
   const uint32_t b = blockIdx.x, t = threadIdx.x;
@@ -507,8 +529,11 @@ __global__ void __launch_bounds__(256)
     if (v.y - B0 < kMergeSpan) push(1, v.y, 1);   // new key: cells above c
     if (v.z - B0 < kMergeSpan) push(1, v.z, -1);  // previous key: cells above c'
   }
-  dS = block_sum(dS, red[0]);
-  dC = block_sum(dC, red[1]);
+  {
+    const int2 s2 = block_sum2(dS, dC, red2);
+    dS = s2.x;
+    dC = s2.y;
+  }
   const uint32_t neS = s_ne[0], neC = s_ne[1];
   const bool spill = neS > kMergeEv || neC > kMergeEv;  // (clustered movers: exact slow path)
   // stayers: new slot s + #{x <= s} - #{a <= s}; movers are skipped
