@@ -277,11 +277,12 @@ def run_ours(args):
             dist.barrier()
 
     with torch.cuda.stream(stream):
-        from paper_1301_1714_b200.dem import (DEM_F_FORCE_LANES, DEM_F_HALF_LISTS,
+        from paper_1301_1714_b200.dem import (DEM_F_FORCE_LANES, DEM_F_FORCE_WS, DEM_F_HALF_LISTS,
                                               DEM_F_THREAD_PER_PARTICLE)
         d = Dem(sc.params, device=local, stream=stream, rank=rank, world=world,
                 flags={"full": 0, "half": DEM_F_HALF_LISTS,
-                       "tpp": DEM_F_THREAD_PER_PARTICLE, "lanes": DEM_F_FORCE_LANES}[args.sweep])
+                       "tpp": DEM_F_THREAD_PER_PARTICLE, "lanes": DEM_F_FORCE_LANES,
+                       "ws": DEM_F_FORCE_WS}[args.sweep])
         # every rank passes the whole set; a slab rank keeps its own planes
         if args.config == "C5" and args.c5_prep > 0:
             # C5: the loose polydisperse lattice is compacted under gravity
@@ -395,7 +396,8 @@ def run_ours(args):
             "kernel": {"half": "sweep = k_detect_half + k_pair + k_finish",
                        "full": "sweep = k_detect + k_force",
                        "tpp": "sweep = k_sweep_tpp",
-                       "lanes": "sweep = k_detect + k_force_lane"}[args.sweep],
+                       "lanes": "sweep = k_detect + k_force_lane",
+                       "ws": "sweep = k_detect + k_force_ws"}[args.sweep],
             "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
             "traffic_source": traffic_src,
@@ -521,7 +523,7 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes"],
+    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes", "ws"],
                     help="full contact lists + warp-flattened force rounds (default); half "
                          "lists, each pair once (Newton's third law); or the paper's fused "
                          "thread per particle")

@@ -95,6 +95,8 @@ enum dem_flags {
                                  sorted order. Bit-identical SCCM and offsets */
   DEM_F_FORCE_LANES = 1u << 11, /* force-kernel configuration: one thread per particle over its
                                    contact list (bitwise-identical results) */
+  DEM_F_FORCE_WS = 1u << 12,    /* ablation: warp-specialised force kernel (producer warps load,
+                                   consumer warps compute; bitwise-identical results) */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };

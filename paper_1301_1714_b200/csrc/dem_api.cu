@@ -331,6 +331,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   // lists (Newton's third law) and the paper's fused mapping are ablations
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
                       : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
+                      : (h->fcfg == 3)                         ? 5
                       : (h->fcfg == 2)                         ? 4
                       : (h->fcfg == 1)                         ? 3
                                                                : 2;
@@ -492,7 +493,7 @@ int validate_params(const dem_params* p) {
   if (p->max_contacts > kMaxContacts) return DEM_EINVAL;
   if ((p->flags & DEM_F_HALF_LISTS) && p->max_contacts > 32) return DEM_EINVAL;
   // the ablations live in libdem_ablations.so
-  if ((p->flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES)) &&
+  if ((p->flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES | DEM_F_FORCE_WS)) &&
       !ablations_built())
     return DEM_EINVAL;
   if (p->world_size > 1 && (p->rank < 0 || p->rank >= p->world_size)) return DEM_EINVAL;
@@ -1073,9 +1074,9 @@ int dem_step(dem_handle* h, int64_t nsteps) {
   }
   if (h->fcfg < 0) {  // choose the k_force configuration
     const uint32_t fl = h->p.flags;
-    if (fl & (DEM_F_FORCE_DENSE | DEM_F_FORCE_LIGHT | DEM_F_FORCE_LANES) ||
+    if (fl & (DEM_F_FORCE_DENSE | DEM_F_FORCE_LIGHT | DEM_F_FORCE_LANES | DEM_F_FORCE_WS) ||
         h->p.model != DEM_MODEL_PRACTICAL) {
-      h->fcfg = (fl & DEM_F_FORCE_LANES) ? 2 : (fl & DEM_F_FORCE_LIGHT) ? 1 : 0;
+      h->fcfg = (fl & DEM_F_FORCE_WS) ? 3 : (fl & DEM_F_FORCE_LANES) ? 2 : (fl & DEM_F_FORCE_LIGHT) ? 1 : 0;
     } else {
       // one eager step in the dense configuration, then the history entries
       // per particle it produced (c̄, walls included) decide the rest

@@ -1513,6 +1513,312 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
 }
 
 #if DEM_ABLATIONS  // (libdem_ablations.so only)
+// ---- ablation: warp-specialised k_force (DEM_F_FORCE_WS) ------------------
+// The same step as k_force, split by role. A block holds 4 producer warps
+// (warpgroup 0, registers cut to 40 by setmaxnreg) and 4 consumer warps
+// (warpgroup 1, raised to 88), paired one to one; each pair walks its
+// 32-slot groups (persistent: one wave of blocks, groups strided). The
+// producer does everything that waits on memory: the group's entry data
+// (sorted position, (base, n) word, list entries, owner state through the
+// old slot, the old history count), the owner map and the slot
+// translation, and per round the partner state and predicted δ_t,old entry
+// (cp.async) plus each contact's (owner lane, list index) — into a ring of
+// shared-memory slots, a group header first, then its rounds. The consumer
+// only computes: owner state from the header into registers (broadcast by
+// shuffles), the contact arithmetic (Eqs. 2-10), the owners' accumulation
+// in candidate order, the walls, the integration and the stores. Ring slots
+// are handed over by mbarriers: "full" completes when the producer's
+// copies have landed (cp.async.mbarrier.arrive.noinc) and its plain stores
+// are released (mbarrier.arrive), "empty" when the consumer has read the
+// slot. Same arithmetic and summation order as k_force: bitwise-identical
+// results.
+#ifndef DEM_WS_SLEEP
+#define DEM_WS_SLEEP 200  // ns the producer sleeps between polls of a busy slot
+#endif
+#ifndef DEM_WS_SLOTS
+#define DEM_WS_SLOTS 3
+#endif
+#ifndef DEM_WS_BLOCKS  // blocks per SM; producer / consumer registers follow
+#define DEM_WS_BLOCKS 4
+#endif
+#ifndef DEM_WS_PREG
+#define DEM_WS_PREG 40
+#endif
+#ifndef DEM_WS_CREG
+#define DEM_WS_CREG 88
+#endif
+constexpr int kWsPairs = 4;  // producer/consumer warp pairs per block
+constexpr int kWsSlots = DEM_WS_SLOTS;  // ring slots per pair
+struct WsSlot {
+  float4 f[4][32];    // round: partner pos, vel, omg, δ_t,old entry; header: P, V, W, (meta, s, nold)
+  uint32_t meta[32];  // round: owner lane | list index << 8 (0xFFFFFFFF: no contact)
+};
+struct WsLayout {  // per pair, inside the block's dynamic shared memory
+  uint32_t slots, bars, own, cq, res, bytes;
+  __host__ __device__ static WsLayout make(uint32_t K) {
+    WsLayout L;
+    uint32_t o = 0;
+    L.slots = o;
+    o += kWsSlots * (uint32_t)sizeof(WsSlot);
+    L.bars = o;
+    o += 2 * kWsSlots * 8;  // full[], empty[] mbarriers
+    L.own = o;
+    o += (K * 32 + 15u) & ~15u;  // producer: owner lane of each contact
+    L.cq = o;
+    o += K * 32 * 4;  // producer: partner old slots [k][lane]
+    L.res = o;
+    o += kResW * 24;  // consumer: results window
+    L.bytes = (o + 15u) & ~15u;
+    return L;
+  }
+};
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared.b64 [%0], %1;" ::"r"(smem_u32(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("{.reg .b64 st; mbarrier.arrive.shared.b64 st, [%0];}" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive_cp_async(uint64_t* b) {
+  asm volatile("cp.async.mbarrier.arrive.noinc.shared.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+// the producer's wait for a free slot backs off, so its spinning does not take
+// issue slots from the consumers (it is ahead by construction)
+__device__ __forceinline__ void mbar_wait_backoff(uint64_t* b, uint32_t parity) {
+  uint32_t ok = 0;
+  for (;;) {
+    asm volatile("{.reg .pred p; mbarrier.try_wait.parity.shared.b64 p, [%1], %2; selp.u32 %0, 1, 0, p;}"
+                 : "=r"(ok) : "r"(smem_u32(b)), "r"(parity) : "memory");
+    if (ok) return;
+    __nanosleep(DEM_WS_SLEEP);
+  }
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{.reg .pred p;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared.b64 p, [%0], %1;\n"
+      "@!p bra WAIT_%=;}" ::"r"(smem_u32(b)),
+      "r"(parity)
+      : "memory");
+}
+
+template <int MODEL, bool DIAG, bool MAT, uint32_t KC = 0>
+__global__ void __launch_bounds__(32 * 2 * kWsPairs, DEM_WS_BLOCKS)
+    k_force_ws(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t Kr) {
+  const uint32_t K = KC ? KC : Kr;
+  extern __shared__ __align__(16) uint8_t smem_raw[];
+  const uint32_t err = ld_volatile(&b.err->code);
+  const WsLayout L = WsLayout::make(K);
+  const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  const bool producer = warp < (uint32_t)kWsPairs;
+  const uint32_t pair = producer ? warp : warp - kWsPairs;
+  uint8_t* ps = smem_raw + (size_t)pair * L.bytes;
+  WsSlot* slots = reinterpret_cast<WsSlot*>(ps + L.slots);
+  uint64_t* full = reinterpret_cast<uint64_t*>(ps + L.bars);
+  uint64_t* empty = full + kWsSlots;
+  if (producer && lane == 0) {
+    for (int i = 0; i < kWsSlots; ++i) {
+      mbar_init(&full[i], 64);   // 32 async (copies landed) + 32 plain arrivals
+      mbar_init(&empty[i], 32);  // the consumer's lanes
+    }
+  }
+  __syncthreads();
+  if (err != 0u) return;  // (block-uniform: before any barrier use)
+  uint32_t jlo, jhi;
+  owned_range(b, g, N, jlo, jhi);
+  const uint32_t ngroups = (jhi - jlo + 31u) >> 5;
+  const uint32_t stride = gridDim.x * kWsPairs;
+  const bool sw = b.sw_r > 0.f;
+  uint32_t use = 0;  // ring uses so far (slot = use % kWsSlots, its phase = use / kWsSlots)
+
+  if (producer) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(DEM_WS_PREG));
+    uint8_t* s_own = ps + L.own;
+    uint32_t* s_cq = reinterpret_cast<uint32_t*>(ps + L.cq);
+    auto acquire = [&]() -> WsSlot* {
+      const uint32_t i = use % kWsSlots;
+      if (use >= (uint32_t)kWsSlots) mbar_wait_backoff(&empty[i], ((use / kWsSlots) - 1u) & 1u);
+      return &slots[i];
+    };
+    auto publish = [&]() {
+      uint64_t* f = &full[use % kWsSlots];
+      mbar_arrive_cp_async(f);
+      mbar_arrive(f);
+      ++use;
+    };
+    for (uint32_t grp = blockIdx.x * kWsPairs + pair; grp < ngroups; grp += stride) {
+      const uint32_t j0 = jlo + grp * 32u, j = j0 + lane;
+      const bool valid = j < jhi;
+      float4 P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
+      const uint32_t meta = valid ? __ldcs(&b.ccount[j]) : 0u;
+      uint32_t t_first[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) t_first[u] = valid && (uint32_t)u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
+      const uint32_t s = !valid ? 0u : sw ? __float_as_uint(P.w) : __ldcs(&b.perm[j]);
+      if (sw) P.w = valid ? b.sw_r : 1.f;
+      const uint32_t npair = (meta >> 16) & 0xFFu, mybase = meta & 0xFFFFu;
+      const uint32_t M = __reduce_max_sync(0xffffffffu, mybase + npair);
+      const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+      // the group header: owner position, velocity, spin, (base/n word, old slot, count)
+      WsSlot* hs = acquire();
+      hs->f[0][lane] = P;
+      if (valid) {
+        cp_async16(&hs->f[1][lane], &b.vel_in[s]);
+        cp_async16(&hs->f[2][lane], &b.omg_in[s]);
+      } else {
+        hs->f[1][lane] = make_float4(0.f, 0.f, 0.f, 1.f);
+        hs->f[2][lane] = make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+      reinterpret_cast<uint4*>(&hs->f[3][0])[lane] = make_uint4(meta, s, n_old, 0u);
+      cp_async_commit();
+      publish();
+      // owner map and partner old slots (round 1's scheme, in the producer)
+      for (uint32_t k = 0; k < npair; ++k) s_own[mybase + k] = (uint8_t)lane;
+      for (uint32_t k0 = 0; k0 < npair; k0 += 4) {
+        uint32_t t4[4];
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          t4[u] = k0 == 0 ? t_first[u]
+                          : (k0 + u < npair ? __ldcs(&b.clist[(size_t)(k0 + u) * N + j]) : 0u);
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          if (k0 + u < npair) s_cq[(k0 + u) * 32u + lane] = sw ? t4[u] : __ldg(&b.perm[t4[u]]);
+      }
+      __syncwarp();
+      for (uint32_t r0 = 0; r0 < M; r0 += 32) {
+        const uint32_t m = r0 + lane;
+        const uint32_t ow = m < M ? s_own[m] : 0u;
+        const uint32_t bo = __shfl_sync(0xffffffffu, mybase, ow);
+        const uint32_t so = __shfl_sync(0xffffffffu, s, ow);
+        WsSlot* rs = acquire();
+        if (m < M) {
+          const uint32_t k = m - bo;
+          const uint32_t q = s_cq[k * 32u + ow];
+          cp_async16(&rs->f[0][lane], &b.pos_in[q]);
+          cp_async16(&rs->f[1][lane], &b.vel_in[q]);
+          if (MODEL == 0) {
+            cp_async16(&rs->f[2][lane], &b.omg_in[q]);
+            cp_async16(&rs->f[3][lane], &b.hist_in[hix(so, k, K)]);  // (k < K: in bounds)
+          }
+          rs->meta[lane] = ow | (k << 8);
+        } else {
+          rs->meta[lane] = 0xFFFFFFFFu;
+        }
+        cp_async_commit();
+        publish();
+      }
+      __syncwarp();  // (s_own / s_cq of this group read by all lanes before the next group)
+    }
+    return;
+  }
+
+  // ---------------------------------------------------------------- consumer
+  asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(DEM_WS_CREG));
+  float4* s_r4 = reinterpret_cast<float4*>(ps + L.res);
+  float2* s_r2 = reinterpret_cast<float2*>(ps + L.res + kResW * 16);
+  auto take = [&]() -> const WsSlot* {
+    const uint32_t i = use % kWsSlots;
+    mbar_wait(&full[i], (use / kWsSlots) & 1u);
+    return &slots[i];
+  };
+  auto give = [&]() {
+    mbar_arrive(&empty[use % kWsSlots]);
+    ++use;
+  };
+  for (uint32_t grp = blockIdx.x * kWsPairs + pair; grp < ngroups; grp += stride) {
+    const uint32_t j0 = jlo + grp * 32u, j = j0 + lane;
+    const bool valid = j < jhi;
+    const WsSlot* hs = take();
+    Own o;
+    o.P = hs->f[0][lane];
+    o.V = hs->f[1][lane];
+    o.W = hs->f[2][lane];
+    const uint4 hm = reinterpret_cast<const uint4*>(&hs->f[3][0])[lane];
+    give();
+    const uint32_t meta = hm.x, s = hm.y, n_old = hm.z;
+    const bool overflow = (meta >> 31) != 0u;
+    const uint32_t npair = (meta >> 16) & 0xFFu, mybase = meta & 0xFFFFu;
+    const uint32_t M = __reduce_max_sync(0xffffffffu, mybase + npair);
+    f3 F = mk(0.f, 0.f, 0.f), T = mk(0.f, 0.f, 0.f);
+    for (uint32_t r0 = 0; r0 < M; r0 += 32) {
+      const WsSlot* rs = take();
+      const float4 Q = rs->f[0][lane], VQ = rs->f[1][lane];
+      const float4 WQ = MODEL == 0 ? rs->f[2][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const float4 Hr = MODEL == 0 ? rs->f[3][lane] : make_float4(0.f, 0.f, 0.f, 0.f);
+      const uint32_t cm = rs->meta[lane];
+      give();
+      const uint32_t m = r0 + lane;
+      const uint32_t ow = m < M ? (cm & 0xFFu) : 0u;
+      const uint32_t k = cm >> 8;
+      Own po;
+      po.P.x = __shfl_sync(0xffffffffu, o.P.x, ow);
+      po.P.y = __shfl_sync(0xffffffffu, o.P.y, ow);
+      po.P.z = __shfl_sync(0xffffffffu, o.P.z, ow);
+      po.P.w = __shfl_sync(0xffffffffu, o.P.w, ow);
+      po.V.x = __shfl_sync(0xffffffffu, o.V.x, ow);
+      po.V.y = __shfl_sync(0xffffffffu, o.V.y, ow);
+      po.V.z = __shfl_sync(0xffffffffu, o.V.z, ow);
+      po.V.w = __shfl_sync(0xffffffffu, o.V.w, ow);
+      po.W.x = __shfl_sync(0xffffffffu, o.W.x, ow);
+      po.W.y = __shfl_sync(0xffffffffu, o.W.y, ow);
+      po.W.z = __shfl_sync(0xffffffffu, o.W.z, ow);
+      po.W.w = __shfl_sync(0xffffffffu, o.W.w, ow);
+      const uint32_t so = __shfl_sync(0xffffffffu, s, ow);
+      const uint32_t no = __shfl_sync(0xffffffffu, n_old, ow);
+      f3 Fc = mk(0.f, 0.f, 0.f), Tc = mk(0.f, 0.f, 0.f);
+      if (m < M) {
+        f3 n;
+        float delta;
+        if (!contact_geometry(po.P, Q, n, delta)) {
+          raise_error(b.err, 9u, j0 - jlo + ow, __float_as_uint(po.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu));
+        } else if (MODEL == 0) {
+          const uint32_t pid = __float_as_uint(WQ.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
+          f3 dold;
+          if (k < no && __float_as_uint(Hr.w) == pid)
+            dold = mk(Hr.x, Hr.y, Hr.z);
+          else
+            dold = old_history(b.hist_in, K, so, no, k, pid);
+          f3 dnew;
+          eval_pair_practical<MAT>(po, Q, VQ, WQ, n, delta, dold, ph, Fc, Tc, dnew);
+          __stcs(&b.hist_out[hix((j0 - jlo) + ow, k, K)],
+                 make_float4(dnew.x, dnew.y, dnew.z, __uint_as_float(pid)));
+        } else {
+          const f3 u = mk(VQ.x - po.V.x, VQ.y - po.V.y, VQ.z - po.V.z);
+          Fc = pair_simple(n, delta, u, ph.ksp, ph.kda, ph.ksh);
+        }
+      }
+      const uint32_t w0 = r0 - r0 % kResW;
+      s_r4[r0 - w0 + lane] = make_float4(Fc.x, Fc.y, Fc.z, Tc.x);
+      if (MODEL == 0) s_r2[r0 - w0 + lane] = make_float2(Tc.y, Tc.z);
+      if (r0 + 32 - w0 == kResW || r0 + 32 >= M) {
+        __syncwarp();
+        const uint32_t lo = max(mybase, w0), hi = min(mybase + npair, r0 + 32);
+#pragma unroll 4
+        for (uint32_t x = lo; x < hi; ++x) {
+          const float4 r4 = s_r4[x - w0];
+          F = mk(F.x + r4.x, F.y + r4.y, F.z + r4.z);
+          if (MODEL == 0) {
+            const float2 r2 = s_r2[x - w0];
+            T = mk(T.x + r4.w, T.y + r2.x, T.z + r2.y);
+          }
+        }
+        __syncwarp();
+      }
+    }
+    if (valid) {
+      if (MODEL == 0) T = mk(o.P.w * T.x, o.P.w * T.y, o.P.w * T.z);  // Eq. 3: r_i Σ n × F_t
+      auto lookup = [&](uint32_t pid) -> f3 {
+        return old_history(b.hist_in, K, s, n_old, n_old, pid);
+      };
+      finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
+    }
+  }
+}
+
+#endif  // DEM_ABLATIONS
+
+#if DEM_ABLATIONS  // (libdem_ablations.so only)
 // k_force_lane (configuration "lanes"): one thread per sorted particle walks
 // its own compacted contact list (k_detect's, so §6's divergence of contacts
 // among candidates stays out of it; what remains is the spread of list
@@ -1883,6 +2189,21 @@ void sweep_prepare(uint32_t K) {
   DEM_SET_SMEM(1, false)
   DEM_SET_SMEM(1, true)
 #undef DEM_SET_SMEM
+#if DEM_ABLATIONS
+  const int sws = (int)(WsLayout::make(K).bytes * kWsPairs);
+  cudaFuncSetAttribute(k_force_ws<0, false, false>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<0, false, true>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<0, true, false>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<0, true, true>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, false, false>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, false, true>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, true, false>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, true, true>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<0, false, false, kForceKC>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<0, true, false, kForceKC>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, false, false, kForceKC>, A, sws);
+  cudaFuncSetAttribute(k_force_ws<1, true, false, kForceKC>, A, sws);
+#endif
 }
 
 // --------------------------------------------------------- slab exchange --
@@ -2487,6 +2808,22 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     else if (K == kForceKC) launch_pdl(k_force_lane<MODEL, DIAG, false, kForceKC>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
     else launch_pdl(k_force_lane<MODEL, DIAG, false>, grid, kLanesThreads, 0, st, b, g, ph, N, K);
   }
+#endif
+#if DEM_ABLATIONS
+  } else if (variant == 5) {  // warp-specialised (DEM_F_FORCE_WS, ablation)
+    const bool mat = ph.nmat > 1 || ph.nplates > 0;
+    const uint32_t smem = WsLayout::make(K).bytes * kWsPairs;
+    auto kern = mat ? k_force_ws<MODEL, DIAG, true>
+                    : K == kForceKC ? k_force_ws<MODEL, DIAG, false, kForceKC> : k_force_ws<MODEL, DIAG, false>;
+    int resident = 0, sms = 0, dev = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&resident, kern, 32 * 2 * kWsPairs, smem);
+    if (resident < 1) resident = 1;
+    const int64_t groups = (n + 31) / 32;
+    int64_t grid = (int64_t)resident * sms;
+    if (grid * kWsPairs > groups) grid = (groups + kWsPairs - 1) / kWsPairs;
+    launch_pdl(kern, (unsigned)grid, 32 * 2 * kWsPairs, smem, st, b, g, ph, N, K);
 #endif
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;

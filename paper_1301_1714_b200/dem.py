@@ -36,6 +36,7 @@ DEM_F_FORCE_LIGHT = 256
 DEM_F_GENERAL_DETECT = 512
 DEM_F_FULL_SORT = 1024
 DEM_F_FORCE_LANES = 2048
+DEM_F_FORCE_WS = 4096
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
@@ -223,7 +224,8 @@ class Dem:
     def __init__(self, sp, *, flags: int = 0, device: int = 0, stream=None,
                  torch_allocator: bool = True, radius: Optional[float] = None,
                  density: float = 2500.0, rank: int = 0, world: int = 1):
-        ablation = flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES)
+        ablation = flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS | DEM_F_FORCE_LANES |
+                            DEM_F_FORCE_WS)
         L = self.L = lib(ABLATIONS_PATH if ablation else LIB_PATH)
         self._keep = []
         alloc_p = None
@@ -437,7 +439,7 @@ class Dem:
                     launches=s.launches, graph_launches=s.graph_launches,
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
                     kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
-                    force_cfg={-1: None, 0: "dense", 1: "light", 2: "lanes"}[s.force_cfg],
+                    force_cfg={-1: None, 0: "dense", 1: "light", 2: "lanes", 3: "ws"}[s.force_cfg],
                     full_sorts=s.full_sorts, max_speed=s.max_speed)
 
 

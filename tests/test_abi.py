@@ -75,7 +75,8 @@ def test_ablations_only_in_their_build(libdem):
     abl = dem.lib(dem.ABLATIONS_PATH)
     for s in dem.exported_symbols():
         assert hasattr(abl, s)
-    for f in (dem.DEM_F_THREAD_PER_PARTICLE, dem.DEM_F_HALF_LISTS, dem.DEM_F_FORCE_LANES):
+    for f in (dem.DEM_F_THREAD_PER_PARTICLE, dem.DEM_F_HALF_LISTS, dem.DEM_F_FORCE_LANES,
+              dem.DEM_F_FORCE_WS):
         p = dem.params_from(scenes.SimParams(), flags=f)
         h = C.c_void_p()
         assert libdem.dem_create(C.byref(p), C.byref(h)) == dem.DEM_EINVAL

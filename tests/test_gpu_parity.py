@@ -10,6 +10,7 @@ import pytest
 from oracle import oracle as orc
 from paper_1301_1714_b200 import scenes as S
 from paper_1301_1714_b200.dem import (DEM_ECOINCIDENT, DEM_EESCAPED, DEM_ENONFINITE, DEM_EOVERFLOW, DEM_F_DIAG, DEM_F_FORCE_DENSE,
+                                      DEM_F_FORCE_WS,
                                       DEM_F_FORCE_LANES, DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
                                       DEM_F_HALF_LISTS,
                                       DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
@@ -168,7 +169,7 @@ def test_merge_resort_equals_counting_sort_bitwise():
 # ------------------------------------------------------ T2 one step -------
 
 @pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
-                                     DEM_F_GENERAL_DETECT, DEM_F_HALF_LISTS,
+                                     DEM_F_FORCE_WS, DEM_F_GENERAL_DETECT, DEM_F_HALF_LISTS,
                                      DEM_F_THREAD_PER_PARTICLE])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
@@ -494,11 +495,11 @@ def test_force_configs_bitwise(name):
     order, so whole runs agree bitwise."""
     sc = S.C2() if name == "C2" else scenes_small()[1]
     runs = []
-    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES):
+    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_FORCE_WS):
         d = make(sc, flags=DEM_F_DIAG | f)
         d.step(12)
         runs.append((d.get_state(forces=True), contacts_dict(d), d.stats()["force_cfg"]))
-    assert [r[2] for r in runs] == ["dense", "light", "lanes"]
+    assert [r[2] for r in runs] == ["dense", "light", "lanes", "ws"]
     for r in runs[1:]:
         for k in ("pos", "vel", "omega", "id", "force", "torque"):
             assert np.array_equal(runs[0][0][k], r[0][k]), k

@@ -6,7 +6,7 @@ import sys
 sys.path.insert(0, ".")
 from paper_1301_1714_b200 import scenes as S  # noqa: E402
 import numpy as np  # noqa: E402
-from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LANES,  # noqa: E402
+from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LANES, DEM_F_FORCE_WS,  # noqa: E402
                                       DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS, DEM_F_NO_GRAPH,
                                       DEM_F_THREAD_PER_PARTICLE, Dem)
 
@@ -24,7 +24,7 @@ def run(sc, flags, steps=3, material=None):
     d.close()
 
 
-for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_HALF_LISTS,
+for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_FORCE_WS, DEM_F_HALF_LISTS,
           DEM_F_THREAD_PER_PARTICLE):
     run(S.C1(), f)
 
