@@ -278,11 +278,12 @@ def run_ours(args):
 
     with torch.cuda.stream(stream):
         from paper_1301_1714_b200.dem import (DEM_F_FORCE_LANES, DEM_F_FORCE_WS, DEM_F_HALF_LISTS,
-                                              DEM_F_THREAD_PER_PARTICLE)
+                                              DEM_F_SPLIT_SWEEP, DEM_F_THREAD_PER_PARTICLE)
         d = Dem(sc.params, device=local, stream=stream, rank=rank, world=world,
                 flags={"full": 0, "half": DEM_F_HALF_LISTS,
                        "tpp": DEM_F_THREAD_PER_PARTICLE, "lanes": DEM_F_FORCE_LANES,
-                       "ws": DEM_F_FORCE_WS}[args.sweep])
+                       "ws": DEM_F_FORCE_WS, "split": DEM_F_SPLIT_SWEEP}[args.sweep]
+                | args.extra_flags)
         # every rank passes the whole set; a slab rank keeps its own planes
         if args.config == "C5" and args.c5_prep > 0:
             # C5: the loose polydisperse lattice is compacted under gravity
@@ -391,6 +392,7 @@ def run_ours(args):
             "n_particles_rank0": n_local,
             "l2": l2_note(b_step * n_local),
             "dt": sc.params.dt, "sweep": args.sweep,
+            **({"extra_flags": args.extra_flags} if args.extra_flags else {}),
             "untimed_graph_build_steps": 6,  # after the W warm-up steps (both parities, 1 and 2 steps)
             "c_bar_after_graph_reps": (st_graph["contacts"] / max(1, st_graph["n"])
                                        if sc.params.model == "practical" else 0.0),
@@ -399,7 +401,9 @@ def run_ours(args):
         "roofline": {
             "bound": "hbm",
             "kernel": {"half": "sweep = k_detect_half + k_pair + k_finish",
-                       "full": "sweep = k_detect + k_force",
+                       "full": ("sweep = k_force with fused detection" if kernel_avg["detect"] == 0
+                                else "sweep = k_detect + k_force"),
+                       "split": "sweep = k_detect + k_force",
                        "tpp": "sweep = k_sweep_tpp",
                        "lanes": "sweep = k_detect + k_force_lane",
                        "ws": "sweep = k_detect + k_force_ws"}[args.sweep],
@@ -528,10 +532,12 @@ def main():
     ap.add_argument("--config", default="C4", choices=["C1", "C2", "C3", "C4", "C5"])
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes", "ws"],
+    ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes", "ws", "split"],
                     help="full contact lists + warp-flattened force rounds (default); half "
                          "lists, each pair once (Newton's third law); or the paper's fused "
                          "thread per particle")
+    ap.add_argument("--extra-flags", type=int, default=0,
+                    help="dem_flags OR-ed into the handle's (A/B runs, e.g. a force configuration)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5, help="timed K-step graph regions (median)")
     ap.add_argument("--c5-prep", type=int, default=40000,

@@ -39,7 +39,7 @@
 extern "C" {
 #endif
 
-#define DEM_ABI_VERSION 3u
+#define DEM_ABI_VERSION 4u
 
 /* Error codes. */
 enum dem_error {
@@ -97,6 +97,10 @@ enum dem_flags {
                                    contact list (bitwise-identical results) */
   DEM_F_FORCE_WS = 1u << 12,    /* ablation: warp-specialised force kernel (producer warps load,
                                    consumer warps compute; bitwise-identical results) */
+  DEM_F_SPLIT_SWEEP = 1u << 13, /* detection (steps 5-6) as its own kernel writing contact lists
+                                   to HBM; default with one radius: each force warp detects its
+                                   own contacts into shared memory first (one fused kernel).
+                                   Same contact lists and bitwise-identical results */
 };
 
 enum dem_mem_kind { DEM_MEM_HOST = 0, DEM_MEM_DEVICE = 1 };
@@ -203,6 +207,9 @@ typedef struct {
                             the others merge the few movers into the last sorted order */
   double max_speed;      /* max |v| of the current state [m/s]: the last step moved no
                             particle farther than max_speed * dt (the §5 termination test) */
+  int32_t fused_sweep;   /* 1: detection (steps 5-6) runs inside the force kernel (one radius,
+                            dense configuration, no DEM_F_SPLIT_SWEEP); 0: k_detect + k_force */
+  int32_t reserved;
 } dem_stats;
 
 /* Kernel indices of dem_stats.kernel_ms. Counting sort: DEM_K_HASH cell

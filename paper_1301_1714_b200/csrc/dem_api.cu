@@ -259,10 +259,24 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   return s;
 }
 
+// one radius, dense force configuration: detection runs inside the force
+// kernel (k_force<..., FUSED>) unless DEM_F_SPLIT_SWEEP. Measured per
+// configuration (profiles/r2_history.md): fused wins where the warps have
+// many contact rounds (C3: 0.0894 -> 0.0816 ms/step); on the light bed (C4)
+// the split kernels win (0.611 vs 0.631: the detection loop then runs at the
+// force kernel's occupancy and L1 share)
+bool fused_sweep(const dem_handle* h) {
+  return h->mono_r > 0.f && !(h->p.flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS |
+                                            DEM_F_SPLIT_SWEEP)) &&
+         h->fcfg == 0;
+}
+
 int kernels_per_step(const dem_handle* h, bool full = false) {
   // counting sort: scan (2) + scatter + rank (+ k_count in merge mode); merge: 2
   const int sort = h->merge ? (full ? 5 : 1) : 4;
-  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3 : 2) +
+  return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3
+          : fused_sweep(h)                         ? 1
+                                                   : 2) +
          sort + (h->slab ? 5 : 0);
 }
 
@@ -329,10 +343,14 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   }
   // default: full contact lists (k_detect + warp-flattened k_force); the half
   // lists (Newton's third law) and the paper's fused mapping are ablations
+  // one radius, dense/light: detection fused into the force kernel unless
+  // DEM_F_SPLIT_SWEEP (6: fused dense, 7: fused light)
+  const bool fused = fused_sweep(h);
   const int variant = (h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1
                       : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
                       : (h->fcfg == 3)                         ? 5
                       : (h->fcfg == 2)                         ? 4
+                      : fused                                  ? 6
                       : (h->fcfg == 1)                         ? 3
                                                                : 2;
   if (variant == 0) {  // half lists: detect, pair, finish
@@ -347,7 +365,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     rec(K_FINISH, false);
     h->launches += 2;
   } else {
-    if (variant >= 2) {
+    if (variant >= 2 && variant < 6) {
       rec(K_DETECT, true);
       launch_detect(h->stream, h->cap, h->K, s, h->g, h->mono_r, variant >= 3);
       rec(K_DETECT, false);
@@ -1399,6 +1417,7 @@ int dem_get_stats(dem_handle* h, dem_stats* out) {
   out->launches = h->launches;
   out->graph_launches = h->graph_launches;
   out->force_cfg = h->fcfg;
+  out->fused_sweep = fused_sweep(h) ? 1 : 0;
   out->full_sorts = (int32_t)h->full_sorts;
   for (int k = 0; k < 8; ++k) {
     out->kernel_ms[k] = h->kernel_ms[k];

@@ -785,11 +785,13 @@ template <int MODEL, bool DIAG, bool MAT = true, class LookupFn>
 __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevGrid& g,
                                                 const DevPhys& ph, uint32_t N, uint32_t K,
                                                 uint32_t oj, const Own& o, f3 F, f3 T,
-                                                uint32_t ncnt, bool overflow, LookupFn lookup) {
+                                                uint32_t ncnt, bool overflow, LookupFn lookup,
+                                                uint32_t sk_known = 0xFFFFFFFFu) {
   const uint32_t j = oj;  // output slot
   // this step's SCM at j (merge re-sort): the key of the sorted position itself
   // (the sort ordered these very coordinates by it), so no SCM array is kept
-  const uint32_t sk = b.mv.list_out ? cell_key(g, o.P.x, o.P.y, o.P.z) : 0u;
+  const uint32_t sk = !b.mv.list_out ? 0u : sk_known != 0xFFFFFFFFu ? sk_known
+                                                                    : cell_key(g, o.P.x, o.P.y, o.P.z);
   const float ri = o.P.w, mi = o.V.w;
   const uint32_t my_id = __float_as_uint(o.W.w) & (MAT ? ph.idmask : 0xFFFFFFFFu);
   // step 8: walls -x,+x,-y,+y,-z,+z as particles of infinite radius (R11)
@@ -1035,15 +1037,17 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // MONO also means pos_sorted[t].w holds the old slot SCCM[t] (b.sw_r): the
 // list stores that (what k_force reads partner state by) and the radius is
 // b.sw_r.
-template <bool EXACT, bool MONO = false>
+// The list goes to `out` with stride `ostride` (k_detect: clist + j, N; the
+// fused sweep: its warp's shared-memory list, [k][lane]).
+template <bool EXACT, bool MONO = false, bool SMEM = false>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
-                                                int cx, int cy, int cz, uint32_t j, uint32_t N,
+                                                int cx, int cy, int cz, uint32_t j,
+                                                uint32_t* out, uint32_t ostride,
                                                 uint32_t K, float& amb, float S2c = 0.f) {
   const uint32_t xa = cx > 0 ? (uint32_t)cx - 1u : 0u;
   const uint32_t xb = cx < g.nx - 1 ? (uint32_t)cx + 1u : (uint32_t)g.nx - 1u;
   const uint32_t nxy = (uint32_t)g.nx * (uint32_t)g.ny;
   uint32_t npair = 0;
-  uint32_t* out = b.clist + j;
   // MONO fast scan: candidates with d² < S²(1 + 16u) take the hit branch, and
   // those of them above S²(1 - 16u) are in the band (the EXACT scan's own
   // thresholds), so a non-touching candidate costs one compare
@@ -1095,8 +1099,11 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
             asm volatile("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f00000000, %3, p;}"
                          : "=f"(amb) : "f"(d2), "f"(S2lo), "f"(amb));
           }
-          if (npair < K) __stcg(out, qs);
-          out += N;
+          if (npair < K) {
+            if (SMEM) *out = qs;
+            else __stcg(out, qs);
+          }
+          out += ostride;
           ++npair;
         }
       }
@@ -1147,8 +1154,9 @@ __global__ void __launch_bounds__(DEM_DETECT_TPB, (LIGHT ? DEM_DETECT_MINB_LIGHT
     const int cy = cell_coord(P.y, g.lo[1], g.inv_h, g.ny);
     const int cz = cell_coord(P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
     float amb = -1.f;
-    npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
-    if (amb >= 0.f) npair = detect_scan<true, MONO>(b, g, P, cx, cy, cz, j, N, K, amb, S2c);
+    npair = detect_scan<false, MONO>(b, g, P, cx, cy, cz, j, b.clist + j, N, K, amb, S2c);
+    if (amb >= 0.f)
+      npair = detect_scan<true, MONO>(b, g, P, cx, cy, cz, j, b.clist + j, N, K, amb, S2c);
   }
   // the warp — the 32 sorted slots of one k_force warp — scans its (capped)
   // counts: each slot's first contact in the warp's flattened order, its
@@ -1207,7 +1215,9 @@ struct WarpSmemLayout {
   uint32_t bytes, pf, cq, res, own, ost, base, slot, nold;
   // fixed-size regions first, so their offsets are compile-time constants;
   // the K-dependent ones (partner slots, owner map) last
-  __host__ __device__ static WarpSmemLayout make(uint32_t K, int cfg) {
+  // fused (k_force<..., FUSED>): the warp's own detection fills the partner
+  // list per (k, lane), as in the dense configuration
+  __host__ __device__ static WarpSmemLayout make(uint32_t K, int cfg, bool fused = false) {
     WarpSmemLayout L;
     uint32_t o = 0;
     L.pf = o;
@@ -1223,7 +1233,7 @@ struct WarpSmemLayout {
     L.nold = o;
     o += 32 * 4;
     L.cq = o;
-    o += (cfg == kForceLight ? ForceCfg<kForceLight>::kChunk : K * 32) * 4;  // partner old slots
+    o += (cfg == kForceLight && !fused ? ForceCfg<kForceLight>::kChunk : K * 32) * 4;  // partner old slots
     L.own = o;
     o += ((K * 32 + 15u) & ~15u);  // owner lane of each contact
     L.bytes = (o + 15u) & ~15u;
@@ -1316,15 +1326,19 @@ __device__ __forceinline__ void cp_async_wait() {
 
 // KC: the list capacity K as a compile-time constant (0: the runtime Kr), so
 // the shared-memory layout and the history addressing fold to constants.
-template <int MODEL, bool DIAG, int CFG, bool MAT, uint32_t KC = 0>
+// FUSED (one radius only, b.sw_r > 0): the warp detects its own contacts
+// first (steps 5-6, the scan of k_detect into its shared-memory list) — no
+// k_detect launch, no contact list or (base, n) words in HBM.
+template <int MODEL, bool DIAG, int CFG, bool MAT, uint32_t KC = 0, bool FUSED = false>
 __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t Kr) {
   using C = ForceCfg<CFG>;
+  constexpr uint32_t kChunk = FUSED ? 0u : C::kChunk;  // 0: partner slots per (k, lane)
   const uint32_t K = KC ? KC : Kr;
   pdl_enter();
   extern __shared__ __align__(16) uint8_t smem_raw[];
   const uint32_t err = ld_volatile(&b.err->code);  // checked once the first loads are out
-  const WarpSmemLayout L = WarpSmemLayout::make(K, CFG);
+  const WarpSmemLayout L = WarpSmemLayout::make(K, CFG, FUSED);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   uint8_t* ws = smem_raw + (size_t)warp * L.bytes;
   float4* pf = reinterpret_cast<float4*>(ws + L.pf);                 // [field][lane]
@@ -1349,24 +1363,54 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   // the count are never used), so they do not wait for it.
   // one radius (b.sw_r > 0): the sorted position carries the old slot SCCM[j]
   // in .w and the lists hold partner old slots, so no SCCM gathers at all
-  const bool sw = b.sw_r > 0.f;
+  const bool sw = FUSED || b.sw_r > 0.f;
   Own o;
   o.P = valid ? __ldg(&b.pos_sorted[j]) : make_float4(0.f, 0.f, 0.f, 1.f);
-  const uint32_t meta = valid ? __ldcs(&b.ccount[j]) : 0u;  // k_detect's (base, n) word
+  const uint32_t meta = valid && !FUSED ? __ldcs(&b.ccount[j]) : 0u;  // k_detect's (base, n) word
   uint32_t t_first[kForceFirst];
 #pragma unroll
   for (int u = 0; u < kForceFirst; ++u)
-    t_first[u] = valid && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
+    t_first[u] = valid && !FUSED && u < K ? __ldcs(&b.clist[(size_t)u * N + j]) : 0u;
   const uint32_t s = !valid ? 0u : sw ? __float_as_uint(o.P.w) : __ldcs(&b.perm[j]);
   if (sw) o.P.w = valid ? b.sw_r : 1.f;
   if (err != 0u) return;  // warp-uniform (one load per warp instruction)
-  const bool overflow = (meta >> 31) != 0u;
-  const uint32_t npair = (meta >> 16) & 0xFFu;
-  const uint32_t mybase = meta & 0xFFFFu;
-  const uint32_t M = __reduce_max_sync(0xffffffffu, mybase + npair);
   o.V = valid ? __ldg(&b.vel_in[s]) : make_float4(0.f, 0.f, 0.f, 1.f);
   o.W = valid ? __ldg(&b.omg_in[s]) : make_float4(0.f, 0.f, 0.f, 0.f);
   const uint32_t n_old = (MODEL == 0 && valid) ? min(__ldcs(&b.cnt_in[s]), K) : 0u;
+  bool overflow;
+  uint32_t npair, mybase, M;
+  uint32_t sk = 0xFFFFFFFFu;  // this step's key of the own position (fused: from the detection)
+  if (FUSED) {
+    // steps 5-6 for the warp's 32 slots (k_detect's scan, the list kept in
+    // shared memory) while the owner state loads above are in flight
+    uint32_t np = 0;
+    if (valid) {
+      const int cx = cell_coord(o.P.x, g.lo[0], g.inv_h, g.nx);
+      const int cy = cell_coord(o.P.y, g.lo[1], g.inv_h, g.ny);
+      const int cz = cell_coord(o.P.z, g.lo[2], g.inv_h, g.nz_global) - g.zlo;
+      sk = (uint32_t)cx + (uint32_t)g.nx * ((uint32_t)cy + (uint32_t)g.ny * (uint32_t)cz);
+      const float S = b.sw_r + b.sw_r, S2c = S * S;
+      float amb = -1.f;
+      np = detect_scan<false, true, true>(b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
+      if (amb >= 0.f)  // a candidate in the ±16u band: the exact rescan (R14)
+        np = detect_scan<true, true, true>(b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
+    }
+    overflow = np > K;
+    npair = min(np, K);
+    uint32_t incl = npair;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint32_t v = __shfl_up_sync(0xffffffffu, incl, d);
+      if (lane >= (uint32_t)d) incl += v;
+    }
+    mybase = incl - npair;
+    M = __shfl_sync(0xffffffffu, incl, 31);
+  } else {
+    overflow = (meta >> 31) != 0u;
+    npair = (meta >> 16) & 0xFFu;
+    mybase = meta & 0xFFFFu;
+    M = __reduce_max_sync(0xffffffffu, mybase + npair);
+  }
   s_slot[lane] = s;
   s_nold[lane] = n_old;
   if (C::kOwnSmem) {
@@ -1380,9 +1424,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   // dense, all of them into s_cq[k*32 + lane]; light, those of the warp's
   // contacts [c0, c0 + kChunk) into s_cq[m - c0]
   auto translate = [&](uint32_t c0) {
-    const uint32_t klo = C::kChunk ? (c0 > mybase ? c0 - mybase : 0u) : 0u;
-    const uint32_t khi = C::kChunk ? min(npair, c0 + C::kChunk > mybase ? c0 + C::kChunk - mybase : 0u)
-                                   : npair;
+    const uint32_t klo = kChunk ? (c0 > mybase ? c0 - mybase : 0u) : 0u;
+    const uint32_t khi = kChunk ? min(npair, c0 + kChunk > mybase ? c0 + kChunk - mybase : 0u)
+                                : npair;
     for (uint32_t k0 = klo; k0 < khi; k0 += 4) {
       uint32_t t4[4], q4[4];
 #pragma unroll
@@ -1394,10 +1438,10 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       for (int u = 0; u < 4; ++u) q4[u] = k0 + u < khi ? (sw ? t4[u] : __ldg(&b.perm[t4[u]])) : 0u;
 #pragma unroll
       for (int u = 0; u < 4; ++u)
-        if (k0 + u < khi) s_cq[C::kChunk ? mybase + k0 + u - c0 : (k0 + u) * 32 + lane] = q4[u];
+        if (k0 + u < khi) s_cq[kChunk ? mybase + k0 + u - c0 : (k0 + u) * 32 + lane] = q4[u];
     }
   };
-  translate(0);
+  if (!FUSED) translate(0);  // (fused: the detection wrote the old slots already)
   __syncwarp();
 
   // prefetch of round r0's partner state + predicted δ_t,old entry (the
@@ -1408,7 +1452,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     if (m < M) {
       const uint32_t ow = s_own[m];
       const uint32_t k = m - s_base[ow];
-      const uint32_t q = C::kChunk ? s_cq[m % C::kChunk] : s_cq[k * 32 + ow];
+      const uint32_t q = kChunk ? s_cq[m % kChunk] : s_cq[k * 32 + ow];
       cp_async16_s(pf_s, &b.pos_in[q]);
       cp_async16_s(pf_s + 32u * 16u, &b.vel_in[q]);
       if (MODEL == 0) {
@@ -1429,7 +1473,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
     const float4 Q = pf[lane], VQ = pf[32 + lane], WQ = pf[64 + lane], Hr = pf[96 + lane];
     if (r0 + 32 < M) {
       __syncwarp();
-      if (C::kChunk && (r0 + 32) % C::kChunk == 0) {  // the next round opens a new chunk
+      if (kChunk && (r0 + 32) % kChunk == 0) {  // the next round opens a new chunk
         translate(r0 + 32);
         __syncwarp();
       }
@@ -1509,7 +1553,7 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
   auto lookup = [&](uint32_t pid) -> f3 {  // walls: after the pair contacts in the old list
     return old_history(b.hist_in, K, s, n_old, n_old, pid);
   };
-  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup);
+  finish_particle<MODEL, DIAG, MAT>(b, g, ph, N, K, j - jlo, o, F, T, npair, overflow, lookup, sk);
 }
 
 #if DEM_ABLATIONS  // (libdem_ablations.so only)
@@ -2176,6 +2220,8 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
 void sweep_prepare(uint32_t K) {
   const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
   const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
+  const int fd = (int)(WarpSmemLayout::make(K, kForceDense, true).bytes * kSweepWarps);
+  const int fl = (int)(WarpSmemLayout::make(K, kForceLight, true).bytes * kSweepWarps);
   const auto A = cudaFuncAttributeMaxDynamicSharedMemorySize;
 #define DEM_SET_SMEM(MODEL, DIAG)                                     \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false>, A, sd); \
@@ -2183,7 +2229,13 @@ void sweep_prepare(uint32_t K) {
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false>, A, sl); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true>, A, sl); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, kForceKC>, A, sd); \
-  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, A, sl);
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, A, sl); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, true, 0, true>, A, fd); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, 0, true>, A, fd); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, kForceKC, true>, A, fd); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true, 0, true>, A, fl); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, 0, true>, A, fl); \
+  cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, kForceKC, true>, A, fl);
   DEM_SET_SMEM(0, false)
   DEM_SET_SMEM(0, true)
   DEM_SET_SMEM(1, false)
@@ -2825,6 +2877,19 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     if (grid * kWsPairs > groups) grid = (groups + kWsPairs - 1) / kWsPairs;
     launch_pdl(kern, (unsigned)grid, 32 * 2 * kWsPairs, smem, st, b, g, ph, N, K);
 #endif
+  } else if (variant >= 6) {  // fused detection + warp-flattened rounds (6: dense, 7: light)
+    const int cfg = variant == 7 ? kForceLight : kForceDense;
+    const uint32_t smem = WarpSmemLayout::make(K, cfg, true).bytes * kSweepWarps;
+    const unsigned grid = blocks_for(n, 32 * kSweepWarps), block = 32 * kSweepWarps;
+    const bool mat = ph.nmat > 1 || ph.nplates > 0;
+    const bool k16 = K == kForceKC;
+#define DEM_FUSED(CFG)                                                                          \
+  (mat ? launch_pdl(k_force<MODEL, DIAG, CFG, true, 0, true>, grid, block, smem, st, b, g, ph, N, K) \
+   : k16 ? launch_pdl(k_force<MODEL, DIAG, CFG, false, kForceKC, true>, grid, block, smem, st, b, g, ph, N, K) \
+         : launch_pdl(k_force<MODEL, DIAG, CFG, false, 0, true>, grid, block, smem, st, b, g, ph, N, K))
+    if (cfg == kForceLight) DEM_FUSED(kForceLight);
+    else DEM_FUSED(kForceDense);
+#undef DEM_FUSED
   } else {  // full contact lists, warp-flattened contact rounds (2: dense, 3: light)
     const int cfg = variant == 3 ? kForceLight : kForceDense;
     const uint32_t smem = WarpSmemLayout::make(K, cfg).bytes * kSweepWarps;

@@ -23,7 +23,7 @@ LIB_PATH = os.environ.get("DEM_LIB") or os.path.join(HERE, "libdem.so")
 # lists, one lane per particle) live in a second build of the same sources
 ABLATIONS_PATH = os.environ.get("DEM_LIB_ABLATIONS") or os.path.join(HERE, "libdem_ablations.so")
 
-DEM_ABI_VERSION = 3
+DEM_ABI_VERSION = 4
 DEM_OK, DEM_EINVAL, DEM_EABI, DEM_ENOMEM, DEM_ECUDA, DEM_ENCCL = 0, -1, -2, -3, -4, -5
 DEM_EOVERFLOW, DEM_ENONFINITE, DEM_EESCAPED, DEM_ECOINCIDENT, DEM_ESTATE = -6, -7, -8, -9, -10
 DEM_EPEER = -11
@@ -37,6 +37,7 @@ DEM_F_GENERAL_DETECT = 512
 DEM_F_FULL_SORT = 1024
 DEM_F_FORCE_LANES = 2048
 DEM_F_FORCE_WS = 4096
+DEM_F_SPLIT_SWEEP = 8192
 DEM_MEM_HOST, DEM_MEM_DEVICE = 0, 1
 DEM_ORDER_INTERNAL, DEM_ORDER_ID = 0, 1
 KERNELS = ("hash", "scan", "scatter", "rank", "sweep", "other", "detect", "finish")
@@ -80,7 +81,8 @@ class DemStats(C.Structure):
                 ("max_contacts_seen", C.c_int64), ("launches", C.c_int64),
                 ("graph_launches", C.c_int64), ("kernel_ms", C.c_double * 8),
                 ("kernel_count", C.c_int64 * 8), ("force_cfg", C.c_int32),
-                ("full_sorts", C.c_int32), ("max_speed", C.c_double)]
+                ("full_sorts", C.c_int32), ("max_speed", C.c_double),
+                ("fused_sweep", C.c_int32), ("reserved", C.c_int32)]
 
 
 class DemAnalysis(C.Structure):
@@ -440,7 +442,8 @@ class Dem:
                     kernel_ms={k: s.kernel_ms[i] for i, k in enumerate(KERNELS)},
                     kernel_count={k: s.kernel_count[i] for i, k in enumerate(KERNELS)},
                     force_cfg={-1: None, 0: "dense", 1: "light", 2: "lanes", 3: "ws"}[s.force_cfg],
-                    full_sorts=s.full_sorts, max_speed=s.max_speed)
+                    full_sorts=s.full_sorts, max_speed=s.max_speed,
+                    fused_sweep=bool(s.fused_sweep))
 
 
     def analyze(self) -> dict:

@@ -13,7 +13,8 @@ from paper_1301_1714_b200.dem import (DEM_ECOINCIDENT, DEM_EESCAPED, DEM_ENONFIN
                                       DEM_F_FORCE_WS,
                                       DEM_F_FORCE_LANES, DEM_F_FORCE_LIGHT, DEM_F_FULL_SORT, DEM_F_GENERAL_DETECT,
                                       DEM_F_HALF_LISTS,
-                                      DEM_F_NO_GRAPH, DEM_F_THREAD_PER_PARTICLE, DEM_ORDER_ID,
+                                      DEM_F_NO_GRAPH, DEM_F_SPLIT_SWEEP, DEM_F_THREAD_PER_PARTICLE,
+                                      DEM_ORDER_ID,
                                       Dem, DemError)
 
 from .parity import assert_T2_forces, assert_T2_history, contacts_dict, oracle_inputs
@@ -170,7 +171,9 @@ def test_merge_resort_equals_counting_sort_bitwise():
 
 @pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
                                      DEM_F_FORCE_WS, DEM_F_GENERAL_DETECT, DEM_F_HALF_LISTS,
-                                     DEM_F_THREAD_PER_PARTICLE])
+                                     DEM_F_THREAD_PER_PARTICLE, DEM_F_SPLIT_SWEEP,
+                                     DEM_F_SPLIT_SWEEP | DEM_F_FORCE_DENSE,
+                                     DEM_F_SPLIT_SWEEP | DEM_F_FORCE_LIGHT])
 @pytest.mark.parametrize("idx", [0, 1])
 def test_one_step_T2(idx, variant):
     sc = scenes_small()[idx]
@@ -196,7 +199,7 @@ def test_one_step_T2(idx, variant):
 
 
 @pytest.mark.parametrize("variant", [0, DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
-                                     DEM_F_THREAD_PER_PARTICLE])
+                                     DEM_F_THREAD_PER_PARTICLE, DEM_F_SPLIT_SWEEP])
 @pytest.mark.parametrize("flags", ["clamp", "truncate", "clamp+truncate", "none"])
 def test_flags_one_step_T2(flags, variant):
     """Readings R3 (DEM_F_CLAMP_FN) and R4 (DEM_F_TRUNCATE_DT) and a scalar
@@ -224,15 +227,20 @@ def test_bench_instantiation_bitwise(name):
     (state and δ_t), in the same force configuration."""
     sc = S.C3() if name == "C3" else S.C4(scale=4)
     runs = []
-    for flags in (DEM_F_DIAG, 0):
+    # the bench's kernel (no DIAG; C3: detection fused into it), its DIAG twin, and the
+    # split path (k_detect writing lists to HBM, then k_force)
+    for flags in (DEM_F_DIAG, 0, DEM_F_SPLIT_SWEEP):
         d = make(sc, flags=flags)
         d.step(12)
-        runs.append((d.get_state(), contacts_dict(d), d.stats()["force_cfg"]))
-    assert runs[0][2] == runs[1][2] == ("dense" if name == "C3" else "light")
-    for k in ("pos", "vel", "omega", "id"):
-        assert np.array_equal(runs[0][0][k], runs[1][0][k]), k
-    assert runs[0][1].keys() == runs[1][1].keys()
-    assert all(np.array_equal(runs[0][1][x], runs[1][1][x]) for x in runs[0][1])
+        runs.append((d.get_state(), contacts_dict(d), d.stats()["force_cfg"],
+                     d.stats()["fused_sweep"]))
+    assert {r[2] for r in runs} == {"dense" if name == "C3" else "light"}
+    assert [r[3] for r in runs] == ([True, True, False] if name == "C3" else [False] * 3)
+    for r in runs[1:]:
+        for k in ("pos", "vel", "omega", "id"):
+            assert np.array_equal(runs[0][0][k], r[0][k]), k
+        assert runs[0][1].keys() == r[1].keys()
+        assert all(np.array_equal(runs[0][1][x], r[1][x]) for x in runs[0][1])
 
 
 def test_one_step_T2_C2_both_models():
@@ -298,6 +306,8 @@ def test_touching_pairs_in_fp32_band(mono):
     in_band = np.abs(d2f.astype(np.float64) - S2) <= 16 * 2.0 ** -24 * S2
     assert in_band.sum() >= 40 and exact[in_band].any() and not exact[in_band].all()
     for flags in (DEM_F_DIAG | DEM_F_FORCE_DENSE, DEM_F_DIAG | DEM_F_FORCE_LIGHT,
+                  DEM_F_DIAG | DEM_F_SPLIT_SWEEP | DEM_F_FORCE_DENSE,
+                  DEM_F_DIAG | DEM_F_SPLIT_SWEEP | DEM_F_FORCE_LIGHT,
                   DEM_F_DIAG | DEM_F_FORCE_LANES, DEM_F_DIAG | DEM_F_GENERAL_DETECT,
                   DEM_F_DIAG | DEM_F_THREAD_PER_PARTICLE, DEM_F_DIAG | DEM_F_HALF_LISTS):
         d = make(sc, flags=flags)
@@ -495,11 +505,12 @@ def test_force_configs_bitwise(name):
     order, so whole runs agree bitwise."""
     sc = S.C2() if name == "C2" else scenes_small()[1]
     runs = []
-    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_FORCE_WS):
+    for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_FORCE_WS,
+              DEM_F_FORCE_DENSE | DEM_F_SPLIT_SWEEP, DEM_F_FORCE_LIGHT | DEM_F_SPLIT_SWEEP):
         d = make(sc, flags=DEM_F_DIAG | f)
         d.step(12)
         runs.append((d.get_state(forces=True), contacts_dict(d), d.stats()["force_cfg"]))
-    assert [r[2] for r in runs] == ["dense", "light", "lanes", "ws"]
+    assert [r[2] for r in runs] == ["dense", "light", "lanes", "ws", "dense", "light"]
     for r in runs[1:]:
         for k in ("pos", "vel", "omega", "id", "force", "torque"):
             assert np.array_equal(runs[0][0][k], r[0][k]), k
@@ -690,7 +701,8 @@ def plate_gas(seed=5, n=2500, materials=False):
 
 
 @pytest.mark.parametrize("variant", [DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES,
-                                     DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE])
+                                     DEM_F_HALF_LISTS, DEM_F_THREAD_PER_PARTICLE,
+                                     DEM_F_SPLIT_SWEEP])
 @pytest.mark.parametrize("kind", ["plates", "plates+materials", "slit"])
 def test_plates_one_step_T2(kind, variant):
     """Plate contacts (faces, edges, corners, both sides) bit-exactly the
@@ -864,9 +876,15 @@ def test_profile_mode_times_every_kernel():
     d.profile(True)
     d.step(10)
     st = d.stats()
-    for k in ("rank", "sweep", "detect"):
+    for k in ("rank", "sweep"):
         assert st["kernel_count"][k] == 10
         assert st["kernel_ms"][k] > 0
+    # C2 (one radius, dense): detection inside the force kernel; split: k_detect
+    assert st["fused_sweep"] and st["kernel_count"]["detect"] == 0
+    sp = make(sc, flags=DEM_F_SPLIT_SWEEP)
+    sp.profile(True)
+    sp.step(10)
+    assert not sp.stats()["fused_sweep"] and sp.stats()["kernel_count"]["detect"] == 10
     # the counting sort (cell counts, scan, scatter) runs only in the first
     # step; the merge re-sort's one kernel is timed as rank afterwards
     assert st["kernel_count"]["hash"] == 1 and st["kernel_count"]["scan"] == 1
