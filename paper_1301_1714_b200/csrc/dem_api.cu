@@ -96,7 +96,7 @@ struct dem_handle {
   uint32_t xbase = 0;  // exchange tag offset of the current set (same sequence on every rank)
   uint32_t nsets = 0;
   XState* xs = nullptr;
-  uint32_t* xtiles = nullptr;  // pack tile counts [4][ntiles]
+  uint32_t* xtiles = nullptr;  // pack tile counts + totals, per state parity [2][xtc_stride]
 
   int cur = 0;
   int64_t steps = 0;  // completed steps since set_particles (== device step_ctr)
@@ -235,6 +235,9 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.ccount = h->ccount;
   s.nslots = h->nslots;
   s.flags = h->flags;
+  s.xtc = h->xtiles ? h->xtiles + (size_t)b * xtc_stride(h->cap) : nullptr;
+  s.xtc_next = h->xtiles ? h->xtiles + (size_t)(b ^ 1) * xtc_stride(h->cap) : nullptr;
+  s.xntiles = xtc_ntiles(h->cap);
   s.cpos = h->cpos;
   s.lcount = h->lcount;
   s.llist = h->llist;
@@ -277,7 +280,7 @@ int kernels_per_step(const dem_handle* h, bool full = false) {
   return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3
           : fused_sweep(h)                         ? 1
                                                    : 2) +
-         sort + (h->slab ? 5 : 0);
+         sort + (h->slab ? 2 : 0);
 }
 
 // Enqueue one step from parity b: the sort (counting: scan, scatter, rank;
@@ -314,7 +317,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
                    h->xright ? h->xright + kXRegionHdr : nullptr, h->xl, h->xs,
                    h->nslots);
     rec(K_OTHER, false);
-    h->launches += 2;
+    h->launches += 1;
   }
   if (h->merge && !full) {  // merge re-sort
     rec(K_RANK, true);
@@ -378,10 +381,9 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
   h->launches += 1;
   if (h->slab) {  // pack and publish the next step's migrants and ghosts
     rec(K_OTHER, true);
-    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xtiles,
-                 h->xs, 0);
+    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 0);
     rec(K_OTHER, false);
-    h->launches += 3;
+    h->launches += 1;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
@@ -910,7 +912,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     h->mov_cap = h->slab ? 0u : mover_cap(cap);
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
-            dalloc(h, &h->xtiles, 4 * ((N + 1023) / 1024) + 4);
+            dalloc(h, &h->xtiles, 2 * (size_t)xtc_stride(N));
     }
     // defined contents everywhere (once per allocation): several kernels load
     // ahead of their bounds checks (entries past a count, slots past nslots)
@@ -1010,7 +1012,12 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     sb.flags = h->flags;
     sb.off = h->off;
     sb.err = h->err;
-    launch_xpack(st, cap, sb, g, h->K, h->xregion + kXRegionHdr, h->xl, h->xtiles, h->xs, 1);
+    // the first step (state parity 0) accumulates into parity 0's counts:
+    // the set state's counts take parity 1's, and everything starts at zero
+    CUDA_TRY(h, cudaMemsetAsync(h->xtiles, 0, 2 * sizeof(uint32_t) * xtc_stride(cap), st));
+    sb.xtc = h->xtiles + xtc_stride(cap);
+    sb.xtc_next = h->xtiles;
+    launch_xpack(st, cap, sb, g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 1);
     DevErr e{};
     CUDA_TRY(h, cudaMemcpyAsync(&e, h->err, sizeof e, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));

@@ -106,6 +106,12 @@ struct StepBuffers {
   const uint32_t* nslots;  // device: input slots of this step (owned + appended)
   uint32_t* flags;     // slab mode: per output slot, bit0/1 migrate to left/right neighbour,
                        // bit2/3 ghost for left/right neighbour
+  uint32_t* xtc;       // slab mode: [4][xntiles] flagged outputs per category and pack tile
+                       // (kXTile output slots), [xntiles] flagged outputs per tile, then the
+                       // number of tiles with any: accumulated by this step's integrator,
+                       // read by its pack (one buffer per state parity)
+  uint32_t* xtc_next;  // the other parity's: zeroed by this step's pack for the next step
+  uint32_t xntiles;
   // half-list path (Newton's third law): the pair (i, t) is
   // evaluated once, by its lower sorted slot i ("upper" contact of i)
   uint8_t* cpos;       // [k*N + i]: position of i in t's lower list
@@ -143,6 +149,11 @@ struct XHeader {
   uint32_t n_ghost; // ghosts packed
   uint32_t pad;
 };
+constexpr uint32_t kXTile = 1024;  // output slots per pack tile (256 threads x 4)
+// per state parity: tile counts [4][ntiles], per-tile sums [ntiles], the
+// number of tiles with flagged outputs (+ padding)
+inline uint32_t xtc_ntiles(int64_t cap) { return (uint32_t)((cap + kXTile - 1) / kXTile); }
+inline uint32_t xtc_stride(int64_t cap) { return 5u * xtc_ntiles(cap) + 4u; }
 // An exchange region = a header holding the writer's XLayout (read by the
 // neighbours at connect time) + 4 blocks (direction x parity).
 constexpr uint64_t kXRegionHdr = 256;
@@ -182,7 +193,8 @@ struct XLayout {  // byte offsets inside one (direction, parity) block
 struct XState {  // device scratch of the exchange of one step
   uint32_t n_out;      // output slots of the last step (base of the appended slots)
   uint32_t appended[4];  // migrants from left, right; ghosts from left, right
-  uint32_t pad[3];
+  uint32_t done;       // pack blocks finished this step (the last one publishes)
+  uint32_t pad[2];
 };
 
 enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5,
@@ -252,7 +264,7 @@ int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 // Slab exchange. `mine` = this rank's exchange region; `left`/`right` = the
 // neighbours' regions (peer pointers, NULL at the ends of the domain).
 int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
-                 uint8_t* mine, XLayout L, uint32_t* tile_counts, XState* xs, int initial);
+                 uint8_t* mine, XLayout L, XState* xs, int initial);
 int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
                    uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
                    uint32_t* nslots_out);

@@ -20,7 +20,7 @@
 // The first step after dem_set_particles (and a step whose movers overflow
 // the list) sorts by counting instead: k_count/k_tile_sum/k_scan_apply (the
 // scan is the offset array), k_scatter, k_rank. Slab ranks add the exchange
-// kernels (k_xwait, k_xappend, k_xpack_*, k_xpublish).
+// kernels (k_xappend at the step start, k_xpack_write at the end).
 // All arithmetic of the step runs here; the host only enqueues.
 #include <cuda_runtime.h>
 #include <math.h>
@@ -875,7 +875,7 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
   const bool finite = isfinite(x) && isfinite(y) && isfinite(z) && isfinite(vx) &&
                       isfinite(vy) && isfinite(vz) && isfinite(wx) && isfinite(wy) &&
                       isfinite(wz);
-  uint32_t k2 = 0;
+  uint32_t k2 = 0, xf = 0;  // (xf: slab exchange flags)
   if (!finite) {
     raise_error(b.err, 7u, j, my_id);
   } else {
@@ -897,7 +897,28 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       if (cz == g.z0) f |= 4u;
       if (cz == g.z1 - 1) f |= 8u;
       b.flags[j] = f;
+      xf = f;
     }
+  }
+  if (g.slab) {
+    // the pack's tile counts per category (tiles of kXTile output slots):
+    // one atomic per (warp, tile, category) with flagged lanes, so the pack
+    // needs no counting pass (most warps have none: boundary planes only)
+    const uint32_t act = __activemask();
+    const uint32_t tile = j / kXTile;
+    const uint32_t peers = __match_any_sync(act, tile);
+    const uint32_t leader = __ffs(peers) - 1;
+    const uint32_t any = __ballot_sync(act, xf != 0u) & peers;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const uint32_t m = __ballot_sync(act, (xf >> q) & 1u) & peers;
+      if (m && lane_id() == leader) atomicAdd(&b.xtc[(uint32_t)q * b.xntiles + tile], __popc(m));
+    }
+    // per-tile sum; the first contribution to a tile counts the tile (the
+    // pack's last writing block publishes)
+    if (any && lane_id() == leader &&
+        atomicAdd(&b.xtc[4u * b.xntiles + tile], __popc(any)) == 0u)
+      atomicAdd(&b.xtc[5u * b.xntiles], 1u);
   }
   st_out(&b.key_out[j], k2);
   if (b.mv.list_out) {  // merge re-sort: list the particles that change cell (warp-aggregated)
@@ -2274,10 +2295,6 @@ __device__ __forceinline__ uint32_t ld_acquire_sys(const uint32_t* p) {
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void st_release_sys(uint32_t* p, uint32_t v) {
-  asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
-}
-
 __device__ __forceinline__ int global_cz(const DevGrid& g, float z) {
   return cell_coord(z, g.lo[2], g.inv_h, g.nz_global);
 }
@@ -2304,19 +2321,18 @@ __global__ void k_flags(int64_t n, const float4* pos, DevGrid g, uint32_t* flags
   flags[i] = (cz == g.z0 ? 4u : 0u) | (cz == g.z1 - 1 ? 8u : 0u);
 }
 
-constexpr int kXTile = 1024;  // output slots per pack tile (256 threads x 4)
 
 __device__ __forceinline__ uint32_t owned_out(const StepBuffers& b, const DevGrid& g) {
   return __ldg(&b.off[g.own_c1]) - __ldg(&b.off[g.own_c0]);
 }
 
-// counts of the four categories per tile; also records n_out for the next unpack
+// counts of the four categories per tile, for the state dem_set_particles
+// publishes (in a step the integrator accumulates them: finish_particle)
 __global__ void __launch_bounds__(256) k_xpack_count(StepBuffers b, DevGrid g, uint32_t* tc,
-                                                     uint32_t ntiles, XState* xs, int initial) {
+                                                     uint32_t ntiles, XState* xs) {
   __shared__ uint32_t s_c[4];
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t n_out = initial ? xs->n_out : owned_out(b, g);
-  if (blockIdx.x == 0 && threadIdx.x == 0 && !initial) xs->n_out = n_out;
+  const uint32_t n_out = xs->n_out;
   if (threadIdx.x < 4) s_c[threadIdx.x] = 0;
   __syncthreads();
   uint32_t c[4] = {0, 0, 0, 0};
@@ -2336,23 +2352,39 @@ __global__ void __launch_bounds__(256) k_xpack_count(StepBuffers b, DevGrid g, u
   }
   __syncthreads();
   if (threadIdx.x < 4) tc[threadIdx.x * ntiles + blockIdx.x] = s_c[threadIdx.x];
+  if (threadIdx.x == 0) {
+    const uint32_t sum = s_c[0] + s_c[1] + s_c[2] + s_c[3];
+    tc[4 * ntiles + blockIdx.x] = sum;
+    if (sum) atomicAdd(&tc[5 * ntiles], 1u);  // tiles with flagged outputs
+  }
 }
 
-// deterministic placement: prefix over earlier tiles + in-tile rank (slot order)
+// deterministic placement: prefix over earlier tiles + in-tile rank (slot
+// order); the last block to finish publishes the header counts and the tag
+// (system-scope release). Each block clears its tile's counts of the other
+// parity (the next step's integrator accumulates there).
+// initial: the state dem_set_particles published (xs->n_out preset), else
+// the step's owned outputs, recorded in xs->n_out for the next step's append.
 __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, uint32_t K,
                                                      uint32_t N, uint8_t* mine, XLayout L,
-                                                     const uint32_t* tc, uint32_t ntiles,
-                                                     XState* xs) {
+                                                     const uint32_t* tc, uint32_t* tc_next,
+                                                     uint32_t ntiles, XState* xs, int initial) {
   __shared__ uint32_t s_base[4];
   __shared__ uint32_t s_warp[4][8];
+  __shared__ uint32_t s_cnt[4][32];  // [category][sub-tile * 8 + warp]
+  __shared__ uint32_t s_last;
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t n_out = xs->n_out;
+  const uint32_t n_out = initial ? xs->n_out : owned_out(b, g);
   const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
   const uint32_t par = tag & 1u;
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
+  // a tile without flagged outputs (all but the boundary planes' few) has
+  // nothing to write: straight to the publication count
+  const bool any = __ldcg(&tc[4 * ntiles + blockIdx.x]) != 0u;
+  const uint32_t writers = __ldcg(&tc[5 * ntiles]);  // tiles with flagged outputs
   // this tile's base per category: the counts of the earlier tiles, summed
   // block-wide (a serial sum by 4 threads cost ~100 us per step at 500 tiles)
-  {
+  if (any) {
     uint32_t acc[4] = {0u, 0u, 0u, 0u};
     for (uint32_t t = threadIdx.x; t < blockIdx.x; t += blockDim.x)
 #pragma unroll
@@ -2370,112 +2402,147 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
     }
     __syncthreads();
   }
-  for (int u = 0; u < 4; ++u) {
-    const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
-    const uint32_t f = o < n_out ? b.flags[o] : 0u;
-    uint32_t rank[4];
+  if (any) {
+    // the tile's four sub-tiles at once (their loads in flight together): a
+    // flagged output's rank in its category = this tile's base + the flagged
+    // outputs before it in slot order (sub-tile, warp, lane)
+    uint32_t f[4], rk[4][4];
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      const uint32_t m = __ballot_sync(0xffffffffu, (f >> q) & 1u);
-      rank[q] = __popc(m & lanemask_lt());
-      if (lane == 0) s_warp[q][warp] = __popc(m);
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
+      f[u] = o < n_out ? __ldcg(&b.flags[o]) : 0u;
     }
-    __syncthreads();
 #pragma unroll
-    for (int q = 0; q < 4; ++q) {
-      uint32_t before = s_base[q];
-      for (uint32_t w = 0; w < warp; ++w) before += s_warp[q][w];
-      rank[q] += before;
-    }
-    if (f) {
-      const float4 P = b.pos_out[o], V = b.vel_out[o], W = b.omg_out[o];
+    for (int u = 0; u < 4; ++u)
 #pragma unroll
       for (int q = 0; q < 4; ++q) {
-        if (!((f >> q) & 1u)) continue;
+        const uint32_t m = __ballot_sync(0xffffffffu, (f[u] >> q) & 1u);
+        rk[u][q] = __popc(m & lanemask_lt());
+        if (lane == 0) s_cnt[q][u * 8 + warp] = __popc(m);
+      }
+    __syncthreads();
+    if (threadIdx.x < 4) {  // exclusive prefix over (sub-tile, warp), per category
+      uint32_t acc = s_base[threadIdx.x];
+      for (int w = 0; w < 32; ++w) {
+        const uint32_t c = s_cnt[threadIdx.x][w];
+        s_cnt[threadIdx.x][w] = acc;
+        acc += c;
+      }
+    }
+    __syncthreads();
+    float4 P[4], V[4], W[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
+      if (f[u]) {
+        P[u] = __ldcg(&b.pos_out[o]);
+        V[u] = __ldcg(&b.vel_out[o]);
+        W[u] = __ldcg(&b.omg_out[o]);
+      }
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (!f[u]) continue;
+      const uint32_t o = blockIdx.x * kXTile + u * 256 + threadIdx.x;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        if (!((f[u] >> q) & 1u)) continue;
         const int dir = q & 1;  // 0: to the left neighbour, 1: to the right
         uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
-        const uint32_t e = rank[q];
+        const uint32_t e = s_cnt[q][u * 8 + warp] + rk[u][q];
         if (q < 2) {  // migrant: state + history
           if (e >= L.mig_cap) {
-            raise_error(b.err, 6u, o, __float_as_uint(W.w));
+            raise_error(b.err, 6u, o, __float_as_uint(W[u].w));
             continue;
           }
-          reinterpret_cast<float4*>(blk + L.mig_pos)[e] = P;
-          reinterpret_cast<float4*>(blk + L.mig_vel)[e] = V;
-          reinterpret_cast<float4*>(blk + L.mig_omg)[e] = W;
+          reinterpret_cast<float4*>(blk + L.mig_pos)[e] = P[u];
+          reinterpret_cast<float4*>(blk + L.mig_vel)[e] = V[u];
+          reinterpret_cast<float4*>(blk + L.mig_omg)[e] = W[u];
           const uint32_t nc = b.cnt_out[o];
           reinterpret_cast<uint32_t*>(blk + L.mig_cnt)[e] = nc;
           float4* h = reinterpret_cast<float4*>(blk + L.mig_hist) + (size_t)e * K;
           for (uint32_t k = 0; k < nc; ++k) h[k] = b.hist_out[hix(o, k, K)];
         } else {  // ghost: state only
           if (e >= L.ghost_cap) {
-            raise_error(b.err, 6u, o, __float_as_uint(W.w));
+            raise_error(b.err, 6u, o, __float_as_uint(W[u].w));
             continue;
           }
-          reinterpret_cast<float4*>(blk + L.gh_pos)[e] = P;
-          reinterpret_cast<float4*>(blk + L.gh_vel)[e] = V;
-          reinterpret_cast<float4*>(blk + L.gh_omg)[e] = W;
+          reinterpret_cast<float4*>(blk + L.gh_pos)[e] = P[u];
+          reinterpret_cast<float4*>(blk + L.gh_vel)[e] = V[u];
+          reinterpret_cast<float4*>(blk + L.gh_omg)[e] = W[u];
         }
       }
     }
     __syncthreads();
-    if (threadIdx.x < 4) {
-      uint32_t tot = 0;
-      for (int w = 0; w < 8; ++w) tot += s_warp[threadIdx.x][w];
-      s_base[threadIdx.x] += tot;
-    }
-    __syncthreads();
   }
-}
-
-// header counts, then the tag with a system-scope release (the data above is
-// complete: this kernel starts after k_xpack_write finished)
-__global__ void k_xpublish(uint8_t* mine, XLayout L, const uint32_t* tc, uint32_t ntiles,
-                           DevErr* err, uint32_t xbase) {
-  __shared__ uint32_t s_w[4][8];
-  if (ld_volatile(&err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u + xbase;
-  const uint32_t par = tag & 1u;
-  // the category totals over all tiles, block-wide (one block of 256)
+  // the next step's counts start from zero (this tile's, and the tile count)
+  if (threadIdx.x < 5) tc_next[threadIdx.x * ntiles + blockIdx.x] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) tc_next[5 * ntiles] = 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0 && !initial) xs->n_out = n_out;
+  // publication by the last of the `writers` blocks that wrote (block 0 when
+  // none did). A block's records are ordered before its count (block
+  // barrier, then a gpu-scope fence); the publisher's system-scope release
+  // fence is cumulative over them
+  if (threadIdx.x == 0) {
+    s_last = 0u;
+    if (any) {
+      __threadfence();
+      s_last = atomicAdd(&xs->done, 1u) == writers - 1u ? 1u : 0u;
+    } else if (writers == 0u && blockIdx.x == 0) {
+      s_last = 1u;
+    }
+  }
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  // the category totals over all tiles, block-wide
   uint32_t tot[4] = {0, 0, 0, 0};
   for (uint32_t t = threadIdx.x; t < ntiles; t += blockDim.x)
 #pragma unroll
-    for (int q = 0; q < 4; ++q) tot[q] += tc[q * ntiles + t];
+    for (int q = 0; q < 4; ++q) tot[q] += __ldcg(&tc[q * ntiles + t]);
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     for (int d = 16; d > 0; d >>= 1) tot[q] += __shfl_xor_sync(0xffffffffu, tot[q], d);
-    if ((threadIdx.x & 31u) == 0u) s_w[q][threadIdx.x >> 5] = tot[q];
+    if ((threadIdx.x & 31u) == 0u) s_warp[q][threadIdx.x >> 5] = tot[q];
   }
   __syncthreads();
   if (threadIdx.x != 0) return;
+  xs->done = 0u;
 #pragma unroll
   for (int q = 0; q < 4; ++q) {
     tot[q] = 0;
-    for (int w = 0; w < 8; ++w) tot[q] += s_w[q][w];
+    for (int w = 0; w < 8; ++w) tot[q] += s_warp[q][w];
   }
+  XHeader* h[2];
   for (int dir = 0; dir < 2; ++dir) {
-    XHeader* h = reinterpret_cast<XHeader*>(mine + (size_t)(dir * 2 + par) * L.bytes + L.header);
-    h->n_mig = tot[dir];
-    h->n_ghost = tot[2 + dir];
-    __threadfence_system();
-    st_release_sys(&h->tag, tag);
+    h[dir] = reinterpret_cast<XHeader*>(mine + (size_t)(dir * 2 + par) * L.bytes + L.header);
+    h[dir]->n_mig = tot[dir];
+    h[dir]->n_ghost = tot[2 + dir];
   }
+  // one system-scope release fence for both tags (a fence.sc.sys + st.release.sys
+  // per tag, as before, was four system membars: ~15 us of a 20 us pack)
+  asm volatile("fence.acq_rel.sys;" ::: "memory");
+  for (int dir = 0; dir < 2; ++dir)
+    asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(&h[dir]->tag), "r"(tag) : "memory");
 }
 
-// acquire the neighbours' tags for this step; the base and counts of the
-// appended slots; capacity check
-__global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
-                        uint32_t* nslots, uint32_t cap, DevErr* err, uint32_t xbase) {
-  __shared__ uint32_t s_cnt[4];
+// Acquire the neighbours' tags for this step (every block: thread 0 the left
+// neighbour's block "to the right", thread 1 the right one's "to the left";
+// a ~30 s bound turns a dead neighbour into DEM_EPEER instead of a hang),
+// then append their migrants (with history) and ghosts at slots n_out..,
+// compute their cell keys and count them into their cells for this step's
+// sort. Block 0 records the counts and this step's input slots.
+__global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint32_t K, uint32_t N,
+                                                 const uint8_t* left, const uint8_t* right,
+                                                 XLayout L, XState* xs, uint32_t* nslots) {
+  __shared__ uint32_t s_cnt[4], s_seen[2];
   __shared__ uint32_t s_ok;
-  if (ld_volatile(&err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&err->step_ctr) + 1u + xbase;
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;
   const uint32_t par = tag & 1u;
-  __shared__ uint32_t s_seen[2];
   if (threadIdx.x == 0) s_ok = 1u;
   __syncthreads();
   if (threadIdx.x < 2) {
-    // lane 0: the left neighbour's block "to the right"; lane 1: the right one's "to the left"
     const uint8_t* peer = threadIdx.x == 0 ? left : right;
     const int dir = threadIdx.x == 0 ? 1 : 0;
     uint32_t nm = 0, ng = 0;
@@ -2499,35 +2566,24 @@ __global__ void k_xwait(const uint8_t* left, const uint8_t* right, XLayout L, XS
     s_cnt[2 + threadIdx.x] = ng;
   }
   __syncthreads();
-  if (threadIdx.x == 0) {
-    if (!s_ok) {  // slot: 0xFFFFFF00 | expected tag's low byte; id: tags seen (left, right)
-      raise_error(err, 11u, 0xFFFFFF00u | (tag & 0xFFu),
+  const uint32_t c0 = s_cnt[0], c1 = s_cnt[1], c2 = s_cnt[2], c3 = s_cnt[3];
+  const uint32_t tot = c0 + c1 + c2 + c3;
+  const uint32_t base = xs->n_out;
+  if (!s_ok) {  // slot: 0xFFFFFF00 | expected tag's low byte; id: tags seen (left, right)
+    if (threadIdx.x == 0)
+      raise_error(b.err, 11u, 0xFFFFFF00u | (tag & 0xFFu),
                   ((s_seen[0] & 0xFFFFu) << 16) | (s_seen[1] & 0xFFFFu));
-      return;
-    }
-    const uint32_t base = xs->n_out;
-    const uint32_t tot = s_cnt[0] + s_cnt[1] + s_cnt[2] + s_cnt[3];
+    return;
+  }
+  if ((uint64_t)base + tot > N) {
+    if (threadIdx.x == 0) raise_error(b.err, 6u, base, 0u);
+    return;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int q = 0; q < 4; ++q) xs->appended[q] = s_cnt[q];
-    if ((uint64_t)base + tot > cap) {
-      raise_error(err, 6u, base, 0u);
-      return;
-    }
     *nslots = base + tot;
   }
-}
-
-// append migrants (with history) and ghosts at slots n_out.., compute their
-// cell keys and count them into their cells for this step's sort
-__global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint32_t K, uint32_t N,
-                                                 const uint8_t* left, const uint8_t* right,
-                                                 XLayout L, const XState* xs) {
-  if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;
-  const uint32_t par = tag & 1u;
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
-  const uint32_t c0 = xs->appended[0], c1 = xs->appended[1], c2 = xs->appended[2],
-                 c3 = xs->appended[3];
-  const uint32_t tot = c0 + c1 + c2 + c3;
   if (i >= tot) return;
   uint32_t q, e;
   if (i < c0) { q = 0; e = i; }
@@ -2538,7 +2594,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
   const uint8_t* peer = from_left ? left : right;
   const int dir = from_left ? 1 : 0;
   const uint8_t* blk = peer + (size_t)(dir * 2 + par) * L.bytes;
-  const uint32_t slot = xs->n_out + i;
+  const uint32_t slot = base + i;
   float4 P, V, W;
   if (q < 2) {
     P = __ldcv(reinterpret_cast<const float4*>(blk + L.mig_pos) + e);
@@ -3011,20 +3067,21 @@ int launch_flags(cudaStream_t st, int64_t n, const float4* pos, DevGrid g, uint3
 
 // initial = 1: publish the state set by dem_set_particles (xs->n_out preset)
 int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
-                 uint8_t* mine, XLayout L, uint32_t* tile_counts, XState* xs, int initial) {
-  const uint32_t ntiles = (uint32_t)((cap + kXTile - 1) / kXTile);
-  k_xpack_count<<<ntiles, 256, 0, st>>>(b, g, tile_counts, ntiles, xs, initial);
-  k_xpack_write<<<ntiles, 256, 0, st>>>(b, g, K, (uint32_t)cap, mine, L, tile_counts, ntiles, xs);
-  k_xpublish<<<1, 256, 0, st>>>(mine, L, tile_counts, ntiles, b.err, g.xbase);
+                 uint8_t* mine, XLayout L, XState* xs, int initial) {
+  const uint32_t ntiles = xtc_ntiles(cap);
+  // in a step the integrator has counted the flagged outputs per tile (b.xtc)
+  if (initial) k_xpack_count<<<ntiles, 256, 0, st>>>(b, g, b.xtc, ntiles, xs);
+  k_xpack_write<<<ntiles, 256, 0, st>>>(b, g, K, (uint32_t)cap, mine, L, b.xtc, b.xtc_next, ntiles,
+                                        xs, initial);
   return K_OTHER;
 }
 
 int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
                    uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
                    uint32_t* nslots_out) {
-  k_xwait<<<1, 32, 0, st>>>(left, right, L, xs, nslots_out, (uint32_t)cap, b.err, g.xbase);
   const uint32_t most = 2 * L.mig_cap + 2 * L.ghost_cap;
-  k_xappend<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs);
+  k_xappend<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs,
+                                               nslots_out);
   return K_OTHER;
 }
 
