@@ -540,7 +540,7 @@ def main():
                     help="dem_flags OR-ed into the handle's (A/B runs, e.g. a force configuration)")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--reps", type=int, default=5, help="timed K-step graph regions (median)")
-    ap.add_argument("--c5-prep", type=int, default=40000,
+    ap.add_argument("--c5-prep", type=int, default=100000,
                     help="C5: untimed compaction steps under gravity before the warm-up")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
