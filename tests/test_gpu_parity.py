@@ -763,22 +763,25 @@ def test_checkpoint_roundtrip_bitwise():
 
 
 @pytest.mark.parametrize("K", [6, 9])
-def test_overflow_rejects_step_and_keeps_last_good_state(K):
+@pytest.mark.parametrize("split", [False, True])
+def test_overflow_rejects_step_and_keeps_last_good_state(K, split):
+    # (C1 has one radius: by default the dense configuration detects inside k_force)
+    fl = DEM_F_SPLIT_SWEEP if split else 0
     sc = S.C1(S.SimParams(max_contacts=K))
-    d = make(sc, flags=0)
+    d = make(sc, flags=fl)
     with pytest.raises(DemError) as e:
         for _ in range(200):
             d.step(1)
     assert e.value.code == DEM_EOVERFLOW
     done = d.stats()["steps"]
-    ref = make(sc, flags=0)
+    ref = make(sc, flags=fl)
     if done:
         ref.step(done)
     a, b = d.get_state(), ref.get_state()
     for k in ("pos", "vel", "omega", "id"):
         assert np.array_equal(a[k], b[k])
     # the same failure happens inside a multi-step graph replay
-    d3 = make(sc, flags=0)
+    d3 = make(sc, flags=fl)
     with pytest.raises(DemError):
         d3.step(200)
     assert d3.stats()["steps"] == done

@@ -8,7 +8,7 @@ from paper_1301_1714_b200 import scenes as S  # noqa: E402
 import numpy as np  # noqa: E402
 from paper_1301_1714_b200.dem import (DEM_F_DIAG, DEM_F_FORCE_DENSE, DEM_F_FORCE_LANES, DEM_F_FORCE_WS,  # noqa: E402
                                       DEM_F_FORCE_LIGHT, DEM_F_HALF_LISTS, DEM_F_NO_GRAPH,
-                                      DEM_F_THREAD_PER_PARTICLE, Dem)
+                                      DEM_F_SPLIT_SWEEP, DEM_F_THREAD_PER_PARTICLE, Dem)
 
 
 def run(sc, flags, steps=3, material=None):
@@ -25,8 +25,8 @@ def run(sc, flags, steps=3, material=None):
 
 
 for f in (DEM_F_FORCE_DENSE, DEM_F_FORCE_LIGHT, DEM_F_FORCE_LANES, DEM_F_FORCE_WS, DEM_F_HALF_LISTS,
-          DEM_F_THREAD_PER_PARTICLE):
-    run(S.C1(), f)
+          DEM_F_THREAD_PER_PARTICLE, DEM_F_SPLIT_SWEEP | DEM_F_FORCE_DENSE):
+    run(S.C1(), f)  # (C1 has one radius: dense = detection fused into k_force)
 
 
 def crossers(n_side, gap=3e-8):
