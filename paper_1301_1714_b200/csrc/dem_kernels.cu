@@ -10,6 +10,8 @@
 //   k_detect  steps 5-6: one thread per sorted slot scans the 27 cells of
 //             Eq. 12 with the fp64-defined contact predicate (R14) and writes
 //             its contact list and its warp-flattened (base, count) word.
+//             (One radius, dense configuration: the same scan runs inside
+//             k_force<..., FUSED>, its lists in shared memory.)
 //   k_force   steps 7-8, 1 and the next step's 2: a warp per 32 sorted slots
 //             deals its contacts 32 per round to all lanes (Eqs. 2-10 with the
 //             tangential history remapped through the old slots, Eq. 7), then
