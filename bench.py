@@ -368,7 +368,7 @@ def run_ours(args):
     # DRAM bytes of one k_detect + k_force launch from a committed ncu --set
     # full capture of this bench command (tools/ncu_traffic.sh), with the c̄ and
     # step of that capture beside it (ncu cannot run inside the timed region)
-    traffic, traffic_src = None, None
+    traffic, traffic_src, issue = None, None, None
     tr_path = os.path.join(ROOT, "profiles", f"traffic_{args.config}_{args.model}.json")
     if os.path.exists(tr_path) and args.sweep == "full":
         try:
@@ -376,8 +376,24 @@ def run_ours(args):
             traffic = tj.get("sweep_dram_bytes_per_step")
             traffic_src = {k: tj.get(k) for k in ("file", "step", "c_bar", "commit",
                                                   "bytes_per_particle", "alg_bytes_per_particle")}
+            # the binding resource of the sweep: instruction issue. Warp
+            # instructions per step from the same capture, over this run's
+            # sweep time, against 4 issue slots per SM per cycle at the clock
+            # sampled during the profiled region (informational: the roofline
+            # above stays the north star's HBM one)
+            wi = tj.get("sweep_warp_inst_per_step")
+            mhz = clk.summary().get("sm_mhz")
+            if wi and mhz and sweep_ms > 0:
+                sms = torch.cuda.get_device_properties(local).multi_processor_count
+                ach = wi / (sweep_ms * 1e-3)
+                peak = sms * 4 * mhz * 1e6
+                issue = {"warp_inst_per_step": wi, "achieved_warp_inst_per_s": ach,
+                         "peak_warp_inst_per_s": peak, "frac": ach / peak,
+                         "peak_basis": f"{sms} SMs x 4 schedulers x 1 warp instruction per "
+                                       f"cycle at {mhz} MHz (profiled-region clock)",
+                         "source": {k: tj.get(k) for k in ("file", "step", "c_bar", "commit")}}
         except Exception:
-            traffic = None
+            traffic, issue = None, None
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": max(args.warmup, 3), "ms_per_step": ms_step, "higher_is_better": True,
@@ -410,6 +426,7 @@ def run_ours(args):
             "achieved": achieved, "peak": peak_gbs,
             "unit": "GB/s", "frac": achieved / peak_gbs, "traffic": traffic,
             "traffic_source": traffic_src,
+            "issue": issue,
             "alg_bytes_per_particle": b_sweep, "peak_source": peak_src,
             "kernel_ms_avg": sweep_ms, "kernel_share_of_step": sweep_ms / step_kernel_ms
             if step_kernel_ms else None,

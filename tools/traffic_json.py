@@ -24,13 +24,15 @@ out = subprocess.check_output(["ncu", "-i", a.rep, "--page", "raw", "--csv"], te
                               stderr=subprocess.DEVNULL)
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[0]
-per = {}
+per, inst = {}, {}
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     name = d["Kernel Name"].split("<")[0].split("(")[0].replace("void ", "").strip()
     b = sum(float(d[k].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             for k, u in ((k, rows[1][hdr.index(k)]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
     per[name] = b
+    if "smsp__inst_executed.sum" in d:  # warp instructions issued by the launch
+        inst[name] = float(d["smsp__inst_executed.sum"].replace(",", ""))
 line = None
 for ln in open(a.log):
     ln = ln.strip()
@@ -42,6 +44,8 @@ commit = subprocess.check_output(["git", "rev-parse", "--short", "HEAD"], text=T
 res = {
     "sweep_dram_bytes_per_step": tot,
     "per_kernel": per,
+    "sweep_warp_inst_per_step": sum(inst.values()) if inst else None,
+    "warp_inst_per_kernel": inst,
     "bytes_per_particle": tot / n,
     "alg_bytes_per_particle": line["roofline"]["alg_bytes_per_particle"],
     "step": a.skip // 2 + 1,
