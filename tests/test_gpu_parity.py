@@ -220,12 +220,12 @@ def test_flags_one_step_T2(flags, variant):
         assert_T2_history(contacts_dict(d), h.as_dict(st.id))
 
 
-@pytest.mark.parametrize("name", ["C3", "C4/4"])
+@pytest.mark.parametrize("name", ["C3", "C4/4", "C5/4"])
 def test_bench_instantiation_bitwise(name):
     """The bench runs k_force without DEM_F_DIAG (no F/T output) while every
     T2 test sets it: the two instantiations must produce the same run bitwise
     (state and δ_t), in the same force configuration."""
-    sc = S.C3() if name == "C3" else S.C4(scale=4)
+    sc = S.C3() if name == "C3" else S.C4(scale=4) if name == "C4/4" else S.C5(scale=4)
     runs = []
     # the bench's kernel (no DIAG; C3: detection fused into it), its DIAG twin, and the
     # split path (k_detect writing lists to HBM, then k_force)
@@ -347,6 +347,48 @@ def test_full_size_C4_sampled():
     res = orc.step(p, st, h, only=mask)
     assert np.array_equal(g["id"], st.id)
     assert_T2_forces(g["force"], g["torque"], res, mask=mask, what="C4 sampled")
+    sample_ids = st.id[mask]
+    id_i, id_j, dt3 = d.get_contacts()
+    keep = np.isin(id_i, sample_ids)
+    gc = {(int(a), int(b)): v.astype(np.float64)
+          for a, b, v in zip(id_i[keep], id_j[keep], dt3[keep])}
+    oc = {}
+    for s in np.nonzero(mask)[0]:
+        for k in range(int(h.cnt[s])):
+            oc[(int(st.id[s]), int(h.pid[s, k]))] = h.dt[s, k].copy()
+    assert_T2_history(gc, oc)
+
+
+def test_full_size_C5_sampled():
+    """2M-particle polydisperse bed (K = 32: per-pair S = r_i + r_j, lists of
+    sorted slots through SCCM — the bench's C5 launch configuration), after
+    200 steps of settling: grid bit-exact for every particle; forces,
+    torques and histories of ~300 sampled particles against the oracle."""
+    sc = S.C5()
+    assert sc.params.max_contacts == 32 and sc.radius.min() < sc.radius.max()
+    p = orc.make_params(sc.params, sc.radius)
+    d = make(sc)
+    d.step(200)
+    assert d.stats()["fused_sweep"] is False
+    K = int(d.stats()["max_contacts_seen"]) + 2
+    st, h = oracle_inputs(d, K)
+    key0, _, _ = d.get_grid()
+    CM = orc.hash_cells(p, st.pos)
+    assert np.array_equal(key0, CM)
+    d.step(1)
+    key1, perm, off = d.get_grid()
+    SCM, SCCM = orc.sort_map(CM)
+    assert np.array_equal(perm, SCCM)
+    assert np.array_equal(off, orc.cell_offsets(SCM, off.shape[0] - 1))
+    g = d.get_state(forces=True)
+    rng = np.random.default_rng(45)
+    mask = np.zeros(sc.n, bool)
+    mask[rng.choice(sc.n, 256, replace=False)] = True
+    busy = np.nonzero(h.cnt >= 3)[0]  # particles with several contacts
+    mask[busy[:48]] = True
+    res = orc.step(p, st, h, only=mask)
+    assert np.array_equal(g["id"], st.id)
+    assert_T2_forces(g["force"], g["torque"], res, mask=mask, what="C5 sampled")
     sample_ids = st.id[mask]
     id_i, id_j, dt3 = d.get_contacts()
     keep = np.isin(id_i, sample_ids)
