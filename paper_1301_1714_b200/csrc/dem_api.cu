@@ -238,6 +238,9 @@ StepBuffers step_buffers(dem_handle* h, int b) {
   s.xtc = h->xtiles ? h->xtiles + (size_t)b * xtc_stride(h->cap) : nullptr;
   s.xtc_next = h->xtiles ? h->xtiles + (size_t)(b ^ 1) * xtc_stride(h->cap) : nullptr;
   s.xntiles = xtc_ntiles(h->cap);
+  // slab ranks with a left neighbour: the owned particles' sorted slots start
+  // past room for the left ghost plane, which is placed right-aligned below
+  s.gl_base = (h->slab && h->rank > 0) ? h->xl.ghost_cap : 0u;
   s.cpos = h->cpos;
   s.lcount = h->lcount;
   s.llist = h->llist;
@@ -280,7 +283,7 @@ int kernels_per_step(const dem_handle* h, bool full = false) {
   return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3
           : fused_sweep(h)                         ? 1
                                                    : 2) +
-         sort + (h->slab ? 2 : 0);
+         sort + (h->slab ? 4 : 0);
 }
 
 // Enqueue one step from parity b: the sort (counting: scan, scatter, rank;
@@ -311,17 +314,20 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
       h->prof.push_back({evb, e, k});
     }
   };
-  if (h->slab) {  // this step's migrants and ghosts from the neighbours (peer memory)
+  const uint8_t* xl_ = h->xleft ? h->xleft + kXRegionHdr : nullptr;
+  const uint8_t* xr_ = h->xright ? h->xright + kXRegionHdr : nullptr;
+  if (h->slab) {  // this step's migrants and ghost-plane state from the neighbours (peer memory)
     rec(K_OTHER, true);
-    launch_xunpack(h->stream, h->cap, s, h->g, h->K, h->xleft ? h->xleft + kXRegionHdr : nullptr,
-                   h->xright ? h->xright + kXRegionHdr : nullptr, h->xl, h->xs,
-                   h->nslots);
+    launch_xrecv(h->stream, h->cap, s, h->g, h->K, xl_, xr_, h->xl, h->xs, h->nslots,
+                 h->merge && !full);
     rec(K_OTHER, false);
     h->launches += 1;
   }
   if (h->merge && !full) {  // merge re-sort
     rec(K_RANK, true);
-    launch_merge(h->stream, h->n, h->g.ncells, s);
+    // (slab: the owned particles, their count from the last step's pack)
+    launch_merge(h->stream, h->slab ? h->cap : h->n, h->g.ncells, s, h->g,
+                 h->slab ? &h->xs->n_out : nullptr);
     rec(K_RANK, false);
     h->launches += 1;
   } else {
@@ -334,7 +340,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     }
     rec(K_SCAN, true);
     launch_scan(h->stream, h->count, h->off, h->g.ncells, h->count, s.scan_status, nullptr,
-                h->err, 1);
+                h->err, 1, s.gl_base);
     rec(K_SCAN, false);
     rec(K_SCATTER, true);
     launch_scatter(h->stream, h->cap, s);
@@ -343,6 +349,12 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     launch_rank(h->stream, h->cap, s);
     rec(K_RANK, false);
     h->launches += 4;  // scan is two kernels
+  }
+  if (h->slab) {  // the neighbours' planes (sorted) and this rank's departed ones: ghost planes
+    rec(K_OTHER, true);
+    launch_xghost_place(h->stream, h->cap, s, h->g, xl_, xr_, h->xl, h->xs);
+    rec(K_OTHER, false);
+    h->launches += 1;
   }
   // default: full contact lists (k_detect + warp-flattened k_force); the half
   // lists (Newton's third law) and the paper's fused mapping are ablations
@@ -379,11 +391,12 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     rec(K_SWEEP, false);
   }
   h->launches += 1;
-  if (h->slab) {  // pack and publish the next step's migrants and ghosts
+  if (h->slab) {  // pack and publish the next step's boundary planes and migrants
     rec(K_OTHER, true);
-    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 0);
+    launch_xpack(h->stream, h->cap, s, h->g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 0,
+                 (h->rank > 0 ? 1 : 0) | (h->rank < h->world - 1 ? 2 : 0));
     rec(K_OTHER, false);
-    h->launches += 1;
+    h->launches += 2;
   }
   cudaError_t e = cudaGetLastError();
   if (e != cudaSuccess) return fail(h, DEM_ECUDA, std::string("step launch: ") + cudaGetErrorString(e));
@@ -873,7 +886,7 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
     const uint32_t gcap = (uint32_t)std::max<int64_t>(4096, 2 * per_plane + 1024);
     const uint32_t mcap = std::max<uint32_t>(1024, gcap / 4);
     cap = n_own + n_own / 4 + 2 * (int64_t)gcap + 2 * (int64_t)mcap;
-    h->xl = XLayout::make(mcap, gcap, h->K);
+    h->xl = XLayout::make(mcap, gcap, h->K, plane);
     memcpy(&h->xl.mono_bits, &h->mono_r, 4);
   }
   const int64_t ncl = g.ncells;  // cells the scan covers (local + trash in slab mode)
@@ -907,9 +920,10 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
       ok &= dalloc(h, &h->cpos, N * h->K) && dalloc(h, &h->lcount, N) &&
             dalloc(h, &h->llist, N * h->K) && dalloc(h, &h->R0, N * h->K) &&
             dalloc(h, &h->R1, N * h->K);
-    if (!h->slab)  // merge re-sort buffers (single GPU)
-      ok &= dalloc(h, &h->mov, 2 * (size_t)mover_cap(cap)) && dalloc(h, &h->mov_n, 2);
-    h->mov_cap = h->slab ? 0u : mover_cap(cap);
+    // merge re-sort buffers (slab ranks: room for the arriving migrants too)
+    const uint32_t mvc = mover_cap(cap) + (h->slab ? 2 * h->xl.mig_cap : 0u);
+    ok &= dalloc(h, &h->mov, 2 * (size_t)mvc) && dalloc(h, &h->mov_n, 2);
+    h->mov_cap = mvc;
     if (h->slab) {
       ok &= dalloc(h, &h->flags, N) && dalloc(h, &h->xs, 1) &&
             dalloc(h, &h->xtiles, 2 * (size_t)xtc_stride(N));
@@ -990,34 +1004,42 @@ int dem_set_particles(dem_handle* h, int64_t n, const dem_particles* src) {
   h->launches += (n > 0) ? 2 : 1;
   // merge re-sort (single GPU unless DEM_F_FULL_SORT): the first step sorts by
   // counting with its own k_count, so the cell counts start from zero
-  h->merge = !h->slab && !(h->p.flags & DEM_F_FULL_SORT);
+  // (slab ranks always merge: a departed migrant is a removal of the merge and
+  // joins this rank's ghost plane in k_xghost_place)
+  h->merge = h->slab || !(h->p.flags & DEM_F_FULL_SORT);
   h->merge_ok = h->full_run = false;
   h->full_sorts = 0;
-  if (h->merge) {
+  if (h->merge && !h->slab) {
     CUDA_TRY(h, cudaMemsetAsync(h->count, 0, sizeof(uint32_t) * ((size_t)ncells_a + 1), st));
     CUDA_TRY(h, cudaMemsetAsync(h->mov_n, 0, 2 * sizeof(uint32_t), st));
   }
   sweep_prepare(h->K);
   if (h->slab) {
-    // 5b. publish the ghosts of the set state for the neighbours' first step
+    // 5b. publish the set state's boundary planes (sorted) for the neighbours'
+    // first step: a counting sort of the owned particles (k_pack counted
+    // them) into pos_sorted from gl_base, then the planes' sorted runs
     dev_free(h, keep);
     dev_free(h, dst);
     launch_flags(st, n_own, h->pos[0], g, h->flags);
-    StepBuffers sb{};
-    sb.pos_out = h->pos[0];
+    StepBuffers sb = step_buffers(h, 0);
+    launch_scan(st, h->count, h->off, g.ncells, h->count, sb.scan_status, nullptr, h->err, 0,
+                sb.gl_base);
+    launch_scatter(st, cap, sb);
+    launch_rank(st, cap, sb);
+    sb.pos_out = h->pos[0];  // (the set state: the planes' state is read through the old slot)
     sb.vel_out = h->vel[0];
     sb.omg_out = h->omg[0];
     sb.cnt_out = h->cnt[0];
     sb.hist_out = h->hist[0];
-    sb.flags = h->flags;
-    sb.off = h->off;
-    sb.err = h->err;
     // the first step (state parity 0) accumulates into parity 0's counts:
     // the set state's counts take parity 1's, and everything starts at zero
     CUDA_TRY(h, cudaMemsetAsync(h->xtiles, 0, 2 * sizeof(uint32_t) * xtc_stride(cap), st));
     sb.xtc = h->xtiles + xtc_stride(cap);
     sb.xtc_next = h->xtiles;
-    launch_xpack(st, cap, sb, g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 1);
+    launch_xpack(st, cap, sb, g, h->K, h->xregion + kXRegionHdr, h->xl, h->xs, 1,
+                 (h->rank > 0 ? 1 : 0) | (h->rank < h->world - 1 ? 2 : 0));
+    // the first step sorts by counting again (k_count); the scan zeroed the counts
+    CUDA_TRY(h, cudaMemsetAsync(h->mov_n, 0, 2 * sizeof(uint32_t), st));
     DevErr e{};
     CUDA_TRY(h, cudaMemcpyAsync(&e, h->err, sizeof e, cudaMemcpyDeviceToHost, st));
     CUDA_TRY(h, cudaStreamSynchronize(st));
@@ -1531,7 +1553,8 @@ static int check_peer_layouts(dem_handle* h) {
     XLayout pl{};
     CUDA_TRY(h, cudaMemcpy(&pl, p, sizeof pl, cudaMemcpyDeviceToHost));
     if (pl.bytes != h->xl.bytes || pl.mig_cap != h->xl.mig_cap ||
-        pl.ghost_cap != h->xl.ghost_cap || pl.K != h->xl.K || pl.mono_bits != h->xl.mono_bits)
+        pl.ghost_cap != h->xl.ghost_cap || pl.K != h->xl.K || pl.mono_bits != h->xl.mono_bits ||
+        pl.plane != h->xl.plane)
       return fail(h, DEM_EINVAL,
                   "neighbour exchange layout differs (ghost capacity " + std::to_string(pl.ghost_cap) +
                       " vs " + std::to_string(h->xl.ghost_cap) +

@@ -112,6 +112,9 @@ struct StepBuffers {
                        // read by its pack (one buffer per state parity)
   uint32_t* xtc_next;  // the other parity's: zeroed by this step's pack for the next step
   uint32_t xntiles;
+  uint32_t gl_base;    // first sorted slot of the owned particles: a slab rank with a left
+                       // neighbour keeps room below it for the left ghost plane (placed
+                       // right-aligned); else 0
   // half-list path (Newton's third law): the pair (i, t) is
   // evaluated once, by its lower sorted slot i ("upper" contact of i)
   uint8_t* cpos;       // [k*N + i]: position of i in t's lower list
@@ -146,7 +149,7 @@ inline uint32_t mover_cap(int64_t n) {
 struct XHeader {
   uint32_t tag;     // step number the data is for (published last, release/acquire)
   uint32_t n_mig;   // migrants packed
-  uint32_t n_ghost; // ghosts packed
+  uint32_t n_ghost; // the sender's boundary plane for the next step, sorted by its keys
   uint32_t pad;
 };
 constexpr uint32_t kXTile = 1024;  // output slots per pack tile (256 threads x 4)
@@ -158,14 +161,18 @@ inline uint32_t xtc_stride(int64_t cap) { return 5u * xtc_ntiles(cap) + 4u; }
 // neighbours at connect time) + 4 blocks (direction x parity).
 constexpr uint64_t kXRegionHdr = 256;
 struct XLayout {  // byte offsets inside one (direction, parity) block
-  uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, bytes;
+  uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, gh_off,
+      bytes;
   uint32_t mig_cap, ghost_cap, K;
+  uint32_t plane;      // cells per z-plane: the ghost plane's cell offsets hold plane + 1
   uint32_t mono_bits;  // the set's one radius (bits; 0: several): neighbours must agree
-  __host__ __device__ static XLayout make(uint32_t mig_cap, uint32_t ghost_cap, uint32_t K) {
+  __host__ __device__ static XLayout make(uint32_t mig_cap, uint32_t ghost_cap, uint32_t K,
+                                          uint32_t plane) {
     XLayout L;
     L.mig_cap = mig_cap;
     L.ghost_cap = ghost_cap;
     L.K = K;
+    L.plane = plane;
     L.mono_bits = 0;
     uint64_t o = 0;
     L.header = o;
@@ -186,6 +193,8 @@ struct XLayout {  // byte offsets inside one (direction, parity) block
     o += (uint64_t)ghost_cap * 16;
     L.gh_omg = o;
     o += (uint64_t)ghost_cap * 16;
+    L.gh_off = o;  // the plane's cell offsets, relative to its first particle
+    o += ((uint64_t)(plane + 1) * 4 + 255) & ~255ull;
     L.bytes = (o + 4095) & ~4095ull;
     return L;
   }
@@ -233,12 +242,19 @@ int launch_idcheck(cudaStream_t st, int64_t n, uint32_t idmask, const float4* om
 
 // One step = scan, scatter, rank, sweep.
 int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
-                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step);
+                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step,
+                uint32_t base0 = 0);  // base0: added to every output (the owned particles' start)
 int launch_scatter(cudaStream_t st, int64_t n, const StepBuffers& b);
 int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
 // merge re-sort: one k_merge in place of the counting sort
 // when the state is in the previous step's sorted order
-int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b);
+// Slab ranks (g.slab): the owned particles — n read from n_dev (the last
+// step's outputs; the host n is the grid's bound), placed from b.gl_base,
+// offsets of the owned cells only; list entries with insertion point
+// 0xFFFFFFFF (migrants that left) are removals, entries with previous key
+// 0xFFFFFFFF (migrants that arrived) insertions
+int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b,
+                 const DevGrid& g, const uint32_t* n_dev = nullptr);
 int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uint32_t* perm);
 // Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the
@@ -263,11 +279,23 @@ int launch_sweep(cudaStream_t st, int64_t n, uint32_t K, int model, bool diag,
 
 // Slab exchange. `mine` = this rank's exchange region; `left`/`right` = the
 // neighbours' regions (peer pointers, NULL at the ends of the domain).
+// step end: the two boundary planes as they will be sorted next step (a
+// merge of the plane's stayers with its movers, from the mover list) and
+// the migrants; the last block releases the tag. initial = 1: the set state
+// (sorted already at set time: its sorted runs are published as they are)
 int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
-                 uint8_t* mine, XLayout L, XState* xs, int initial);
-int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
-                   uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
-                   uint32_t* nslots_out);
+                 uint8_t* mine, XLayout L, XState* xs, int initial, int nbr);
+// step start: acquire the neighbours' tags; append their migrants (state +
+// history) at slots n_out.. (merge step: listed as insertions; counting
+// step: counted into their cells) and their boundary planes' state after them
+int launch_xrecv(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
+                 const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
+                 uint32_t* nslots_out, bool merge);
+// after the owned sort: the received planes as this rank's ghost planes,
+// merged with its own departed particles (sorted slots right-aligned below
+// gl_base and right after the owned particles), and the ghost cells' offsets
+int launch_xghost_place(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
+                        const uint8_t* left, const uint8_t* right, XLayout L, XState* xs);
 // set_particles in slab mode: keep[i] = particle i's z-cell is owned by this rank.
 int launch_keep(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* keep);
 int launch_plane_hist(cudaStream_t st, int64_t n, const float* pos, DevGrid g, uint32_t* hist);

@@ -22,7 +22,8 @@
 // The first step after dem_set_particles (and a step whose movers overflow
 // the list) sorts by counting instead: k_count/k_tile_sum/k_scan_apply (the
 // scan is the offset array), k_scatter, k_rank. Slab ranks add the exchange
-// kernels (k_xappend at the step start, k_xpack_write at the end).
+// kernels (k_xrecv at the step start, k_xghost_place after the sort,
+// k_xpack_planes + k_xpack_write at the end).
 // All arithmetic of the step runs here; the host only enqueues.
 #include <cuda_runtime.h>
 #include <math.h>
@@ -273,7 +274,7 @@ __global__ void __launch_bounds__(kScanThreads)
 
 __global__ void __launch_bounds__(kScanThreads)
     k_scan_apply(const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
-                 const uint32_t* __restrict__ tsum, DevErr* err) {
+                 const uint32_t* __restrict__ tsum, DevErr* err, uint32_t base0) {
   pdl_enter();
   __shared__ uint32_t s_warp[kScanThreads / 32];
   __shared__ uint32_t s_excl[kScanThreads / 32];
@@ -286,7 +287,7 @@ __global__ void __launch_bounds__(kScanThreads)
   uint32_t acc = 0;
   for (uint32_t t = threadIdx.x; t < tile; t += kScanThreads) acc += __ldg(&tsum[t]);
   if (e != 0u) return;
-  const uint32_t prefix = block_sum(acc, s_warp);
+  const uint32_t prefix = base0 + block_sum(acc, s_warp);
   uint32_t local = 0;
 #pragma unroll
   for (int q = 0; q < kScanItems; ++q) local += v[q];
@@ -387,17 +388,18 @@ __global__ void __launch_bounds__(256)
     k_rank(int64_t n, const uint32_t* __restrict__ key, const uint32_t* __restrict__ off,
            const uint32_t* __restrict__ tmp, uint32_t* __restrict__ perm,
            const float4* __restrict__ pos_in, float4* __restrict__ pos_sorted,
-           const uint32_t* __restrict__ nslots, const DevErr* err, bool sw) {
+           const uint32_t* __restrict__ nslots, const DevErr* err, bool sw, uint32_t base0) {
   pdl_enter();
   // error word, slot count and the first loads go out together (tmp below the
-  // capacity n is always in bounds; entries past nslots are ignored)
+  // capacity n is always in bounds; entries past nslots are ignored). The
+  // sorted slots start at base0 (slab ranks: past the left ghost plane's room)
   const uint32_t ecode = ld_volatile(&err->code);
   const int64_t ns = (int64_t)__ldg(nslots);
   const int64_t base = (int64_t)blockIdx.x * blockDim.x * kItems + threadIdx.x;
   uint32_t s[kItems], c[kItems], a[kItems], e[kItems];
 #pragma unroll
   for (int u = 0; u < kItems; ++u) {
-    const int64_t j = base + (int64_t)u * blockDim.x;
+    const int64_t j = base0 + base + (int64_t)u * blockDim.x;
     s[u] = j < n ? __ldg(&tmp[j]) : 0u;
   }
   if (ecode != 0u) return;
@@ -487,10 +489,17 @@ __device__ __forceinline__ int block_sum(int v, int* red) {  // 256 threads
   return s;
 }
 
+// Slab ranks: n from n_dev (the previous step's owned outputs), sorted slots
+// from `base` (constant across steps), offsets of cells [c_lo, c_hi] only; a
+// list entry with insertion point 0xFFFFFFFF (a migrant that left) is a
+// removal only, one with previous key 0xFFFFFFFF (an arrived migrant,
+// appended past the outputs) an insertion only. Single GPU: n_dev null,
+// base 0, [0, ncells].
 __global__ void __launch_bounds__(256)
     k_merge(uint32_t n, uint32_t ncells, MergeBuffers mb, const float4* __restrict__ pos_in,
             uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
-            uint32_t* __restrict__ off, DevErr* err, bool sw) {
+            uint32_t* __restrict__ off, DevErr* err, bool sw, const uint32_t* n_dev,
+            uint32_t base, uint32_t c_lo, uint32_t c_hi) {
   pdl_enter();
   __shared__ int red[2][8];
   __shared__ int2 red2[8];
@@ -501,6 +510,7 @@ __global__ void __launch_bounds__(256)
   // the error word, the mover count and this block's positions go out together
   const uint32_t e = ld_volatile(&err->code);
   const uint32_t m = ld_volatile(mb.n_in);
+  if (n_dev) n = *n_dev;
   float4 P[kMergeItems];
 #pragma unroll
   for (int u = 0; u < kMergeItems; ++u) {
@@ -520,15 +530,16 @@ __global__ void __launch_bounds__(256)
   int dS = 0, dC = 0;
   for (uint32_t i = t; i < m; i += 256u) {
     const uint4 v = __ldcg(&mb.list_in[i]);  // (a, c, c', x)
+    const bool ins = v.w != 0xFFFFFFFFu;      // (not a migrant that left)
     dS += (int)(v.w < B0) - (int)(v.x < B0);
-    dC += (int)(v.y < B0) - (int)(v.z < B0);
+    dC += (int)(ins && v.y < B0) - (int)(v.z < B0);
     auto push = [&](int k, uint32_t p, int w) {
       const uint32_t q = atomicAdd(&s_ne[k], 1u);
       if (q < kMergeEv) s_ev[k][q] = make_int2((int)p, w);
     };
     if (v.w - B0 < kMergeSpan) push(0, v.w, 1);   // insertion point: stayers from x on
     if (v.x - B0 < kMergeSpan) push(0, v.x, -1);  // mover slot: stayers from a on
-    if (v.y - B0 < kMergeSpan) push(1, v.y, 1);   // new key: cells above c
+    if (ins && v.y - B0 < kMergeSpan) push(1, v.y, 1);  // new key: cells above c
     if (v.z - B0 < kMergeSpan) push(1, v.z, -1);  // previous key: cells above c'
   }
   {
@@ -560,7 +571,7 @@ __global__ void __launch_bounds__(256)
       }
     }
     if (mover) continue;
-    const uint32_t j = (uint32_t)((int)s + d);
+    const uint32_t j = base + (uint32_t)((int)s + d);
     // one radius: .w carries the old slot, and nothing on that path reads
     // perm (dem_get_grid extracts it from .w), so it is not written
     if (sw) P[u].w = __uint_as_float(s);
@@ -568,11 +579,11 @@ __global__ void __launch_bounds__(256)
     pos_sorted[j] = P[u];
   }
   // offsets, in place, only where the shift is not zero
-  if (B0 <= ncells && !(dC == 0 && neC == 0)) {
+  if (B0 <= c_hi && !(dC == 0 && neC == 0)) {
 #pragma unroll
     for (int u = 0; u < kMergeItems; ++u) {
       const uint32_t c = B0 + u * 256u + t;
-      if (c > ncells) continue;
+      if (c > c_hi || c < c_lo) continue;
       int d = dC;
       if (!spill) {
         for (uint32_t k = 0; k < neC; ++k) {
@@ -583,7 +594,7 @@ __global__ void __launch_bounds__(256)
         d = 0;
         for (uint32_t i = 0; i < m; ++i) {
           const uint4 v = __ldcg(&mb.list_in[i]);
-          d += (int)(v.y < c) - (int)(v.z < c);
+          d += (int)(v.w != 0xFFFFFFFFu && v.y < c) - (int)(v.z < c);
         }
       }
       if (d != 0) off[c] = (uint32_t)((int)__ldcs(&off[c]) + d);
@@ -592,14 +603,16 @@ __global__ void __launch_bounds__(256)
   // movers b, b + grid, ...: r_i + x_i - #{a_j < x_i}, counted block-wide
   for (uint32_t i = b; i < m; i += gridDim.x) {
     const uint4 mi = __ldcg(&mb.list_in[i]);
+    if (mi.w == 0xFFFFFFFFu) continue;  // (block-uniform) a migrant that left: no insertion
     int r = 0;
     for (uint32_t jj = t; jj < m; jj += 256u) {
       const uint4 v = __ldcg(&mb.list_in[jj]);
-      r += (int)(v.y < mi.y || (v.y == mi.y && v.x < mi.x)) - (int)(v.x < mi.w);
+      r += (int)(v.w != 0xFFFFFFFFu && (v.y < mi.y || (v.y == mi.y && v.x < mi.x))) -
+           (int)(v.x < mi.w);
     }
     r = block_sum(r, red[0]);
     if (t == 0) {
-      const uint32_t j = (uint32_t)(r + (int)mi.w);
+      const uint32_t j = base + (uint32_t)(r + (int)mi.w);
       float4 Pm = __ldg(&pos_in[mi.x]);
       if (sw) Pm.w = __uint_as_float(mi.x);
       else perm[j] = mi.x;
@@ -887,17 +900,15 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       raise_error(b.err, 8u, j, my_id);
     k2 = cell_key(g, x, y, z);  // step 2 of the next step: CM of the new position
     if (g.slab) {
-      // slab exchange flags: leaving the owned planes = migrant;
-      // on a boundary plane = ghost for the neighbour. A migrant keeps its key:
-      // it lands in this rank's ghost plane, where this rank's boundary
+      // slab exchange flags: leaving the owned planes = a
+      // migrant to the left (bit 0) or right (bit 1) neighbour. It keeps its
+      // key: it lies in this rank's ghost plane, where this rank's boundary
       // particles need it as a neighbour next step (the receiver, which did
-      // not own it when it packed its ghosts, cannot send it back in time).
+      // not own it when it packed its plane, cannot send it back in time).
       const int cz = cell_coord(z, g.lo[2], g.inv_h, g.nz_global);
       uint32_t f = 0;
       if (cz < g.z0) f |= 1u;
       if (cz >= g.z1) f |= 2u;
-      if (cz == g.z0) f |= 4u;
-      if (cz == g.z1 - 1) f |= 8u;
       b.flags[j] = f;
       xf = f;
     }
@@ -934,8 +945,12 @@ __device__ __forceinline__ void finish_particle(const StepBuffers& b, const DevG
       const uint32_t idx = base + (uint32_t)__popc(mv & lanemask_lt());
       if (k2 != sk && idx < b.mv.cap) {
         // slot, new key, previous key and the insertion point among this
-        // step's order (these offsets are the next step's previous ones)
-        const uint32_t x = min(max(j, __ldg(&b.off[k2])), __ldg(&b.off[k2 + 1]));
+        // step's order (these offsets are the next step's previous ones;
+        // slab ranks: relative to the owned particles' first sorted slot). A
+        // migrant leaves the owned particles: insertion point 0xFFFFFFFF
+        const uint32_t gl = b.gl_base;
+        const uint32_t x = (xf & 3u) ? 0xFFFFFFFFu
+                                     : min(max(j, __ldg(&b.off[k2]) - gl), __ldg(&b.off[k2 + 1]) - gl);
         b.mv.list_out[idx] = make_uint4(j, k2, sk, x);
       }
     }
@@ -2320,7 +2335,7 @@ __global__ void k_flags(int64_t n, const float4* pos, DevGrid g, uint32_t* flags
   const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= n) return;
   const int cz = global_cz(g, pos[i].z);
-  flags[i] = (cz == g.z0 ? 4u : 0u) | (cz == g.z1 - 1 ? 8u : 0u);
+  flags[i] = (cz < g.z0 ? 1u : 0u) | (cz >= g.z1 ? 2u : 0u);  // (none: the set keeps owned ones)
 }
 
 
@@ -2518,8 +2533,7 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
   XHeader* h[2];
   for (int dir = 0; dir < 2; ++dir) {
     h[dir] = reinterpret_cast<XHeader*>(mine + (size_t)(dir * 2 + par) * L.bytes + L.header);
-    h[dir]->n_mig = tot[dir];
-    h[dir]->n_ghost = tot[2 + dir];
+    h[dir]->n_mig = tot[dir];  // (n_ghost: k_xpack_planes / k_xplanes_initial)
   }
   // one system-scope release fence for both tags (a fence.sc.sys + st.release.sys
   // per tag, as before, was four system membars: ~15 us of a 20 us pack)
@@ -2528,15 +2542,33 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
     asm volatile("st.relaxed.sys.global.u32 [%0], %1;" ::"l"(&h[dir]->tag), "r"(tag) : "memory");
 }
 
-// Acquire the neighbours' tags for this step (every block: thread 0 the left
-// neighbour's block "to the right", thread 1 the right one's "to the left";
-// a ~30 s bound turns a dead neighbour into DEM_EPEER instead of a hang),
-// then append their migrants (with history) and ghosts at slots n_out..,
-// compute their cell keys and count them into their cells for this step's
-// sort. Block 0 records the counts and this step's input slots.
-__global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint32_t K, uint32_t N,
-                                                 const uint8_t* left, const uint8_t* right,
-                                                 XLayout L, XState* xs, uint32_t* nslots) {
+// Thread-level acquire of a neighbour's tag, bounded (~30 s): a dead
+// neighbour becomes DEM_EPEER instead of a hang. false on time-out.
+__device__ __forceinline__ bool wait_tag(const uint32_t* t, uint32_t want, uint32_t* seen) {
+  unsigned long long spins = 0;
+  uint32_t v;
+  while ((v = ld_acquire_sys(t)) != want) {
+    if (++spins > (1ull << 27)) {
+      *seen = v;
+      return false;
+    }
+    __nanosleep(200);
+  }
+  return true;
+}
+
+// Step start: every block acquires the neighbours' tags (thread 0 the left
+// neighbour's block "to the right", thread 1 the right one's "to the left"),
+// then appends their migrants (state + tangential history) at slots n_out..,
+// left first, in the senders' slot order, hashed — a merge step lists each as
+// an insertion for k_merge (new key, previous key 0xFFFFFFFF, insertion point
+// the end of its cell in the last order), a counting step counts it into its
+// cell — and after them the state of their boundary planes (left, then
+// right), which k_xghost_place sorts in. Block 0 records the counts and the
+// input slots the sort takes (owned outputs + migrants).
+__global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_t K, uint32_t N,
+                                               const uint8_t* left, const uint8_t* right,
+                                               XLayout L, XState* xs, uint32_t* nslots, int merge) {
   __shared__ uint32_t s_cnt[4], s_seen[2];
   __shared__ uint32_t s_ok;
   if (ld_volatile(&b.err->code) != 0u) return;
@@ -2551,16 +2583,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
     if (peer) {
       const XHeader* h =
           reinterpret_cast<const XHeader*>(peer + (size_t)(dir * 2 + par) * L.bytes + L.header);
-      unsigned long long spins = 0;
-      uint32_t seen;
-      while ((seen = ld_acquire_sys(&h->tag)) != tag) {
-        if (++spins > (1ull << 27)) {  // peer never published (~30 s): fail, do not hang
-          s_ok = 0u;
-          s_seen[threadIdx.x] = seen;
-          break;
-        }
-        __nanosleep(200);
-      }
+      if (!wait_tag(&h->tag, tag, &s_seen[threadIdx.x])) s_ok = 0u;
       nm = ld_volatile(&h->n_mig);
       ng = ld_volatile(&h->n_ghost);
     }
@@ -2583,7 +2606,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int q = 0; q < 4; ++q) xs->appended[q] = s_cnt[q];
-    *nslots = base + tot;
+    *nslots = base + c0 + c1;
   }
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i >= tot) return;
@@ -2593,9 +2616,7 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
   else if (i < c0 + c1 + c2) { q = 2; e = i - c0 - c1; }
   else { q = 3; e = i - c0 - c1 - c2; }
   const bool from_left = (q & 1u) == 0u;
-  const uint8_t* peer = from_left ? left : right;
-  const int dir = from_left ? 1 : 0;
-  const uint8_t* blk = peer + (size_t)(dir * 2 + par) * L.bytes;
+  const uint8_t* blk = (from_left ? left : right) + (size_t)((from_left ? 1 : 0) * 2 + par) * L.bytes;
   const uint32_t slot = base + i;
   float4 P, V, W;
   if (q < 2) {
@@ -2616,13 +2637,233 @@ __global__ void __launch_bounds__(256) k_xappend(StepBuffers b, DevGrid g, uint3
   const_cast<float4*>(b.pos_in)[slot] = P;
   const_cast<float4*>(b.vel_in)[slot] = V;
   const_cast<float4*>(b.omg_in)[slot] = W;
-  uint32_t k2 = cell_key(g, P.x, P.y, P.z);
-  if (q < 2) {  // a migrant must land in this rank's owned planes (one plane per step)
-    const int cz = global_cz(g, P.z);
-    if (cz < g.z0 || cz >= g.z1) raise_error(b.err, 11u, slot, __float_as_uint(W.w));
+  if (q >= 2) return;  // (ghosts: placed by k_xghost_place in the senders' sorted order)
+  const uint32_t k2 = cell_key(g, P.x, P.y, P.z);
+  // a migrant must land in this rank's owned planes (one plane per step)
+  const int cz = global_cz(g, P.z);
+  if (cz < g.z0 || cz >= g.z1) {
+    raise_error(b.err, 11u, slot, __float_as_uint(W.w));
+    return;
   }
   const_cast<uint32_t*>(b.key_in)[slot] = k2;
-  b.prank[slot] = count_into_cell(b.count, k2);
+  if (merge) {
+    const uint32_t idx = atomicAdd(const_cast<uint32_t*>(b.mv.n_in), 1u);  // (order-free counts)
+    if (idx < b.mv.cap)
+      const_cast<uint4*>(b.mv.list_in)[idx] =
+          make_uint4(slot, k2, 0xFFFFFFFFu, __ldg(&b.off[k2 + 1]) - b.gl_base);
+  } else {
+    b.prank[slot] = count_into_cell(b.count, k2);
+  }
+}
+
+constexpr uint32_t kXDep = 1024;  // departed particles per ghost plane held in shared memory
+
+// After the owned sort: the neighbours' boundary planes (already sorted by
+// their keys, with their cell offsets) become this rank's ghost planes,
+// merged with this rank's own departed particles of that plane (listed by
+// the last integrator with insertion point 0xFFFFFFFF): within a cell the
+// departed ones come first, in slot order — the stable order of a sort over
+// this rank's input slots, where departed particles (outputs) precede the
+// appended planes. Left plane right-aligned below gl_base, right plane
+// right after the owned particles; the ghost cells' offsets, then the trash
+// cell's and the total. One thread per ghost cell.
+__global__ void __launch_bounds__(256) k_xghost_place(StepBuffers b, DevGrid g, uint32_t N,
+                                                      const uint8_t* left, const uint8_t* right,
+                                                      XLayout L, XState* xs) {
+  __shared__ uint2 s_dep[kXDep];  // (key, slot) of this side's departed particles
+  __shared__ uint32_t s_nd;
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + g.xbase;  // (the sort counted this step)
+  const uint32_t par = tag & 1u;
+  const uint32_t P = L.plane;
+  const uint32_t half = gridDim.x / 2;
+  const int side = blockIdx.x < half ? 0 : 1;  // 0: the left ghost plane
+  const uint32_t k = (blockIdx.x - (side ? half : 0)) * blockDim.x + threadIdx.x;  // plane cell
+  const uint8_t* peer = side == 0 ? left : right;
+  const uint32_t end_own = __ldg(&b.off[g.own_c1]);
+  if (!peer) {  // no neighbour on this side: no ghost plane (the trash cell and the total)
+    if (side == 1 && k == 0) {
+      b.off[g.trash] = end_own;
+      b.off[g.ncells] = end_own;
+    }
+    return;
+  }
+  const uint32_t cf = side == 0 ? 0u : g.own_c1;  // the ghost plane's first cell
+  // this side's departed particles from the mover list
+  if (threadIdx.x == 0) s_nd = 0u;
+  __syncthreads();
+  const uint32_t m = min(ld_volatile(b.mv.n_in), b.mv.cap);
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint4 v = __ldcg(&b.mv.list_in[i]);
+    if (v.w == 0xFFFFFFFFu && v.y - cf < P) {
+      const uint32_t d = atomicAdd(&s_nd, 1u);
+      if (d < kXDep) s_dep[d] = make_uint2(v.y, v.x);
+    }
+  }
+  __syncthreads();
+  const uint32_t nd = s_nd;
+  if (nd > kXDep) {
+    if (k == 0) raise_error(b.err, 6u, cf, nd);
+    return;
+  }
+  const uint32_t nG = xs->appended[2 + side];
+  const uint32_t gs = xs->n_out + xs->appended[0] + xs->appended[1] + (side ? xs->appended[2] : 0u);
+  const uint32_t base = side == 0 ? b.gl_base - nG - nd : end_own;
+  if ((side == 0 && nG + nd > b.gl_base) || (uint64_t)base + nG + nd > N) {
+    if (k == 0) raise_error(b.err, 6u, cf, nG + nd);
+    return;
+  }
+  if (k > P) return;
+  const uint8_t* blk = peer + (size_t)((side == 0 ? 1 : 0) * 2 + par) * L.bytes;
+  const uint32_t* goff = reinterpret_cast<const uint32_t*>(blk + L.gh_off);
+  const uint32_t c = cf + k;
+  uint32_t d_lt = 0, d_eq = 0;  // departed particles in cells below c, in c
+  for (uint32_t d = 0; d < nd; ++d) {
+    d_lt += s_dep[d].x < c ? 1u : 0u;
+    d_eq += s_dep[d].x == c ? 1u : 0u;
+  }
+  const uint32_t g0 = __ldcv(goff + k);
+  const uint32_t start = base + g0 + d_lt;  // the cell's first sorted slot
+  const bool sw = b.sw_r > 0.f;
+  auto place = [&](uint32_t j, uint32_t q) {  // sorted slot j <- input slot q
+    float4 S = __ldg(&b.pos_in[q]);
+    if (sw) S.w = __uint_as_float(q);
+    else b.perm[j] = q;
+    b.pos_sorted[j] = S;
+  };
+  if (k == P) {  // one past the plane: the owned particles' start / the trash cell
+    if (side == 1) {
+      b.off[g.trash] = start;
+      b.off[g.ncells] = start;
+    }
+    return;
+  }
+  b.off[c] = start;
+  if (d_eq) {  // departed particles of this cell, in slot order
+    for (uint32_t d = 0; d < nd; ++d) {
+      if (s_dep[d].x != c) continue;
+      uint32_t r = 0;
+      for (uint32_t e = 0; e < nd; ++e) r += (s_dep[e].x == c && s_dep[e].y < s_dep[d].y) ? 1u : 0u;
+      place(start + r, s_dep[d].y);
+    }
+  }
+  const uint32_t g1 = __ldcv(goff + k + 1);
+  for (uint32_t i = g0; i < g1; ++i) place(start + d_eq + (i - g0), gs + i);
+}
+
+constexpr uint32_t kXPlaneMv = 1024;  // movers in or out of a boundary plane held in shared memory
+
+// Step end: this rank's boundary plane (the first owned plane for the left
+// neighbour, dir 0; the last for the right one) as the next step's sort will
+// order it — the plane's stayers, minus the movers that left it, plus those
+// that entered it, by k_merge's counts restricted to the plane's cells (the
+// mover list is complete once the integrator is done) — with the new state
+// and the plane's cell offsets relative to its first particle; its count in
+// the header (the pack's last block releases the tag). Threads over the
+// plane's previous slots, its entering movers and its cells.
+__global__ void __launch_bounds__(256) k_xpack_planes(StepBuffers b, DevGrid g, uint8_t* mine,
+                                                      XLayout L, int nbr) {
+  __shared__ uint4 s_in[kXPlaneMv];   // (key, slot, insertion point) of the entering movers
+  __shared__ uint2 s_out[kXPlaneMv];  // (previous slot, previous key) of the leaving ones
+  __shared__ uint32_t s_ni, s_no;
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
+  const uint32_t par = tag & 1u;
+  const uint32_t P = L.plane;
+  const uint32_t half = gridDim.x / 2;
+  const int dir = blockIdx.x < half ? 0 : 1;
+  if (!((nbr >> dir) & 1)) return;
+  const uint32_t t = (blockIdx.x - (dir ? half : 0)) * blockDim.x + threadIdx.x;
+  const uint32_t cf = dir == 0 ? g.own_c0 : g.own_c1 - P;
+  const uint32_t gl = b.gl_base;
+  const uint32_t A = __ldg(&b.off[cf]) - gl, B = __ldg(&b.off[cf + P]) - gl;  // output slots
+  if (threadIdx.x == 0) s_ni = s_no = 0u;
+  __syncthreads();
+  const uint32_t m = min(ld_volatile(b.mv.n_out), b.mv.cap);
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint4 v = __ldcg(&b.mv.list_out[i]);  // (a, c, c', x)
+    if (v.w != 0xFFFFFFFFu && v.y - cf < P) {
+      const uint32_t q = atomicAdd(&s_ni, 1u);
+      if (q < kXPlaneMv) s_in[q] = make_uint4(v.y, v.x, v.w, 0u);
+    }
+    if (v.z - cf < P) {
+      const uint32_t q = atomicAdd(&s_no, 1u);
+      if (q < kXPlaneMv) s_out[q] = make_uint2(v.x, v.z);
+    }
+  }
+  __syncthreads();
+  const uint32_t ni = s_ni, no = s_no;
+  uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
+  const uint32_t n_new = (B - A) - no + ni;
+  if (ni > kXPlaneMv || no > kXPlaneMv || n_new > L.ghost_cap) {
+    if (t == 0) raise_error(b.err, 6u, cf, n_new);
+    return;
+  }
+  if (t == 0) reinterpret_cast<XHeader*>(blk + L.header)->n_ghost = n_new;
+  auto put = [&](uint32_t p, uint32_t s) {  // plane position p <- output slot s (new state)
+    reinterpret_cast<float4*>(blk + L.gh_pos)[p] = __ldg(&b.pos_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_vel)[p] = __ldg(&b.vel_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_omg)[p] = __ldg(&b.omg_out[s]);
+  };
+  if (t < B - A) {  // a previous member: kept unless it left
+    const uint32_t s = A + t;
+    int d = 0;
+    bool gone = false;
+    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].z <= s ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) {
+      d -= s_out[i].x <= s ? 1 : 0;
+      gone |= s_out[i].x == s;
+    }
+    if (!gone) put((uint32_t)((int)t + d), s);
+  }
+  if (t < ni) {  // an entering mover: its rank among them + the stayers before its point
+    const uint4 mi = s_in[t];
+    int r = 0;
+    for (uint32_t i = 0; i < ni; ++i)
+      r += (s_in[i].x < mi.x || (s_in[i].x == mi.x && s_in[i].y < mi.y)) ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) r -= s_out[i].x < mi.z ? 1 : 0;
+    put((uint32_t)(r + (int)(mi.z - A)), mi.y);
+  }
+  if (t <= P) {  // the cell offsets, relative to the plane's first particle
+    const uint32_t c = cf + t;
+    int d = (int)(__ldg(&b.off[c]) - gl - A);
+    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].x < c ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) d -= s_out[i].y < c ? 1 : 0;
+    reinterpret_cast<uint32_t*>(blk + L.gh_off)[t] = (uint32_t)d;
+  }
+}
+
+// The set state's boundary planes (dem_set_particles sorts it by counting
+// before publishing): each plane is a sorted run of pos_sorted, its state in
+// the set arrays (b.*_out here) through the old slot; the cell offsets
+// relative to the run's start.
+__global__ void __launch_bounds__(256) k_xplanes_initial(StepBuffers b, DevGrid g, uint8_t* mine,
+                                                         XLayout L, int nbr) {
+  if (ld_volatile(&b.err->code) != 0u) return;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;
+  const uint32_t par = tag & 1u;
+  const uint32_t P = L.plane;
+  const uint32_t half = gridDim.x / 2;
+  const int dir = blockIdx.x < half ? 0 : 1;
+  if (!((nbr >> dir) & 1)) return;
+  const uint32_t t = (blockIdx.x - (dir ? half : 0)) * blockDim.x + threadIdx.x;
+  const uint32_t cf = dir == 0 ? g.own_c0 : g.own_c1 - P;
+  const uint32_t lo = __ldg(&b.off[cf]), hi = __ldg(&b.off[cf + P]);
+  uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
+  if (hi - lo > L.ghost_cap) {
+    if (t == 0) raise_error(b.err, 6u, cf, hi - lo);
+    return;
+  }
+  if (t == 0) reinterpret_cast<XHeader*>(blk + L.header)->n_ghost = hi - lo;
+  const bool sw = b.sw_r > 0.f;
+  if (t < hi - lo) {
+    float4 Pp = __ldg(&b.pos_sorted[lo + t]);
+    const uint32_t s = sw ? __float_as_uint(Pp.w) : __ldg(&b.perm[lo + t]);
+    reinterpret_cast<float4*>(blk + L.gh_pos)[t] = __ldg(&b.pos_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_vel)[t] = __ldg(&b.vel_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_omg)[t] = __ldg(&b.omg_out[s]);
+  }
+  if (t <= P) reinterpret_cast<uint32_t*>(blk + L.gh_off)[t] = __ldg(&b.off[cf + t]) - lo;
 }
 
 // --------------------------------------------------- introspection ---------
@@ -2850,14 +3091,15 @@ static void launch_pdl(void (*kern)(KArgs...), unsigned grid, unsigned block, si
 }
 
 int launch_scan(cudaStream_t st, const uint32_t* in, uint32_t* out, uint32_t n, uint32_t* zero,
-                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step) {
+                unsigned long long* status, uint32_t* ctr, DevErr* err, int count_step,
+                uint32_t base0) {
   // `status` holds at least ceil(n / kScanTile) words: used as the tile sums
   (void)ctr;
   const unsigned tiles = (unsigned)((n + kScanTile - 1) / kScanTile);
   uint32_t* tsum = reinterpret_cast<uint32_t*>(status);
   launch_pdl(k_tile_sum, tiles > 0 ? tiles : 1, kScanThreads, 0, st, in, n, tsum, err, count_step);
   launch_pdl(k_scan_apply, tiles > 0 ? tiles : 1, kScanThreads, 0, st, in, out, n, zero,
-             (const uint32_t*)tsum, err);
+             (const uint32_t*)tsum, err, base0);
   return K_SCAN;
 }
 
@@ -2874,15 +3116,17 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
   if (n <= 0) return K_RANK;
   const int64_t per = 256 * kItems;
   launch_pdl(k_rank, (unsigned)((n + per - 1) / per), 256, 0, st, n, b.key_in, b.off, b.tmp, b.perm,
-             b.pos_in, b.pos_sorted, b.nslots, b.err, b.sw_r > 0.f);
+             b.pos_in, b.pos_sorted, b.nslots, b.err, b.sw_r > 0.f, b.gl_base);
   return K_RANK;
 }
 
-int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b) {
+int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b,
+                 const DevGrid& g, const uint32_t* n_dev) {
   const int64_t span = n > (int64_t)ncells + 1 ? n : (int64_t)ncells + 1;
   const unsigned grid = (unsigned)((span + kMergeSpan - 1) / kMergeSpan);
+  const uint32_t c_lo = g.slab ? g.own_c0 : 0u, c_hi = g.slab ? g.own_c1 : ncells;
   launch_pdl(k_merge, grid, 256, 0, st, (uint32_t)n, ncells, b.mv, b.pos_in, b.perm, b.pos_sorted,
-             b.off, b.err, b.sw_r > 0.f);
+             b.off, b.err, b.sw_r > 0.f, n_dev, b.gl_base, c_lo, c_hi);
   return K_RANK;
 }
 
@@ -3069,8 +3313,12 @@ int launch_flags(cudaStream_t st, int64_t n, const float4* pos, DevGrid g, uint3
 
 // initial = 1: publish the state set by dem_set_particles (xs->n_out preset)
 int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
-                 uint8_t* mine, XLayout L, XState* xs, int initial) {
+                 uint8_t* mine, XLayout L, XState* xs, int initial, int nbr) {
   const uint32_t ntiles = xtc_ntiles(cap);
+  const uint32_t per = L.ghost_cap > L.plane + 1 ? L.ghost_cap : L.plane + 1;
+  const unsigned half = (per + 255) / 256;
+  if (initial) k_xplanes_initial<<<2 * half, 256, 0, st>>>(b, g, mine, L, nbr);
+  else k_xpack_planes<<<2 * half, 256, 0, st>>>(b, g, mine, L, nbr);
   // in a step the integrator has counted the flagged outputs per tile (b.xtc)
   if (initial) k_xpack_count<<<ntiles, 256, 0, st>>>(b, g, b.xtc, ntiles, xs);
   k_xpack_write<<<ntiles, 256, 0, st>>>(b, g, K, (uint32_t)cap, mine, L, b.xtc, b.xtc_next, ntiles,
@@ -3078,12 +3326,19 @@ int launch_xpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGr
   return K_OTHER;
 }
 
-int launch_xunpack(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
-                   uint32_t K, const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
-                   uint32_t* nslots_out) {
+int launch_xrecv(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g, uint32_t K,
+                 const uint8_t* left, const uint8_t* right, XLayout L, XState* xs,
+                 uint32_t* nslots_out, bool merge) {
   const uint32_t most = 2 * L.mig_cap + 2 * L.ghost_cap;
-  k_xappend<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs,
-                                               nslots_out);
+  k_xrecv<<<(most + 255) / 256, 256, 0, st>>>(b, g, K, (uint32_t)cap, left, right, L, xs,
+                                             nslots_out, merge ? 1 : 0);
+  return K_OTHER;
+}
+
+int launch_xghost_place(cudaStream_t st, int64_t cap, const StepBuffers& b, const DevGrid& g,
+                        const uint8_t* left, const uint8_t* right, XLayout L, XState* xs) {
+  const unsigned half = (L.plane + 1 + 255) / 256;
+  k_xghost_place<<<2 * half, 256, 0, st>>>(b, g, (uint32_t)cap, left, right, L, xs);
   return K_OTHER;
 }
 
