@@ -283,7 +283,7 @@ int kernels_per_step(const dem_handle* h, bool full = false) {
   return ((h->p.flags & DEM_F_THREAD_PER_PARTICLE) ? 1 : (h->p.flags & DEM_F_HALF_LISTS) ? 3
           : fused_sweep(h)                         ? 1
                                                    : 2) +
-         sort + (h->slab ? 4 : 0);
+         sort + (h->slab ? (h->merge && !full ? 3 : 4) : 0);
 }
 
 // Enqueue one step from parity b: the sort (counting: scan, scatter, rank;
@@ -327,7 +327,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     rec(K_RANK, true);
     // (slab: the owned particles, their count from the last step's pack)
     launch_merge(h->stream, h->slab ? h->cap : h->n, h->g.ncells, s, h->g,
-                 h->slab ? &h->xs->n_out : nullptr);
+                 h->slab ? &h->xs->n_out : nullptr, xl_, xr_, h->slab ? &h->xl : nullptr, h->xs);
     rec(K_RANK, false);
     h->launches += 1;
   } else {
@@ -350,7 +350,8 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
     rec(K_RANK, false);
     h->launches += 4;  // scan is two kernels
   }
-  if (h->slab) {  // the neighbours' planes (sorted) and this rank's departed ones: ghost planes
+  if (h->slab && (full || !h->merge)) {  // (merge steps: blocks of k_merge do it)
+    // the neighbours' planes (sorted) and this rank's departed ones: ghost planes
     rec(K_OTHER, true);
     launch_xghost_place(h->stream, h->cap, s, h->g, xl_, xr_, h->xl, h->xs);
     rec(K_OTHER, false);

@@ -203,7 +203,7 @@ struct XState {  // device scratch of the exchange of one step
   uint32_t n_out;      // output slots of the last step (base of the appended slots)
   uint32_t appended[4];  // migrants from left, right; ghosts from left, right
   uint32_t done;       // pack blocks finished this step (the last one publishes)
-  uint32_t pad[2];
+  uint32_t pad[2];     // pad[0]: this step's exchange tag (set by k_xrecv)
 };
 
 enum KernelId { K_HASH = 0, K_SCAN = 1, K_SCATTER = 2, K_RANK = 3, K_SWEEP = 4, K_OTHER = 5,
@@ -253,8 +253,12 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b);
 // offsets of the owned cells only; list entries with insertion point
 // 0xFFFFFFFF (migrants that left) are removals, entries with previous key
 // 0xFFFFFFFF (migrants that arrived) insertions
+// L non-null (slab): the ghost planes are placed by extra blocks of the same
+// kernel (k_xghost_place's work, the owned end counted from the mover list)
 int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b,
-                 const DevGrid& g, const uint32_t* n_dev = nullptr);
+                 const DevGrid& g, const uint32_t* n_dev = nullptr,
+                 const uint8_t* left = nullptr, const uint8_t* right = nullptr,
+                 const XLayout* L = nullptr, XState* xs = nullptr);
 int launch_perm_from_w(cudaStream_t st, int64_t n, const float4* pos_sorted, uint32_t* perm);
 // Default: k_detect (steps 5-6: contact lists) then k_force (steps 7-8 + 1,
 // warp-cooperative). Variant 1 (ablation): one thread per particle for the

@@ -489,17 +489,138 @@ __device__ __forceinline__ int block_sum(int v, int* red) {  // 256 threads
   return s;
 }
 
+constexpr uint32_t kXDep = 1024;  // departed particles per ghost plane held in shared memory
+
+// After the owned sort: the neighbours' boundary planes (already sorted by
+// their keys, with their cell offsets) become this rank's ghost planes,
+// merged with this rank's own departed particles of that plane (listed by
+// the last integrator with insertion point 0xFFFFFFFF): within a cell the
+// departed ones come first, in slot order — the stable order of a sort over
+// this rank's input slots, where departed particles (outputs) precede the
+// appended planes. Left plane right-aligned below gl_base, right plane
+// right after the owned particles; the ghost cells' offsets, then the trash
+// cell's and the total. One thread per ghost cell.
+struct GhostSmem {
+  uint2 dep[kXDep];  // (key, slot) of this side's departed particles
+  uint32_t nd, ins, rem;
+};
+
+// One block `pb` of the 2 x half ghost-placement blocks. end_from_list: the
+// owned particles' end (the right plane's start) counted from the mover list
+// (gl_base + n + insertions - removals), for blocks that run beside the
+// merge that places the owned particles; else read from off[own_c1].
+__device__ __forceinline__ void ghost_place_block(const StepBuffers& b, const DevGrid& g, uint32_t N,
+                                                  const uint8_t* left, const uint8_t* right,
+                                                  const XLayout& L, XState* xs, uint32_t par,
+                                                  uint32_t pb, uint32_t half, bool end_from_list,
+                                                  uint32_t n_own_in, GhostSmem& sm) {
+  const uint32_t P = L.plane;
+  const int side = pb < half ? 0 : 1;  // 0: the left ghost plane
+  const uint32_t k = (pb - (side ? half : 0)) * blockDim.x + threadIdx.x;  // plane cell
+  const uint8_t* peer = side == 0 ? left : right;
+  const uint32_t cf = side == 0 ? 0u : g.own_c1;  // the ghost plane's first cell
+  // this side's departed particles from the mover list (and its counts)
+  if (threadIdx.x == 0) sm.nd = sm.ins = sm.rem = 0u;
+  __syncthreads();
+  const uint32_t m = min(ld_volatile(b.mv.n_in), b.mv.cap);
+  uint32_t ins = 0, rem = 0;
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint4 v = __ldcg(&b.mv.list_in[i]);
+    if (peer && v.w == 0xFFFFFFFFu && v.y - cf < P) {
+      const uint32_t d = atomicAdd(&sm.nd, 1u);
+      if (d < kXDep) sm.dep[d] = make_uint2(v.y, v.x);
+    }
+    ins += v.w != 0xFFFFFFFFu ? 1u : 0u;
+    rem += v.x < n_own_in ? 1u : 0u;
+  }
+  if (end_from_list) {
+    atomicAdd(&sm.ins, ins);
+    atomicAdd(&sm.rem, rem);
+  }
+  __syncthreads();
+  const uint32_t end_own = end_from_list ? b.gl_base + n_own_in + sm.ins - sm.rem
+                                         : __ldg(&b.off[g.own_c1]);
+  if (!peer) {  // no neighbour on this side: no ghost plane (the trash cell and the total)
+    if (side == 1 && k == 0) {
+      b.off[g.trash] = end_own;
+      b.off[g.ncells] = end_own;
+    }
+    return;
+  }
+  const uint32_t nd = sm.nd;
+  if (nd > kXDep) {
+    if (k == 0) raise_error(b.err, 6u, cf, nd);
+    return;
+  }
+  const uint32_t nG = xs->appended[2 + side];
+  const uint32_t gs = xs->n_out + xs->appended[0] + xs->appended[1] + (side ? xs->appended[2] : 0u);
+  const uint32_t base = side == 0 ? b.gl_base - nG - nd : end_own;
+  if ((side == 0 && nG + nd > b.gl_base) || (uint64_t)base + nG + nd > N) {
+    if (k == 0) raise_error(b.err, 6u, cf, nG + nd);
+    return;
+  }
+  if (k > P) return;
+  const uint8_t* blk = peer + (size_t)((side == 0 ? 1 : 0) * 2 + par) * L.bytes;
+  const uint32_t* goff = reinterpret_cast<const uint32_t*>(blk + L.gh_off);
+  const uint32_t c = cf + k;
+  uint32_t d_lt = 0, d_eq = 0;  // departed particles in cells below c, in c
+  for (uint32_t d = 0; d < nd; ++d) {
+    d_lt += sm.dep[d].x < c ? 1u : 0u;
+    d_eq += sm.dep[d].x == c ? 1u : 0u;
+  }
+  const uint32_t g0 = __ldcv(goff + k);
+  const uint32_t start = base + g0 + d_lt;  // the cell's first sorted slot
+  const bool sw = b.sw_r > 0.f;
+  auto place = [&](uint32_t j, uint32_t q) {  // sorted slot j <- input slot q
+    float4 S = __ldg(&b.pos_in[q]);
+    if (sw) S.w = __uint_as_float(q);
+    else b.perm[j] = q;
+    b.pos_sorted[j] = S;
+  };
+  if (k == P) {  // one past the plane: the owned particles' start / the trash cell
+    if (side == 1) {
+      b.off[g.trash] = start;
+      b.off[g.ncells] = start;
+    }
+    return;
+  }
+  b.off[c] = start;
+  if (d_eq) {  // departed particles of this cell, in slot order
+    for (uint32_t d = 0; d < nd; ++d) {
+      if (sm.dep[d].x != c) continue;
+      uint32_t r = 0;
+      for (uint32_t e = 0; e < nd; ++e)
+        r += (sm.dep[e].x == c && sm.dep[e].y < sm.dep[d].y) ? 1u : 0u;
+      place(start + r, sm.dep[d].y);
+    }
+  }
+  const uint32_t g1 = __ldcv(goff + k + 1);
+  for (uint32_t i = g0; i < g1; ++i) place(start + d_eq + (i - g0), gs + i);
+}
+
 // Slab ranks: n from n_dev (the previous step's owned outputs), sorted slots
 // from `base` (constant across steps), offsets of cells [c_lo, c_hi] only; a
 // list entry with insertion point 0xFFFFFFFF (a migrant that left) is a
 // removal only, one with previous key 0xFFFFFFFF (an arrived migrant,
 // appended past the outputs) an insertion only. Single GPU: n_dev null,
 // base 0, [0, ncells].
+struct GhostArgs {  // slab ranks: the ghost-placement blocks that run beside the merge
+  StepBuffers b;
+  DevGrid g;
+  const uint8_t *left, *right;
+  XLayout L;
+  XState* xs;
+  uint32_t N;
+  uint32_t nghost;  // blocks at the end of k_merge's grid (0: single GPU)
+};
+
+// GH: slab ranks, the ghost planes placed by the last ga.nghost blocks
+template <bool GH>
 __global__ void __launch_bounds__(256)
     k_merge(uint32_t n, uint32_t ncells, MergeBuffers mb, const float4* __restrict__ pos_in,
             uint32_t* __restrict__ perm, float4* __restrict__ pos_sorted,
             uint32_t* __restrict__ off, DevErr* err, bool sw, const uint32_t* n_dev,
-            uint32_t base, uint32_t c_lo, uint32_t c_hi) {
+            uint32_t base, uint32_t c_lo, uint32_t c_hi, const __grid_constant__ GhostArgs ga) {
   pdl_enter();
   __shared__ int red[2][8];
   __shared__ int2 red2[8];
@@ -510,7 +631,20 @@ __global__ void __launch_bounds__(256)
   // the error word, the mover count and this block's positions go out together
   const uint32_t e = ld_volatile(&err->code);
   const uint32_t m = ld_volatile(mb.n_in);
-  if (n_dev) n = *n_dev;
+  if (GH) n = *n_dev;
+  if (!GH) {  // (single GPU: every slot and cell from 0)
+    base = 0u;
+    c_lo = 0u;
+    c_hi = ncells;
+  }
+  const uint32_t mgrid = GH ? gridDim.x - ga.nghost : gridDim.x;  // the merge's own blocks
+  if (GH && b >= mgrid) {  // slab: place the ghost planes (they need no result of the merge)
+    __shared__ GhostSmem gsm;
+    if (e != 0u || m > mb.cap) return;
+    ghost_place_block(ga.b, ga.g, ga.N, ga.left, ga.right, ga.L, ga.xs, ga.xs->pad[0] & 1u,
+                      b - mgrid, ga.nghost / 2, true, n, gsm);
+    return;
+  }
   float4 P[kMergeItems];
 #pragma unroll
   for (int u = 0; u < kMergeItems; ++u) {
@@ -601,7 +735,7 @@ __global__ void __launch_bounds__(256)
     }
   }
   // movers b, b + grid, ...: r_i + x_i - #{a_j < x_i}, counted block-wide
-  for (uint32_t i = b; i < m; i += gridDim.x) {
+  for (uint32_t i = b; i < m; i += mgrid) {
     const uint4 mi = __ldcg(&mb.list_in[i]);
     if (mi.w == 0xFFFFFFFFu) continue;  // (block-uniform) a migrant that left: no insertion
     int r = 0;
@@ -2376,6 +2510,105 @@ __global__ void __launch_bounds__(256) k_xpack_count(StepBuffers b, DevGrid g, u
   }
 }
 
+constexpr uint32_t kXPlaneMv = 1024;  // movers in or out of a boundary plane held in shared memory
+
+// Step end: this rank's boundary plane (the first owned plane for the left
+// neighbour, dir 0; the last for the right one) as the next step's sort will
+// order it — the plane's stayers, minus the movers that left it, plus those
+// that entered it, by k_merge's counts restricted to the plane's cells (the
+// mover list is complete once the integrator is done) — with the new state
+// and the plane's cell offsets relative to its first particle; its count in
+// the header (the pack's last block releases the tag). Threads over the
+// plane's previous slots, its entering movers and its cells.
+struct PlaneSmem {
+  uint4 in[kXPlaneMv];   // (key, slot, insertion point) of the entering movers
+  uint2 out[kXPlaneMv];  // (previous slot, previous key) of the leaving ones
+  uint32_t ni, no;
+};
+
+// (one block `pb` of the 2 x half plane blocks; returns without writing for
+// a direction with no neighbour)
+__device__ __forceinline__ void xpack_plane_block(const StepBuffers& b, const DevGrid& g,
+                                                  uint8_t* mine, const XLayout& L, int nbr,
+                                                  uint32_t pb, uint32_t half, PlaneSmem& sm) {
+  uint4* s_in = sm.in;
+  uint2* s_out = sm.out;
+  uint32_t& s_ni = sm.ni;
+  uint32_t& s_no = sm.no;
+  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
+  const uint32_t par = tag & 1u;
+  const uint32_t P = L.plane;
+  const int dir = pb < half ? 0 : 1;
+  if (!((nbr >> dir) & 1)) return;
+  const uint32_t t = (pb - (dir ? half : 0)) * blockDim.x + threadIdx.x;
+  const uint32_t cf = dir == 0 ? g.own_c0 : g.own_c1 - P;
+  const uint32_t gl = b.gl_base;
+  const uint32_t A = __ldg(&b.off[cf]) - gl, B = __ldg(&b.off[cf + P]) - gl;  // output slots
+  if (threadIdx.x == 0) s_ni = s_no = 0u;
+  __syncthreads();
+  const uint32_t m = min(ld_volatile(b.mv.n_out), b.mv.cap);
+  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
+    const uint4 v = __ldcg(&b.mv.list_out[i]);  // (a, c, c', x)
+    if (v.w != 0xFFFFFFFFu && v.y - cf < P) {
+      const uint32_t q = atomicAdd(&s_ni, 1u);
+      if (q < kXPlaneMv) s_in[q] = make_uint4(v.y, v.x, v.w, 0u);
+    }
+    if (v.z - cf < P) {
+      const uint32_t q = atomicAdd(&s_no, 1u);
+      if (q < kXPlaneMv) s_out[q] = make_uint2(v.x, v.z);
+    }
+  }
+  __syncthreads();
+  const uint32_t ni = s_ni, no = s_no;
+  uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
+  const uint32_t n_new = (B - A) - no + ni;
+  if (ni > kXPlaneMv || no > kXPlaneMv || n_new > L.ghost_cap) {
+    if (t == 0) raise_error(b.err, 6u, cf, n_new);
+    return;
+  }
+  if (t == 0) reinterpret_cast<XHeader*>(blk + L.header)->n_ghost = n_new;
+  auto put = [&](uint32_t p, uint32_t s) {  // plane position p <- output slot s (new state)
+    reinterpret_cast<float4*>(blk + L.gh_pos)[p] = __ldg(&b.pos_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_vel)[p] = __ldg(&b.vel_out[s]);
+    reinterpret_cast<float4*>(blk + L.gh_omg)[p] = __ldg(&b.omg_out[s]);
+  };
+  if (t < B - A) {  // a previous member: kept unless it left
+    const uint32_t s = A + t;
+    int d = 0;
+    bool gone = false;
+    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].z <= s ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) {
+      d -= s_out[i].x <= s ? 1 : 0;
+      gone |= s_out[i].x == s;
+    }
+    if (!gone) put((uint32_t)((int)t + d), s);
+  }
+  if (t < ni) {  // an entering mover: its rank among them + the stayers before its point
+    const uint4 mi = s_in[t];
+    int r = 0;
+    for (uint32_t i = 0; i < ni; ++i)
+      r += (s_in[i].x < mi.x || (s_in[i].x == mi.x && s_in[i].y < mi.y)) ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) r -= s_out[i].x < mi.z ? 1 : 0;
+    put((uint32_t)(r + (int)(mi.z - A)), mi.y);
+  }
+  if (t <= P) {  // the cell offsets, relative to the plane's first particle
+    const uint32_t c = cf + t;
+    int d = (int)(__ldg(&b.off[c]) - gl - A);
+    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].x < c ? 1 : 0;
+    for (uint32_t i = 0; i < no; ++i) d -= s_out[i].y < c ? 1 : 0;
+    reinterpret_cast<uint32_t*>(blk + L.gh_off)[t] = (uint32_t)d;
+  }
+}
+
+__global__ void __launch_bounds__(256) k_xpack_planes(StepBuffers b, DevGrid g, uint8_t* mine,
+                                                      XLayout L, int nbr) {
+  __shared__ PlaneSmem sm;
+  if (ld_volatile(&b.err->code) != 0u) return;
+  if (threadIdx.x == 0) sm.ni = sm.no = 0u;
+  __syncthreads();
+  xpack_plane_block(b, g, mine, L, nbr, blockIdx.x, gridDim.x / 2, sm);
+}
+
 // deterministic placement: prefix over earlier tiles + in-tile rank (slot
 // order); the last block to finish publishes the header counts and the tag
 // (system-scope release). Each block clears its tile's counts of the other
@@ -2391,14 +2624,15 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
   __shared__ uint32_t s_cnt[4][32];  // [category][sub-tile * 8 + warp]
   __shared__ uint32_t s_last;
   if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t n_out = initial ? xs->n_out : owned_out(b, g);
+  const uint32_t writers = __ldcg(&tc[5 * ntiles]);  // tiles with flagged outputs
   const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
   const uint32_t par = tag & 1u;
+  {
+  const uint32_t n_out = initial ? xs->n_out : owned_out(b, g);
   const uint32_t lane = lane_id(), warp = threadIdx.x >> 5;
   // a tile without flagged outputs (all but the boundary planes' few) has
   // nothing to write: straight to the publication count
   const bool any = __ldcg(&tc[4 * ntiles + blockIdx.x]) != 0u;
-  const uint32_t writers = __ldcg(&tc[5 * ntiles]);  // tiles with flagged outputs
   // this tile's base per category: the counts of the earlier tiles, summed
   // block-wide (a serial sum by 4 threads cost ~100 us per step at 500 tiles)
   if (any) {
@@ -2509,6 +2743,7 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
       s_last = 1u;
     }
   }
+  }
   __syncthreads();
   if (!s_last) return;
   __threadfence();
@@ -2606,6 +2841,7 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
   }
   if (blockIdx.x == 0 && threadIdx.x == 0) {
     for (int q = 0; q < 4; ++q) xs->appended[q] = s_cnt[q];
+    xs->pad[0] = tag;  // this step's tag (k_merge's ghost blocks take its parity)
     *nslots = base + c0 + c1;
   }
   const uint32_t i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -2656,181 +2892,15 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
   }
 }
 
-constexpr uint32_t kXDep = 1024;  // departed particles per ghost plane held in shared memory
-
-// After the owned sort: the neighbours' boundary planes (already sorted by
-// their keys, with their cell offsets) become this rank's ghost planes,
-// merged with this rank's own departed particles of that plane (listed by
-// the last integrator with insertion point 0xFFFFFFFF): within a cell the
-// departed ones come first, in slot order — the stable order of a sort over
-// this rank's input slots, where departed particles (outputs) precede the
-// appended planes. Left plane right-aligned below gl_base, right plane
-// right after the owned particles; the ghost cells' offsets, then the trash
-// cell's and the total. One thread per ghost cell.
+// (after a counting sort: the owned particles are placed, off[own_c1] is set)
 __global__ void __launch_bounds__(256) k_xghost_place(StepBuffers b, DevGrid g, uint32_t N,
                                                       const uint8_t* left, const uint8_t* right,
                                                       XLayout L, XState* xs) {
-  __shared__ uint2 s_dep[kXDep];  // (key, slot) of this side's departed particles
-  __shared__ uint32_t s_nd;
+  __shared__ GhostSmem sm;
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t tag = ld_volatile(&b.err->step_ctr) + g.xbase;  // (the sort counted this step)
-  const uint32_t par = tag & 1u;
-  const uint32_t P = L.plane;
-  const uint32_t half = gridDim.x / 2;
-  const int side = blockIdx.x < half ? 0 : 1;  // 0: the left ghost plane
-  const uint32_t k = (blockIdx.x - (side ? half : 0)) * blockDim.x + threadIdx.x;  // plane cell
-  const uint8_t* peer = side == 0 ? left : right;
-  const uint32_t end_own = __ldg(&b.off[g.own_c1]);
-  if (!peer) {  // no neighbour on this side: no ghost plane (the trash cell and the total)
-    if (side == 1 && k == 0) {
-      b.off[g.trash] = end_own;
-      b.off[g.ncells] = end_own;
-    }
-    return;
-  }
-  const uint32_t cf = side == 0 ? 0u : g.own_c1;  // the ghost plane's first cell
-  // this side's departed particles from the mover list
-  if (threadIdx.x == 0) s_nd = 0u;
-  __syncthreads();
-  const uint32_t m = min(ld_volatile(b.mv.n_in), b.mv.cap);
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const uint4 v = __ldcg(&b.mv.list_in[i]);
-    if (v.w == 0xFFFFFFFFu && v.y - cf < P) {
-      const uint32_t d = atomicAdd(&s_nd, 1u);
-      if (d < kXDep) s_dep[d] = make_uint2(v.y, v.x);
-    }
-  }
-  __syncthreads();
-  const uint32_t nd = s_nd;
-  if (nd > kXDep) {
-    if (k == 0) raise_error(b.err, 6u, cf, nd);
-    return;
-  }
-  const uint32_t nG = xs->appended[2 + side];
-  const uint32_t gs = xs->n_out + xs->appended[0] + xs->appended[1] + (side ? xs->appended[2] : 0u);
-  const uint32_t base = side == 0 ? b.gl_base - nG - nd : end_own;
-  if ((side == 0 && nG + nd > b.gl_base) || (uint64_t)base + nG + nd > N) {
-    if (k == 0) raise_error(b.err, 6u, cf, nG + nd);
-    return;
-  }
-  if (k > P) return;
-  const uint8_t* blk = peer + (size_t)((side == 0 ? 1 : 0) * 2 + par) * L.bytes;
-  const uint32_t* goff = reinterpret_cast<const uint32_t*>(blk + L.gh_off);
-  const uint32_t c = cf + k;
-  uint32_t d_lt = 0, d_eq = 0;  // departed particles in cells below c, in c
-  for (uint32_t d = 0; d < nd; ++d) {
-    d_lt += s_dep[d].x < c ? 1u : 0u;
-    d_eq += s_dep[d].x == c ? 1u : 0u;
-  }
-  const uint32_t g0 = __ldcv(goff + k);
-  const uint32_t start = base + g0 + d_lt;  // the cell's first sorted slot
-  const bool sw = b.sw_r > 0.f;
-  auto place = [&](uint32_t j, uint32_t q) {  // sorted slot j <- input slot q
-    float4 S = __ldg(&b.pos_in[q]);
-    if (sw) S.w = __uint_as_float(q);
-    else b.perm[j] = q;
-    b.pos_sorted[j] = S;
-  };
-  if (k == P) {  // one past the plane: the owned particles' start / the trash cell
-    if (side == 1) {
-      b.off[g.trash] = start;
-      b.off[g.ncells] = start;
-    }
-    return;
-  }
-  b.off[c] = start;
-  if (d_eq) {  // departed particles of this cell, in slot order
-    for (uint32_t d = 0; d < nd; ++d) {
-      if (s_dep[d].x != c) continue;
-      uint32_t r = 0;
-      for (uint32_t e = 0; e < nd; ++e) r += (s_dep[e].x == c && s_dep[e].y < s_dep[d].y) ? 1u : 0u;
-      place(start + r, s_dep[d].y);
-    }
-  }
-  const uint32_t g1 = __ldcv(goff + k + 1);
-  for (uint32_t i = g0; i < g1; ++i) place(start + d_eq + (i - g0), gs + i);
-}
-
-constexpr uint32_t kXPlaneMv = 1024;  // movers in or out of a boundary plane held in shared memory
-
-// Step end: this rank's boundary plane (the first owned plane for the left
-// neighbour, dir 0; the last for the right one) as the next step's sort will
-// order it — the plane's stayers, minus the movers that left it, plus those
-// that entered it, by k_merge's counts restricted to the plane's cells (the
-// mover list is complete once the integrator is done) — with the new state
-// and the plane's cell offsets relative to its first particle; its count in
-// the header (the pack's last block releases the tag). Threads over the
-// plane's previous slots, its entering movers and its cells.
-__global__ void __launch_bounds__(256) k_xpack_planes(StepBuffers b, DevGrid g, uint8_t* mine,
-                                                      XLayout L, int nbr) {
-  __shared__ uint4 s_in[kXPlaneMv];   // (key, slot, insertion point) of the entering movers
-  __shared__ uint2 s_out[kXPlaneMv];  // (previous slot, previous key) of the leaving ones
-  __shared__ uint32_t s_ni, s_no;
-  if (ld_volatile(&b.err->code) != 0u) return;
-  const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
-  const uint32_t par = tag & 1u;
-  const uint32_t P = L.plane;
-  const uint32_t half = gridDim.x / 2;
-  const int dir = blockIdx.x < half ? 0 : 1;
-  if (!((nbr >> dir) & 1)) return;
-  const uint32_t t = (blockIdx.x - (dir ? half : 0)) * blockDim.x + threadIdx.x;
-  const uint32_t cf = dir == 0 ? g.own_c0 : g.own_c1 - P;
-  const uint32_t gl = b.gl_base;
-  const uint32_t A = __ldg(&b.off[cf]) - gl, B = __ldg(&b.off[cf + P]) - gl;  // output slots
-  if (threadIdx.x == 0) s_ni = s_no = 0u;
-  __syncthreads();
-  const uint32_t m = min(ld_volatile(b.mv.n_out), b.mv.cap);
-  for (uint32_t i = threadIdx.x; i < m; i += blockDim.x) {
-    const uint4 v = __ldcg(&b.mv.list_out[i]);  // (a, c, c', x)
-    if (v.w != 0xFFFFFFFFu && v.y - cf < P) {
-      const uint32_t q = atomicAdd(&s_ni, 1u);
-      if (q < kXPlaneMv) s_in[q] = make_uint4(v.y, v.x, v.w, 0u);
-    }
-    if (v.z - cf < P) {
-      const uint32_t q = atomicAdd(&s_no, 1u);
-      if (q < kXPlaneMv) s_out[q] = make_uint2(v.x, v.z);
-    }
-  }
-  __syncthreads();
-  const uint32_t ni = s_ni, no = s_no;
-  uint8_t* blk = mine + (size_t)(dir * 2 + par) * L.bytes;
-  const uint32_t n_new = (B - A) - no + ni;
-  if (ni > kXPlaneMv || no > kXPlaneMv || n_new > L.ghost_cap) {
-    if (t == 0) raise_error(b.err, 6u, cf, n_new);
-    return;
-  }
-  if (t == 0) reinterpret_cast<XHeader*>(blk + L.header)->n_ghost = n_new;
-  auto put = [&](uint32_t p, uint32_t s) {  // plane position p <- output slot s (new state)
-    reinterpret_cast<float4*>(blk + L.gh_pos)[p] = __ldg(&b.pos_out[s]);
-    reinterpret_cast<float4*>(blk + L.gh_vel)[p] = __ldg(&b.vel_out[s]);
-    reinterpret_cast<float4*>(blk + L.gh_omg)[p] = __ldg(&b.omg_out[s]);
-  };
-  if (t < B - A) {  // a previous member: kept unless it left
-    const uint32_t s = A + t;
-    int d = 0;
-    bool gone = false;
-    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].z <= s ? 1 : 0;
-    for (uint32_t i = 0; i < no; ++i) {
-      d -= s_out[i].x <= s ? 1 : 0;
-      gone |= s_out[i].x == s;
-    }
-    if (!gone) put((uint32_t)((int)t + d), s);
-  }
-  if (t < ni) {  // an entering mover: its rank among them + the stayers before its point
-    const uint4 mi = s_in[t];
-    int r = 0;
-    for (uint32_t i = 0; i < ni; ++i)
-      r += (s_in[i].x < mi.x || (s_in[i].x == mi.x && s_in[i].y < mi.y)) ? 1 : 0;
-    for (uint32_t i = 0; i < no; ++i) r -= s_out[i].x < mi.z ? 1 : 0;
-    put((uint32_t)(r + (int)(mi.z - A)), mi.y);
-  }
-  if (t <= P) {  // the cell offsets, relative to the plane's first particle
-    const uint32_t c = cf + t;
-    int d = (int)(__ldg(&b.off[c]) - gl - A);
-    for (uint32_t i = 0; i < ni; ++i) d += s_in[i].x < c ? 1 : 0;
-    for (uint32_t i = 0; i < no; ++i) d -= s_out[i].y < c ? 1 : 0;
-    reinterpret_cast<uint32_t*>(blk + L.gh_off)[t] = (uint32_t)d;
-  }
+  ghost_place_block(b, g, N, left, right, L, xs, tag & 1u, blockIdx.x, gridDim.x / 2, false, 0u,
+                    sm);
 }
 
 // The set state's boundary planes (dem_set_particles sorts it by counting
@@ -3121,12 +3191,31 @@ int launch_rank(cudaStream_t st, int64_t n, const StepBuffers& b) {
 }
 
 int launch_merge(cudaStream_t st, int64_t n, uint32_t ncells, const StepBuffers& b,
-                 const DevGrid& g, const uint32_t* n_dev) {
+                 const DevGrid& g, const uint32_t* n_dev, const uint8_t* left,
+                 const uint8_t* right, const XLayout* L, XState* xs) {
   const int64_t span = n > (int64_t)ncells + 1 ? n : (int64_t)ncells + 1;
-  const unsigned grid = (unsigned)((span + kMergeSpan - 1) / kMergeSpan);
-  const uint32_t c_lo = g.slab ? g.own_c0 : 0u, c_hi = g.slab ? g.own_c1 : ncells;
-  launch_pdl(k_merge, grid, 256, 0, st, (uint32_t)n, ncells, b.mv, b.pos_in, b.perm, b.pos_sorted,
-             b.off, b.err, b.sw_r > 0.f, n_dev, b.gl_base, c_lo, c_hi);
+  unsigned grid = (unsigned)((span + kMergeSpan - 1) / kMergeSpan);
+  // (slab: off[own_c1], the owned particles' end, is written by the ghost
+  // blocks, which count it from the list: the merge blocks leave it alone)
+  const uint32_t c_lo = g.slab ? g.own_c0 : 0u, c_hi = g.slab ? g.own_c1 - (L ? 1u : 0u) : ncells;
+  GhostArgs ga{};
+  if (L) {  // slab ranks: the ghost planes' blocks after the merge's
+    ga.b = b;
+    ga.g = g;
+    ga.left = left;
+    ga.right = right;
+    ga.L = *L;
+    ga.xs = xs;
+    ga.N = (uint32_t)n;
+    ga.nghost = 2 * ((L->plane + 1 + 255) / 256);
+    grid += ga.nghost;
+  }
+  if (L)
+    launch_pdl(k_merge<true>, grid, 256, 0, st, (uint32_t)n, ncells, b.mv, b.pos_in, b.perm,
+               b.pos_sorted, b.off, b.err, b.sw_r > 0.f, n_dev, b.gl_base, c_lo, c_hi, ga);
+  else
+    launch_pdl(k_merge<false>, grid, 256, 0, st, (uint32_t)n, ncells, b.mv, b.pos_in, b.perm,
+               b.pos_sorted, b.off, b.err, b.sw_r > 0.f, n_dev, b.gl_base, c_lo, c_hi, ga);
   return K_RANK;
 }
 
