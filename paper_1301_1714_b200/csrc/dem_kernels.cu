@@ -585,17 +585,23 @@ __device__ __forceinline__ void ghost_place_block(const StepBuffers& b, const De
     return;
   }
   b.off[c] = start;
+  // within a cell, where one sorted order of all the particles (a single
+  // GPU's) puts them: this rank's departed particles came from the plane
+  // above the left ghost plane (later slots: after the cell's particles)
+  // and from the plane below the right one (earlier slots: before them)
+  const uint32_t g1 = __ldcv(goff + k + 1);
+  const uint32_t dep0 = side == 0 ? start + (g1 - g0) : start;  // the departed ones' first slot
+  const uint32_t gh0 = side == 0 ? start : start + d_eq;        // the received ones' first slot
   if (d_eq) {  // departed particles of this cell, in slot order
     for (uint32_t d = 0; d < nd; ++d) {
       if (sm.dep[d].x != c) continue;
       uint32_t r = 0;
       for (uint32_t e = 0; e < nd; ++e)
         r += (sm.dep[e].x == c && sm.dep[e].y < sm.dep[d].y) ? 1u : 0u;
-      place(start + r, sm.dep[d].y);
+      place(dep0 + r, sm.dep[d].y);
     }
   }
-  const uint32_t g1 = __ldcv(goff + k + 1);
-  for (uint32_t i = g0; i < g1; ++i) place(start + d_eq + (i - g0), gs + i);
+  for (uint32_t i = g0; i < g1; ++i) place(gh0 + (i - g0), gs + i);
 }
 
 // Slab ranks: n from n_dev (the previous step's owned outputs), sorted slots
@@ -741,7 +747,10 @@ __global__ void __launch_bounds__(256)
     int r = 0;
     for (uint32_t jj = t; jj < m; jj += 256u) {
       const uint4 v = __ldcg(&mb.list_in[jj]);
-      r += (int)(v.w != 0xFFFFFFFFu && (v.y < mi.y || (v.y == mi.y && v.x < mi.x))) -
+      // (c, arrival from the left first, slot) order of the insertions
+      const bool vl = v.z == 0xFFFFFFFEu, ml = mi.z == 0xFFFFFFFEu;
+      r += (int)(v.w != 0xFFFFFFFFu &&
+                 (v.y < mi.y || (v.y == mi.y && (vl > ml || (vl == ml && v.x < mi.x))))) -
            (int)(v.x < mi.w);
     }
     r = block_sum(r, red[0]);
@@ -2883,10 +2892,15 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
   }
   const_cast<uint32_t*>(b.key_in)[slot] = k2;
   if (merge) {
+    // where one sorted order of all the particles puts it: an arrival from
+    // the left came from earlier slots (first in its cell, before the cell's
+    // movers: previous key 0xFFFFFFFE ranks it first), one from the right
+    // from later slots (last in its cell)
     const uint32_t idx = atomicAdd(const_cast<uint32_t*>(b.mv.n_in), 1u);  // (order-free counts)
     if (idx < b.mv.cap)
       const_cast<uint4*>(b.mv.list_in)[idx] =
-          make_uint4(slot, k2, 0xFFFFFFFFu, __ldg(&b.off[k2 + 1]) - b.gl_base);
+          from_left ? make_uint4(slot, k2, 0xFFFFFFFEu, __ldg(&b.off[k2]) - b.gl_base)
+                    : make_uint4(slot, k2, 0xFFFFFFFFu, __ldg(&b.off[k2 + 1]) - b.gl_base);
   } else {
     b.prank[slot] = count_into_cell(b.count, k2);
   }
