@@ -1220,6 +1220,13 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // b.sw_r.
 // The list goes to `out` with stride `ostride` (k_detect: clist + j, N; the
 // fused sweep: its warp's shared-memory list, [k][lane]).
+#ifndef DEM_DETECT_FLAT
+#define DEM_DETECT_FLAT 3
+#endif
+// fused sweep (SMEM): each plane's 3 rows scanned as one run, kDetectFlat
+// candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
+// with it, +27% there — profiles/r2_history.md #26)
+constexpr int kDetectFlat = DEM_DETECT_FLAT;
 template <bool EXACT, bool MONO = false, bool SMEM = false>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
                                                 int cx, int cy, int cz, uint32_t j,
@@ -1233,6 +1240,54 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
   // those of them above S²(1 - 16u) are in the band (the EXACT scan's own
   // thresholds), so a non-touching candidate costs one compare
   const float S2lo = S2c * 0.99999904632568359375f, S2hi = S2c * 1.00000095367431640625f;
+  if (!EXACT && MONO && SMEM && kDetectFlat > 1) {
+    // the plane's 3 rows as one flattened run u = 0..n0+n1+n2 (the same
+    // candidate order), kDetectFlat candidate loads in flight per iteration
+#pragma unroll 1
+    for (int dz = -1; dz <= 1; ++dz) {
+      const int z = cz + dz;
+      if (z < 0 || z >= g.nz) continue;
+      uint32_t t0[3], t1[3];
+#pragma unroll
+      for (int r = 0; r < 3; ++r) {
+        const int y = cy + r - 1;
+        const bool in = y >= 0 && y < g.ny;
+        const uint32_t row = (uint32_t)z * nxy + (uint32_t)(in ? y : 0) * (uint32_t)g.nx;
+        t0[r] = in ? __ldg(&b.off[row + xa]) : 0u;
+        t1[r] = in ? __ldg(&b.off[row + xb + 1]) : 0u;
+      }
+      const uint32_t c1 = t1[0] - t0[0], c2 = c1 + (t1[1] - t0[1]), nt = c2 + (t1[2] - t0[2]);
+      const uint32_t b0 = t0[0], b1 = t0[1] - c1, b2 = t0[2] - c2;  // t = u + b(row of u)
+#pragma unroll 1
+      for (uint32_t u = 0; u < nt; u += (uint32_t)(kDetectFlat > 1 ? kDetectFlat : 1)) {
+        constexpr int U = kDetectFlat > 1 ? kDetectFlat : 1;
+        float4 Q[U];
+        uint32_t tt[U];
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+          const uint32_t uu = u + (uint32_t)v;
+          tt[v] = uu + (uu < c1 ? b0 : uu < c2 ? b1 : b2);
+          Q[v] = uu < nt ? __ldg(&b.pos_sorted[tt[v]]) : make_float4(3.0e38f, 0.f, 0.f, 0.f);
+        }
+#pragma unroll
+        for (int v = 0; v < U; ++v) {
+          const float dx = Q[v].x - P.x, dy = Q[v].y - P.y, dz2 = Q[v].z - P.z;
+          const float d2 = dx * dx + dy * dy + dz2 * dz2;
+          if (d2 < S2hi && tt[v] != j) {
+            asm volatile("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f00000000, %3, p;}"
+                         : "=f"(amb) : "f"(d2), "f"(S2lo), "f"(amb));
+            if (npair < K) {
+              if (SMEM) *out = __float_as_uint(Q[v].w);
+              else __stcg(out, __float_as_uint(Q[v].w));
+            }
+            out += ostride;
+            ++npair;
+          }
+        }
+      }
+    }
+    return npair;
+  }
 #pragma unroll 1
   for (int dz = -1; dz <= 1; ++dz) {
     const int z = cz + dz;
