@@ -271,10 +271,13 @@ StepBuffers step_buffers(dem_handle* h, int b) {
 // many contact rounds (C3: 0.0894 -> 0.0816 ms/step); on the light bed (C4)
 // the split kernels win (0.611 vs 0.631: the detection loop then runs at the
 // force kernel's occupancy and L1 share)
+#ifndef DEM_FUSED_LIGHT
+#define DEM_FUSED_LIGHT 1
+#endif
 bool fused_sweep(const dem_handle* h) {
   return h->mono_r > 0.f && !(h->p.flags & (DEM_F_THREAD_PER_PARTICLE | DEM_F_HALF_LISTS |
                                             DEM_F_SPLIT_SWEEP)) &&
-         h->fcfg == 0;
+         (h->fcfg == 0 || (DEM_FUSED_LIGHT && h->fcfg == 1));
 }
 
 int kernels_per_step(const dem_handle* h, bool full = false) {
@@ -366,7 +369,7 @@ int enqueue_step(dem_handle* h, int b, bool profile, bool full = false) {
                       : (h->p.flags & DEM_F_HALF_LISTS)        ? 0
                       : (h->fcfg == 3)                         ? 5
                       : (h->fcfg == 2)                         ? 4
-                      : fused                                  ? 6
+                      : fused                                  ? (h->fcfg == 1 ? 7 : 6)
                       : (h->fcfg == 1)                         ? 3
                                                                : 2;
   if (variant == 0) {  // half lists: detect, pair, finish

@@ -227,7 +227,7 @@ def test_bench_instantiation_bitwise(name):
     (state and δ_t), in the same force configuration."""
     sc = S.C3() if name == "C3" else S.C4(scale=4) if name == "C4/4" else S.C5(scale=4)
     runs = []
-    # the bench's kernel (no DIAG; C3: detection fused into it), its DIAG twin, and the
+    # the bench's kernel (no DIAG; one radius: detection fused into it), its DIAG twin, and the
     # split path (k_detect writing lists to HBM, then k_force)
     for flags in (DEM_F_DIAG, 0, DEM_F_SPLIT_SWEEP):
         d = make(sc, flags=flags)
@@ -235,7 +235,7 @@ def test_bench_instantiation_bitwise(name):
         runs.append((d.get_state(), contacts_dict(d), d.stats()["force_cfg"],
                      d.stats()["fused_sweep"]))
     assert {r[2] for r in runs} == {"dense" if name == "C3" else "light"}
-    assert [r[3] for r in runs] == ([True, True, False] if name == "C3" else [False] * 3)
+    assert [r[3] for r in runs] == ([True, True, False] if name != "C5/4" else [False] * 3)
     for r in runs[1:]:
         for k in ("pos", "vel", "omega", "id"):
             assert np.array_equal(runs[0][0][k], r[0][k]), k

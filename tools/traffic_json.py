@@ -1,7 +1,9 @@
 """Write profiles/traffic_<config>_<model>.json from an ncu --set full capture
-of one k_detect + one k_force launch (tools/ncu_sweep_full.sh) and the bench
-line that run printed: DRAM bytes of the sweep per step, with the capture's
-step index and c̄ beside it (bench.py copies them into roofline.traffic).
+of the sweep's launches (k_detect + k_force, or the fused k_force alone; one
+or more steps: per-kernel figures are averaged over that kernel's launches)
+and the bench line that run printed: DRAM bytes of the sweep per step, with
+the capture's first step index and c̄ beside it (bench.py copies them into
+roofline.traffic).
 
     python tools/traffic_json.py gpurun_out/full_C4_TAG.ncu-rep gpurun_out/ncu_TAG.log \
         --skip 8 --warmup 5 [--config C4 --model practical]
@@ -24,15 +26,19 @@ out = subprocess.check_output(["ncu", "-i", a.rep, "--page", "raw", "--csv"], te
                               stderr=subprocess.DEVNULL)
 rows = list(csv.reader(io.StringIO(out)))
 hdr = rows[0]
-per, inst = {}, {}
+per, inst, cnt = {}, {}, {}
 for r in rows[2:]:
     d = dict(zip(hdr, r))
     name = d["Kernel Name"].split("<")[0].split("(")[0].replace("void ", "").strip()
     b = sum(float(d[k].replace(",", "")) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[u]
             for k, u in ((k, rows[1][hdr.index(k)]) for k in ("dram__bytes_read.sum", "dram__bytes_write.sum")))
-    per[name] = b
+    cnt[name] = cnt.get(name, 0) + 1
+    per[name] = per.get(name, 0.0) + b
     if "smsp__inst_executed.sum" in d:  # warp instructions issued by the launch
-        inst[name] = float(d["smsp__inst_executed.sum"].replace(",", ""))
+        inst[name] = inst.get(name, 0.0) + float(d["smsp__inst_executed.sum"].replace(",", ""))
+per = {k: v / cnt[k] for k, v in per.items()}
+inst = {k: v / cnt[k] for k, v in inst.items()}
+kps = len(per)  # sweep kernels per step
 line = None
 for ln in open(a.log):
     ln = ln.strip()
@@ -48,13 +54,14 @@ res = {
     "warp_inst_per_kernel": inst,
     "bytes_per_particle": tot / n,
     "alg_bytes_per_particle": line["roofline"]["alg_bytes_per_particle"],
-    "step": a.skip // 2 + 1,
+    "step": a.skip // kps + 1,
+    "launches_averaged": cnt,
     "c_bar": line["config"]["c_bar"],
     "n_particles": n,
     "commit": commit,
     "file": os.path.basename(a.rep),
     "source": (f"ncu --set full --clock-control none of bench.py --config {a.config}: launch "
-               f"pair {a.skip // 2 + 1} of k_detect + k_force (dram__bytes_read.sum + "
+               f"step {a.skip // kps + 1} on of {' + '.join(sorted(per))} (dram__bytes_read.sum + "
                f"dram__bytes_write.sum); c_bar = the bench line of the same run (its "
                f"profiled region, steps warmup+1..warmup+K)"),
 }
