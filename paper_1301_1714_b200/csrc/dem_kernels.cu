@@ -1227,7 +1227,11 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
 // with it, +27% there — profiles/r2_history.md #26)
 constexpr int kDetectFlat = DEM_DETECT_FLAT;
-template <bool EXACT, bool MONO = false, bool SMEM = false>
+// PRED (fused sweep, dense configuration): a hit handled by predicated
+// instructions instead of a branch — with ~10 contacts per particle some lane
+// of the warp hits almost every candidate index, so the branch was always
+// taken (C2 -5%, C3 -1%; the light bed C4 +2%: r2 history #29)
+template <bool EXACT, bool MONO = false, bool SMEM = false, bool PRED = false>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
                                                 int cx, int cy, int cz, uint32_t j,
                                                 uint32_t* out, uint32_t ostride,
@@ -1273,7 +1277,12 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
         for (int v = 0; v < U; ++v) {
           const float dx = Q[v].x - P.x, dy = Q[v].y - P.y, dz2 = Q[v].z - P.z;
           const float d2 = dx * dx + dy * dy + dz2 * dz2;
-          if (d2 < S2hi && tt[v] != j) {
+          if (PRED) {
+            const bool hit = d2 < S2hi && tt[v] != j;
+            amb = hit && d2 > S2lo ? 0.f : amb;
+            if (hit && npair < K) out[npair * ostride] = __float_as_uint(Q[v].w);
+            npair += hit ? 1u : 0u;
+          } else if (d2 < S2hi && tt[v] != j) {
             asm volatile("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f00000000, %3, p;}"
                          : "=f"(amb) : "f"(d2), "f"(S2lo), "f"(amb));
             if (npair < K) {
@@ -1627,7 +1636,8 @@ __global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
       sk = (uint32_t)cx + (uint32_t)g.nx * ((uint32_t)cy + (uint32_t)g.ny * (uint32_t)cz);
       const float S = b.sw_r + b.sw_r, S2c = S * S;
       float amb = -1.f;
-      np = detect_scan<false, true, true>(b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
+      np = detect_scan<false, true, true, CFG == kForceDense>(b, g, o.P, cx, cy, cz, j, s_cq + lane,
+                                                               32u, K, amb, S2c);
       if (amb >= 0.f)  // a candidate in the ±16u band: the exact rescan (R14)
         np = detect_scan<true, true, true>(b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
     }
