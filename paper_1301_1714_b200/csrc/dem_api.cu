@@ -452,7 +452,12 @@ int check_step_error(dem_handle* h, int64_t ctr0, int cur0, int64_t nsteps) {
   }
   if (h->slab) {  // no roll-back across ranks: the handle must be set again
     char buf[240];
-    if (e.code == 11u && (e.slot & 0xFFFFFF00u) == 0xFFFFFF00u)
+    if (e.code == 11u && e.slot == 0xFFFFFE00u)
+      snprintf(buf, sizeof buf,
+               "slab exchange failed (slab rank %d): a neighbour's step failed (its publication "
+               "is poisoned) before step %u; set the particles again on every rank",
+               h->rank, e.step);
+    else if (e.code == 11u && (e.slot & 0xFFFFFF00u) == 0xFFFFFF00u)
       snprintf(buf, sizeof buf,
                "slab exchange failed (slab rank %d): neighbour publication of tag %u never "
                "arrived (seen: left %u, right %u, low bits) in step %u; set the particles again",

@@ -160,6 +160,7 @@ inline uint32_t xtc_stride(int64_t cap) { return 5u * xtc_ntiles(cap) + 4u; }
 // An exchange region = a header holding the writer's XLayout (read by the
 // neighbours at connect time) + 4 blocks (direction x parity).
 constexpr uint64_t kXRegionHdr = 256;
+constexpr uint32_t kXPoison = 0xFFFFFFFFu;  // XHeader.n_mig of a failed step's publication
 struct XLayout {  // byte offsets inside one (direction, parity) block
   uint64_t header, mig_pos, mig_vel, mig_omg, mig_cnt, mig_hist, gh_pos, gh_vel, gh_omg, gh_off,
       bytes;

@@ -2697,7 +2697,10 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
   __shared__ uint32_t s_warp[4][8];
   __shared__ uint32_t s_cnt[4][32];  // [category][sub-tile * 8 + warp]
   __shared__ uint32_t s_last;
-  if (ld_volatile(&b.err->code) != 0u) return;
+  // a failed step still publishes (a poisoned header, below), so that its
+  // neighbours fail at once instead of waiting out the tag timeout: its
+  // blocks skip the writes but take part in the publication count
+  const bool failed = ld_volatile(&b.err->code) != 0u;
   const uint32_t writers = __ldcg(&tc[5 * ntiles]);  // tiles with flagged outputs
   const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;  // the step that reads it
   const uint32_t par = tag & 1u;
@@ -2707,9 +2710,10 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
   // a tile without flagged outputs (all but the boundary planes' few) has
   // nothing to write: straight to the publication count
   const bool any = __ldcg(&tc[4 * ntiles + blockIdx.x]) != 0u;
+  const bool work = any && !failed;
   // this tile's base per category: the counts of the earlier tiles, summed
   // block-wide (a serial sum by 4 threads cost ~100 us per step at 500 tiles)
-  if (any) {
+  if (work) {
     uint32_t acc[4] = {0u, 0u, 0u, 0u};
     for (uint32_t t = threadIdx.x; t < blockIdx.x; t += blockDim.x)
 #pragma unroll
@@ -2727,7 +2731,7 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
     }
     __syncthreads();
   }
-  if (any) {
+  if (work) {
     // the tile's four sub-tiles at once (their loads in flight together): a
     // flagged output's rank in its category = this tile's base + the flagged
     // outputs before it in slot order (sub-tile, warp, lane)
@@ -2839,10 +2843,13 @@ __global__ void __launch_bounds__(256) k_xpack_write(StepBuffers b, DevGrid g, u
     tot[q] = 0;
     for (int w = 0; w < 8; ++w) tot[q] += s_warp[q][w];
   }
+  // poisoned when this rank's step failed (its error word, any block's
+  // overflow included) or more migrants left than a block holds
+  const bool poison = ld_volatile(&b.err->code) != 0u || tot[0] > L.mig_cap || tot[1] > L.mig_cap;
   XHeader* h[2];
   for (int dir = 0; dir < 2; ++dir) {
     h[dir] = reinterpret_cast<XHeader*>(mine + (size_t)(dir * 2 + par) * L.bytes + L.header);
-    h[dir]->n_mig = tot[dir];  // (n_ghost: k_xpack_planes / k_xplanes_initial)
+    h[dir]->n_mig = poison ? kXPoison : tot[dir];  // (n_ghost: k_xpack_planes / k_xplanes_initial)
   }
   // one system-scope release fence for both tags (a fence.sc.sys + st.release.sys
   // per tag, as before, was four system membars: ~15 us of a 20 us pack)
@@ -2879,11 +2886,14 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
                                                const uint8_t* left, const uint8_t* right,
                                                XLayout L, XState* xs, uint32_t* nslots, int merge) {
   __shared__ uint32_t s_cnt[4], s_seen[2];
-  __shared__ uint32_t s_ok;
+  __shared__ uint32_t s_ok, s_bad;
   if (ld_volatile(&b.err->code) != 0u) return;
   const uint32_t tag = ld_volatile(&b.err->step_ctr) + 1u + g.xbase;
   const uint32_t par = tag & 1u;
-  if (threadIdx.x == 0) s_ok = 1u;
+  if (threadIdx.x == 0) {
+    s_ok = 1u;
+    s_bad = 0u;
+  }
   __syncthreads();
   if (threadIdx.x < 2) {
     const uint8_t* peer = threadIdx.x == 0 ? left : right;
@@ -2895,6 +2905,11 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
       if (!wait_tag(&h->tag, tag, &s_seen[threadIdx.x])) s_ok = 0u;
       nm = ld_volatile(&h->n_mig);
       ng = ld_volatile(&h->n_ghost);
+      // the neighbour's step failed (kXPoison), or counts past the blocks
+      if (nm > L.mig_cap || ng > L.ghost_cap) {
+        s_bad = 1u;
+        nm = ng = 0u;
+      }
     }
     s_cnt[threadIdx.x] = nm;
     s_cnt[2 + threadIdx.x] = ng;
@@ -2903,6 +2918,10 @@ __global__ void __launch_bounds__(256) k_xrecv(StepBuffers b, DevGrid g, uint32_
   const uint32_t c0 = s_cnt[0], c1 = s_cnt[1], c2 = s_cnt[2], c3 = s_cnt[3];
   const uint32_t tot = c0 + c1 + c2 + c3;
   const uint32_t base = xs->n_out;
+  if (s_ok && s_bad) {  // slot 0xFFFFFE00: a neighbour published a failed step
+    if (threadIdx.x == 0) raise_error(b.err, 11u, 0xFFFFFE00u, 0u);
+    return;
+  }
   if (!s_ok) {  // slot: 0xFFFFFF00 | expected tag's low byte; id: tags seen (left, right)
     if (threadIdx.x == 0)
       raise_error(b.err, 11u, 0xFFFFFF00u | (tag & 0xFFu),

@@ -305,3 +305,38 @@ def test_slab_ranks_with_different_sets_refuse_to_connect():
     with pytest.raises(DemError) as e:
         ds[0].connect_local(None, ds[1])
     assert "layout" in str(e.value)
+
+
+def test_slab_overflow_fails_fast():
+    """A whole z-plane of spheres (49 x 49) crosses the slab boundary in one
+    step: more migrants than the exchange blocks hold (capacity from the most
+    populated plane: max(1024, (2 x 2,402 + 1,024) / 4) = 1,457). The sending
+    rank's step fails with DEM_EOVERFLOW; its publication carries the failure,
+    so the neighbour's next step fails with DEM_EPEER at once — not after the
+    ~30 s tag timeout, and without reading past the exchange block."""
+    import time
+
+    from paper_1301_1714_b200.dem import DEM_EOVERFLOW, DEM_EPEER
+
+    L = 60e-3
+    params = S.SimParams(gravity=(0.0, 0.0, 0.0), box_hi=(L, L, L))
+    h = 2 * S.R * (1 + 2.0**-10)
+    nz = int(np.floor(L / h))
+    zb = (nz // 2) * h  # rank 1's first plane (planes split evenly)
+    g = 0.6e-3 + 1.2e-3 * np.arange(49)
+    x, y = np.meshgrid(g, g, indexing="ij")
+    pos = np.stack([x.ravel(), y.ravel(), np.full(x.size, zb - 0.2e-3)], 1)
+    vel = np.zeros_like(pos)
+    vel[:, 2] = 0.4e-3 / params.dt  # 0.4 mm in one step: into rank 1's first plane
+    sc = S.make_scene("plane_crossing", params, pos, vel)
+    ds = make_slabs(sc, 2, flags=0)
+    assert len(ds[0].get_state()["id"]) == sc.n
+    with pytest.raises(DemError) as e:
+        ds[0].step(1)
+    assert e.value.code == DEM_EOVERFLOW
+    ds[1].step(1)  # reads rank 0's publication from dem_set_particles: fine
+    t0 = time.perf_counter()
+    with pytest.raises(DemError) as e:
+        ds[1].step(1)  # reads rank 0's failed step
+    assert e.value.code == DEM_EPEER and "neighbour's step failed" in str(e.value)
+    assert time.perf_counter() - t0 < 10.0
