@@ -208,7 +208,7 @@ typedef struct {
   double max_speed;      /* max |v| of the current state [m/s]: the last step moved no
                             particle farther than max_speed * dt (the §5 termination test) */
   int32_t fused_sweep;   /* 1: detection (steps 5-6) runs inside the force kernel (one radius,
-                            dense configuration, no DEM_F_SPLIT_SWEEP); 0: k_detect + k_force */
+                            no DEM_F_SPLIT_SWEEP or ablation flag); 0: k_detect + k_force */
   int32_t reserved;
 } dem_stats;
 

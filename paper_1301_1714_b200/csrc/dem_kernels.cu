@@ -1,7 +1,8 @@
 // dem_kernels.cu — the sm_100a kernels of one DEM timestep (arXiv 1301.1714).
 //
-// One step on the default single-GPU path (§4.2),
-// three kernels:
+// One step on the default single-GPU path (§4.2):
+// k_merge and k_force with the detection inside it (one radius), or k_merge,
+// k_detect, k_force (per-particle radii, DEM_F_SPLIT_SWEEP):
 //   k_merge   steps 3-4: the stable sort of Eq. 11 as a merge of the few
 //             particles that changed cell into the last sorted order (every
 //             quantity is a count over the mover list the integrator made);
@@ -10,8 +11,8 @@
 //   k_detect  steps 5-6: one thread per sorted slot scans the 27 cells of
 //             Eq. 12 with the fp64-defined contact predicate (R14) and writes
 //             its contact list and its warp-flattened (base, count) word.
-//             (One radius, dense configuration: the same scan runs inside
-//             k_force<..., FUSED>, its lists in shared memory.)
+//             (One radius: the same scan runs inside k_force<..., FUSED>,
+//             its lists in shared memory, each z-plane's rows as one run.)
 //   k_force   steps 7-8, 1 and the next step's 2: a warp per 32 sorted slots
 //             deals its contacts 32 per round to all lanes (Eqs. 2-10 with the
 //             tangential history remapped through the old slots, Eq. 7), then
