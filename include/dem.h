@@ -203,7 +203,8 @@ typedef struct {
   int64_t kernel_count[8];
   int32_t force_cfg;     /* force configuration in use: 0 dense, 1 light, 2 lanes, -1 not chosen yet */
   int32_t full_sorts;    /* steps sorted by the counting sort since dem_set_particles: the
-                            first, and any in which more than 4,096 particles changed cell;
+                            first, and any in which more than max(4,096, n/512) particles
+                            changed cell (slab ranks: plus twice the migrant capacity);
                             the others merge the few movers into the last sorted order */
   double max_speed;      /* max |v| of the current state [m/s]: the last step moved no
                             particle farther than max_speed * dt (the §5 termination test) */
