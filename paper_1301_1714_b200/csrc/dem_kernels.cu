@@ -1575,8 +1575,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // FUSED (one radius only, b.sw_r > 0): the warp detects its own contacts
 // first (steps 5-6, the scan of k_detect into its shared-memory list) — no
 // k_detect launch, no contact list or (base, n) words in HBM.
+// With the detection fused in, both configurations take 28 blocks per SM (72
+// registers): the light one measured 2% faster than at 32 (r2 history #32)
+#ifndef DEM_FUSED_MINB
+#define DEM_FUSED_MINB (28 / DEM_SWEEP_WARPS)
+#endif
 template <int MODEL, bool DIAG, int CFG, bool MAT, uint32_t KC = 0, bool FUSED = false>
-__global__ void __launch_bounds__(32 * kSweepWarps, ForceCfg<CFG>::kMinBlocks)
+__global__ void __launch_bounds__(32 * kSweepWarps, FUSED ? DEM_FUSED_MINB : ForceCfg<CFG>::kMinBlocks)
     k_force(StepBuffers b, DevGrid g, DevPhys ph, uint32_t N, uint32_t Kr) {
   using C = ForceCfg<CFG>;
   constexpr uint32_t kChunk = FUSED ? 0u : C::kChunk;  // 0: partner slots per (k, lane)
