@@ -1228,6 +1228,11 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
 // with it, +27% there — profiles/r2_history.md #26)
 constexpr int kDetectFlat = DEM_DETECT_FLAT;
+// the dense configuration's (PRED) runs: five loads per trip (C3 -3%, r2 history #33)
+#ifndef DEM_DETECT_FLAT_DENSE
+#define DEM_DETECT_FLAT_DENSE 5
+#endif
+constexpr int kDetectFlatDense = DEM_DETECT_FLAT_DENSE;
 // PRED (fused sweep, dense configuration): a hit handled by predicated
 // instructions instead of a branch — with ~10 contacts per particle some lane
 // of the warp hits almost every candidate index, so the branch was always
@@ -1245,9 +1250,10 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
   // those of them above S²(1 - 16u) are in the band (the EXACT scan's own
   // thresholds), so a non-touching candidate costs one compare
   const float S2lo = S2c * 0.99999904632568359375f, S2hi = S2c * 1.00000095367431640625f;
-  if (!EXACT && MONO && SMEM && kDetectFlat > 1) {
+  constexpr int kFlat = PRED ? kDetectFlatDense : kDetectFlat;
+  if (!EXACT && MONO && SMEM && kFlat > 1) {
     // the plane's 3 rows as one flattened run u = 0..n0+n1+n2 (the same
-    // candidate order), kDetectFlat candidate loads in flight per iteration
+    // candidate order), kFlat candidate loads in flight per iteration
 #pragma unroll 1
     for (int dz = -1; dz <= 1; ++dz) {
       const int z = cz + dz;
@@ -1264,8 +1270,8 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
       const uint32_t c1 = t1[0] - t0[0], c2 = c1 + (t1[1] - t0[1]), nt = c2 + (t1[2] - t0[2]);
       const uint32_t b0 = t0[0], b1 = t0[1] - c1, b2 = t0[2] - c2;  // t = u + b(row of u)
 #pragma unroll 1
-      for (uint32_t u = 0; u < nt; u += (uint32_t)(kDetectFlat > 1 ? kDetectFlat : 1)) {
-        constexpr int U = kDetectFlat > 1 ? kDetectFlat : 1;
+      for (uint32_t u = 0; u < nt; u += (uint32_t)(kFlat > 1 ? kFlat : 1)) {
+        constexpr int U = kFlat > 1 ? kFlat : 1;
         float4 Q[U];
         uint32_t tt[U];
 #pragma unroll
