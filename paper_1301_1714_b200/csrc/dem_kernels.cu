@@ -1237,7 +1237,8 @@ constexpr int kDetectFlatDense = DEM_DETECT_FLAT_DENSE;
 // instructions instead of a branch — with ~10 contacts per particle some lane
 // of the warp hits almost every candidate index, so the branch was always
 // taken (C2 -5%, C3 -1%; the light bed C4 +2%: r2 history #29)
-template <bool EXACT, bool MONO = false, bool SMEM = false, bool PRED = false>
+template <bool EXACT, bool MONO = false, bool SMEM = false, bool PRED = false,
+          int FLAT = kDetectFlat>
 __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevGrid& g, float4 P,
                                                 int cx, int cy, int cz, uint32_t j,
                                                 uint32_t* out, uint32_t ostride,
@@ -1250,7 +1251,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
   // those of them above S²(1 - 16u) are in the band (the EXACT scan's own
   // thresholds), so a non-touching candidate costs one compare
   const float S2lo = S2c * 0.99999904632568359375f, S2hi = S2c * 1.00000095367431640625f;
-  constexpr int kFlat = PRED ? kDetectFlatDense : kDetectFlat;
+  constexpr int kFlat = FLAT;
   if (!EXACT && MONO && SMEM && kFlat > 1) {
     // the plane's 3 rows as one flattened run u = 0..n0+n1+n2 (the same
     // candidate order), kFlat candidate loads in flight per iteration
@@ -1648,8 +1649,9 @@ __global__ void __launch_bounds__(32 * kSweepWarps, FUSED ? DEM_FUSED_MINB : For
       sk = (uint32_t)cx + (uint32_t)g.nx * ((uint32_t)cy + (uint32_t)g.ny * (uint32_t)cz);
       const float S = b.sw_r + b.sw_r, S2c = S * S;
       float amb = -1.f;
-      np = detect_scan<false, true, true, CFG == kForceDense>(b, g, o.P, cx, cy, cz, j, s_cq + lane,
-                                                               32u, K, amb, S2c);
+      np = detect_scan<false, true, true, CFG == kForceDense,
+                       CFG == kForceDense ? kDetectFlatDense : kDetectFlat>(
+          b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
       if (amb >= 0.f)  // a candidate in the ±16u band: the exact rescan (R14)
         np = detect_scan<true, true, true>(b, g, o.P, cx, cy, cz, j, s_cq + lane, 32u, K, amb, S2c);
     }
