@@ -1228,6 +1228,13 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
 // with it, +27% there — profiles/r2_history.md #26)
 constexpr int kDetectFlat = DEM_DETECT_FLAT;
+// per-particle radii: the fast scan's band test (the EXACT scan's own
+// thresholds S²(1 ± 16u)) inside the hit branch, as with one radius, instead
+// of a running max of 16u S² - |d² - S²| over every candidate
+#ifndef DEM_DETECT_BAND_BRANCH
+#define DEM_DETECT_BAND_BRANCH 1
+#endif
+constexpr bool kDetectBandBranch = DEM_DETECT_BAND_BRANCH != 0;
 // the dense configuration's (PRED) runs: five loads per trip (C3 -3%, r2 history #33)
 #ifndef DEM_DETECT_FLAT_DENSE
 #define DEM_DETECT_FLAT_DENSE 5
@@ -1338,6 +1345,8 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
             const double Sd = (double)P.w + (double)Q.w;
             hit = exact_d2(P, Q) < __dmul_rn(Sd, Sd);
           }
+        } else if (kDetectBandBranch) {
+          hit = d2 < S2 * 1.00000095367431640625f;  // as MONO, with this pair's S²
         } else {
           const float rr = d2 - S2;
           hit = rr < 0.f;
@@ -1346,11 +1355,12 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
         // only the middle row (y = cy) can hold slot j itself: the other two
         // rows skip the self test (r is unrolled, so it folds away there)
         if (hit && (r != 1 || t != j)) {
-          if (!EXACT && MONO) {
+          if (!EXACT && (MONO || kDetectBandBranch)) {
             // band: the caller rescans exactly. volatile keeps the test in this
             // branch (if-converted, it would cost every candidate two instructions)
+            const float lo = MONO ? S2lo : S2 * 0.99999904632568359375f;
             asm volatile("{.reg .pred p; setp.gt.f32 p, %1, %2; selp.f32 %0, 0f00000000, %3, p;}"
-                         : "=f"(amb) : "f"(d2), "f"(S2lo), "f"(amb));
+                         : "=f"(amb) : "f"(d2), "f"(lo), "f"(amb));
           }
           if (npair < K) {
             if (SMEM) *out = qs;
