@@ -1228,6 +1228,12 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
 // with it, +27% there — profiles/r2_history.md #26)
 constexpr int kDetectFlat = DEM_DETECT_FLAT;
+// the per-row candidate loop with per-particle radii unrolled by two:
+// two candidate loads in flight per trip (C5 k_detect -2%, r2 history #37)
+#ifndef DEM_ROW_UNROLL
+#define DEM_ROW_UNROLL 2
+#endif
+constexpr int kRowUnroll = DEM_ROW_UNROLL;
 // per-particle radii: the fast scan's band test (the EXACT scan's own
 // thresholds S²(1 ± 16u)) inside the hit branch, as with one radius, instead
 // of a running max of 16u S² - |d² - S²| over every candidate
@@ -1327,7 +1333,7 @@ __device__ __forceinline__ uint32_t detect_scan(const StepBuffers& b, const DevG
     }
 #pragma unroll
     for (int r = 0; r < 3; ++r) {
-#pragma unroll 1
+#pragma unroll (MONO ? 1 : kRowUnroll)
       for (uint32_t t = t0[r]; t < t1[r]; ++t) {
         float4 Q = __ldg(&b.pos_sorted[t]);
         const uint32_t qs = MONO ? __float_as_uint(Q.w) : t;  // what the list stores
