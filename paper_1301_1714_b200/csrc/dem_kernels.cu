@@ -1511,6 +1511,10 @@ struct WarpSmemLayout {
 };
 constexpr int kSweepWarps = DEM_SWEEP_WARPS;  // warps per k_force block
 constexpr uint32_t kForceKC = 16;  // K with its own k_force instantiation
+// K = 32 (the polydisperse C5) with its own light instantiation too
+#ifndef DEM_FORCE_KC32
+#define DEM_FORCE_KC32 1
+#endif
 #ifndef DEM_FORCE_FIRST
 #define DEM_FORCE_FIRST 4
 #endif
@@ -2493,6 +2497,11 @@ __global__ void __launch_bounds__(128) k_finish(StepBuffers b, DevGrid g, DevPhy
 
 // Set the dynamic shared-memory limit of every k_force instantiation once,
 // outside any stream capture (cudaFuncSetAttribute is not capturable).
+#if DEM_FORCE_KC32
+#define DEM_KC32_ATTR(MODEL, DIAG) cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, 32u>, A, sl);
+#else
+#define DEM_KC32_ATTR(MODEL, DIAG)
+#endif
 void sweep_prepare(uint32_t K) {
   const int sd = (int)(WarpSmemLayout::make(K, kForceDense).bytes * kSweepWarps);
   const int sl = (int)(WarpSmemLayout::make(K, kForceLight).bytes * kSweepWarps);
@@ -2506,6 +2515,7 @@ void sweep_prepare(uint32_t K) {
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, true>, A, sl); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, kForceKC>, A, sd); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, A, sl); \
+  DEM_KC32_ATTR(MODEL, DIAG)                                                        \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, true, 0, true>, A, fd); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, 0, true>, A, fd); \
   cudaFuncSetAttribute(k_force<MODEL, DIAG, kForceDense, false, kForceKC, true>, A, fd); \
@@ -3418,6 +3428,9 @@ static void sweep_dispatch(cudaStream_t st, int64_t n, uint32_t K, const StepBuf
     if (cfg == kForceLight) {
       if (mat) launch_pdl(k_force<MODEL, DIAG, kForceLight, true>, grid, block, smem, st, b, g, ph, N, K);
       else if (k16) launch_pdl(k_force<MODEL, DIAG, kForceLight, false, kForceKC>, grid, block, smem, st, b, g, ph, N, K);
+#if DEM_FORCE_KC32
+      else if (K == 32u) launch_pdl(k_force<MODEL, DIAG, kForceLight, false, 32u>, grid, block, smem, st, b, g, ph, N, K);
+#endif
       else launch_pdl(k_force<MODEL, DIAG, kForceLight, false>, grid, block, smem, st, b, g, ph, N, K);
     } else {
       if (mat) launch_pdl(k_force<MODEL, DIAG, kForceDense, true>, grid, block, smem, st, b, g, ph, N, K);
