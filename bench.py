@@ -550,9 +550,11 @@ def main():
     ap.add_argument("--model", default="practical", choices=["practical", "simple"])
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--sweep", default="full", choices=["full", "half", "tpp", "lanes", "ws", "split"],
-                    help="full contact lists + warp-flattened force rounds (default); half "
-                         "lists, each pair once (Newton's third law); or the paper's fused "
-                         "thread per particle")
+                    help="full: the default path (one radius: detection inside k_force; "
+                         "else k_detect + k_force, warp-flattened force rounds); split: "
+                         "k_detect + k_force always; ablations: half lists (each pair once, "
+                         "Newton's third law), tpp (the paper's fused thread per particle), "
+                         "lanes, ws (warp-specialised)")
     ap.add_argument("--extra-flags", type=int, default=0,
                     help="dem_flags OR-ed into the handle's (A/B runs, e.g. a force configuration)")
     ap.add_argument("--e2e-steps", type=int, default=5)
