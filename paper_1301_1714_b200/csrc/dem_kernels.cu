@@ -1479,7 +1479,10 @@ struct ForceCfg {
   static constexpr uint32_t kChunk = CFG == kForceLight ? DEM_LIGHT_CHUNK : 0u;  // 0: per (k, lane)
   static constexpr int kMinBlocks = CFG == kForceLight ? DEM_LIGHT_MINB : 28 / DEM_SWEEP_WARPS;
 };
-constexpr uint32_t kResW = 64;  // contacts per accumulation window (two rounds)
+#ifndef DEM_RES_W
+#define DEM_RES_W 64
+#endif
+constexpr uint32_t kResW = DEM_RES_W;  // contacts per accumulation window (two rounds)
 struct WarpSmemLayout {
   uint32_t bytes, pf, cq, res, own, ost, base, slot, nold;
   // fixed-size regions first, so their offsets are compile-time constants;
