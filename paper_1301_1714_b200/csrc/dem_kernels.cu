@@ -1228,10 +1228,10 @@ __device__ __forceinline__ void owned_range(const StepBuffers& b, const DevGrid&
 // candidate loads per trip (C3 -4%; k_detect's 32-register threads spill
 // with it, +27% there — profiles/r2_history.md #26)
 constexpr int kDetectFlat = DEM_DETECT_FLAT;
-// the per-row candidate loop with per-particle radii unrolled by two:
-// two candidate loads in flight per trip (C5 k_detect -2%, r2 history #37)
+// the per-row candidate loop with per-particle radii unrolled by six:
+// several candidate loads in flight per trip (C5 k_detect -6%, r2 history #37)
 #ifndef DEM_ROW_UNROLL
-#define DEM_ROW_UNROLL 2
+#define DEM_ROW_UNROLL 6
 #endif
 constexpr int kRowUnroll = DEM_ROW_UNROLL;
 // per-particle radii: the fast scan's band test (the EXACT scan's own
